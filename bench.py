@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark: BGV Comp throughput (entries/s) and latency at N=2^14, s=16
+(BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step is one full Comp (pack_pair + BSGS matvec, compress.py:488-514) of a
+seeded synthetic database: bench.run_point's recipe (bench.py:72-94 of the
+reference): HeParams(8192, 65537, 3), keygen over plan_rotation_amounts,
+a random s-sparse payload (random.Random(seed)), encrypted d and index hint.
+
+* value  -- device-resident: inputs, keys and plan already in HBM; each timed
+            step is one CUDA-graph launch of the Comp, timed with CUDA events
+            on its stream; L2 is flushed (256 MiB write) between steps.
+* e2e    -- through the public C-ABI call hc_comp_async with pinned HOST
+            buffers: H2D of the 2*C input ciphertexts, the Comp, D2H of the
+            level-0 output, all inside the event-timed region.
+* N > 1  -- replicas (SURVEY 8(e) "batched independent queries"): every rank
+            runs its own query (own seed and keys); value = total entries
+            over all ranks / max-over-ranks time; scaling "weak".
+* --impl reference -- the CPU oracle port of the reference's Comp
+            (oracle/, C + OpenMP, every host thread) on the same config;
+            rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT, S_DEFAULT, P_DEFAULT, RING = 1 << 14, 16, 65537, 8192
+METRIC = "Comp encrypted entries/sec (N=2^14, s=16)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--N", type=int, default=N_DEFAULT)
+    ap.add_argument("--s", type=int, default=S_DEFAULT)
+    ap.add_argument("--p", type=int, default=0, help="plaintext prime (default: 65537, or per SURVEY F4 for N >= p)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def pick_p(N: int, p: int) -> int:
+    if p:
+        return p
+    if N < 65537:
+        return 65537
+    for cand in (786433, 1097729, 4423681):
+        if cand > N:
+            return cand
+    raise SystemExit("N too large")
+
+
+def workload(args, p):
+    return {
+        "workload": f"BGV Comp (hint path, packed) N={args.N} s={args.s} n={RING} p={p} max_level=3",
+        "N": args.N,
+        "s": args.s,
+        "n": RING,
+        "p": p,
+        "max_level": 3,
+        "seeded_synthetic": "bench.run_point recipe: random.Random(seed) s-sparse payload, encrypted d + index hint",
+        "l2": "flushed between timed steps (256 MiB write, untimed)",
+        "parallelism": "replicas" if args.gpus > 1 else "single",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+            )
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def plant(N, s, p, seed):
+    rng = random.Random(seed)
+    support = sorted(rng.sample(range(1, N + 1), s))
+    dense = [0] * N
+    for i in support:
+        dense[i - 1] = rng.randrange(1, p)
+    return dense
+
+
+def run_reference(args, p, rank):
+    """CPU arm: the oracle port of the reference Comp with every host thread."""
+    if rank != 0:
+        return None
+    from oracle import bgv_oracle as O
+
+    O.lib()
+    threads = O.lib().orc_num_threads()
+    be = O.OracleBgv(RING, p, 3, seed=0, check_noise=False)
+    keys = be.keygen(*O.plan_rotation_amounts(args.s, RING))
+    dense = plant(args.N, args.s, p, 0)
+    cts = O.encrypt_vector(dense, args.N, be, keys)
+    hint = O.encrypt_vector([1 if x else 0 for x in dense], args.N, be, keys)
+    for _ in range(args.warmup):
+        O.comp(cts, args.N, args.s, be, keys, hint)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.comp(cts, args.N, args.s, be, keys, hint)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.N * args.steps / total
+    line = {
+        "metric": METRIC,
+        "impl": "reference",
+        "value": value,
+        "unit": "entries/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (RNS, 54-bit primes)",
+        "data": "synthetic (seeded; bench.run_point recipe)",
+        "config": workload(args, p),
+        "cpu_baseline": {
+            "value": value,
+            "unit": "entries/s",
+            "cores": threads,
+            "kind": "port",
+            "sample": f"{args.steps} full Comps (N={args.N}, s={args.s}) with the C/OpenMP oracle port of the reference's Comp",
+        },
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def cpu_baseline_sample(args, p, budget_s):
+    """Oracle port timed on this host on full Comps until ~budget_s of work."""
+    from oracle import bgv_oracle as O
+
+    O.lib()
+    be = O.OracleBgv(RING, p, 3, seed=0, check_noise=False)
+    keys = be.keygen(*O.plan_rotation_amounts(args.s, RING))
+    dense = plant(args.N, args.s, p, 0)
+    cts = O.encrypt_vector(dense, args.N, be, keys)
+    hint = O.encrypt_vector([1 if x else 0 for x in dense], args.N, be, keys)
+    n, t_total = 0, 0.0
+    while t_total < budget_s or n == 0:
+        t0 = time.perf_counter()
+        O.comp(cts, args.N, args.s, be, keys, hint)
+        t_total += time.perf_counter() - t0
+        n += 1
+        if n >= 50:
+            break
+    return {
+        "value": args.N * n / t_total,
+        "unit": "entries/s",
+        "cores": O.lib().orc_num_threads(),
+        "kind": "port",
+        "sample": f"{n} full Comps (N={args.N}, s={args.s}), {t_total:.1f} s, C/OpenMP oracle port of the reference Comp",
+    }
+
+
+def main():
+    args = parse()
+    p = pick_p(args.N, args.p)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        line = run_reference(args, p, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_2408_17063_b200 as P
+    from paper_2408_17063_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    he = P.HeParams(RING, p, 3)
+    params = P.CompressionParams(args.N, args.s, he)
+    be = P.B200BgvBackend(he, seed=rank, device=local, noise_guard=False)
+    keys = be.keygen(*P.plan_rotation_amounts(args.s, RING))
+    dense = plant(args.N, args.s, p, rank)
+    cts = P.encrypt_vector(dense, params, be, keys)
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    dc = P.DeviceComp(be, params, keys)
+    cd = np.ascontiguousarray(np.stack([c.payload.res for c in cts]))
+    cv = np.ascontiguousarray(np.stack([c.payload.res for c in hint]))
+    dc.set_inputs(cd, cv)
+    info = be.plan_info()
+
+    stream = torch.cuda.Stream()
+    sh = stream.cuda_stream
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    L = _lib.lib()
+    h = be._ctx()
+
+    # correctness gate: the timed Comp must decrypt to the payload's power sums
+    dc.launch(sh)
+    torch.cuda.synchronize()
+    out = dc.output()
+    ct = P.Ciphertext(be.backend_id, keys.key_id, 0, P.RnsPayload(out, 0.0, (be.q[0],)))
+    m = be.decrypt(ct, keys)
+    w = [int(x) for x in m.rows[0][: args.s]]
+    want_w = [sum(pow(i + 1, j + 1, p) for i, v in enumerate(dense) if v) % p for j in range(args.s)]
+    assert w == want_w, "Comp output does not decrypt to the expected power sums"
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            flush.zero_()
+            dc.launch(sh)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for a, b in evs:
+            flush.zero_()
+            a.record(stream)
+            dc.launch(sh)
+            b.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_ms = sum(step_ms)
+
+    # ---- end-to-end through the public C-ABI with pinned host buffers ----
+    cd_h = torch.from_numpy(cd).pin_memory()
+    cv_h = torch.from_numpy(cv).pin_memory()
+    out_h = torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()
+    e2e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            _lib.check(L.hc_comp_async(h, cd_h.data_ptr(), cv_h.data_ptr(), cd.shape[0], out_h.data_ptr(), sh))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        for a, b in e2e_evs:
+            flush.zero_()
+            a.record(stream)
+            _lib.check(L.hc_comp_async(h, cd_h.data_ptr(), cv_h.data_ptr(), cd.shape[0], out_h.data_ptr(), sh))
+            b.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    assert np.array_equal(out_h.numpy().view(np.uint64), out), "e2e output differs from the device-resident run"
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
+
+    if dist:
+        tt = torch.tensor([t_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms, e2e_ms = tt.tolist()
+
+    # ---- live roofline of the dominant kernel (k_xform) ----
+    max_steps = 4096
+    sm_ = np.zeros(max_steps, dtype=np.float32)
+    sk = np.zeros(max_steps, dtype=np.int32)
+    sj = np.zeros(max_steps, dtype=np.int32)
+    nsteps = L.hc_comp_profile(h, sh, max_steps, _lib.ptr(sm_), _lib.ptr(sk), _lib.ptr(sj))
+    if nsteps < 0:
+        _lib.check(nsteps)
+    kinds = {}
+    for i in range(nsteps):
+        d = kinds.setdefault(int(sk[i]), [0.0, 0, 0])
+        d[0] += float(sm_[i])
+        d[1] += int(sj[i])
+        d[2] += 1
+    xf_ms, xf_jobs, xf_launch = kinds.get(0, [0.0, 0, 0])
+    prof_total = float(sm_[:nsteps].sum())
+    peak = ctypes.c_double()
+    _lib.check(L.hc_bf_peak(h, ctypes.byref(peak)))
+    bfly_per_ntt = (RING // 2) * 13
+    achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
+    peak_g = peak.value / 1e9
+
+    per_step_ms = t_ms / args.steps
+    value = args.N * world / (per_step_ms * 1e-3)
+    e2e_value = args.N * world / (e2e_ms / args.steps * 1e-3)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "entries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": per_step_ms,
+        "latency_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (RNS, 54-bit primes)",
+        "data": "synthetic (seeded; bench.run_point recipe; real keygen + encryption)",
+        "config": workload(args, p),
+        "e2e": {
+            "value": e2e_value,
+            "unit": "entries/s",
+            "ms_per_step": e2e_ms / args.steps,
+            "h2d_bytes_per_step": int(cd.nbytes + cv.nbytes),
+            "d2h_bytes_per_step": int(out.nbytes),
+        },
+        "gpu_launches": int(info["kernel_launches"]) * args.steps * 2,
+        "kernel_launches_per_comp": int(info["kernel_launches"]),
+        "roofline": {
+            "kernel": "k_xform (8192-point NTT/INTT, 1 CTA per transform, fused loaders/epilogues)",
+            "bound": "int-modmul (IMAD pipe; SURVEY 8(d))",
+            "achieved": achieved,
+            "peak": peak_g,
+            "unit": "Gbutterfly/s",
+            "frac": achieved / peak_g if peak_g else None,
+            "peak_source": "measured live: hc_bf_peak register-only microbenchmark of the same butterfly (MEASURED_PEAKS.json has no integer peak)",
+            "traffic": None,
+            "xform_share_of_step": xf_ms / prof_total if prof_total else None,
+            "xform_jobs_per_comp": xf_jobs,
+            "xform_launches_per_comp": xf_launch,
+            "profiled_step_ms_ungraphed": prof_total,
+            "per_kind_ms": {str(k): round(v[0], 4) for k, v in sorted(kinds.items())},
+        },
+        "clocks": clk,
+        "plan": info,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(args, p, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

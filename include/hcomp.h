@@ -1,0 +1,132 @@
+/*
+ * hcomp -- B200-native (sm_100a) BGV Comp for arXiv 2408.17063.
+ *
+ * C ABI of libhcomp.so.  Plain pointers and sizes only; the library owns all
+ * device memory tied to a context.  One context per CUDA stream; a context is
+ * not re-entrant (the reference backend is not thread-safe either:
+ * bgv.py:358-359, heiface.py:174).
+ *
+ * The reference (Python, /root/reference/pkg/src/hcpdq) has no native ABI;
+ * the Python package paper_2408_17063_b200 binds these entry points with
+ * ctypes behind the reference's own API (comp / BgvBackend methods).  Each
+ * entry point below names the reference interface it replaces.
+ *
+ * Data layout of every ring element: RNS residues uint64[P][n], row k the
+ * residue modulo level_prime(k) (bgv.py:104-106: row 0 = smallest prime,
+ * the last row is the prime a modulus switch divides out), values in [0, q_k).
+ * A ciphertext at level l is uint64[2][l+1][n] (c0 then c1), NTT domain.
+ * Only n = 8192 and max_level <= 3 are supported.
+ */
+#ifndef HCOMP_H
+#define HCOMP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python layer maps them onto the reference exceptions */
+#define HC_OK 0
+#define HC_ERR_ARG 1      /* ValueError            (compress.py:282-283, 348-349) */
+#define HC_ERR_LEVEL 2    /* LevelExhausted        (bgv.py:721-722) */
+#define HC_ERR_KEY 3      /* MissingRotationKey    (bgv.py:760-761, 767-768) */
+#define HC_ERR_MISMATCH 4 /* BackendMismatch       (bgv.py:443-450, 654-655) */
+#define HC_ERR_CUDA 5     /* CUDA runtime failure (no reference analogue) */
+#define HC_ERR_STATE 6    /* call out of order (e.g. comp before plan) */
+
+typedef struct hc_ctx hc_ctx;
+
+/* last error message of the calling thread (static storage) */
+const char* hc_last_error(void);
+
+/* Replaces BgvBackend.__init__ tables (bgv.py:328-363) and NttContext.__init__
+ * (bgv.py:150-174).  primes: the L+1 chain primes in LEVEL order
+ * (primes[k] = level_prime(k), ascending); p: plaintext modulus;
+ * ksw_base_bits must be 16 (bgv.py:333).  device: CUDA ordinal. */
+int hc_ctx_create(int n, int max_level, const uint64_t* primes, uint64_t p, int ksw_base_bits,
+                  int device, hc_ctx** out);
+void hc_ctx_destroy(hc_ctx* h);
+/* digits D_l per level (bgv.py:360-363) into digits[0..max_level] */
+int hc_ctx_digits(const hc_ctx* h, int* digits);
+
+/* Replaces KeySet.rotation_keys / col_swap_key material (bgv.py:482-509,
+ * _KskPair bgv.py:294-312).  Uploads one gadget key-switch key for the
+ * Galois element t (3^r mod 2n for rot_row(r), 2n-1 for rot_col):
+ * ksk = uint64[D_L][2][L+1][n] = (b_j, a_j) pairs, NTT domain residues. */
+int hc_load_ksk(hc_ctx* h, uint32_t galois_t, const uint64_t* ksk);
+int hc_clear_keys(hc_ctx* h);
+
+/* Replaces compress._plan / build_plan (compress.py:198-270, packed mode,
+ * no cleartext database): generates every diagonal, the pack masks and the
+ * output mask on the device and records the Comp schedule (a CUDA graph).
+ * chunk_blocks: blocks processed per pass (0 = automatic).
+ * Fails with HC_ERR_KEY if a needed rotation key is not loaded. */
+int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks);
+/* schedule facts: [B, C, baby, giant, F, s_pad, live_diagonals, kernel_launches] */
+int hc_plan_info(const hc_ctx* h, int64_t* info8);
+
+/* Replaces compress.comp(cd, ..., index_hint=cv) (compress.py:488-514),
+ * host buffers: cd, cv = uint64[C][2][4][n] at level 3; out = uint64[2][1][n]
+ * (the level-0 ciphertext of the CompressedAnswer).  Synchronous. */
+int hc_comp(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* out);
+
+/* Device-resident variant for timing: inputs already uploaded with
+ * hc_comp_set_inputs; hc_comp_launch enqueues the whole Comp (one graph
+ * launch) on `stream` (a cudaStream_t, NULL = legacy default stream). */
+int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C);
+int hc_comp_launch(hc_ctx* h, void* stream);
+int hc_comp_get_output(hc_ctx* h, uint64_t* out);
+/* Asynchronous end-to-end Comp on `stream`: H2D of cd/cv, the Comp graph and
+ * D2H of the output, all stream-ordered (pass pinned host buffers for
+ * overlap; the caller synchronises). */
+int hc_comp_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* out, void* stream);
+
+/* Block-sharded Comp.  hc_comp_partial runs pack + baby
+ * steps + diagonal products for blocks [b0, b1) of the database (inputs:
+ * the C ciphertexts of hc_comp_set_inputs, i.e. the full standard layout)
+ * and writes the partial accumulators to partial_dev, a DEVICE buffer of
+ * hc_partial_words() uint64 (every word < 2^54, so up to 1023 partials may
+ * be summed as uint64 before hc_comp_finish reduces mod q).  hc_comp_finish
+ * runs giant steps, folds and the output mask from a (summed) partial. */
+int64_t hc_partial_words(const hc_ctx* h);
+int hc_comp_partial(hc_ctx* h, int64_t b0, int64_t b1, uint64_t* partial_dev, void* stream);
+int hc_comp_finish(hc_ctx* h, const uint64_t* partial_dev, void* stream);
+
+/* Ring helpers on HOST buffers, executed on the GPU (used by the host-side
+ * keygen / encrypt / decrypt / serialization of the backend, bgv.py:464-575,
+ * 777-790).  rows of n values; row r uses RNS prime prime_idx[r]
+ * (0..max_level = chain primes in level order, 4 = p).
+ * hc_ntt: inverse = 0 -> NttContext.fwd, 1 -> NttContext.inv.
+ * hc_pointwise: op 0 mul, 1 add, 2 sub (bgv.py:431-437). */
+int hc_ntt(hc_ctx* h, uint64_t* data, int rows, const int* prime_idx, int inverse);
+int hc_pointwise(hc_ctx* h, const uint64_t* a, const uint64_t* b, uint64_t* out, int rows,
+                 const int* prime_idx, int op);
+
+/* Single backend operations (BgvBackend.mul_plain bgv.py:717-733 and
+ * _apply_galois bgv.py:735-747) on host buffers.
+ * hc_mul_plain: ct uint64[2][l+1][n] at level l >= 1, pt = NttContext
+ * residues of the plaintext at level l, uint64[l+1][n]; out uint64[2][l][n].
+ * hc_rotate: key switch by Galois element t at level l (1..3); out [2][l+1][n]. */
+int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint64_t* pt, uint64_t* out);
+int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t galois_t, uint64_t* out);
+
+/* Measurement: run the Comp schedule un-graphed with CUDA events around
+ * every step (kind: 0 transform, 1 CRT/digits, 2 key-switch MAC, 3 diagonal
+ * MAC, 4 copy fold, 5 memset).  Returns the number of steps written. */
+int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind, int* step_jobs);
+/* Measured butterfly-throughput ceiling of this GPU for the NTT butterfly
+ * used by the transform kernel (register-only microbenchmark). */
+int hc_bf_peak(hc_ctx* h, double* bfly_per_s);
+
+/* Pure host helpers (no GPU needed): Galois tables for element t.
+ * coef: uint16[n] (source index | negate << 15) realising X -> X^t on
+ * coefficients (coeff_automorphism, bgv.py:273-284, as a gather);
+ * perm: uint16[n] NTT-domain gather (galois_permutation, bgv.py:258-261). */
+int hc_galois_tables(int n, uint32_t galois_t, uint16_t* coef, uint16_t* perm);
+/* primitive 2n-th root used by the tables (bgv.py:120-126) */
+uint64_t hc_prim_root_2n(uint64_t q, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

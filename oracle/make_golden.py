@@ -1,0 +1,174 @@
+"""TEST INFRASTRUCTURE ONLY -- generate tests/golden/*.json by running the
+read-only Python REFERENCE (imported with the gmpy2 stand-in, see
+oracle/refimport.py) in the build container.  The GPU box has no
+/root/reference; the fixtures travel instead.
+
+For each case the reference runs exactly the bench.run_point recipe
+(bench.py:72-94): BgvBackend(HeParams(n, p, 3), seed), keygen over
+plan_rotation_amounts, a sparse payload planted with random.Random(seed)
+(bench.py:65-69), encrypt d then the index hint, then the timed
+`comp(..., index_hint=hint)`.  Recorded: SHA-256 of the serialized
+CompressedAnswer, decrypted (w, e), final noise_bits, Comp's counter
+deltas, key_id, and SHA-256 digests of the key material and input
+ciphertexts in RNS residue form (pins the oracle's keygen/encrypt).
+
+Small-ring cases (n=64) also store every residue (inputs, keys, output) so
+the oracle can be checked without regenerating anything.
+
+Usage:  python oracle/make_golden.py [case-name ...]
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import random
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, ROOT)
+
+from oracle import refimport  # noqa: E402
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+# name: (n, p, N, s, seed, guard_disabled)
+CASES = {
+    "small_n64_N200_s5": (64, 257, 200, 5, 11, True),
+    "small_n64_N64_s8": (64, 257, 64, 8, 12, True),
+    "c1_N8192_s8": (8192, 65537, 8192, 8, 0, False),
+    "c3_N8192_s16": (8192, 65537, 8192, 16, 1, False),
+    "c2_N16384_s16": (8192, 65537, 16384, 16, 0, False),
+    "odd_N10000_s5": (8192, 65537, 10000, 5, 3, True),
+    "c2_N16384_s32": (8192, 65537, 16384, 32, 0, True),
+}
+
+
+def residues_of(vals, primes_rns):
+    return np.array([[int(v) % q for v in vals] for q in primes_rns], dtype=np.uint64)
+
+
+def digest_arrays(arrs) -> str:
+    h = hashlib.sha256()
+    for a in arrs:
+        h.update(np.ascontiguousarray(a, dtype=np.uint64).tobytes())
+    return h.hexdigest()
+
+
+def keys_residues(be, keys):
+    """Key material in RNS order: pk_b, pk_a, relin pairs, rotation keys by
+    amount, col-swap key; each ring element [L+1][n]."""
+    L = be.params.max_level
+    primes = [be.chain.level_prime(k) for k in range(L + 1)]
+    out = [residues_of(keys.public.pk_b, primes), residues_of(keys.public.pk_a, primes)]
+
+    def ksk(k):
+        for b, a in k.pairs:
+            out.append(residues_of(b, primes))
+            out.append(residues_of(a, primes))
+
+    ksk(keys.relin_key)
+    for r in sorted(keys.rotation_keys):
+        ksk(keys.rotation_keys[r][1])
+    if keys.col_swap_key is not None:
+        ksk(keys.col_swap_key[1])
+    return out
+
+
+def ct_residues(be, c):
+    primes = [be.chain.level_prime(k) for k in range(c.level + 1)]
+    return np.stack([residues_of(c.payload.c0, primes), residues_of(c.payload.c1, primes)])
+
+
+def run_case(name):
+    n, p, N, s, seed, guard_off = CASES[name]
+    hc = refimport.load()
+    from hcpdq.bgv import BgvBackend
+    from hcpdq.compress import (
+        CompressionParams,
+        comp,
+        decomp,
+        encrypt_vector,
+        plan_rotation_amounts,
+    )
+    from hcpdq.heiface import HeParams
+
+    he = HeParams(n, p, 3)
+    params = CompressionParams(N, s, he)
+    be = BgvBackend(he, seed=seed)
+    amounts, col = plan_rotation_amounts(s, n)
+    t0 = time.time()
+    keys = be.keygen(amounts, col_swap=col)
+    rng = random.Random(seed)
+    support = sorted(rng.sample(range(1, N + 1), s))
+    dense = [0] * N
+    for i in support:
+        dense[i - 1] = rng.randrange(1, p)
+    cts = encrypt_vector(dense, params, be, keys)
+    hint = encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    t1 = time.time()
+    before = be.counters.snapshot()
+    if guard_off:
+        with refimport.noise_guard_disabled():
+            ans = comp(cts, params, be, keys, index_hint=hint)
+    else:
+        ans = comp(cts, params, be, keys, index_hint=hint)
+    t2 = time.time()
+    delta = be.counters.delta(before)
+    blob = ans.serialize(be)
+    w, e = ans.payload_slots(be, keys)
+    rec = decomp(ans, params, be, keys)
+    assert rec.entries == tuple((i, dense[i - 1]) for i in support), "reference round trip failed"
+    out = ans.cts[0]
+    L = he.max_level
+    rec_json = {
+        "case": name,
+        "generator": "oracle/make_golden.py (reference hcpdq run in the build container)",
+        "n": n,
+        "p": p,
+        "max_level": L,
+        "N": N,
+        "s": s,
+        "seed": seed,
+        "noise_guard_disabled": guard_off,
+        "chain_primes_desc": list(be.chain.primes),
+        "key_id": keys.key_id.hex(),
+        "support": support,
+        "values": [dense[i - 1] for i in support],
+        "answer_sha256": hashlib.sha256(blob).hexdigest(),
+        "answer_len": len(blob),
+        "w": w,
+        "e": e,
+        "noise_bits": out.payload.noise_bits,
+        "out_level": out.level,
+        "counters": delta.as_dict(),
+        "keys_sha256": digest_arrays(keys_residues(be, keys)),
+        "cts_sha256": digest_arrays([ct_residues(be, c) for c in cts]),
+        "hint_sha256": digest_arrays([ct_residues(be, c) for c in hint]),
+        "out_sha256": digest_arrays([ct_residues(be, out)]),
+        "ref_comp_seconds": round(t2 - t1, 3),
+        "ref_setup_seconds": round(t1 - t0, 3),
+    }
+    if n <= 256:
+        rec_json["full"] = {
+            "cts": [ct_residues(be, c).tolist() for c in cts],
+            "hint": [ct_residues(be, c).tolist() for c in hint],
+            "out": ct_residues(be, out).tolist(),
+            "secret": list(keys.secret),
+        }
+    path = os.path.join(GOLDEN, f"{name}.json")
+    with open(path, "w") as fh:
+        json.dump(rec_json, fh, indent=1)
+    print(f"{name}: comp {t2 - t1:.1f}s sha {rec_json['answer_sha256'][:16]} -> {path}", flush=True)
+
+
+if __name__ == "__main__":
+    os.makedirs(GOLDEN, exist_ok=True)
+    names = sys.argv[1:] or list(CASES)
+    for nm in names:
+        run_case(nm)

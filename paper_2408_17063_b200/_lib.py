@@ -1,0 +1,108 @@
+"""ctypes binding of libhcomp.so (include/hcomp.h).
+
+The CUDA library is the only compute path of this package: if it is missing
+or no GPU is present, operations raise instead of falling back to any CPU
+code.  The library is built in-tree by `python -m paper_2408_17063_b200.build`
+(or `__graft_entry__.build()`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .params import BackendMismatch, LevelExhausted, MissingRotationKey
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhcomp.so")
+
+HC_OK = 0
+HC_ERR_ARG = 1
+HC_ERR_LEVEL = 2
+HC_ERR_KEY = 3
+HC_ERR_MISMATCH = 4
+HC_ERR_CUDA = 5
+HC_ERR_STATE = 6
+
+
+class HcompError(RuntimeError):
+    """CUDA / state failure inside libhcomp (no reference analogue)."""
+
+
+_lib = None
+
+# (name, restype, argtypes)
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+_U32 = ctypes.c_uint32
+_U64 = ctypes.c_uint64
+_SIGS = [
+    ("hc_last_error", ctypes.c_char_p, []),
+    ("hc_ctx_create", _I, [_I, _I, _P, _U64, _I, _I, ctypes.POINTER(_P)]),
+    ("hc_ctx_destroy", None, [_P]),
+    ("hc_ctx_digits", _I, [_P, _P]),
+    ("hc_load_ksk", _I, [_P, _U32, _P]),
+    ("hc_clear_keys", _I, [_P]),
+    ("hc_plan", _I, [_P, _I64, _I, _I]),
+    ("hc_plan_info", _I, [_P, _P]),
+    ("hc_comp", _I, [_P, _P, _P, _I, _P]),
+    ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),
+    ("hc_comp_set_inputs", _I, [_P, _P, _P, _I]),
+    ("hc_comp_launch", _I, [_P, _P]),
+    ("hc_comp_get_output", _I, [_P, _P]),
+    ("hc_partial_words", _I64, [_P]),
+    ("hc_comp_partial", _I, [_P, _I64, _I64, _P, _P]),
+    ("hc_comp_finish", _I, [_P, _P, _P]),
+    ("hc_ntt", _I, [_P, _P, _I, _P, _I]),
+    ("hc_pointwise", _I, [_P, _P, _P, _P, _I, _P, _I]),
+    ("hc_mul_plain", _I, [_P, _P, _I, _P, _P]),
+    ("hc_rotate", _I, [_P, _P, _I, _U32, _P]),
+    ("hc_comp_profile", _I, [_P, _P, _I, _P, _P, _P]),
+    ("hc_bf_peak", _I, [_P, ctypes.POINTER(ctypes.c_double)]),
+    ("hc_galois_tables", _I, [_I, _U32, _P, _P]),
+    ("hc_prim_root_2n", _U64, [_U64, _I]),
+]
+EXPORTS = [s[0] for s in _SIGS]
+
+
+def lib():
+    """Load the CUDA library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise HcompError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2408_17063_b200.build` "
+                "(there is no CPU fallback for Comp)"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for name, res, args in _SIGS:
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def ptr(a: np.ndarray):
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def check(rc: int) -> None:
+    """Map libhcomp status codes onto the reference's exceptions."""
+    if rc == HC_OK:
+        return
+    msg = lib().hc_last_error().decode(errors="replace")
+    if rc == HC_ERR_ARG:
+        raise ValueError(msg)
+    if rc == HC_ERR_LEVEL:
+        raise LevelExhausted(msg)
+    if rc == HC_ERR_KEY:
+        raise MissingRotationKey(msg)
+    if rc == HC_ERR_MISMATCH:
+        raise BackendMismatch(msg)
+    raise HcompError(msg)

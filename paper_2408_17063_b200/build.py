@@ -1,0 +1,62 @@
+"""Build libhcomp.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2408_17063_b200.build            # libhcomp.so
+    python -m paper_2408_17063_b200.build --selftest  # + host self-test lib (CPU tests)
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libhcomp.so")
+SELFTEST = os.path.join(HERE, "libhcomp_hosttest.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _sources():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC))] + [
+        os.path.join(os.path.dirname(HERE), "include", "hcomp.h")
+    ]
+
+
+def _stale(target: str) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in _sources())
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> str:
+    if force or _stale(LIB):
+        cmd = [
+            NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+            "-o", LIB, os.path.join(CSRC, "hcomp.cu"),
+        ]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+    return LIB
+
+
+def build_selftest(force: bool = False) -> str:
+    """The device arithmetic/NTT schedule compiled for the host (g++), used by
+    tests/test_csrc_host.py to check the exact GPU code paths on the CPU."""
+    if force or _stale(SELFTEST):
+        cmd = [
+            "/usr/bin/g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", SELFTEST,
+            os.path.join(CSRC, "hosttest.cpp"),
+        ]
+        subprocess.check_call(cmd)
+    return SELFTEST
+
+
+if __name__ == "__main__":
+    build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    if "--selftest" in sys.argv:
+        build_selftest(force="--force" in sys.argv)
+    print(LIB)

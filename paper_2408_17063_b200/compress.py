@@ -1,0 +1,251 @@
+"""Drop-in `comp` (compress.py:488-518) on the B200 backend.
+
+`comp(cd, params, backend, keys, index_hint=cv)` with the default packed
+layout runs the whole Comp -- pack_pair (compress.py:338-367) and
+bsgs_matvec (compress.py:273-310) -- as one fused CUDA-graph launch in
+libhcomp.  The host only checks arguments exactly as the reference does,
+replays the reference's deterministic noise-bits / op-counter sequence
+(so `CompressedAnswer.serialize` is byte-identical and `backend.counters`
+move exactly as the reference's), and wraps the level-0 result.
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .backend import B200BgvBackend, Ciphertext, KeySet, RnsPayload, SlotMatrix
+from .params import (
+    BackendMismatch,
+    CompressionParams,
+    LevelExhausted,
+    MissingRotationKey,
+    bsgs_shape,
+    fold_amounts,
+)
+
+LAYOUT_VERSION = 1
+
+
+@dataclass(frozen=True)
+class CompressedAnswer:
+    """compress.py:375-430 (packed layout: w in row 0, e in row 1)."""
+
+    cts: tuple
+    s: int
+    packed: bool
+
+    def payload_slots(self, backend, keys: KeySet) -> tuple[list[int], list[int]]:
+        if self.packed:
+            m = backend.decrypt(self.cts[0], keys)
+            return [int(x) for x in m.rows[0][: self.s]], [int(x) for x in m.rows[1][: self.s]]
+        mw = backend.decrypt(self.cts[0], keys)
+        me = backend.decrypt(self.cts[1], keys)
+        return [int(x) for x in mw.rows[0][: self.s]], [int(x) for x in me.rows[0][: self.s]]
+
+    def serialize(self, backend) -> bytes:
+        head = struct.pack(
+            "<HIBBBIIB", LAYOUT_VERSION, self.s, 1 if self.packed else 0, 0, 1 if self.packed else 0, 0, 0, len(self.cts)
+        )
+        blobs = [backend.serialize_ciphertext(c) for c in self.cts]
+        return head + b"".join(struct.pack("<I", len(b)) + b for b in blobs)
+
+
+def encode_vector(values: Sequence[int], params: CompressionParams) -> list[SlotMatrix]:
+    """compress.py:318-329."""
+    he = params.he
+    vals = list(values)
+    if len(vals) != params.N:
+        raise ValueError(f"expected a length-{params.N} vector")
+    return [
+        SlotMatrix.from_vector(vals[t * he.n : (t + 1) * he.n], he.n, he.p) for t in range(params.num_ciphertexts)
+    ]
+
+
+def encrypt_vector(values: Sequence[int], params: CompressionParams, backend, keys: KeySet) -> list[Ciphertext]:
+    """compress.py:332-335."""
+    return [backend.encrypt(m, keys) for m in encode_vector(values, params)]
+
+
+def live_diagonals(params: CompressionParams) -> np.ndarray:
+    """[B][s_pad] mask of nonzero plan diagonals (build_plan, compress.py:226-233):
+    only the last block can hold all-zero diagonals (columns past N)."""
+    m = params.block_width
+    B = params.num_blocks
+    s, s_pad = params.s, params.s_pad
+    baby, giant = bsgs_shape(s)
+    live = np.ones((B, s_pad), dtype=bool)
+    t = B - 1
+    pos = np.arange(m)
+    for g in range(giant):
+        rows = (pos - g * baby) % s_pad
+        for b in range(baby):
+            cols = (pos + b) % m
+            live[t, g * baby + b] = bool(np.any((rows < s) & (t * m + cols + 1 <= params.N)))
+    return live
+
+
+class _NoiseSim:
+    """Replays the reference's noise_bits float sequence and op counters for
+    the hint path of comp (pack_pair then bsgs_matvec) without touching
+    ciphertext values (bgv.py:421-429, 606-607, 640-646, 660, 724, 745)."""
+
+    def __init__(self, be: B200BgvBackend):
+        self.be = be
+        self.ks = 0
+        self.pt = 0
+        self.adds = 0
+
+    def mul_plain(self, bits: float, lvl: int) -> float:
+        be = self.be
+        if lvl < 1:
+            raise LevelExhausted("plaintext multiply at level 0")
+        b = bits + math.log2(be.params.p) + math.log2(be.params.n)
+        be._check_noise(b, lvl)
+        self.pt += 1
+        return be._ms_bits(b, lvl)
+
+    def add(self, a: float, b: float, lvl: int) -> float:
+        self.adds += 1
+        return self.be._check_noise(max(a, b) + 1, lvl)
+
+    def rot(self, bits: float, lvl: int) -> float:
+        r = self.be._check_noise(max(bits, self.be._ks_noise(lvl)) + 1, lvl)
+        self.ks += 1
+        return r
+
+
+def comp_noise(be: B200BgvBackend, params: CompressionParams, cv_bits, cd_bits, live) -> tuple[float, _NoiseSim]:
+    """noise_bits of comp's output and the counter deltas, in reference order."""
+    sim = _NoiseSim(be)
+    L = be.params.max_level
+    m = params.block_width
+    u = []
+    for j in range(params.num_blocks):
+        src = j // 2
+        if j % 2 == 0:
+            a = sim.mul_plain(cv_bits[src], L)
+            r = sim.rot(sim.mul_plain(cd_bits[src], L), L - 1)
+            u.append(sim.add(a, r, L - 1))
+        else:
+            r = sim.rot(sim.mul_plain(cv_bits[src], L), L - 1)
+            b = sim.mul_plain(cd_bits[src], L)
+            u.append(sim.add(r, b, L - 1))
+    baby, giant = bsgs_shape(params.s)
+    acc = [None] * giant
+    lv = L - 1
+    for t, ub in enumerate(u):
+        rotated = [ub] + [sim.rot(ub, lv) for _ in range(1, baby)]
+        for g in range(giant):
+            for b in range(baby):
+                if not live[t, g * baby + b]:
+                    continue
+                prod = sim.mul_plain(rotated[b], lv)
+                acc[g] = prod if acc[g] is None else sim.add(acc[g], prod, lv - 1)
+    res = acc[0]
+    lv -= 1
+    for g in range(1, giant):
+        if acc[g] is None:
+            continue
+        part = acc[g] if (g * baby) % m == 0 else sim.rot(acc[g], lv)
+        res = part if res is None else sim.add(res, part, lv)
+    if res is None:
+        raise ValueError("matrix plan had no nonzero diagonals")
+    for _ in fold_amounts(params.s_pad, m):
+        res = sim.add(res, sim.rot(res, lv), lv)
+    out = sim.mul_plain(res, lv)
+    return out, sim
+
+
+def _stack_level3(cts: Sequence[Ciphertext], L: int) -> np.ndarray:
+    return np.ascontiguousarray(np.stack([c.payload.res for c in cts]), dtype=np.uint64)
+
+
+def _check_inputs(cd, cv, params: CompressionParams, backend: B200BgvBackend, keys: KeySet):
+    if len(cv) != params.num_ciphertexts or len(cd) != params.num_ciphertexts:
+        raise ValueError("expected standard-layout ciphertext lists")  # compress.py:348-349
+    for c in list(cv) + list(cd):
+        backend._check_keys(c, keys)
+        if c.level != backend.params.max_level:
+            raise ValueError("the fused B200 Comp takes fresh max-level ciphertexts (mixed levels: SURVEY 8(f)#2)")
+    if keys.col_swap_key is None:
+        raise MissingRotationKey("column-swap key was not declared at keygen")
+
+
+def comp(
+    cd: Sequence[Ciphertext],
+    params: CompressionParams,
+    backend,
+    keys: KeySet,
+    index_hint: Sequence[Ciphertext] | None = None,
+    pack: bool = True,
+    masked=None,
+) -> CompressedAnswer:
+    """Compress ciphertexts of an s-sparse vector d into (w, e) (compress.py:488-518)."""
+    if not isinstance(backend, B200BgvBackend):
+        raise BackendMismatch("paper_2408_17063_b200.comp needs a B200BgvBackend")
+    if masked is not None or index_hint is None or not pack:
+        raise NotImplementedError(
+            "the B200 path implements comp with an index hint in the packed layout "
+            "(the reference's hint path); comp_masked / power_fermat / pack=False are not built"
+        )
+    if backend.params != params.he:
+        raise BackendMismatch("compression parameters do not match the backend")
+    cv = list(index_hint)
+    cd = list(cd)
+    _check_inputs(cd, cv, params, backend, keys)
+    live = live_diagonals(params)
+    bits, sim = comp_noise(
+        backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live
+    )
+    backend.plan(params.N, params.s, keys)
+    L = backend.params.max_level
+    cd_arr = _stack_level3(cd, L)
+    cv_arr = _stack_level3(cv, L)
+    out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
+    _lib.check(
+        _lib.lib().hc_comp(backend._ctx(), _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd), _lib.ptr(out))
+    )
+    backend.counters.keyswitches += sim.ks
+    backend.counters.pt_mults += sim.pt
+    backend.counters.adds += sim.adds
+    ct = Ciphertext(backend.backend_id, keys.key_id, 0, RnsPayload(out, bits, (backend.q[0],)))
+    return CompressedAnswer((ct,), params.s, True)
+
+
+class DeviceComp:
+    """Device-resident Comp for timing and serving loops: inputs uploaded once
+    (`set_inputs`), each `launch(stream)` enqueues one full Comp (one CUDA
+    graph launch), `output()` reads the level-0 ciphertext residues."""
+
+    def __init__(self, backend: B200BgvBackend, params: CompressionParams, keys: KeySet, chunk_blocks: int = 0):
+        self.be = backend
+        self.params = params
+        self.keys = keys
+        backend.plan(params.N, params.s, keys, chunk_blocks)
+
+    def set_inputs(self, cd: np.ndarray, cv: np.ndarray) -> None:
+        cd = np.ascontiguousarray(cd, dtype=np.uint64)
+        cv = np.ascontiguousarray(cv, dtype=np.uint64)
+        _lib.check(_lib.lib().hc_comp_set_inputs(self.be._ctx(), _lib.ptr(cd), _lib.ptr(cv), cd.shape[0]))
+
+    def launch(self, stream_handle: int = 0) -> None:
+        _lib.check(_lib.lib().hc_comp_launch(self.be._ctx(), stream_handle or None))
+
+    def output(self) -> np.ndarray:
+        out = np.empty((2, 1, self.be.params.n), dtype=np.uint64)
+        _lib.check(_lib.lib().hc_comp_get_output(self.be._ctx(), _lib.ptr(out)))
+        return out
+
+    def run_host(self, cd: np.ndarray, cv: np.ndarray) -> np.ndarray:
+        """End to end from host buffers: H2D inputs, Comp, D2H output."""
+        cd = np.ascontiguousarray(cd, dtype=np.uint64)
+        cv = np.ascontiguousarray(cv, dtype=np.uint64)
+        out = np.empty((2, 1, self.be.params.n), dtype=np.uint64)
+        _lib.check(_lib.lib().hc_comp(self.be._ctx(), _lib.ptr(cd), _lib.ptr(cv), cd.shape[0], _lib.ptr(out)))
+        return out

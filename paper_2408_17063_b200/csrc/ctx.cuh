@@ -1,0 +1,45 @@
+// Device-visible context: per-prime constants, per-level rescale / CRT
+// constants, twiddle tables and slot/Galois index tables.  Built on the host
+// by hcomp.cu (HostCtx) from the chain primes; consumed by kernels.cuh.
+#pragma once
+#include "ntt.cuh"
+
+namespace hc {
+
+constexpr int MAXL = 3;        // max level supported (4 chain primes)
+constexpr int NPR = MAXL + 2;  // chain primes + plaintext prime p (index 4)
+constexpr int PIDX = 4;        // RNS index of p in the tables
+constexpr int NLIMB = 4;       // limbs for composed integers (216 bits max)
+constexpr int MAXD = 14;       // digits at level 3 (216-bit modulus, base 2^16)
+
+// Constants for level l (P = l+1 primes at RNS indices 0..l).
+struct LevelC {
+    int P, D;             // primes, base-2^16 digits of Q_l (bgv.py:360-363)
+    int nlimb;            // limbs of Q_l
+    int pad;
+    // modulus switch l -> l-1 (drops prime l), bgv.py:579-608
+    u64 half_qd;          // q_l >> 1
+    u64 qinv[MAXL + 1];   // q_l^-1 mod q_k (k < l)
+    u64 qinv_s[MAXL + 1];
+    u64 qinv_r[MAXL + 1]; // q_l^-1 * R mod q_k (Montgomery, folded into plaintexts)
+    u64 qinv_rs[MAXL + 1];
+    // CRT compose at level l
+    u64 Minv[MAXL + 1], Minv_s[MAXL + 1];  // (Q_l/q_k)^-1 mod q_k
+    u64 M[MAXL + 1][NLIMB];                // Q_l/q_k
+    u64 Q[NLIMB];                          // Q_l
+    double qrecip[MAXL + 1];               // 1/q_k
+};
+
+struct DevCtx {
+    PrimeC pc[NPR];
+    u64 p, half_p;
+    double pinv;
+    int L;  // max level
+    int pad;
+    LevelC lv[MAXL + 1];
+    const Tw* twf;       // [NPR][n]
+    const Tw* twi;       // [NPR][n]
+    const uint16_t* slot_of;  // [n]: NTT index -> (row << 12 | col)
+};
+
+}  // namespace hc

@@ -1,0 +1,133 @@
+// Per-coefficient building blocks of the Comp path (host+device so the CPU
+// self-test can check them against the oracle):
+//   crt_compose   exact CRT of RNS residues to the integer in [0, Q_l)
+//                 (the reference keeps that integer natively, bgv.py:622)
+//   digits16      its base-2^16 digits (bgv.py:627-629)
+//   rescale_corr  the per-coefficient part of the modulus switch
+//                 (bgv.py:592-603), in the linear-split form used on the GPU:
+//                   out_k = x_k * q^-1 + e_k,  e_k = (d - r * q^-1) mod q_k
+//                 with r = centered(x mod q), d = centered_p(r mod p);
+//                 e_k depends only on the dropped prime's residue.
+#pragma once
+#include "ctx.cuh"
+
+namespace hc {
+
+// X = CRT(x_0..x_L) in [0, Q_L), x_k canonical residues; Q_L has L+1 limbs
+// (every chain prime is 54 bits).  Compile-time L keeps arrays in registers.
+template <int L>
+HD void crt_compose(const LevelC& C, const PrimeC* pc, const u64* x, u64 (&X)[NLIMB]) {
+    constexpr int P = L + 1, nl = L + 1;
+    u64 y[P];
+    double f = 0.0;
+    HC_UNROLL
+    for (int k = 0; k < P; k++) {
+        y[k] = mul_shoup(x[k], C.Minv[k], C.Minv_s[k], pc[k].q);
+        f += (double)y[k] * C.qrecip[k];
+    }
+    u64 S[nl];
+    HC_UNROLL
+    for (int i = 0; i < nl; i++) S[i] = 0;
+    HC_UNROLL
+    for (int k = 0; k < P; k++) {
+        u64 carry = 0;
+        HC_UNROLL
+        for (int i = 0; i < nl; i++) {
+            u128 t = (u128)y[k] * C.M[k][i] + S[i] + carry;
+            S[i] = (u64)t;
+            carry = (u64)(t >> 64);
+        }
+    }
+    // X = S - kappa*Q with kappa = floor(sum y_k/q_k) (estimated, then fixed)
+    const u64 kappa = (u64)f;
+    u64 borrow = 0, carry = 0;
+    HC_UNROLL
+    for (int i = 0; i < nl; i++) {
+        u128 t = (u128)kappa * C.Q[i] + carry;
+        u64 tl = (u64)t;
+        carry = (u64)(t >> 64);
+        u64 s = S[i];
+        u64 d = s - tl - borrow;
+        borrow = (s < tl) || (s - tl < borrow) ? 1 : 0;
+        X[i] = d;
+    }
+    HC_UNROLL
+    for (int i = nl; i < NLIMB; i++) X[i] = 0;
+    if (borrow) {  // went negative: add Q back
+        u64 c = 0;
+        HC_UNROLL
+        for (int i = 0; i < nl; i++) {
+            u128 t = (u128)X[i] + C.Q[i] + c;
+            X[i] = (u64)t;
+            c = (u64)(t >> 64);
+        }
+    } else {  // may be >= Q: subtract once
+        int ge = 1, done = 0;
+        HC_UNROLL
+        for (int i = nl - 1; i >= 0; i--) {
+            if (!done && X[i] != C.Q[i]) {
+                ge = X[i] > C.Q[i];
+                done = 1;
+            }
+        }
+        if (ge) {
+            u64 b = 0;
+            HC_UNROLL
+            for (int i = 0; i < nl; i++) {
+                u64 s = X[i];
+                u64 d = s - C.Q[i] - b;
+                b = (s < C.Q[i]) || (s - C.Q[i] < b) ? 1 : 0;
+                X[i] = d;
+            }
+        }
+    }
+}
+
+// Q - X for X != 0 (0 stays 0): the coefficient a negated automorphism
+// image carries (coeff_automorphism, bgv.py:273-284)
+template <int L>
+HD void neg_mod_Q(const LevelC& C, u64 (&X)[NLIMB]) {
+    int nz = 0;
+    HC_UNROLL
+    for (int i = 0; i < L + 1; i++) nz |= X[i] != 0;
+    if (!nz) return;
+    u64 b = 0;
+    HC_UNROLL
+    for (int i = 0; i < L + 1; i++) {
+        u64 q = C.Q[i], x = X[i];
+        u64 d = q - x - b;
+        b = (q < x) || (q - x < b) ? 1 : 0;
+        X[i] = d;
+    }
+}
+
+HD uint16_t digit16(const u64 (&X)[NLIMB], int j) {
+    return (uint16_t)(X[j >> 2] >> (16 * (j & 3)));
+}
+
+// Modulus-switch correction (see file header).  x = canonical residue of the
+// coefficient modulo the dropped prime q_l.  Writes e_k for k < l.
+HD void rescale_corr(const DevCtx& D, int l, u64 x, u64* e) {
+    const LevelC& C = D.lv[l];
+    const u64 ql = D.pc[l].q;
+    const int neg = x > C.half_qd;
+    const u64 mag = neg ? ql - x : x;  // |r|
+    u64 rm = mod_small(mag, D.p, D.pinv);
+    if (neg && rm) rm = D.p - rm;       // r mod p in [0, p)
+    const int dneg = rm > D.half_p;
+    const u64 dmag = dneg ? D.p - rm : rm;  // |d|
+    HC_UNROLL
+    for (int k = 0; k < MAXL; k++) {
+        if (k >= l) break;
+        const u64 q = D.pc[k].q;
+        u64 rk = neg ? (mag ? q - mag : 0) : mag;  // r mod q_k (|r| < q_k)
+        u64 t = mul_shoup(rk, C.qinv[k], C.qinv_s[k], q);
+        u64 dk = dneg ? (dmag ? q - dmag : 0) : dmag;
+        e[k] = sub_mod(dk, t, q);
+    }
+}
+
+// any 64-bit value -> [0, q)
+HD u64 red64(u64 a, u64 q, u64 one_s) { return reduce_once(mul_shoup_lazy(a, 1, one_s, q), q); }
+
+}  // namespace hc

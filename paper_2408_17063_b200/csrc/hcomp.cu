@@ -1,0 +1,1296 @@
+// libhcomp: host orchestration + C ABI (include/hcomp.h) for the B200 Comp path.
+//
+// The Comp schedule (compress.py:273-367 with the reference's per-operation
+// BGV semantics, bgv.py:579-770) is compiled once per (N, s) plan into job
+// lists for the kernels in kernels.cuh and captured into one CUDA graph.
+// DESIGN.md section 3 walks through the steps S1..S10 / T1..T4 / F1..F4 /
+// D1..D2 named in the comments below.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hcomp.h"
+#include "kernels.cuh"
+#include "host_tables.hpp"
+
+using namespace hc;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CU(x)                                                                         \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            return fail(HC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+        }                                                                             \
+    } while (0)
+
+extern "C" const char* hc_last_error(void) { return g_err.c_str(); }
+
+extern "C" uint64_t hc_prim_root_2n(uint64_t q, int n) { return prim_root_2n_host(q, n); }
+
+extern "C" int hc_galois_tables(int n, uint32_t t, uint16_t* coef, uint16_t* perm) {
+    if (galois_tables_host(n, t, coef, perm)) return fail(HC_ERR_ARG, "galois: n must be 8192 and t odd");
+    return HC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct DevKey {
+    u64* key = nullptr;        // [D_L][2][L+1][n] Montgomery form
+    uint16_t* gal = nullptr;   // coefficient gather
+    uint16_t* perm = nullptr;  // NTT-domain permutation
+};
+
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET };
+struct Step {
+    int kind = 0;
+    int njobs = 0;
+    int gy = 1;
+    void* djobs = nullptr;
+    // ST_SUMC / ST_MEMSET
+    const u64* in = nullptr;
+    u64* out = nullptr;
+    long long rows = 0, cstride = 0;
+    int period = 0, copies = 0;
+    size_t bytes = 0;
+};
+
+struct Schedule {
+    std::vector<Step> steps;
+    std::vector<void*> allocs;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+    ~Schedule() {
+        if (exec) cudaGraphExecDestroy(exec);
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+struct Plan;
+
+struct hc_ctx {
+    int dev = 0, L = 3, n = NPOLY;
+    u64 p = 0;
+    DevCtx hctx{};             // host copy (device pointers inside)
+    DevCtx* d_ctx = nullptr;
+    Tw* d_twf = nullptr;
+    Tw* d_twi = nullptr;
+    uint16_t* d_slot_of = nullptr;
+    cudaStream_t stream = nullptr;
+    std::map<uint32_t, DevKey> keys;
+    std::unique_ptr<Plan> plan;
+    int digits[MAXL + 1] = {0, 0, 0, 0};
+};
+
+static void release_key(DevKey& k) {
+    cudaFree(k.key);
+    cudaFree(k.gal);
+    cudaFree(k.perm);
+}
+
+static int kernels_configured = 0;
+static int configure_kernels() {
+    if (kernels_configured) return HC_OK;
+    CU(cudaFuncSetAttribute(k_xform, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));
+    CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
+    kernels_configured = 1;
+    return HC_OK;
+}
+
+extern "C" int hc_ctx_create(int n, int max_level, const uint64_t* primes, uint64_t p, int ksw_base_bits,
+                             int device, hc_ctx** out) {
+    if (n != NPOLY) return fail(HC_ERR_ARG, "only n = 8192 is supported");
+    if (max_level < 1 || max_level > MAXL) return fail(HC_ERR_ARG, "max_level must be 1..3");
+    if (ksw_base_bits != 16) return fail(HC_ERR_ARG, "only ksw_base_bits = 16 is supported");
+    if (p >= (1ull << 31) || p % (2 * (u64)n) != 1) return fail(HC_ERR_ARG, "bad plaintext modulus");
+    for (int k = 0; k <= max_level; k++) {
+        if (primes[k] >= (1ull << 54) || primes[k] < (1ull << 53))
+            return fail(HC_ERR_ARG, "chain primes must be 54-bit");
+        if (primes[k] % (2 * (u64)n) != 1 || primes[k] % p != 1)
+            return fail(HC_ERR_ARG, "chain prime not = 1 mod 2n and mod p");
+        if (k && primes[k] <= primes[k - 1]) return fail(HC_ERR_ARG, "primes must be in level order (ascending)");
+    }
+    std::unique_ptr<hc_ctx> h(new hc_ctx());
+    h->dev = device;
+    h->L = max_level;
+    h->p = p;
+    CU(cudaSetDevice(device));
+    int rc = configure_kernels();
+    if (rc) return rc;
+    // blocking stream: ordered after legacy-stream copies (pageable cudaMemcpy
+    // may return before its DMA lands)
+    CU(cudaStreamCreate(&h->stream));
+
+    DevCtx& D = h->hctx;
+    std::vector<Tw> twf, twi;
+    std::vector<uint16_t> slot_of;
+    build_host_ctx(D, twf, twi, slot_of, n, max_level, primes, p, h->digits);
+    CU(cudaMalloc(&h->d_twf, twf.size() * sizeof(Tw)));
+    CU(cudaMalloc(&h->d_twi, twi.size() * sizeof(Tw)));
+    CU(cudaMalloc(&h->d_slot_of, n * sizeof(uint16_t)));
+    CU(cudaMemcpy(h->d_twf, twf.data(), twf.size() * sizeof(Tw), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_twi, twi.data(), twi.size() * sizeof(Tw), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(h->d_slot_of, slot_of.data(), n * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    D.twf = h->d_twf;
+    D.twi = h->d_twi;
+    D.slot_of = h->d_slot_of;
+    CU(cudaMalloc(&h->d_ctx, sizeof(DevCtx)));
+    CU(cudaMemcpy(h->d_ctx, &D, sizeof(DevCtx), cudaMemcpyHostToDevice));
+    *out = h.release();
+    return HC_OK;
+}
+
+extern "C" int hc_ctx_digits(const hc_ctx* h, int* digits) {
+    if (!h) return fail(HC_ERR_ARG, "null context");
+    for (int l = 0; l <= h->L; l++) digits[l] = h->digits[l];
+    return HC_OK;
+}
+
+extern "C" int hc_clear_keys(hc_ctx* h) {
+    if (!h) return fail(HC_ERR_ARG, "null context");
+    cudaSetDevice(h->dev);
+    for (auto& kv : h->keys) release_key(kv.second);
+    h->keys.clear();
+    return HC_OK;
+}
+
+extern "C" int hc_load_ksk(hc_ctx* h, uint32_t t, const uint64_t* ksk) {
+    if (!h || !ksk) return fail(HC_ERR_ARG, "null argument");
+    if ((t & 1) == 0 || t >= 2u * NPOLY) return fail(HC_ERR_ARG, "galois element must be odd and < 2n");
+    CU(cudaSetDevice(h->dev));
+    auto it = h->keys.find(t);
+    if (it != h->keys.end()) {
+        release_key(it->second);
+        h->keys.erase(it);
+    }
+    DevKey k;
+    const int L1 = h->L + 1, D = h->digits[h->L];
+    const size_t rows = (size_t)D * 2 * L1;
+    CU(cudaMalloc(&k.key, rows * NPOLY * 8));
+    CU(cudaMemcpyAsync(k.key, ksk, rows * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
+    k_to_mont<<<592, 256, 0, h->stream>>>(h->d_ctx, k.key, (long long)rows, L1);
+    CU(cudaGetLastError());
+    std::vector<uint16_t> gal(NPOLY), perm(NPOLY);
+    int rc = hc_galois_tables(NPOLY, t, gal.data(), perm.data());
+    if (rc) return rc;
+    CU(cudaMalloc(&k.gal, NPOLY * 2));
+    CU(cudaMalloc(&k.perm, NPOLY * 2));
+    CU(cudaMemcpy(k.gal, gal.data(), NPOLY * 2, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(k.perm, perm.data(), NPOLY * 2, cudaMemcpyHostToDevice));
+    CU(cudaStreamSynchronize(h->stream));
+    h->keys[t] = k;
+    return HC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// schedule helpers
+// ---------------------------------------------------------------------------
+static int upload_jobs(Schedule& S, Step& st, const void* host, size_t bytes) {
+    void* d = nullptr;
+    CU(cudaMalloc(&d, bytes));
+    CU(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+    CU(cudaDeviceSynchronize());  // the DMA must land before any stream uses the jobs
+    S.allocs.push_back(d);
+    st.djobs = d;
+    return HC_OK;
+}
+
+static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
+    if (jobs.empty()) return HC_OK;
+    Step st;
+    st.kind = ST_XF;
+    st.njobs = (int)jobs.size();
+    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(XJob));
+    if (rc) return rc;
+    S.steps.push_back(st);
+    return HC_OK;
+}
+static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
+    if (jobs.empty()) return HC_OK;
+    Step st;
+    st.kind = ST_CO;
+    st.njobs = (int)jobs.size();
+    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(CJob));
+    if (rc) return rc;
+    S.steps.push_back(st);
+    return HC_OK;
+}
+static int add_ma(Schedule& S, const std::vector<MJob>& jobs, int nprime) {
+    if (jobs.empty()) return HC_OK;
+    Step st;
+    st.kind = ST_MA;
+    st.njobs = (int)jobs.size();
+    st.gy = nprime;
+    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(MJob));
+    if (rc) return rc;
+    S.steps.push_back(st);
+    return HC_OK;
+}
+static int add_dx(Schedule& S, const std::vector<DXJob>& jobs, int nprime) {
+    if (jobs.empty()) return HC_OK;
+    Step st;
+    st.kind = ST_DX;
+    st.njobs = (int)jobs.size();
+    st.gy = nprime;
+    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(DXJob));
+    if (rc) return rc;
+    S.steps.push_back(st);
+    return HC_OK;
+}
+static void add_memset(Schedule& S, void* p, size_t bytes) {
+    Step st;
+    st.kind = ST_MEMSET;
+    st.out = (u64*)p;
+    st.bytes = bytes;
+    S.steps.push_back(st);
+}
+
+static int enqueue(const hc_ctx* h, const Schedule& S, cudaStream_t s) {
+    for (const Step& st : S.steps) {
+        switch (st.kind) {
+            case ST_XF:
+                k_xform<<<st.njobs, NT, NPOLY * 8, s>>>(h->d_ctx, (const XJob*)st.djobs);
+                break;
+            case ST_CO:
+                k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->d_ctx, (const CJob*)st.djobs);
+                break;
+            case ST_MA:
+                k_ksmac<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->d_ctx, (const MJob*)st.djobs);
+                break;
+            case ST_DX:
+                k_diagx<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->d_ctx, (const DXJob*)st.djobs);
+                break;
+            case ST_SUMC:
+                k_sum_copies<<<592, 256, 0, s>>>(h->d_ctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride);
+                break;
+            case ST_MEMSET:
+                CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
+                break;
+        }
+        CU(cudaGetLastError());
+    }
+    return HC_OK;
+}
+
+static int count_launches(const Schedule& S) {
+    int c = 0;
+    for (const Step& st : S.steps) c += st.kind != ST_MEMSET;
+    return c;
+}
+
+static int run_now(hc_ctx* h, const Schedule& S) {
+    int rc = enqueue(h, S, h->stream);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
+static int capture(hc_ctx* h, Schedule& S) {
+    cudaGraph_t g = nullptr;
+    CU(cudaDeviceSynchronize());  // job/pointer arrays fully uploaded
+    CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue(h, S, h->stream);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return fail(HC_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&S.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(HC_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    S.launches = count_launches(S);
+    return HC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Comp plan (compress.py:198-367 on the BGV semantics of bgv.py:579-770)
+// ---------------------------------------------------------------------------
+struct Plan {
+    long long N = 0;
+    int s = 0, s_pad = 0, baby = 0, giant = 0, m = 0, F = 0, CB = 0, ncopy = 1;
+    long long B = 0, C = 0;
+    int D1 = 0, D2 = 0;
+    std::vector<int> fold;
+    std::vector<uint8_t> live;      // [B][s_pad]
+    std::vector<uint8_t> acc_live;  // [giant]
+    long long live_count = 0;
+    // Galois elements
+    uint32_t t_col = 0;
+    std::vector<uint32_t> t_baby, t_giant, t_fold;
+    // device buffers
+    std::vector<void*> allocs;
+    u64 *cv = nullptr, *cd = nullptr, *mask = nullptr, *diag = nullptr, *omask = nullptr;
+    u64 *ecor = nullptr, *rc1raw = nullptr, *pn = nullptr, *rc0n = nullptr, *dnttR = nullptr;
+    u64 *U = nullptr, *Ucoef = nullptr, *dnttB = nullptr, *ROT = nullptr;
+    uint16_t *digR = nullptr, *digU = nullptr;
+    u64 *Ecp = nullptr, *PX = nullptr;
+    u64 *A0 = nullptr, *A1 = nullptr, *A1coef = nullptr, *dnttG = nullptr, *RES = nullptr;
+    u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr;
+    uint16_t *digG = nullptr, *digF = nullptr;
+    std::unique_ptr<Schedule> full, fin;
+    std::map<std::pair<long long, long long>, std::unique_ptr<Schedule>> partials;
+    ~Plan() {
+        full.reset();
+        fin.reset();
+        partials.clear();
+        for (void* p : allocs) cudaFree(p);
+    }
+    size_t px_words() const { return (size_t)2 * giant * 2 * 2 * NPOLY; }
+};
+
+template <typename T>
+static int palloc(Plan& P, T** ptr, size_t count) {
+    void* d = nullptr;
+    CU(cudaMalloc(&d, count * sizeof(T)));
+    P.allocs.push_back(d);
+    *ptr = (T*)d;
+    return HC_OK;
+}
+
+static int bsgs_shape(int s, int* baby, int* giant, int* s_pad) {
+    int sp = 1;
+    while (sp < s) sp <<= 1;  // 1 << (s-1).bit_length()
+    int bl = 0;
+    while ((1 << bl) <= 2 * sp) bl++;  // (2*s_pad).bit_length()
+    double log_target = (bl - 1) / 2.0;
+    int b = 1 << (int)log_target;
+    b = std::min(std::max(b, 1), sp);
+    *baby = b;
+    *giant = sp / b;
+    *s_pad = sp;
+    return 0;
+}
+
+static uint32_t rot_t(long long r, int n) {
+    const long long two_n = 2LL * n;
+    long long t = 1, b = 3, e = r;
+    while (e) {
+        if (e & 1) t = t * b % two_n;
+        b = b * b % two_n;
+        e >>= 1;
+    }
+    return (uint32_t)t;
+}
+
+static const DevKey* need_key(hc_ctx* h, uint32_t t) {
+    auto it = h->keys.find(t);
+    return it == h->keys.end() ? nullptr : &it->second;
+}
+
+extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
+    if (!h) return fail(HC_ERR_ARG, "null context");
+    if (h->L != 3) return fail(HC_ERR_ARG, "Comp needs max_level = 3 (SURVEY F3)");
+    const int n = NPOLY, m = n / 2;
+    if (N < 1 || s < 1) return fail(HC_ERR_ARG, "N and s must be positive");
+    if ((u64)N >= h->p) return fail(HC_ERR_ARG, "p must exceed N (compress.py:52-53)");
+    if (2 * s > n) return fail(HC_ERR_ARG, "2s must fit the slots of one ciphertext");
+    CU(cudaSetDevice(h->dev));
+    h->plan.reset();
+    std::unique_ptr<Plan> P(new Plan());
+    P->N = N;
+    P->s = s;
+    P->m = m;
+    bsgs_shape(s, &P->baby, &P->giant, &P->s_pad);
+    P->B = (N + m - 1) / m;
+    P->C = (P->B + 1) / 2;
+    for (int step = P->s_pad; step < m; step <<= 1) P->fold.push_back(step);
+    P->F = (int)P->fold.size();
+    P->D1 = h->digits[1];
+    P->D2 = h->digits[2];
+    P->CB = chunk_blocks > 0 ? chunk_blocks : (int)std::min<long long>(P->B, P->baby >= 8 ? 16 : 32);
+    P->ncopy = (int)std::max<long long>(1, (P->B * P->baby + 999) / 1000);
+    // live diagonals: only the last block can have all-zero diagonals
+    P->live.assign((size_t)P->B * P->s_pad, 1);
+    {
+        const long long t = P->B - 1;
+        for (int g = 0; g < P->giant; g++)
+            for (int b = 0; b < P->baby; b++) {
+                bool any = false;
+                for (int pos = 0; pos < m && !any; pos++) {
+                    int row = ((pos - g * P->baby) % P->s_pad + P->s_pad) % P->s_pad;
+                    int col = (pos + b) % m;
+                    any = row < s && t * m + col + 1 <= N;
+                }
+                P->live[(size_t)t * P->s_pad + g * P->baby + b] = any;
+            }
+    }
+    P->acc_live.assign(P->giant, 0);
+    P->live_count = 0;
+    for (long long t = 0; t < P->B; t++)
+        for (int i = 0; i < P->s_pad; i++)
+            if (P->live[(size_t)t * P->s_pad + i]) {
+                P->acc_live[i / P->baby] = 1;
+                P->live_count++;
+            }
+    if (!P->acc_live[0]) {
+        bool any = false;
+        for (int g = 0; g < P->giant; g++) any |= P->acc_live[g];
+        if (!any) return fail(HC_ERR_ARG, "matrix plan had no nonzero diagonals");
+    }
+    // keys (plan_rotation_amounts, compress.py:87-100)
+    P->t_col = 2 * n - 1;
+    if (!need_key(h, P->t_col)) return fail(HC_ERR_KEY, "column-swap key was not declared at keygen");
+    P->t_baby.assign(P->baby, 1);
+    for (int b = 1; b < P->baby; b++) {
+        P->t_baby[b] = rot_t(b, n);
+        if (!need_key(h, P->t_baby[b])) return fail(HC_ERR_KEY, "rotation by " + std::to_string(b) + " was not declared at keygen");
+    }
+    P->t_giant.assign(P->giant, 1);
+    for (int g = 1; g < P->giant; g++) {
+        long long r = ((long long)g * P->baby) % m;
+        P->t_giant[g] = rot_t(r, n);
+        if (P->acc_live[g] && r != 0 && !need_key(h, P->t_giant[g]))
+            return fail(HC_ERR_KEY, "rotation by " + std::to_string(r) + " was not declared at keygen");
+    }
+    for (int a : P->fold) {
+        P->t_fold.push_back(rot_t(a, n));
+        if (!need_key(h, P->t_fold.back())) return fail(HC_ERR_KEY, "rotation by " + std::to_string(a) + " was not declared at keygen");
+    }
+
+    const size_t NB = NPOLY;
+    const int CB = P->CB, bm1 = std::max(P->baby - 1, 0), G = P->giant;
+    int rc = 0;
+#define PA(ptr, cnt)                    \
+    do {                                \
+        rc = palloc(*P, &(ptr), (cnt)); \
+        if (rc) return rc;              \
+    } while (0)
+    PA(P->cv, (size_t)P->C * 2 * 4 * NB);
+    PA(P->cd, (size_t)P->C * 2 * 4 * NB);
+    PA(P->mask, (size_t)2 * 4 * NB);
+    PA(P->diag, (size_t)P->B * P->s_pad * 3 * NB);
+    PA(P->omask, (size_t)2 * NB);
+    PA(P->ecor, (size_t)CB * 4 * 3 * NB);
+    PA(P->rc1raw, (size_t)CB * 3 * NB);
+    PA(P->pn, (size_t)CB * 2 * 3 * NB);
+    PA(P->rc0n, (size_t)CB * 3 * NB);
+    PA(P->digR, (size_t)CB * P->D2 * NB);
+    PA(P->dnttR, (size_t)CB * P->D2 * 3 * NB);
+    PA(P->U, (size_t)CB * 2 * 3 * NB);
+    PA(P->Ucoef, (size_t)CB * 3 * NB);
+    PA(P->digU, (size_t)CB * 2 * P->D2 * NB);
+    PA(P->dnttB, (size_t)std::max(1, CB * bm1) * P->D2 * 3 * NB);
+    PA(P->ROT, (size_t)std::max(1, CB * bm1) * 2 * 3 * NB);
+    PA(P->Ecp, (size_t)P->ncopy * G * 2 * 2 * NB);
+    PA(P->PX, P->px_words());
+    PA(P->A0, (size_t)G * 2 * NB);
+    PA(P->A1, (size_t)2 * NB);
+    PA(P->A1coef, (size_t)G * 2 * NB);
+    PA(P->digG, (size_t)G * P->D1 * NB);
+    PA(P->dnttG, (size_t)G * P->D1 * 2 * NB);
+    PA(P->RES, (size_t)2 * 2 * 2 * NB);
+    PA(P->rc1coef, (size_t)2 * NB);
+    PA(P->digF, (size_t)P->D1 * NB);
+    PA(P->dnttF, (size_t)P->D1 * 2 * NB);
+    PA(P->corr, (size_t)2 * NB);
+    PA(P->OUT, (size_t)2 * NB);
+#undef PA
+
+    // ---- plaintexts on device (K6) ----
+    {
+        std::vector<PJob> pj;
+        PJob j{};
+        j.kind = PT_TOP; j.level = 3; j.out = P->mask; pj.push_back(j);
+        j.kind = PT_BOT; j.level = 3; j.out = P->mask + 4 * NB; pj.push_back(j);
+        j.kind = PT_OUTMASK; j.level = 1; j.out = P->omask; pj.push_back(j);
+        for (long long t = 0; t < P->B; t++)
+            for (int g = 0; g < P->giant; g++)
+                for (int b = 0; b < P->baby; b++) {
+                    int i = g * P->baby + b;
+                    if (!P->live[(size_t)t * P->s_pad + i]) continue;
+                    PJob d{};
+                    d.kind = PT_DIAG; d.t = (int)t; d.g = g; d.b = b; d.level = 2;
+                    d.out = P->diag + ((size_t)t * P->s_pad + i) * 3 * NB;
+                    pj.push_back(d);
+                }
+        PlanShape S{N, s, P->s_pad, P->baby, m};
+        PJob* dj = nullptr;
+        const size_t maxb = 65535;
+        CU(cudaMalloc(&dj, pj.size() * sizeof(PJob)));
+        CU(cudaMemcpy(dj, pj.data(), pj.size() * sizeof(PJob), cudaMemcpyHostToDevice));
+        for (size_t off = 0; off < pj.size(); off += maxb) {
+            int cnt = (int)std::min(maxb, pj.size() - off);
+            k_plain<<<cnt, NT, 2 * NPOLY * 8, h->stream>>>(h->d_ctx, dj + off, S);
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        cudaFree(dj);
+        if (e != cudaSuccess) return fail(HC_ERR_CUDA, std::string("plaintext generation: ") + cudaGetErrorString(e));
+    }
+    h->plan = std::move(P);
+    return HC_OK;
+}
+
+extern "C" int hc_plan_info(const hc_ctx* h, int64_t* info) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "no plan");
+    const Plan& P = *h->plan;
+    info[0] = P.B;
+    info[1] = P.C;
+    info[2] = P.baby;
+    info[3] = P.giant;
+    info[4] = P.F;
+    info[5] = P.s_pad;
+    info[6] = P.live_count;
+    info[7] = P.full ? P.full->launches : -1;
+    return HC_OK;
+}
+
+extern "C" int64_t hc_partial_words(const hc_ctx* h) {
+    if (!h || !h->plan) return -1;
+    return (int64_t)h->plan->px_words();
+}
+
+// Steps S1..S10 for blocks [b0, b1): pack_pair (compress.py:338-367), baby
+// rotations and the diagonal products (compress.py:286-297), accumulated
+// into the partial PX = [E | X].
+static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedule& S) {
+    const size_t NB = NPOLY;
+    const int D2 = P.D2, baby = P.baby, G = P.giant, sp = P.s_pad;
+    const DevKey* kcol = need_key(h, P.t_col);
+    int rc;
+    add_memset(S, P.Ecp, (size_t)P.ncopy * G * 2 * 2 * NB * 8);
+    add_memset(S, P.PX, P.px_words() * 8);
+    for (long long c0 = b0; c0 < b1; c0 += P.CB) {
+        const int cb = (int)std::min<long long>(P.CB, b1 - c0);
+        std::vector<XJob> s1, s2, s3, s5, s7, s9;
+        std::vector<CJob> s2c, s6;
+        std::vector<MJob> s4, s8;
+        for (int tl = 0; tl < cb; tl++) {
+            const long long t = c0 + tl;
+            const long long src = t / 2;
+            const int par = (int)(t % 2);
+            const u64* mk = P.mask + (size_t)par * 4 * NB;
+            const u64* cv = P.cv + (size_t)src * 2 * 4 * NB;
+            const u64* cd = P.cd + (size_t)src * 2 * 4 * NB;
+            // even block: u = mp(cv, top) + rot_col(mp(cd, top)); odd: rot_col(mp(cv, bot)) + mp(cd, bot)
+            const u64* ctP = par == 0 ? cv : cd;
+            const u64* ctR = par == 0 ? cd : cv;
+            u64* ecor = P.ecor + (size_t)tl * 4 * 3 * NB;  // [P0,P1,R0,R1][3][n]
+            for (int mm = 0; mm < 2; mm++)
+                for (int poly = 0; poly < 2; poly++) {
+                    const u64* ct = mm == 0 ? ctP : ctR;
+                    XJob j{};
+                    j.dir = 1; j.k = 3; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 3;
+                    j.a = ct + ((size_t)poly * 4 + 3) * NB;
+                    j.b = mk + 3 * NB;
+                    j.out = ecor + (size_t)(mm * 2 + poly) * 3 * NB;
+                    j.ostride = NB;
+                    s1.push_back(j);
+                }
+            for (int k = 0; k < 3; k++) {
+                XJob j{};
+                j.dir = 1; j.k = k; j.ld = LD_MONT; j.ep = EP_STORE;
+                j.a = ctR + ((size_t)1 * 4 + k) * NB;
+                j.b = mk + (size_t)k * NB;
+                j.out = P.rc1raw + ((size_t)tl * 3 + k) * NB;
+                s1.push_back(j);
+            }
+            // S2: NTT of corrections + plaintext-product combine
+            for (int which = 0; which < 3; which++) {  // P.c0, P.c1, R.c0
+                const int mm = which < 2 ? 0 : 1, poly = which < 2 ? which : 0;
+                const u64* ct = mm == 0 ? ctP : ctR;
+                for (int k = 0; k < 3; k++) {
+                    XJob j{};
+                    j.dir = 0; j.k = k; j.ld = LD_U64; j.ep = EP_ADDMONT;
+                    j.a = ecor + ((size_t)(mm * 2 + poly) * 3 + k) * NB;
+                    j.ea = ct + ((size_t)poly * 4 + k) * NB;
+                    j.eb = mk + (size_t)k * NB;
+                    j.out = which < 2 ? P.pn + (((size_t)tl * 2 + poly) * 3 + k) * NB : P.rc0n + ((size_t)tl * 3 + k) * NB;
+                    s2.push_back(j);
+                }
+            }
+            {
+                CJob c{};
+                c.level = 2; c.mode = 0;
+                c.x = P.rc1raw + (size_t)tl * 3 * NB;
+                c.xadd = ecor + (size_t)3 * 3 * NB;
+                c.xstride = NB;
+                c.gal = kcol->gal;
+                c.dig = P.digR + (size_t)tl * D2 * NB;
+                s2c.push_back(c);
+            }
+            for (int jj = 0; jj < D2; jj++)
+                for (int k = 0; k < 3; k++) {
+                    XJob j{};
+                    j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+                    j.a = (const u64*)(P.digR + ((size_t)tl * D2 + jj) * NB);
+                    j.out = P.dnttR + (((size_t)tl * D2 + jj) * 3 + k) * NB;
+                    s3.push_back(j);
+                }
+            {
+                MJob mj{};
+                mj.level = 2; mj.nterm = 1;
+                mj.t[0].dntt = P.dnttR + (size_t)tl * D2 * 3 * NB;
+                mj.t[0].key = kcol->key;
+                mj.t[0].c0src = P.rc0n + (size_t)tl * 3 * NB;
+                mj.t[0].perm = kcol->perm;
+                mj.add0 = P.pn + ((size_t)tl * 2 + 0) * 3 * NB;
+                mj.add1 = P.pn + ((size_t)tl * 2 + 1) * 3 * NB;
+                mj.out0 = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
+                mj.out1 = P.U + ((size_t)tl * 2 + 1) * 3 * NB;
+                s4.push_back(mj);
+            }
+            if (baby > 1) {
+                for (int k = 0; k < 3; k++) {
+                    XJob j{};
+                    j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+                    j.a = P.U + (((size_t)tl * 2 + 1) * 3 + k) * NB;
+                    j.out = P.Ucoef + ((size_t)tl * 3 + k) * NB;
+                    s5.push_back(j);
+                }
+                CJob c{};
+                c.level = 2; c.mode = 1;
+                c.x = P.Ucoef + (size_t)tl * 3 * NB;
+                c.xstride = NB;
+                c.dig = P.digU + (size_t)tl * 2 * D2 * NB;
+                s6.push_back(c);
+                for (int b = 1; b < baby; b++) {
+                    const DevKey* kb = need_key(h, P.t_baby[b]);
+                    const size_t rb = (size_t)tl * (baby - 1) + (b - 1);
+                    for (int jj = 0; jj < D2; jj++)
+                        for (int k = 0; k < 3; k++) {
+                            XJob j{};
+                            j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_STORE;
+                            j.a = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + jj) * NB);
+                            j.b = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
+                            j.gal = kb->gal;
+                            j.out = P.dnttB + ((rb * D2 + jj) * 3 + k) * NB;
+                            s7.push_back(j);
+                        }
+                    MJob mj{};
+                    mj.level = 2; mj.nterm = 1;
+                    mj.t[0].dntt = P.dnttB + rb * D2 * 3 * NB;
+                    mj.t[0].key = kb->key;
+                    mj.t[0].c0src = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
+                    mj.t[0].perm = kb->perm;
+                    mj.out0 = P.ROT + (rb * 2 + 0) * 3 * NB;
+                    mj.out1 = P.ROT + (rb * 2 + 1) * 3 * NB;
+                    s8.push_back(mj);
+                }
+            }
+            // S9: dropped-prime half of each diagonal product (INTT + rescale correction)
+            for (int g = 0; g < G; g++)
+                for (int b = 0; b < baby; b++) {
+                    const int i = g * baby + b;
+                    if (!P.live[(size_t)t * sp + i]) continue;
+                    const u64* dg = P.diag + ((size_t)t * sp + i) * 3 * NB;
+                    const int copy = (int)((t * baby + b) % P.ncopy);
+                    for (int poly = 0; poly < 2; poly++) {
+                        const u64* srcp = b == 0 ? P.U + ((size_t)tl * 2 + poly) * 3 * NB
+                                                 : P.ROT + (((size_t)tl * (baby - 1) + (b - 1)) * 2 + poly) * 3 * NB;
+                        XJob j{};
+                        j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE_ATOMIC; j.level = 2;
+                        j.a = srcp + 2 * NB;
+                        j.b = dg + 2 * NB;
+                        j.out = P.Ecp + ((((size_t)copy * G + g) * 2 + poly) * 2) * NB;
+                        j.ostride = NB;
+                        s9.push_back(j);
+                    }
+                }
+        }
+        rc = add_xf(S, s1); if (rc) return rc;
+        rc = add_xf(S, s2); if (rc) return rc;
+        rc = add_co(S, s2c); if (rc) return rc;
+        rc = add_xf(S, s3); if (rc) return rc;
+        rc = add_ma(S, s4, 3); if (rc) return rc;
+        rc = add_xf(S, s5); if (rc) return rc;
+        rc = add_co(S, s6); if (rc) return rc;
+        rc = add_xf(S, s7); if (rc) return rc;
+        rc = add_ma(S, s8, 3); if (rc) return rc;
+        rc = add_xf(S, s9); if (rc) return rc;
+        // S10: kept-prime half of the diagonal products, X[g] += sum src * diag * q^-1
+        {
+            std::vector<DXJob> dx;
+            std::vector<const u64*> srcs, dgs;
+            struct Rng { size_t off, cnt; int g, poly; };
+            std::vector<Rng> rngs;
+            for (int g = 0; g < G; g++)
+                for (int poly = 0; poly < 2; poly++) {
+                    size_t off = srcs.size();
+                    for (int tl = 0; tl < cb; tl++) {
+                        const long long t = c0 + tl;
+                        for (int b = 0; b < baby; b++) {
+                            const int i = g * baby + b;
+                            if (!P.live[(size_t)t * sp + i]) continue;
+                            srcs.push_back(b == 0 ? P.U + ((size_t)tl * 2 + poly) * 3 * NB
+                                                  : P.ROT + (((size_t)tl * (baby - 1) + (b - 1)) * 2 + poly) * 3 * NB);
+                            dgs.push_back(P.diag + ((size_t)t * sp + i) * 3 * NB);
+                        }
+                    }
+                    rngs.push_back({off, srcs.size() - off, g, poly});
+                }
+            if (!srcs.empty()) {
+                const u64** dsrc = nullptr;
+                const u64** ddg = nullptr;
+                CU(cudaMalloc(&dsrc, srcs.size() * sizeof(u64*)));
+                S.allocs.push_back(dsrc);
+                CU(cudaMalloc(&ddg, dgs.size() * sizeof(u64*)));
+                S.allocs.push_back(ddg);
+                CU(cudaMemcpy(dsrc, srcs.data(), srcs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+                CU(cudaMemcpy(ddg, dgs.data(), dgs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+                for (const Rng& r : rngs) {
+                    if (!r.cnt) continue;
+                    DXJob d{};
+                    d.nterm = (int)r.cnt;
+                    d.src = dsrc + r.off;
+                    d.dg = ddg + r.off;
+                    d.X = P.PX + (size_t)1 * G * 2 * 2 * NB + (((size_t)r.g * 2 + r.poly) * 2) * NB;
+                    dx.push_back(d);
+                }
+                rc = add_dx(S, dx, 2);
+                if (rc) return rc;
+            }
+        }
+    }
+    // fold E copies into PX[0]
+    Step st;
+    st.kind = ST_SUMC;
+    st.in = P.Ecp;
+    st.out = P.PX;
+    st.rows = (long long)G * 2 * 2;
+    st.period = 2;
+    st.copies = P.ncopy;
+    st.cstride = (long long)G * 2 * 2 * NB;
+    S.steps.push_back(st);
+    return HC_OK;
+}
+
+// T1..T4, folds F1..F4 and the output mask D1..D2 (compress.py:298-310).
+static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
+    const size_t NB = NPOLY;
+    const int G = P.giant, D1 = P.D1;
+    const u64* E = P.PX;
+    const u64* X = P.PX + (size_t)G * 2 * 2 * NB;
+    auto ex = [&](const u64* base, int g, int poly, int k) { return base + (((size_t)g * 2 + poly) * 2 + k) * NB; };
+    int rc;
+    // T1: acc[g] = X[g] + NTT(E[g]); c1 of g >= 1 in coefficient domain
+    std::vector<XJob> t1;
+    for (int g = 0; g < G; g++) {
+        if (!P.acc_live[g]) continue;
+        for (int k = 0; k < 2; k++) {
+            XJob j{};
+            j.dir = 0; j.k = k; j.ld = LD_RED; j.ep = EP_ADDRED;
+            j.a = ex(E, g, 0, k);
+            j.ea = ex(X, g, 0, k);
+            j.out = P.A0 + ((size_t)g * 2 + k) * NB;
+            t1.push_back(j);
+            if (g == 0) {
+                XJob c = j;
+                c.a = ex(E, g, 1, k);
+                c.ea = ex(X, g, 1, k);
+                c.out = P.A1 + (size_t)k * NB;
+                t1.push_back(c);
+            } else {
+                XJob c{};
+                c.dir = 1; c.k = k; c.ld = LD_RED; c.ep = EP_ADDRED;
+                c.a = ex(X, g, 1, k);
+                c.ea = ex(E, g, 1, k);
+                c.out = P.A1coef + ((size_t)g * 2 + k) * NB;
+                t1.push_back(c);
+            }
+        }
+    }
+    rc = add_xf(S, t1); if (rc) return rc;
+    // T2/T3/T4: giant-step rotations summed into res (level 1)
+    std::vector<CJob> t2;
+    std::vector<XJob> t3;
+    MJob t4{};
+    t4.level = 1;
+    t4.nterm = 0;
+    if (P.acc_live[0]) {
+        t4.add0 = P.A0;
+        t4.add1 = P.A1;
+    }
+    std::vector<MJob> t4extra;  // more than MAXTERM terms: chain extra jobs
+    for (int g = 1; g < G; g++) {
+        if (!P.acc_live[g]) continue;
+        const DevKey* kg = need_key(h, P.t_giant[g]);
+        CJob c{};
+        c.level = 1; c.mode = 0;
+        c.x = P.A1coef + (size_t)g * 2 * NB;
+        c.xstride = NB;
+        c.gal = kg->gal;
+        c.dig = P.digG + (size_t)g * D1 * NB;
+        t2.push_back(c);
+        for (int jj = 0; jj < D1; jj++)
+            for (int k = 0; k < 2; k++) {
+                XJob j{};
+                j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+                j.a = (const u64*)(P.digG + ((size_t)g * D1 + jj) * NB);
+                j.out = P.dnttG + (((size_t)g * D1 + jj) * 2 + k) * NB;
+                t3.push_back(j);
+            }
+        if (t4.nterm == MAXTERM) return fail(HC_ERR_ARG, "too many giant steps");
+        MTerm& T = t4.t[t4.nterm++];
+        T.dntt = P.dnttG + (size_t)g * D1 * 2 * NB;
+        T.key = kg->key;
+        T.c0src = P.A0 + (size_t)g * 2 * NB;
+        T.perm = kg->perm;
+    }
+    rc = add_co(S, t2); if (rc) return rc;
+    rc = add_xf(S, t3); if (rc) return rc;
+    u64* res[2] = {P.RES, P.RES + (size_t)2 * 2 * NB};
+    t4.out0 = res[0];
+    t4.out1 = res[0] + 2 * NB;
+    rc = add_ma(S, std::vector<MJob>{t4}, 2); if (rc) return rc;
+    // folds: res += rot_row(res, a)
+    for (int f = 0; f < P.F; f++) {
+        u64* cur = res[f % 2];
+        u64* nxt = res[(f + 1) % 2];
+        const DevKey* ka = need_key(h, P.t_fold[f]);
+        std::vector<XJob> f1, f3;
+        for (int k = 0; k < 2; k++) {
+            XJob j{};
+            j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+            j.a = cur + (size_t)(2 + k) * NB;
+            j.out = P.rc1coef + (size_t)k * NB;
+            f1.push_back(j);
+        }
+        CJob c{};
+        c.level = 1; c.mode = 0;
+        c.x = P.rc1coef;
+        c.xstride = NB;
+        c.gal = ka->gal;
+        c.dig = P.digF;
+        for (int jj = 0; jj < D1; jj++)
+            for (int k = 0; k < 2; k++) {
+                XJob j{};
+                j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+                j.a = (const u64*)(P.digF + (size_t)jj * NB);
+                j.out = P.dnttF + ((size_t)jj * 2 + k) * NB;
+                f3.push_back(j);
+            }
+        MJob mj{};
+        mj.level = 1; mj.nterm = 1;
+        mj.t[0].dntt = P.dnttF;
+        mj.t[0].key = ka->key;
+        mj.t[0].c0src = cur;
+        mj.t[0].perm = ka->perm;
+        mj.add0 = cur;
+        mj.add1 = cur + 2 * NB;
+        mj.out0 = nxt;
+        mj.out1 = nxt + 2 * NB;
+        rc = add_xf(S, f1); if (rc) return rc;
+        rc = add_co(S, std::vector<CJob>{c}); if (rc) return rc;
+        rc = add_xf(S, f3); if (rc) return rc;
+        rc = add_ma(S, std::vector<MJob>{mj}, 2); if (rc) return rc;
+    }
+    // D1/D2: mul_plain(res, output_mask) level 1 -> 0
+    u64* fin = res[P.F % 2];
+    std::vector<XJob> d1, d2;
+    for (int poly = 0; poly < 2; poly++) {
+        XJob j{};
+        j.dir = 1; j.k = 1; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 1;
+        j.a = fin + ((size_t)poly * 2 + 1) * NB;
+        j.b = P.omask + NB;
+        j.out = P.corr + (size_t)poly * NB;
+        j.ostride = NB;
+        d1.push_back(j);
+        XJob o{};
+        o.dir = 0; o.k = 0; o.ld = LD_U64; o.ep = EP_ADDMONT;
+        o.a = P.corr + (size_t)poly * NB;
+        o.ea = fin + ((size_t)poly * 2 + 0) * NB;
+        o.eb = P.omask;
+        o.out = P.OUT + (size_t)poly * NB;
+        d2.push_back(o);
+    }
+    rc = add_xf(S, d1); if (rc) return rc;
+    rc = add_xf(S, d2); if (rc) return rc;
+    return HC_OK;
+}
+
+static int ensure_full(hc_ctx* h) {
+    Plan& P = *h->plan;
+    if (P.full) return HC_OK;
+    std::unique_ptr<Schedule> S(new Schedule());
+    int rc = build_partial(h, P, 0, P.B, *S);
+    if (rc) return rc;
+    rc = build_finish(h, P, *S);
+    if (rc) return rc;
+    rc = capture(h, *S);
+    if (rc) return rc;
+    P.full = std::move(S);
+    return HC_OK;
+}
+
+extern "C" int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    CU(cudaSetDevice(h->dev));
+    const size_t bytes = (size_t)C * 2 * 4 * NPOLY * 8;
+    CU(cudaMemcpyAsync(P.cd, cd, bytes, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(P.cv, cv, bytes, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
+extern "C" int hc_comp_launch(hc_ctx* h, void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    CU(cudaSetDevice(h->dev));
+    int rc = ensure_full(h);
+    if (rc) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    CU(cudaGraphLaunch(h->plan->full->exec, s));
+    return HC_OK;
+}
+
+extern "C" int hc_comp_get_output(hc_ctx* h, uint64_t* out) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    CU(cudaSetDevice(h->dev));
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(out, h->plan->OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost));
+    return HC_OK;
+}
+
+extern "C" int hc_comp(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* out) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    CU(cudaSetDevice(h->dev));
+    int rc = ensure_full(h);
+    if (rc) return rc;
+    const size_t bytes = (size_t)C * 2 * 4 * NPOLY * 8;
+    CU(cudaMemcpyAsync(P.cd, cd, bytes, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(P.cv, cv, bytes, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaGraphLaunch(P.full->exec, h->stream));
+    CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
+extern "C" int hc_comp_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* out,
+                             void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    CU(cudaSetDevice(h->dev));
+    int rc = ensure_full(h);
+    if (rc) return rc;
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    const size_t bytes = (size_t)C * 2 * 4 * NPOLY * 8;
+    CU(cudaMemcpyAsync(P.cd, cd, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(P.cv, cv, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaGraphLaunch(P.full->exec, s));
+    CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, s));
+    return HC_OK;
+}
+
+extern "C" int hc_comp_partial(hc_ctx* h, int64_t b0, int64_t b1, uint64_t* partial_dev, void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (b0 < 0 || b1 > P.B || b0 > b1) return fail(HC_ERR_ARG, "block range out of bounds");
+    CU(cudaSetDevice(h->dev));
+    auto key = std::make_pair((long long)b0, (long long)b1);
+    auto it = P.partials.find(key);
+    if (it == P.partials.end()) {
+        std::unique_ptr<Schedule> S(new Schedule());
+        int rc = build_partial(h, P, b0, b1, *S);
+        if (rc) return rc;
+        rc = capture(h, *S);
+        if (rc) return rc;
+        it = P.partials.emplace(key, std::move(S)).first;
+    }
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    CU(cudaGraphLaunch(it->second->exec, s));
+    CU(cudaMemcpyAsync(partial_dev, P.PX, P.px_words() * 8, cudaMemcpyDeviceToDevice, s));
+    return HC_OK;
+}
+
+extern "C" int hc_comp_finish(hc_ctx* h, const uint64_t* partial_dev, void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    CU(cudaSetDevice(h->dev));
+    if (!P.fin) {
+        std::unique_ptr<Schedule> S(new Schedule());
+        int rc = build_finish(h, P, *S);
+        if (rc) return rc;
+        rc = capture(h, *S);
+        if (rc) return rc;
+        P.fin = std::move(S);
+    }
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    CU(cudaMemcpyAsync(P.PX, partial_dev, P.px_words() * 8, cudaMemcpyDeviceToDevice, s));
+    CU(cudaGraphLaunch(P.fin->exec, s));
+    return HC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// ring helpers and single operations (host buffers)
+// ---------------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() { cudaFree(p); }
+};
+
+extern "C" int hc_ntt(hc_ctx* h, uint64_t* data, int rows, const int* pidx, int inverse) {
+    if (!h || rows < 0) return fail(HC_ERR_ARG, "bad arguments");
+    if (rows == 0) return HC_OK;
+    CU(cudaSetDevice(h->dev));
+    DevBuf buf;
+    const size_t bytes = (size_t)rows * NPOLY * 8;
+    CU(cudaMalloc(&buf.p, bytes));
+    CU(cudaMemcpy(buf.p, data, bytes, cudaMemcpyHostToDevice));
+    std::vector<XJob> jobs;
+    for (int r = 0; r < rows; r++) {
+        if (pidx[r] < 0 || pidx[r] >= NPR || (pidx[r] > h->L && pidx[r] != PIDX))
+            return fail(HC_ERR_ARG, "bad prime index");
+        XJob j{};
+        j.dir = inverse ? 1 : 0;
+        j.k = pidx[r];
+        j.ld = LD_RED;
+        j.ep = EP_STORE;
+        j.a = (u64*)buf.p + (size_t)r * NPOLY;
+        j.out = (u64*)buf.p + (size_t)r * NPOLY;
+        jobs.push_back(j);
+    }
+    Schedule S;
+    int rc = add_xf(S, jobs);
+    if (rc) return rc;
+    rc = run_now(h, S);
+    if (rc) return rc;
+    CU(cudaMemcpy(data, buf.p, bytes, cudaMemcpyDeviceToHost));
+    return HC_OK;
+}
+
+extern "C" int hc_pointwise(hc_ctx* h, const uint64_t* a, const uint64_t* b, uint64_t* out, int rows,
+                            const int* pidx, int op) {
+    if (!h || rows < 0 || op < 0 || op > 2) return fail(HC_ERR_ARG, "bad arguments");
+    if (rows == 0) return HC_OK;
+    CU(cudaSetDevice(h->dev));
+    const size_t bytes = (size_t)rows * NPOLY * 8;
+    DevBuf da, db, dp;
+    CU(cudaMalloc(&da.p, bytes));
+    CU(cudaMalloc(&db.p, bytes));
+    CU(cudaMalloc(&dp.p, rows * sizeof(int)));
+    CU(cudaMemcpy(da.p, a, bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dp.p, pidx, rows * sizeof(int), cudaMemcpyHostToDevice));
+    k_pointwise<<<592, 256, 0, h->stream>>>(h->d_ctx, (u64*)da.p, (u64*)db.p, (u64*)da.p, rows, (int*)dp.p, op);
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaMemcpy(out, da.p, bytes, cudaMemcpyDeviceToHost));
+    return HC_OK;
+}
+
+extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint64_t* pt, uint64_t* out) {
+    if (!h) return fail(HC_ERR_ARG, "null context");
+    if (level < 1) return fail(HC_ERR_LEVEL, "plaintext multiply at level 0");
+    if (level > h->L) return fail(HC_ERR_ARG, "level above max_level");
+    CU(cudaSetDevice(h->dev));
+    const int l = level, P1 = l + 1;
+    const size_t NB = NPOLY;
+    // plaintext in Montgomery form with the modulus-switch factor folded in
+    std::vector<u64> ptm((size_t)P1 * NB);
+    const LevelC& LV = h->hctx.lv[l];
+    for (int k = 0; k <= l; k++) {
+        const PrimeC& pc = h->hctx.pc[k];
+        u64 w = k == l ? pc.rmod : LV.qinv_r[k];
+        for (size_t j = 0; j < NB; j++) ptm[k * NB + j] = mulmod_slow(pt[k * NB + j] % pc.q, w, pc.q);
+    }
+    DevBuf dct, dpt, dcorr, dout;
+    CU(cudaMalloc(&dct.p, (size_t)2 * P1 * NB * 8));
+    CU(cudaMalloc(&dpt.p, (size_t)P1 * NB * 8));
+    CU(cudaMalloc(&dcorr.p, (size_t)2 * l * NB * 8));
+    CU(cudaMalloc(&dout.p, (size_t)2 * l * NB * 8));
+    CU(cudaMemcpy(dct.p, ct, (size_t)2 * P1 * NB * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dpt.p, ptm.data(), (size_t)P1 * NB * 8, cudaMemcpyHostToDevice));
+    const u64* c = (const u64*)dct.p;
+    const u64* p = (const u64*)dpt.p;
+    u64* corr = (u64*)dcorr.p;
+    u64* o = (u64*)dout.p;
+    std::vector<XJob> a, b;
+    for (int poly = 0; poly < 2; poly++) {
+        XJob j{};
+        j.dir = 1; j.k = l; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = l;
+        j.a = c + ((size_t)poly * P1 + l) * NB;
+        j.b = p + (size_t)l * NB;
+        j.out = corr + (size_t)poly * l * NB;
+        j.ostride = NB;
+        a.push_back(j);
+        for (int k = 0; k < l; k++) {
+            XJob f{};
+            f.dir = 0; f.k = k; f.ld = LD_U64; f.ep = EP_ADDMONT;
+            f.a = corr + ((size_t)poly * l + k) * NB;
+            f.ea = c + ((size_t)poly * P1 + k) * NB;
+            f.eb = p + (size_t)k * NB;
+            f.out = o + ((size_t)poly * l + k) * NB;
+            b.push_back(f);
+        }
+    }
+    Schedule S;
+    int rc = add_xf(S, a);
+    if (!rc) rc = add_xf(S, b);
+    if (!rc) rc = run_now(h, S);
+    if (rc) return rc;
+    CU(cudaMemcpy(out, o, (size_t)2 * l * NB * 8, cudaMemcpyDeviceToHost));
+    return HC_OK;
+}
+
+extern "C" int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t t, uint64_t* out) {
+    if (!h) return fail(HC_ERR_ARG, "null context");
+    if (level < 1 || level > h->L) return fail(HC_ERR_ARG, "rotation level must be 1..max_level");
+    const DevKey* key = need_key(h, t);
+    if (!key) return fail(HC_ERR_KEY, "rotation key was not declared at keygen");
+    CU(cudaSetDevice(h->dev));
+    const int l = level, P1 = l + 1, D = h->digits[l];
+    const size_t NB = NPOLY;
+    DevBuf dct, dcoef, ddig, dntt, dout;
+    CU(cudaMalloc(&dct.p, (size_t)2 * P1 * NB * 8));
+    CU(cudaMalloc(&dcoef.p, (size_t)P1 * NB * 8));
+    CU(cudaMalloc(&ddig.p, (size_t)D * NB * 2));
+    CU(cudaMalloc(&dntt.p, (size_t)D * P1 * NB * 8));
+    CU(cudaMalloc(&dout.p, (size_t)2 * P1 * NB * 8));
+    CU(cudaMemcpy(dct.p, ct, (size_t)2 * P1 * NB * 8, cudaMemcpyHostToDevice));
+    const u64* c = (const u64*)dct.p;
+    std::vector<XJob> inv, fwd;
+    for (int k = 0; k < P1; k++) {
+        XJob j{};
+        j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+        j.a = c + ((size_t)1 * P1 + k) * NB;
+        j.out = (u64*)dcoef.p + (size_t)k * NB;
+        inv.push_back(j);
+    }
+    CJob cj{};
+    cj.level = l; cj.mode = 0;
+    cj.x = (u64*)dcoef.p;
+    cj.xstride = NB;
+    cj.gal = key->gal;
+    cj.dig = (uint16_t*)ddig.p;
+    for (int jj = 0; jj < D; jj++)
+        for (int k = 0; k < P1; k++) {
+            XJob j{};
+            j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+            j.a = (const u64*)((uint16_t*)ddig.p + (size_t)jj * NB);
+            j.out = (u64*)dntt.p + ((size_t)jj * P1 + k) * NB;
+            fwd.push_back(j);
+        }
+    MJob mj{};
+    mj.level = l; mj.nterm = 1;
+    mj.t[0].dntt = (u64*)dntt.p;
+    mj.t[0].key = key->key;
+    mj.t[0].c0src = c;
+    mj.t[0].perm = key->perm;
+    mj.out0 = (u64*)dout.p;
+    mj.out1 = (u64*)dout.p + (size_t)P1 * NB;
+    Schedule S;
+    int rc = add_xf(S, inv);
+    if (!rc) rc = add_co(S, std::vector<CJob>{cj});
+    if (!rc) rc = add_xf(S, fwd);
+    if (!rc) rc = add_ma(S, std::vector<MJob>{mj}, P1);
+    if (!rc) rc = run_now(h, S);
+    if (rc) return rc;
+    CU(cudaMemcpy(out, dout.p, (size_t)2 * P1 * NB * 8, cudaMemcpyDeviceToHost));
+    return HC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// measurement helpers
+// ---------------------------------------------------------------------------
+extern "C" int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind,
+                               int* step_jobs) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    CU(cudaSetDevice(h->dev));
+    int rc = ensure_full(h);
+    if (rc) return rc;
+    const Schedule& S = *h->plan->full;
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    const int ns = (int)S.steps.size();
+    std::vector<cudaEvent_t> ev(ns + 1);
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    CU(cudaEventRecord(ev[0], s));
+    for (int i = 0; i < ns; i++) {
+        Schedule one;
+        one.steps.push_back(S.steps[i]);
+        rc = enqueue(h, one, s);
+        one.steps.clear();
+        if (rc) return rc;
+        CU(cudaEventRecord(ev[i + 1], s));
+    }
+    CU(cudaStreamSynchronize(s));
+    int k = 0;
+    for (int i = 0; i < ns && k < max_steps; i++, k++) {
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        step_ms[k] = ms;
+        step_kind[k] = S.steps[i].kind;
+        step_jobs[k] = S.steps[i].njobs;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return k;
+}
+
+// Butterfly-throughput ceiling: the CT butterfly of the NTT kernels
+// (Harvey lazy Shoup, bf_ct) in registers at full occupancy, no memory
+// traffic.  Returns butterflies per second; the integer-ALU roofline
+// denominator for k_xform.
+__global__ void __launch_bounds__(256) k_bf_peak(const DevCtx* __restrict__ C, int iters, u64* sink) {
+    const PrimeC P = C->pc[0];
+    u64 x[16];
+    for (int i = 0; i < 16; i++) x[i] = (threadIdx.x * 977 + i * 131 + blockIdx.x) % P.q;
+    u64 w = C->twf[5].w, ws = C->twf[5].ws;
+    for (int it = 0; it < iters; it++) {
+        HC_UNROLL
+        for (int i = 0; i < 8; i++) bf_ct(x[i], x[i + 8], w, ws, P.q, P.q2);
+        HC_UNROLL
+        for (int i = 0; i < 16; i += 2) bf_ct(x[i], x[i + 1], w, ws, P.q, P.q2);
+    }
+    u64 acc = 0;
+    for (int i = 0; i < 16; i++) acc ^= x[i];
+    if (acc == 0x12345) sink[0] = acc;
+}
+
+extern "C" int hc_bf_peak(hc_ctx* h, double* bfly_per_s) {
+    if (!h) return fail(HC_ERR_ARG, "null context");
+    CU(cudaSetDevice(h->dev));
+    int nsm = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+    DevBuf sink;
+    CU(cudaMalloc(&sink.p, 8));
+    const int blocks = nsm * 8, iters = 4096;
+    k_bf_peak<<<blocks, 256, 0, h->stream>>>(h->d_ctx, 64, (u64*)sink.p);  // warm-up
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    CU(cudaEventRecord(a, h->stream));
+    k_bf_peak<<<blocks, 256, 0, h->stream>>>(h->d_ctx, iters, (u64*)sink.p);
+    CU(cudaEventRecord(b, h->stream));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *bfly_per_s = (double)blocks * 256 * iters * 16 / (ms * 1e-3);
+    return HC_OK;
+}
+
+extern "C" void hc_ctx_destroy(hc_ctx* h) {
+    if (!h) return;
+    cudaSetDevice(h->dev);
+    cudaDeviceSynchronize();
+    h->plan.reset();
+    for (auto& kv : h->keys) release_key(kv.second);
+    cudaFree(h->d_twf);
+    cudaFree(h->d_twi);
+    cudaFree(h->d_slot_of);
+    cudaFree(h->d_ctx);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}

@@ -1,0 +1,101 @@
+// CPU self-test shim (tests/test_csrc_host.py): compiles the device-side
+// arithmetic, the 256-thread NTT schedule (emulated thread by thread), the
+// CRT/digit split and the modulus-switch correction for the host with g++,
+// so the exact code the GPU runs is checked against the oracle on a machine
+// without a GPU.  Not part of the product library.
+#include <cstdint>
+#include <vector>
+
+#include "elem.cuh"
+#include "host_tables.hpp"
+
+using namespace hc;
+
+static DevCtx g_ctx;
+static std::vector<Tw> g_twf, g_twi;
+static std::vector<uint16_t> g_slot;
+static int g_digits[MAXL + 1];
+
+extern "C" int ht_init(const uint64_t* primes, int max_level, uint64_t p) {
+    build_host_ctx(g_ctx, g_twf, g_twi, g_slot, NPOLY, max_level, primes, p, g_digits);
+    g_ctx.twf = g_twf.data();
+    g_ctx.twi = g_twi.data();
+    g_ctx.slot_of = g_slot.data();
+    return 0;
+}
+
+extern "C" int ht_digits(int level) { return g_digits[level]; }
+
+// exact device NTT schedule on the host; k = RNS index (4 = p)
+extern "C" void ht_ntt(int k, uint64_t* a, int inverse) {
+    if (inverse) host_emulate_inv(a, g_ctx.twi + (size_t)k * NPOLY, g_ctx.pc[k]);
+    else host_emulate_fwd(a, g_ctx.twf + (size_t)k * NPOLY, g_ctx.pc[k]);
+}
+
+template <int L>
+static void compose_all(const uint64_t* x, const uint16_t* gal, int mode, uint16_t* dig) {
+    const LevelC& LV = g_ctx.lv[L];
+    const int D = LV.D;
+    for (int pos = 0; pos < NPOLY; pos++) {
+        int src = pos, neg = 0;
+        if (mode == 0 && gal) {
+            src = gal[pos] & 0x7FFF;
+            neg = gal[pos] >> 15;
+        }
+        u64 xr[L + 1];
+        for (int k = 0; k <= L; k++) xr[k] = x[(size_t)k * NPOLY + src];
+        u64 X[NLIMB];
+        crt_compose<L>(LV, g_ctx.pc, xr, X);
+        if (mode == 0) {
+            if (neg) neg_mod_Q<L>(LV, X);
+            for (int j = 0; j < D; j++) dig[(size_t)j * NPOLY + pos] = digit16(X, j);
+        } else {
+            for (int j = 0; j < D; j++) dig[(size_t)j * NPOLY + pos] = digit16(X, j);
+            neg_mod_Q<L>(LV, X);
+            for (int j = 0; j < D; j++) dig[(size_t)(D + j) * NPOLY + pos] = digit16(X, j);
+        }
+    }
+}
+
+extern "C" int ht_compose(int level, const uint64_t* x, const uint16_t* gal, int mode, uint16_t* dig) {
+    switch (level) {
+        case 1: compose_all<1>(x, gal, mode, dig); return 0;
+        case 2: compose_all<2>(x, gal, mode, dig); return 0;
+        case 3: compose_all<3>(x, gal, mode, dig); return 0;
+        default: return 1;
+    }
+}
+
+// e[k][j] for k < level from the dropped-prime residues x[j]
+extern "C" void ht_rescale_corr(int level, const uint64_t* x, uint64_t* e) {
+    for (int j = 0; j < NPOLY; j++) {
+        u64 ek[MAXL];
+        rescale_corr(g_ctx, level, x[j], ek);
+        for (int k = 0; k < level; k++) e[(size_t)k * NPOLY + j] = ek[k];
+    }
+}
+
+// Montgomery / Shoup helpers on arrays: op 0 = a*b mod q via mul_mont(a, b*R),
+// op 1 = redc(hi, lo) of 128-bit a*b, op 2 = red64(a)
+extern "C" void ht_modops(int k, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, int count) {
+    const PrimeC& P = g_ctx.pc[k];
+    for (int i = 0; i < count; i++) {
+        if (op == 0) {
+            u64 bm = mul_shoup(b[i], P.rmod, P.rmod_s, P.q);
+            out[i] = mul_mont(a[i], bm, P.q, P.qneg);
+        } else if (op == 1) {
+            u64 hi, lo;
+            mul128(hi, lo, a[i], b[i]);
+            u64 t = redc(hi, lo, P.q, P.qneg);
+            out[i] = mul_shoup(t, P.rmod, P.rmod_s, P.q);
+        } else {
+            out[i] = red64(a[i], P.q, P.one_s);
+        }
+    }
+}
+
+extern "C" void ht_galois(uint32_t t, uint16_t* coef, uint16_t* perm) { galois_tables_host(NPOLY, t, coef, perm); }
+
+extern "C" void ht_slot_of(uint16_t* out) {
+    for (int i = 0; i < NPOLY; i++) out[i] = g_slot[i];
+}

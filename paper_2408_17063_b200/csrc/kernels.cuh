@@ -1,0 +1,412 @@
+// sm_100a kernels of the Comp path.  All are job-list kernels: a launch
+// carries an array of descriptors, so one launch batches every independent
+// transform / CRT / MAC of a schedule step (hcomp.cu builds the lists once
+// per plan and replays them in a CUDA graph).
+//
+//   k_xform    one 8192-point NTT or INTT per CTA (256 threads, 64 KiB smem),
+//              with a fused loader (pointwise Montgomery product, digit
+//              gather through a Galois table, ...) and a fused epilogue
+//              (plaintext-multiply combine, modulus-switch correction, ...).
+//   k_compose  exact CRT + base-2^16 digit split (optionally through the
+//              coefficient-domain Galois gather), one thread per coefficient.
+//   k_ksmac    key-switch inner product sum_j NTT(digit_j) * ksk_j with
+//              128-bit lazy accumulation and one Montgomery reduction, fused
+//              with the automorphism of c0 and the ciphertext additions.
+//   k_diagx    diagonal multiply-accumulate of the BSGS matvec (kept primes).
+//   k_plain    on-device plaintext generation (Vandermonde diagonals and
+//              masks: slot values -> INTT mod p -> NTT mod q_k -> Montgomery).
+#pragma once
+#include "elem.cuh"
+
+namespace hc {
+
+// ---------------------------------------------------------------------------
+// k_xform
+// ---------------------------------------------------------------------------
+enum : int {
+    LD_U64 = 0,    // a[j]
+    LD_MONT = 1,   // a[j] * b[j] (b in Montgomery form)
+    LD_ADD = 2,    // a[j] + b[j] mod q
+    LD_RED = 3,    // a[j] reduced from any u64 (+ b[j] likewise if b)
+    LD_DIG = 4,    // u16 digit a[j]
+    LD_DIGGAL = 5, // u16 digit gathered: gal[j] -> (neg ? b : a)[src]
+};
+enum : int {
+    EP_STORE = 0,          // out[j] = x
+    EP_ADDMONT = 1,        // out[j] = x + ea[j]*eb[j]   (eb Montgomery)
+    EP_ADD = 2,            // out[j] = x + ea[j]
+    EP_ADDRED = 3,         // out[j] = x + red(ea[j])
+    EP_RESCALE = 4,        // out[k*ostride + j] = e_k (k < level)
+    EP_RESCALE_ATOMIC = 5, // atomic += e_k
+};
+
+struct XJob {
+    int dir;    // 0 forward, 1 inverse
+    int k;      // RNS prime index of the transform
+    int ld, ep;
+    int level;  // EP_RESCALE*: level switched from (k == level)
+    int pad;
+    const u64* a;
+    const u64* b;
+    const uint16_t* gal;
+    const u64* ea;
+    const u64* eb;
+    u64* out;
+    long long ostride;
+};
+
+__global__ void __launch_bounds__(NT, 2) k_xform(const DevCtx* __restrict__ C, const XJob* __restrict__ jobs) {
+    extern __shared__ u64 sm[];
+    const XJob J = jobs[blockIdx.x];
+    const int tid = threadIdx.x;
+    const PrimeC P = C->pc[J.k];
+    u64 x[EPT];
+    switch (J.ld) {
+        case LD_U64:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) x[i] = J.a[tid + NT * i];
+            break;
+        case LD_MONT:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) x[i] = mul_mont(J.a[tid + NT * i], J.b[tid + NT * i], P.q, P.qneg);
+            break;
+        case LD_ADD:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) x[i] = add_mod(J.a[tid + NT * i], J.b[tid + NT * i], P.q);
+            break;
+        case LD_RED:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) {
+                u64 v = red64(J.a[tid + NT * i], P.q, P.one_s);
+                if (J.b) v = add_mod(v, red64(J.b[tid + NT * i], P.q, P.one_s), P.q);
+                x[i] = v;
+            }
+            break;
+        case LD_DIG: {
+            const uint16_t* d = reinterpret_cast<const uint16_t*>(J.a);
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) x[i] = d[tid + NT * i];
+            break;
+        }
+        case LD_DIGGAL: {
+            const uint16_t* dp = reinterpret_cast<const uint16_t*>(J.a);
+            const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) {
+                const unsigned e = J.gal[tid + NT * i];
+                x[i] = (e >> 15) ? dn[e & 0x7FFF] : dp[e & 0x7FFF];
+            }
+            break;
+        }
+    }
+    if (J.dir == 0) cta_ntt_fwd(x, C->twf + (size_t)J.k * NPOLY, P, sm);
+    else cta_ntt_inv(x, C->twi + (size_t)J.k * NPOLY, P, sm);
+    switch (J.ep) {
+        case EP_STORE:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) J.out[tid + NT * i] = x[i];
+            break;
+        case EP_ADDMONT:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) {
+                const int j = tid + NT * i;
+                J.out[j] = add_mod(x[i], mul_mont(J.ea[j], J.eb[j], P.q, P.qneg), P.q);
+            }
+            break;
+        case EP_ADD:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) {
+                const int j = tid + NT * i;
+                J.out[j] = add_mod(x[i], J.ea[j], P.q);
+            }
+            break;
+        case EP_ADDRED:
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) {
+                const int j = tid + NT * i;
+                J.out[j] = add_mod(x[i], red64(J.ea[j], P.q, P.one_s), P.q);
+            }
+            break;
+        case EP_RESCALE:
+        case EP_RESCALE_ATOMIC: {
+            const int l = J.level;
+            const DevCtx& D = *C;
+            HC_UNROLL
+            for (int i = 0; i < EPT; i++) {
+                const int j = tid + NT * i;
+                u64 e[MAXL];
+                rescale_corr(D, l, x[i], e);
+                HC_UNROLL
+                for (int k = 0; k < MAXL; k++) {
+                    if (k >= l) break;
+                    u64* o = J.out + (size_t)k * J.ostride + j;
+                    if (J.ep == EP_RESCALE) *o = e[k];
+                    else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)e[k]);
+                }
+            }
+            break;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_compose: grid (n/256, njobs)
+// ---------------------------------------------------------------------------
+struct CJob {
+    int level;
+    int mode;  // 0: digits of (gathered, signed) X -> dig[D][n]; 1: X and Q-X -> dig[2][D][n]
+    const u64* x;      // [P][xstride]
+    const u64* xadd;   // optional addend, same layout
+    long long xstride;
+    const uint16_t* gal;  // mode 0: optional coefficient-domain gather
+    uint16_t* dig;
+};
+
+template <int L>
+__device__ __forceinline__ void compose_one(const DevCtx* __restrict__ C, const CJob& J, int pos) {
+    const LevelC& LV = C->lv[L];
+    constexpr int P = L + 1;
+    const int D = LV.D;
+    int src = pos, neg = 0;
+    if (J.mode == 0 && J.gal) {
+        const unsigned e = J.gal[pos];
+        src = e & 0x7FFF;
+        neg = e >> 15;
+    }
+    u64 xr[P];
+    HC_UNROLL
+    for (int k = 0; k < P; k++) {
+        u64 v = J.x[(size_t)k * J.xstride + src];
+        if (J.xadd) v = add_mod(v, J.xadd[(size_t)k * J.xstride + src], C->pc[k].q);
+        xr[k] = v;
+    }
+    u64 X[NLIMB];
+    crt_compose<L>(LV, C->pc, xr, X);
+    constexpr int DMAX = 4 * (L + 1);
+    if (J.mode == 0) {
+        if (neg) neg_mod_Q<L>(LV, X);
+        HC_UNROLL
+        for (int j = 0; j < DMAX; j++)
+            if (j < D) J.dig[(size_t)j * NPOLY + pos] = digit16(X, j);
+    } else {
+        HC_UNROLL
+        for (int j = 0; j < DMAX; j++)
+            if (j < D) J.dig[(size_t)j * NPOLY + pos] = digit16(X, j);
+        neg_mod_Q<L>(LV, X);
+        HC_UNROLL
+        for (int j = 0; j < DMAX; j++)
+            if (j < D) J.dig[(size_t)(D + j) * NPOLY + pos] = digit16(X, j);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_compose(const DevCtx* __restrict__ C, const CJob* __restrict__ jobs) {
+    const CJob J = jobs[blockIdx.y];
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    switch (J.level) {
+        case 1: compose_one<1>(C, J, pos); break;
+        case 2: compose_one<2>(C, J, pos); break;
+        case 3: compose_one<3>(C, J, pos); break;
+        default: break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_ksmac: grid (n/256, P, njobs)
+//   out0 = add0 + sum_t ( c0src_t[perm_t[j]] + sum_j dntt_t[j] * b_t[j] )
+//   out1 = add1 + sum_t ( sum_j dntt_t[j] * a_t[j] )
+// dntt: [D][P][n]; key: [D_L][2][L+1][n] (Montgomery form).
+// ---------------------------------------------------------------------------
+constexpr int MAXTERM = 8;
+struct MTerm {
+    const u64* dntt;
+    const u64* key;
+    const u64* c0src;     // [P][n] NTT domain (nullable)
+    const uint16_t* perm; // NTT-domain Galois permutation for c0src
+};
+struct MJob {
+    int level, nterm;
+    MTerm t[MAXTERM];
+    const u64* add0;
+    const u64* add1;
+    u64* out0;
+    u64* out1;
+};
+
+__global__ void __launch_bounds__(256) k_ksmac(const DevCtx* __restrict__ C, const MJob* __restrict__ jobs) {
+    const MJob& J = jobs[blockIdx.z];
+    const int k = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const LevelC& LV = C->lv[J.level];
+    const int P = LV.P, D = LV.D, L1 = C->L + 1;
+    const PrimeC pc = C->pc[k];
+    const size_t kn = (size_t)k * NPOLY + j;
+    u64 o0 = J.add0 ? J.add0[kn] : 0;
+    u64 o1 = J.add1 ? J.add1[kn] : 0;
+    const int nt = J.nterm;
+    for (int t = 0; t < nt; t++) {
+        const MTerm T = J.t[t];
+        u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+        for (int d = 0; d < D; d++) {
+            const u64 v = T.dntt[((size_t)d * P + k) * NPOLY + j];
+            const u64 kb = T.key[((size_t)(d * 2 + 0) * L1 + k) * NPOLY + j];
+            const u64 ka = T.key[((size_t)(d * 2 + 1) * L1 + k) * NPOLY + j];
+            mac128(h0, l0, v, kb);
+            mac128(h1, l1, v, ka);
+        }
+        o0 = add_mod(o0, redc(h0, l0, pc.q, pc.qneg), pc.q);
+        o1 = add_mod(o1, redc(h1, l1, pc.q, pc.qneg), pc.q);
+        if (T.c0src) o0 = add_mod(o0, T.c0src[(size_t)k * NPOLY + T.perm[j]], pc.q);
+    }
+    J.out0[kn] = o0;
+    J.out1[kn] = o1;
+}
+
+// ---------------------------------------------------------------------------
+// k_diagx: grid (n/256, nprime, njobs).  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
+// (dg Montgomery with q^-1 folded in) -- the kept-prime half of each
+// plaintext product; the dropped-prime half goes through k_xform/EP_RESCALE*.
+// ---------------------------------------------------------------------------
+struct DXJob {
+    int nterm, pad;
+    const u64* const* src;  // nterm pointers, each [>=nprime][n]
+    const u64* const* dg;   // nterm pointers, each [>=nprime][n]
+    u64* X;                 // [nprime][n], canonical, updated in place
+};
+
+__global__ void __launch_bounds__(256) k_diagx(const DevCtx* __restrict__ C, const DXJob* __restrict__ jobs) {
+    const DXJob& J = jobs[blockIdx.z];
+    const int k = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const PrimeC pc = C->pc[k];
+    const size_t kn = (size_t)k * NPOLY + j;
+    u64 h = 0, l = 0;
+    for (int t = 0; t < J.nterm; t++) mac128(h, l, J.src[t][kn], J.dg[t][kn]);
+    J.X[kn] = add_mod(J.X[kn], redc(h, l, pc.q, pc.qneg), pc.q);
+}
+
+// ---------------------------------------------------------------------------
+// k_plain: on-device plaintext encoding, one CTA per plaintext.
+// Slot values (compress.py:186-195 diagonals / :242-243,351-352 masks) ->
+// slot_encode (INTT mod p, bgv.py:379-385) -> NTT mod q_k (bgv.py:452-460)
+// -> Montgomery form with the modulus-switch factor folded in:
+//   k == level (dropped prime): pt * R;  k < level: pt * q_level^-1 * R.
+// ---------------------------------------------------------------------------
+enum : int { PT_DIAG = 0, PT_TOP = 1, PT_BOT = 2, PT_OUTMASK = 3 };
+struct PJob {
+    int kind, t, g, b, level, pad;
+    u64* out;  // [level+1][n]
+};
+struct PlanShape {
+    long long N;
+    int s, s_pad, baby, m;
+};
+
+HD u64 powmod_small(u64 b, int e, u64 p, double pinv) {
+    u64 r = 1;
+    while (e) {
+        if (e & 1) r = mod_small(r * b, p, pinv);
+        b = mod_small(b * b, p, pinv);
+        e >>= 1;
+    }
+    return r;
+}
+
+HD u64 plain_slot_value(const PJob& J, const PlanShape& S, int r, int c, u64 p, double pinv) {
+    switch (J.kind) {
+        case PT_DIAG: {
+            // entry[pos=c] = M[(c - g*baby) mod s_pad][(c + b) mod m], M[row][col] = (t*m+col+1)^(row+1)
+            int row = ((c - J.g * S.baby) % S.s_pad + S.s_pad) % S.s_pad;
+            int col = (c + J.b) % S.m;
+            long long idx = (long long)J.t * S.m + col + 1;
+            if (row >= S.s || idx > S.N) return 0;
+            return powmod_small((u64)(idx % (long long)p), row + 1, p, pinv);
+        }
+        case PT_TOP: return r == 0 ? 1 : 0;
+        case PT_BOT: return r == 1 ? 1 : 0;
+        default: return c < S.s ? 1 : 0;  // PT_OUTMASK
+    }
+}
+
+__global__ void __launch_bounds__(NT) k_plain(const DevCtx* __restrict__ C, const PJob* __restrict__ jobs, PlanShape S) {
+    extern __shared__ u64 sm[];
+    u64* coef = sm + NPOLY;
+    const PJob J = jobs[blockIdx.x];
+    const int tid = threadIdx.x;
+    u64 x[EPT];
+    HC_UNROLL
+    for (int i = 0; i < EPT; i++) {
+        const unsigned so = C->slot_of[tid + NT * i];
+        x[i] = plain_slot_value(J, S, so >> 12, so & 4095, C->p, C->pinv);
+    }
+    cta_ntt_inv(x, C->twi + (size_t)PIDX * NPOLY, C->pc[PIDX], sm);
+    HC_UNROLL
+    for (int i = 0; i < EPT; i++) coef[tid + NT * i] = x[i];
+    const LevelC& LV = C->lv[J.level];
+    for (int k = 0; k <= J.level; k++) {
+        const PrimeC P = C->pc[k];
+        HC_UNROLL
+        for (int i = 0; i < EPT; i++) x[i] = coef[tid + NT * i];
+        cta_ntt_fwd(x, C->twf + (size_t)k * NPOLY, P, sm);
+        const u64 w = (k == J.level) ? P.rmod : LV.qinv_r[k];
+        const u64 ws = (k == J.level) ? P.rmod_s : LV.qinv_rs[k];
+        HC_UNROLL
+        for (int i = 0; i < EPT; i++) J.out[(size_t)k * NPOLY + tid + NT * i] = mul_shoup(x[i], w, ws, P.q);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// small utility kernels
+// ---------------------------------------------------------------------------
+
+// in-place x -> x*R mod q (Montgomery form); prime of row r = r % period
+__global__ void k_to_mont(const DevCtx* __restrict__ C, u64* data, long long rows, int period) {
+    const long long total = rows * NPOLY;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)((i / NPOLY) % period);
+        const PrimeC P = C->pc[k];
+        data[i] = mul_shoup(data[i], P.rmod, P.rmod_s, P.q);
+    }
+}
+
+// out[r][j] = sum_c red(in[c][r][j]) mod q_{r % period}
+__global__ void k_sum_copies(const DevCtx* __restrict__ C, const u64* in, u64* out, long long rows,
+                             int period, int copies, long long cstride) {
+    const long long total = rows * NPOLY;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)((i / NPOLY) % period);
+        const PrimeC P = C->pc[k];
+        u64 s = 0;
+        for (int c = 0; c < copies; c++) s = add_mod(s, red64(in[c * cstride + i], P.q, P.one_s), P.q);
+        out[i] = s;
+    }
+}
+
+// pointwise op over rows; prime of row r = pidx[r]
+__global__ void k_pointwise(const DevCtx* __restrict__ C, const u64* a, const u64* b, u64* out, int rows,
+                            const int* pidx, int op) {
+    const long long total = (long long)rows * NPOLY;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const PrimeC P = C->pc[pidx[i / NPOLY]];
+        const u64 x = a[i], y = b[i];
+        u64 r;
+        if (op == 0) {
+            u64 hi, lo;
+            mul128(hi, lo, x, y);
+            // x*y mod q via Montgomery twice: redc(x*y) = x*y*R^-1; then * R^2 ... use
+            // x*y*R^-1 then multiply by R^2 mod q = (R mod q)^2 through two Shoup steps
+            u64 t = redc(hi, lo, P.q, P.qneg);             // x*y*R^-1
+            t = mul_shoup(t, P.rmod, P.rmod_s, P.q);        // x*y
+            r = t;
+        } else if (op == 1) {
+            r = add_mod(x, y, P.q);
+        } else {
+            r = sub_mod(x, y, P.q);
+        }
+        out[i] = r;
+    }
+}
+
+}  // namespace hc

@@ -1,0 +1,170 @@
+"""CPU check of the exact device code: the CUDA headers' arithmetic, the
+256-thread NTT schedule (emulated thread by thread, same passes/swizzles as
+on the GPU), the CRT/digit split and the modulus-switch correction are
+compiled for the host (paper_2408_17063_b200/csrc/hosttest.cpp) and compared
+bit-for-bit with the oracle."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2408_17063_b200 import build as hbuild
+
+N8K = 8192
+
+
+@pytest.fixture(scope="module")
+def ht():
+    path = hbuild.build_selftest()
+    L = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    L.ht_init.argtypes = [P, ctypes.c_int, ctypes.c_uint64]
+    L.ht_ntt.argtypes = [ctypes.c_int, P, ctypes.c_int]
+    L.ht_compose.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P]
+    L.ht_rescale_corr.argtypes = [ctypes.c_int, P, P]
+    L.ht_modops.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
+    L.ht_galois.argtypes = [ctypes.c_uint32, P, P]
+    L.ht_slot_of.argtypes = [P]
+    L.ht_digits.argtypes = [ctypes.c_int]
+    return L
+
+
+def p_(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+@pytest.fixture(scope="module", params=[65537, 786433])
+def setup(request, ht, oracle):
+    p = request.param
+    be = oracle.OracleBgv(N8K, p, 3, seed=0)
+    primes = np.asarray(be.q, dtype=np.uint64)
+    ht.ht_init(p_(primes), 3, p)
+    return ht, be, p
+
+
+def rand_res(rng, q, n=N8K):
+    return np.array([rng.randrange(q) for _ in range(n)], dtype=np.uint64)
+
+
+def test_ntt_schedule_matches_reference_transform(setup):
+    ht, be, p = setup
+    import random
+
+    rng = random.Random(5)
+    for k, q in enumerate(be.q + [p]):
+        a = rand_res(rng, q)
+        want_f = (be.ntt if k < 4 else be.ntt_p).fwd(a[None, :], [k if k < 4 else 0])[0]
+        want_i = (be.ntt if k < 4 else be.ntt_p).inv(a[None, :], [k if k < 4 else 0])[0]
+        got = a.copy()
+        ht.ht_ntt(k, p_(got), 0)
+        assert np.array_equal(got, want_f), f"forward NTT mismatch for prime {k}"
+        got = a.copy()
+        ht.ht_ntt(k, p_(got), 1)
+        assert np.array_equal(got, want_i), f"inverse NTT mismatch for prime {k}"
+    # lazy-range inputs up to 4q (forward) are accepted
+    q = be.q[0]
+    a = rand_res(rng, q)
+    lazy = a + np.uint64(3 * q) * (np.arange(N8K) % 2 == 0).astype(np.uint64)
+    ht.ht_ntt(0, p_(lazy), 0)
+    assert np.array_equal(lazy, be.ntt.fwd(a[None, :], [0])[0])
+
+
+def test_crt_digits_match_reference_digit_split(setup, oracle):
+    ht, be, p = setup
+    import random
+
+    rng = random.Random(7)
+    for level in (1, 2, 3):
+        P = level + 1
+        x = np.stack([rand_res(rng, q) for q in be.q[:P]])
+        # edge values: 0, Q-1, and q_k-1 everywhere
+        x[:, 0] = 0
+        for k in range(P):
+            x[k, 1] = be.q[k] - 1
+        D = be.digits[level]
+        assert ht.ht_digits(level) == D
+        want = np.empty((D, N8K), dtype=np.uint64)
+        qv = np.asarray(be.q[:P], dtype=np.uint64)
+        oracle.lib().orc_digits(p_(np.ascontiguousarray(x)), p_(want), P, N8K, p_(qv), D, 16)
+        got = np.empty((2 * D, N8K), dtype=np.uint16)
+        assert ht.ht_compose(level, p_(np.ascontiguousarray(x)), None, 1, p_(got)) == 0
+        assert np.array_equal(got[:D].astype(np.uint64), want)
+        # negated image digits = digits of (Q - X) (0 stays 0)
+        Q = be.moduli[level]
+        ints = be.compose(x, level)
+        neg = [(Q - v) % Q for v in ints]
+        want_neg = np.array([[(v >> (16 * j)) & 0xFFFF for v in neg] for j in range(D)], dtype=np.uint16)
+        assert np.array_equal(got[D:], want_neg)
+
+
+def test_rescale_correction_equals_mod_switch(setup, oracle):
+    """out_k = x_k * q^-1 + e_k (coefficient domain) must equal the
+    reference's modulus switch evaluated on the composed integer."""
+    ht, be, p = setup
+    import random
+
+    rng = random.Random(9)
+    for level in (1, 2, 3):
+        P = level + 1
+        x = np.stack([rand_res(rng, q) for q in be.q[:P]])
+        x[:, :4] = 0
+        x[level, 1] = be.q[level] >> 1          # r = +floor(q/2)
+        x[level, 2] = (be.q[level] >> 1) + 1    # r = -floor(q/2)
+        want = np.empty((level, N8K), dtype=np.uint64)
+        qv = np.asarray(be.q[:P], dtype=np.uint64)
+        oracle.lib().orc_rescale(p_(np.ascontiguousarray(x)), p_(want), P, N8K, p_(qv), p)
+        e = np.empty((level, N8K), dtype=np.uint64)
+        ht.ht_rescale_corr(level, p_(np.ascontiguousarray(x[level])), p_(e))
+        qd = be.q[level]
+        for k in range(level):
+            q = be.q[k]
+            qinv = pow(qd, -1, q)
+            got = [(int(a) * qinv + int(b)) % q for a, b in zip(x[k], e[k])]
+            assert np.array_equal(np.array(got, dtype=np.uint64), want[k]), f"level {level} prime {k}"
+
+
+def test_modular_helpers(setup):
+    ht, be, p = setup
+    import random
+
+    rng = random.Random(11)
+    for k, q in enumerate(be.q):
+        a = np.array([rng.randrange(q) for _ in range(2000)] + [0, q - 1], dtype=np.uint64)
+        b = np.array([rng.randrange(q) for _ in range(2000)] + [q - 1, q - 1], dtype=np.uint64)
+        want = np.array([int(x) * int(y) % q for x, y in zip(a, b)], dtype=np.uint64)
+        for op in (0, 1):
+            out = np.empty_like(a)
+            ht.ht_modops(k, op, p_(a), p_(b), p_(out), a.size)
+            assert np.array_equal(out, want)
+        big = np.array([rng.getrandbits(64) for _ in range(2000)] + [2**64 - 1, 0], dtype=np.uint64)
+        out = np.empty_like(big)
+        ht.ht_modops(k, 2, p_(big), p_(big), p_(out), big.size)
+        assert np.array_equal(out, np.array([int(v) % q for v in big], dtype=np.uint64))
+
+
+def test_galois_tables_match_reference_maps(setup):
+    """NTT-domain permutation == galois_permutation (bgv.py:258-261, via the
+    oracle's calibrated eval exponents); coefficient gather == coeff_automorphism."""
+    ht, be, p = setup
+    n = N8K
+    for t in (3, pow(3, 5, 2 * n), pow(3, 1024, 2 * n), 2 * n - 1):
+        coef = np.empty(n, dtype=np.uint16)
+        perm = np.empty(n, dtype=np.uint16)
+        ht.ht_galois(t, p_(coef), p_(perm))
+        assert np.array_equal(perm.astype(np.int64), be.galois_perm(t))
+        c = np.arange(1, n + 1, dtype=np.int64)
+        want = np.asarray(be.coeff_automorphism(list(c), t))
+        src = coef & 0x7FFF
+        sign = np.where(coef >> 15, -1, 1)
+        assert np.array_equal(sign * c[src], want)
+
+
+def test_slot_map_matches_reference(setup):
+    ht, be, p = setup
+    slot_of = np.empty(N8K, dtype=np.uint16)
+    ht.ht_slot_of(p_(slot_of))
+    for r in range(2):
+        for c in range(0, N8K // 2, 97):
+            i = be.slot_index[r][c]
+            assert slot_of[i] == (r << 12 | c)

@@ -1,0 +1,225 @@
+"""GPU parity: the CUDA path (libhcomp via the package API) against the
+oracle and the reference's golden vectors.  Bit-exact everywhere (integer
+work).  Run on a B200 with `pytest -m gpu`."""
+
+import random
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+N8K = 8192
+
+
+def _need_gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA GPU required for -m gpu tests")
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    _need_gpu()
+    import paper_2408_17063_b200 as P
+    from paper_2408_17063_b200 import build
+
+    build.build_lib()
+    return P
+
+
+def make_case(P, O, n, p, N, s, seed, guard=True):
+    """Product backend and oracle backend with the same seed/keys/inputs."""
+    he = P.HeParams(n, p, 3)
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed, noise_guard=guard)
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    rng = random.Random(seed)
+    dense = O.plant_sparse(rng, N, s, p)
+    cts = P.encrypt_vector(dense, params, be, keys)
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    return be, params, keys, dense, cts, hint
+
+
+@pytest.fixture(scope="module")
+def c1(pkg, oracle):
+    P, O = pkg, oracle
+    be, params, keys, dense, cts, hint = make_case(P, O, N8K, 65537, 8192, 8, 0)
+    obe = O.OracleBgv(N8K, 65537, 3, seed=0)
+    okeys = obe.keygen(*O.plan_rotation_amounts(8, N8K))
+    octs = O.encrypt_vector(dense, 8192, obe, okeys)
+    ohint = O.encrypt_vector([1 if x else 0 for x in dense], 8192, obe, okeys)
+    return dict(be=be, params=params, keys=keys, dense=dense, cts=cts, hint=hint,
+                obe=obe, okeys=okeys, octs=octs, ohint=ohint)
+
+
+def test_ring_transforms(pkg, oracle):
+    P, O = pkg, oracle
+    be = P.B200BgvBackend(P.HeParams(N8K, 65537, 3), seed=1)
+    obe = O.OracleBgv(N8K, 65537, 3, seed=1)
+    rng = np.random.default_rng(3)
+    a = np.stack([rng.integers(0, q, N8K, dtype=np.uint64) for q in be.q])
+    assert np.array_equal(be.ntt(a, 3), obe.fwd(a, 3))
+    assert np.array_equal(be.ntt(a, 3, inverse=True), obe.inv(a, 3))
+    b = np.stack([rng.integers(0, q, N8K, dtype=np.uint64) for q in be.q])
+    for op in ("mul", "add", "sub"):
+        assert np.array_equal(be.pointwise(a, b, 3, op), obe.pointwise(a, b, 3, op))
+    ev = rng.integers(0, 65537, N8K, dtype=np.uint64)
+    assert np.array_equal(be.ntt_p(ev, inverse=True), obe.ntt_p.inv(ev[None], [0])[0])
+
+
+def test_keygen_and_encrypt_bit_exact(c1):
+    keys, okeys = c1["keys"], c1["okeys"]
+    assert keys.key_id == okeys.key_id
+    assert keys.secret == okeys.secret
+    assert np.array_equal(keys.public.pk_b, okeys.pk_b)
+    assert np.array_equal(keys.public.pk_a, okeys.pk_a)
+    assert np.array_equal(keys.relin_key, okeys.relin)
+    assert sorted(keys.rotation_keys) == sorted(okeys.rotation_keys)
+    for r in keys.rotation_keys:
+        assert keys.rotation_keys[r][0] == okeys.rotation_keys[r][0]
+        assert np.array_equal(keys.rotation_keys[r][1], okeys.rotation_keys[r][1])
+    assert np.array_equal(keys.col_swap_key[1], okeys.col_swap_key[1])
+    for c, oc in zip(c1["cts"] + c1["hint"], c1["octs"] + c1["ohint"]):
+        assert np.array_equal(c.payload.res, oc.c)
+        assert c.payload.noise_bits == oc.noise_bits
+
+
+def test_single_ops_match_oracle(c1):
+    be, keys, obe, okeys = c1["be"], c1["keys"], c1["obe"], c1["okeys"]
+    P_rng = np.random.default_rng(5)
+    rows = P_rng.integers(0, 65537, (2, N8K // 2)).astype(np.int64)
+    from paper_2408_17063_b200 import SlotMatrix
+
+    m = SlotMatrix(65537, rows)
+    ct, oct_ = c1["cts"][0], c1["octs"][0]
+    # mul_plain down the chain 3 -> 2 -> 1 -> 0
+    cur, ocur = ct, oct_
+    for _ in range(3):
+        cur = be.mul_plain(cur, m)
+        ocur = obe.mul_plain(ocur, rows)
+        assert cur.level == ocur.level
+        assert np.array_equal(cur.payload.res, ocur.c)
+        assert cur.payload.noise_bits == ocur.noise_bits
+    # rotations at levels 3, 2 and 1
+    cur, ocur = ct, oct_
+    for lvl in (3, 2, 1):
+        for r in (1, 8):
+            a = be.rot_row(cur, r, keys)
+            b = obe.rot_row(ocur, r, okeys)
+            assert np.array_equal(a.payload.res, b.c), f"rot_row {r} at level {lvl}"
+        a = be.rot_col(cur, keys)
+        b = obe.rot_col(ocur, okeys)
+        assert np.array_equal(a.payload.res, b.c), f"rot_col at level {lvl}"
+        cur = be.mul_plain(cur, m)
+        ocur = obe.mul_plain(ocur, rows)
+    # add
+    a = be.add(ct, c1["cts"][0])
+    b = obe.add(oct_, c1["octs"][0])
+    assert np.array_equal(a.payload.res, b.c)
+
+
+def test_decrypt_roundtrip(c1):
+    be, keys = c1["be"], c1["keys"]
+    m = be.decrypt(c1["cts"][0], keys)
+    dense = c1["dense"]
+    assert [int(x) for x in m.rows[0]] == dense[:4096]
+    assert [int(x) for x in m.rows[1]] == dense[4096:8192]
+
+
+GOLDEN_8K = [g for g in golden_names() if not g.startswith("small_")]
+
+
+@pytest.mark.parametrize("name", GOLDEN_8K)
+def test_comp_matches_reference_golden(pkg, oracle, name):
+    P, O = pkg, oracle
+    g = load_golden(name)
+    be, params, keys, dense, cts, hint = make_case(
+        P, O, g["n"], g["p"], g["N"], g["s"], g["seed"], guard=not g["noise_guard_disabled"]
+    )
+    assert keys.key_id.hex() == g["key_id"]
+    before = be.counters.snapshot()
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    delta = be.counters.delta(before)
+    out = ans.cts[0]
+    assert out.level == 0
+    blob = ans.serialize(be)
+    assert len(blob) == g["answer_len"]
+    assert O.sha256(blob) == g["answer_sha256"], "Comp output differs from the reference"
+    assert out.payload.noise_bits == g["noise_bits"]
+    assert delta.as_dict() == g["counters"]
+    w, e = ans.payload_slots(be, keys)
+    assert (w, e) == (g["w"], g["e"])
+
+
+def test_comp_p786433_N2_17_vs_oracle(pkg, oracle):
+    """Config-3 endpoint N = 2^17 (p = 786433), guard disabled (F5):
+    bit-exact against the oracle and decrypts to the power sums."""
+    P, O = pkg, oracle
+    N, s, p, seed = 1 << 17, 16, 786433, 4
+    be, params, keys, dense, cts, hint = make_case(P, O, N8K, p, N, s, seed, guard=False)
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    obe = O.OracleBgv(N8K, p, 3, seed=seed, check_noise=False)
+    okeys = obe.keygen(*O.plan_rotation_amounts(s, N8K))
+    ocv = O.encrypt_vector(dense, N, obe, okeys)
+    ohint = O.encrypt_vector([1 if x else 0 for x in dense], N, obe, okeys)
+    oout = O.comp(ocv, N, s, obe, okeys, ohint)
+    assert np.array_equal(ans.cts[0].payload.res, oout.c)
+    w, e = ans.payload_slots(be, keys)
+    assert (w, e) == O.expected_slots(dense, s, p)
+
+
+def test_comp_noise_guard_raises_like_reference(pkg, oracle):
+    """(2^14, 32) overflows the reference's heuristic guard."""
+    P, O = pkg, oracle
+    be, params, keys, dense, cts, hint = make_case(P, O, N8K, 65537, 1 << 14, 32, 0, guard=True)
+    with pytest.raises(P.NoiseOverflow):
+        P.comp(cts, params, be, keys, index_hint=hint)
+
+
+def test_device_comp_idempotent_and_sharded_sum(c1, pkg):
+    """Repeated graph launches give identical output; partial(blocks 0..1) +
+    partial(1..2) summed as uint64 then finish == the single-pass Comp."""
+    import ctypes
+
+    import torch
+
+    from paper_2408_17063_b200 import _lib
+
+    P = pkg
+    be, params, keys = c1["be"], c1["params"], c1["keys"]
+    dc = P.DeviceComp(be, params, keys)
+    cd = np.stack([c.payload.res for c in c1["cts"]])
+    cv = np.stack([c.payload.res for c in c1["hint"]])
+    dc.set_inputs(cd, cv)
+    dc.launch()
+    o1 = dc.output()
+    dc.launch()
+    dc.launch()
+    o2 = dc.output()
+    assert np.array_equal(o1, o2)
+    assert np.array_equal(o1, dc.run_host(cd, cv))
+    L = _lib.lib()
+    h = be._ctx()
+    words = L.hc_partial_words(h)
+    B = params.num_blocks
+    parts = []
+    for b0, b1 in ((0, 1), (1, B)):
+        t = torch.zeros(words, dtype=torch.int64, device="cuda")
+        _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(t.data_ptr()), None))
+        torch.cuda.synchronize()
+        parts.append(t)
+    total = parts[0] + parts[1]
+    _lib.check(L.hc_comp_finish(h, ctypes.c_void_p(total.data_ptr()), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(dc.output(), o1)
+
+
+def test_missing_rotation_key_raises(c1, pkg):
+    P = pkg
+    be, keys = c1["be"], c1["keys"]
+    with pytest.raises(P.MissingRotationKey):
+        be.rot_row(c1["cts"][0], 5, keys)
