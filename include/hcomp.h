@@ -117,6 +117,12 @@ int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int*
 /* Measured butterfly-throughput ceiling of this GPU for the NTT butterfly
  * used by the transform kernel (register-only microbenchmark). */
 int hc_bf_peak(hc_ctx* h, double* bfly_per_s);
+/* Transform microbenchmark: njobs plain NTTs (dir 0) or INTTs (dir 1) per
+ * launch, iters back-to-back launches; writes microseconds per launch. */
+int hc_bench_xform(hc_ctx* h, int njobs, int dir, int iters, double* us_per_launch);
+/* Transform launches with <= max_jobs jobs use the 8-CTA cluster kernel
+ * (latency path); larger launches use one CTA per transform.  Default 16. */
+int hc_set_cluster_threshold(int max_jobs);
 
 /* Pure host helpers (no GPU needed): Galois tables for element t.
  * coef: uint16[n] (source index | negate << 15) realising X -> X^t on

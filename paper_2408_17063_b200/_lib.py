@@ -62,6 +62,8 @@ _SIGS = [
     ("hc_rotate", _I, [_P, _P, _I, _U32, _P]),
     ("hc_comp_profile", _I, [_P, _P, _I, _P, _P, _P]),
     ("hc_bf_peak", _I, [_P, ctypes.POINTER(ctypes.c_double)]),
+    ("hc_bench_xform", _I, [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_double)]),
+    ("hc_set_cluster_threshold", _I, [_I]),
     ("hc_galois_tables", _I, [_I, _U32, _P, _P]),
     ("hc_prim_root_2n", _U64, [_U64, _I]),
 ]

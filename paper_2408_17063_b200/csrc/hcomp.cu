@@ -57,6 +57,9 @@ struct DevKey {
     uint16_t* perm = nullptr;  // NTT-domain permutation
 };
 
+// transform launches with at most this many jobs use the cluster kernel
+static int CL_MAX_JOBS = 16;
+
 enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET };
 struct Step {
     int kind = 0;
@@ -107,7 +110,8 @@ static void release_key(DevKey& k) {
 static int kernels_configured = 0;
 static int configure_kernels() {
     if (kernels_configured) return HC_OK;
-    CU(cudaFuncSetAttribute(k_xform, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));
+    CU(cudaFuncSetAttribute(k_xform<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));
+    CU(cudaFuncSetAttribute(k_xform<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));
     CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
     kernels_configured = 1;
     return HC_OK;
@@ -211,14 +215,21 @@ static int upload_jobs(Schedule& S, Step& st, const void* host, size_t bytes) {
     return HC_OK;
 }
 
+// one step per transform direction (k_xform<0> / k_xform<1>)
 static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
-    if (jobs.empty()) return HC_OK;
-    Step st;
-    st.kind = ST_XF;
-    st.njobs = (int)jobs.size();
-    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(XJob));
-    if (rc) return rc;
-    S.steps.push_back(st);
+    for (int dir = 0; dir < 2; dir++) {
+        std::vector<XJob> sel;
+        for (const XJob& j : jobs)
+            if (j.dir == dir) sel.push_back(j);
+        if (sel.empty()) continue;
+        Step st;
+        st.kind = ST_XF;
+        st.gy = dir;
+        st.njobs = (int)sel.size();
+        int rc = upload_jobs(S, st, sel.data(), sel.size() * sizeof(XJob));
+        if (rc) return rc;
+        S.steps.push_back(st);
+    }
     return HC_OK;
 }
 static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
@@ -265,7 +276,13 @@ static int enqueue(const hc_ctx* h, const Schedule& S, cudaStream_t s) {
     for (const Step& st : S.steps) {
         switch (st.kind) {
             case ST_XF:
-                k_xform<<<st.njobs, NT, NPOLY * 8, s>>>(h->d_ctx, (const XJob*)st.djobs);
+                if (st.njobs <= CL_MAX_JOBS) {  // latency path: one 8-CTA cluster per transform
+                    if (st.gy == 0) k_xform_cl<0><<<st.njobs * CL, CNT, 0, s>>>(h->d_ctx, (const XJob*)st.djobs);
+                    else k_xform_cl<1><<<st.njobs * CL, CNT, 0, s>>>(h->d_ctx, (const XJob*)st.djobs);
+                } else {
+                    if (st.gy == 0) k_xform<0><<<st.njobs, NT, NPOLY * 8, s>>>(h->d_ctx, (const XJob*)st.djobs);
+                    else k_xform<1><<<st.njobs, NT, NPOLY * 8, s>>>(h->d_ctx, (const XJob*)st.djobs);
+                }
                 break;
             case ST_CO:
                 k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->d_ctx, (const CJob*)st.djobs);
@@ -1278,6 +1295,52 @@ extern "C" int hc_bf_peak(hc_ctx* h, double* bfly_per_s) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     *bfly_per_s = (double)blocks * 256 * iters * 16 / (ms * 1e-3);
+    return HC_OK;
+}
+
+// Transform microbenchmark: `njobs` independent plain transforms (LD_U64 /
+// EP_STORE) per launch, `iters` back-to-back launches; returns us/launch.
+extern "C" int hc_set_cluster_threshold(int max_jobs) {
+    CL_MAX_JOBS = max_jobs;
+    return HC_OK;
+}
+
+extern "C" int hc_bench_xform(hc_ctx* h, int njobs, int dir, int iters, double* us_per_launch) {
+    if (!h || njobs < 1 || iters < 1) return fail(HC_ERR_ARG, "bad arguments");
+    CU(cudaSetDevice(h->dev));
+    DevBuf buf;
+    CU(cudaMalloc(&buf.p, (size_t)njobs * NPOLY * 8));
+    CU(cudaMemset(buf.p, 0, (size_t)njobs * NPOLY * 8));
+    std::vector<XJob> jobs;
+    for (int i = 0; i < njobs; i++) {
+        XJob j{};
+        j.dir = dir; j.k = i % (h->L + 1); j.ld = LD_U64; j.ep = EP_STORE;
+        j.a = (u64*)buf.p + (size_t)i * NPOLY;
+        j.out = (u64*)buf.p + (size_t)i * NPOLY;
+        jobs.push_back(j);
+    }
+    Schedule S;
+    int rc = add_xf(S, jobs);
+    if (rc) return rc;
+    for (int w = 0; w < 3; w++) {
+        rc = enqueue(h, S, h->stream);
+        if (rc) return rc;
+    }
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    CU(cudaEventRecord(a, h->stream));
+    for (int i = 0; i < iters; i++) {
+        rc = enqueue(h, S, h->stream);
+        if (rc) return rc;
+    }
+    CU(cudaEventRecord(b, h->stream));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *us_per_launch = 1e3 * ms / iters;
     return HC_OK;
 }
 

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "elem.cuh"
+#include "ntt_cl.cuh"
 #include "host_tables.hpp"
 
 using namespace hc;
@@ -30,6 +31,11 @@ extern "C" int ht_digits(int level) { return g_digits[level]; }
 extern "C" void ht_ntt(int k, uint64_t* a, int inverse) {
     if (inverse) host_emulate_inv(a, g_ctx.twi + (size_t)k * NPOLY, g_ctx.pc[k]);
     else host_emulate_fwd(a, g_ctx.twf + (size_t)k * NPOLY, g_ctx.pc[k]);
+}
+
+extern "C" void ht_ntt_cl(int k, uint64_t* a, int inverse) {
+    if (inverse) host_emulate_cl_inv(a, g_ctx.twi + (size_t)k * NPOLY, g_ctx.pc[k]);
+    else host_emulate_cl_fwd(a, g_ctx.twf + (size_t)k * NPOLY, g_ctx.pc[k]);
 }
 
 template <int L>

@@ -16,7 +16,10 @@
 //   k_plain    on-device plaintext generation (Vandermonde diagonals and
 //              masks: slot values -> INTT mod p -> NTT mod q_k -> Montgomery).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "elem.cuh"
+#include "ntt_cl.cuh"
 
 namespace hc {
 
@@ -55,97 +58,274 @@ struct XJob {
     long long ostride;
 };
 
-__global__ void __launch_bounds__(NT, 2) k_xform(const DevCtx* __restrict__ C, const XJob* __restrict__ jobs) {
-    extern __shared__ u64 sm[];
-    const XJob J = jobs[blockIdx.x];
-    const int tid = threadIdx.x;
-    const PrimeC P = C->pc[J.k];
-    u64 x[EPT];
+// Loader: fill the smem tile (coefficient j at sm[swz(j)], thread t owns
+// j = t + 512 v).  Global loads are issued 16-wide per thread before any use
+// (latency overlap); each loader kind is its own unrolled loop.
+__device__ __forceinline__ void xf_load(const XJob& J, const PrimeC& P, u64* sm, int tid) {
+    u64 a[EPT];
     switch (J.ld) {
-        case LD_U64:
+        case LD_MONT: {
+            u64 b[EPT];
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) x[i] = J.a[tid + NT * i];
+            for (int v = 0; v < EPT; v++) { a[v] = J.a[tid + NT * v]; b[v] = J.b[tid + NT * v]; }
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) a[v] = mul_mont(a[v], b[v], P.q, P.qneg);
             break;
-        case LD_MONT:
+        }
+        case LD_ADD: {
+            u64 b[EPT];
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) x[i] = mul_mont(J.a[tid + NT * i], J.b[tid + NT * i], P.q, P.qneg);
+            for (int v = 0; v < EPT; v++) { a[v] = J.a[tid + NT * v]; b[v] = J.b[tid + NT * v]; }
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) a[v] = add_mod(a[v], b[v], P.q);
             break;
-        case LD_ADD:
+        }
+        case LD_RED: {
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) x[i] = add_mod(J.a[tid + NT * i], J.b[tid + NT * i], P.q);
-            break;
-        case LD_RED:
+            for (int v = 0; v < EPT; v++) a[v] = J.a[tid + NT * v];
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) {
-                u64 v = red64(J.a[tid + NT * i], P.q, P.one_s);
-                if (J.b) v = add_mod(v, red64(J.b[tid + NT * i], P.q, P.one_s), P.q);
-                x[i] = v;
+            for (int v = 0; v < EPT; v++) a[v] = red64(a[v], P.q, P.one_s);
+            if (J.b) {
+                u64 b[EPT];
+                HC_UNROLL
+                for (int v = 0; v < EPT; v++) b[v] = J.b[tid + NT * v];
+                HC_UNROLL
+                for (int v = 0; v < EPT; v++) a[v] = add_mod(a[v], red64(b[v], P.q, P.one_s), P.q);
             }
             break;
+        }
         case LD_DIG: {
             const uint16_t* d = reinterpret_cast<const uint16_t*>(J.a);
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) x[i] = d[tid + NT * i];
+            for (int v = 0; v < EPT; v++) a[v] = d[tid + NT * v];
             break;
         }
         case LD_DIGGAL: {
+            unsigned e[EPT];
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) e[v] = J.gal[tid + NT * v];
             const uint16_t* dp = reinterpret_cast<const uint16_t*>(J.a);
             const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) {
-                const unsigned e = J.gal[tid + NT * i];
-                x[i] = (e >> 15) ? dn[e & 0x7FFF] : dp[e & 0x7FFF];
-            }
+            for (int v = 0; v < EPT; v++) a[v] = ((e[v] >> 15) ? dn : dp)[e[v] & 0x7FFF];
             break;
         }
+        default:  // LD_U64
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) a[v] = J.a[tid + NT * v];
     }
-    if (J.dir == 0) cta_ntt_fwd(x, C->twf + (size_t)J.k * NPOLY, P, sm);
-    else cta_ntt_inv(x, C->twi + (size_t)J.k * NPOLY, P, sm);
+    sm_store(a, sm, tid, NT);
+}
+
+// Epilogue: consume the canonical transform output (smem tile).
+__device__ __forceinline__ void xf_store(const XJob& J, const DevCtx& D, const PrimeC& P, const u64* sm, int tid) {
+    u64 x[EPT];
+    sm_load(x, sm, tid, NT);
     switch (J.ep) {
-        case EP_STORE:
+        case EP_ADDMONT: {
+            u64 a[EPT], b[EPT];
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) J.out[tid + NT * i] = x[i];
-            break;
-        case EP_ADDMONT:
+            for (int v = 0; v < EPT; v++) { a[v] = J.ea[tid + NT * v]; b[v] = J.eb[tid + NT * v]; }
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) {
-                const int j = tid + NT * i;
-                J.out[j] = add_mod(x[i], mul_mont(J.ea[j], J.eb[j], P.q, P.qneg), P.q);
-            }
+            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = add_mod(x[v], mul_mont(a[v], b[v], P.q, P.qneg), P.q);
             break;
-        case EP_ADD:
+        }
+        case EP_ADD: {
+            u64 a[EPT];
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) {
-                const int j = tid + NT * i;
-                J.out[j] = add_mod(x[i], J.ea[j], P.q);
-            }
-            break;
-        case EP_ADDRED:
+            for (int v = 0; v < EPT; v++) a[v] = J.ea[tid + NT * v];
             HC_UNROLL
-            for (int i = 0; i < EPT; i++) {
-                const int j = tid + NT * i;
-                J.out[j] = add_mod(x[i], red64(J.ea[j], P.q, P.one_s), P.q);
-            }
+            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = add_mod(x[v], a[v], P.q);
             break;
+        }
+        case EP_ADDRED: {
+            u64 a[EPT];
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) a[v] = J.ea[tid + NT * v];
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = add_mod(x[v], red64(a[v], P.q, P.one_s), P.q);
+            break;
+        }
         case EP_RESCALE:
         case EP_RESCALE_ATOMIC: {
             const int l = J.level;
-            const DevCtx& D = *C;
-            HC_UNROLL
-            for (int i = 0; i < EPT; i++) {
-                const int j = tid + NT * i;
+            const bool atom = J.ep == EP_RESCALE_ATOMIC;
+            HC_NOUNROLL
+            for (int v = 0; v < EPT; v++) {
+                u64 xv = sm[swz(tid + NT * v)];
                 u64 e[MAXL];
-                rescale_corr(D, l, x[i], e);
+                rescale_corr(D, l, xv, e);
                 HC_UNROLL
                 for (int k = 0; k < MAXL; k++) {
                     if (k >= l) break;
-                    u64* o = J.out + (size_t)k * J.ostride + j;
-                    if (J.ep == EP_RESCALE) *o = e[k];
+                    u64* o = J.out + (size_t)k * J.ostride + tid + NT * v;
+                    if (!atom) *o = e[k];
                     else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)e[k]);
                 }
             }
             break;
         }
+        default:  // EP_STORE
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = x[v];
+    }
+}
+
+// One transform job per CTA: loader -> smem tile -> NTT/INTT -> epilogue.
+// DIR 0 = forward, 1 = inverse (J.dir must match).
+template <int DIR>
+__global__ void __launch_bounds__(NT, 1) k_xform(const DevCtx* __restrict__ C, const XJob* __restrict__ jobs) {
+    extern __shared__ u64 sm[];
+    const XJob J = jobs[blockIdx.x];
+    const int tid = threadIdx.x;
+    const PrimeC P = C->pc[J.k];
+    xf_load(J, P, sm, tid);
+    __syncthreads();
+    if (DIR == 0) cta_ntt_fwd(C->twf + (size_t)J.k * NPOLY, P, sm);
+    else cta_ntt_inv(C->twi + (size_t)J.k * NPOLY, P, sm);
+    xf_store(J, *C, P, sm, tid);
+}
+
+// ---------------------------------------------------------------------------
+// k_xform_cl: the same jobs on the latency path, one job per 8-CTA cluster
+// (ntt_cl.cuh).  Loads/stores go through per-coefficient loader/epilogue
+// helpers (8 independent accesses per thread, unrolled).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u64 ld_elem(const XJob& J, const PrimeC& P, int j) {
+    switch (J.ld) {
+        case LD_MONT: return mul_mont(J.a[j], J.b[j], P.q, P.qneg);
+        case LD_ADD: return add_mod(J.a[j], J.b[j], P.q);
+        case LD_RED: {
+            u64 v = red64(J.a[j], P.q, P.one_s);
+            if (J.b) v = add_mod(v, red64(J.b[j], P.q, P.one_s), P.q);
+            return v;
+        }
+        case LD_DIG: return reinterpret_cast<const uint16_t*>(J.a)[j];
+        case LD_DIGGAL: {
+            const unsigned e = J.gal[j];
+            return reinterpret_cast<const uint16_t*>((e >> 15) ? J.b : J.a)[e & 0x7FFF];
+        }
+        default: return J.a[j];
+    }
+}
+
+__device__ __forceinline__ void st_elem(const XJob& J, const DevCtx& D, const PrimeC& P, int j, u64 x) {
+    switch (J.ep) {
+        case EP_ADDMONT: J.out[j] = add_mod(x, mul_mont(J.ea[j], J.eb[j], P.q, P.qneg), P.q); break;
+        case EP_ADD: J.out[j] = add_mod(x, J.ea[j], P.q); break;
+        case EP_ADDRED: J.out[j] = add_mod(x, red64(J.ea[j], P.q, P.one_s), P.q); break;
+        case EP_RESCALE:
+        case EP_RESCALE_ATOMIC: {
+            const int l = J.level;
+            u64 e[MAXL];
+            rescale_corr(D, l, x, e);
+            HC_UNROLL
+            for (int k = 0; k < MAXL; k++) {
+                if (k >= l) break;
+                u64* o = J.out + (size_t)k * J.ostride + j;
+                if (J.ep == EP_RESCALE) *o = e[k];
+                else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)e[k]);
+            }
+            break;
+        }
+        default: J.out[j] = x;
+    }
+}
+
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive_release() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int DIR>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
+    k_xform_cl(const DevCtx* __restrict__ C, const XJob* __restrict__ jobs) {
+    __shared__ u64 tile[CTILE];
+    __shared__ u64 recv[DIR ? CTILE : 1];
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    const int c = (int)cl.block_rank();
+    const int t = threadIdx.x;
+    cluster_arrive_relaxed();  // "this CTA has started" (waited on before DSMEM stores)
+    const XJob J = jobs[blockIdx.x / CL];
+    const PrimeC P = C->pc[J.k];
+    const DevCtx& D = *C;
+    if (DIR == 0) {
+        const Tw* tw = C->twf + (size_t)J.k * NPOLY;
+        u64 x[CEPT];
+        const int b = 128 * c + t;
+        HC_UNROLL
+        for (int r = 0; r < CEPT; r++) x[r] = ld_elem(J, P, r * CTILE + b);
+        c_phaseA_fwd(x, tw, P.q, P.q2);
+        cluster_wait();
+        HC_UNROLL
+        for (int r = 0; r < CEPT; r++) {
+            u64* peer = cl.map_shared_rank(tile, r);
+            peer[cswz(b)] = x[r];
+        }
+        cluster_arrive_release();
+        cluster_wait();
+        HC_NOUNROLL
+        for (int p = 0; p < 3; p++) {
+            const CPass I = cpass(p, c, t);
+            c_load(x, tile, I);
+            r8_ct(x, tw, I.s0, I.G, P.q, P.q2);
+            if (p == 2) {
+                u64 o[CEPT];
+                HC_UNROLL
+                for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
+                c_st12(c, t, x, o, tw, P.q, P.q2);
+            }
+            c_store(x, tile, I);
+            __syncthreads();
+        }
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) {
+            const int bb = t + 128 * v;
+            st_elem(J, D, P, c * CTILE + bb, tile[cswz(bb)]);
+        }
+    } else {
+        const Tw* tw = C->twi + (size_t)J.k * NPOLY;
+        u64 x[CEPT];
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) x[v] = ld_elem(J, P, c * CTILE + t + 128 * v);
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+        __syncthreads();
+        HC_NOUNROLL
+        for (int p = 0; p < 3; p++) {
+            const CPass I = cpass(2 - p, c, t);
+            c_load(x, tile, I);
+            if (p == 0) {
+                u64 o[CEPT];
+                HC_UNROLL
+                for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
+                c_st0(c, t, x, o, tw, P.q, P.q2);
+            }
+            r8_gs(x, tw, 1 + 3 * p, I.G, P.q, P.q2);
+            if (p < 2) {
+                c_store(x, tile, I);
+                __syncthreads();
+            }
+        }
+        // all-to-all: element (row c, column t + 128 v) -> CTA v, slot c*128 + t
+        cluster_wait();
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) {
+            u64* peer = cl.map_shared_rank(recv, v);
+            peer[c * 128 + t] = x[v];
+        }
+        cluster_arrive_release();
+        cluster_wait();
+        HC_UNROLL
+        for (int r = 0; r < CEPT; r++) x[r] = recv[r * 128 + t];
+        c_phaseA_inv(x, tw, P);
+        HC_UNROLL
+        for (int r = 0; r < CEPT; r++) st_elem(J, D, P, r * CTILE + 128 * c + t, x[r]);
     }
 }
 
@@ -327,30 +507,32 @@ HD u64 plain_slot_value(const PJob& J, const PlanShape& S, int r, int c, u64 p, 
     }
 }
 
-__global__ void __launch_bounds__(NT) k_plain(const DevCtx* __restrict__ C, const PJob* __restrict__ jobs, PlanShape S) {
+__global__ void __launch_bounds__(NT, 1) k_plain(const DevCtx* __restrict__ C, const PJob* __restrict__ jobs, PlanShape S) {
     extern __shared__ u64 sm[];
     u64* coef = sm + NPOLY;
     const PJob J = jobs[blockIdx.x];
     const int tid = threadIdx.x;
-    u64 x[EPT];
-    HC_UNROLL
-    for (int i = 0; i < EPT; i++) {
-        const unsigned so = C->slot_of[tid + NT * i];
-        x[i] = plain_slot_value(J, S, so >> 12, so & 4095, C->p, C->pinv);
+    HC_NOUNROLL
+    for (int j = tid; j < NPOLY; j += NT) {
+        const unsigned so = C->slot_of[j];
+        sm[swz(j)] = plain_slot_value(J, S, so >> 12, so & 4095, C->p, C->pinv);
     }
-    cta_ntt_inv(x, C->twi + (size_t)PIDX * NPOLY, C->pc[PIDX], sm);
-    HC_UNROLL
-    for (int i = 0; i < EPT; i++) coef[tid + NT * i] = x[i];
+    __syncthreads();
+    cta_ntt_inv(C->twi + (size_t)PIDX * NPOLY, C->pc[PIDX], sm);
+    HC_NOUNROLL
+    for (int j = tid; j < NPOLY; j += NT) coef[j] = sm[swz(j)];
     const LevelC& LV = C->lv[J.level];
     for (int k = 0; k <= J.level; k++) {
         const PrimeC P = C->pc[k];
-        HC_UNROLL
-        for (int i = 0; i < EPT; i++) x[i] = coef[tid + NT * i];
-        cta_ntt_fwd(x, C->twf + (size_t)k * NPOLY, P, sm);
+        __syncthreads();
+        HC_NOUNROLL
+        for (int j = tid; j < NPOLY; j += NT) sm[swz(j)] = coef[j];
+        __syncthreads();
+        cta_ntt_fwd(C->twf + (size_t)k * NPOLY, P, sm);
         const u64 w = (k == J.level) ? P.rmod : LV.qinv_r[k];
         const u64 ws = (k == J.level) ? P.rmod_s : LV.qinv_rs[k];
-        HC_UNROLL
-        for (int i = 0; i < EPT; i++) J.out[(size_t)k * NPOLY + tid + NT * i] = mul_shoup(x[i], w, ws, P.q);
+        HC_NOUNROLL
+        for (int j = tid; j < NPOLY; j += NT) J.out[(size_t)k * NPOLY + j] = mul_shoup(sm[swz(j)], w, ws, P.q);
     }
 }
 

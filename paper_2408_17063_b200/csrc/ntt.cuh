@@ -1,37 +1,43 @@
-// Negacyclic NTT / INTT for n = 8192 over one 54-bit prime, one CTA of 256
-// threads per polynomial, 32 coefficients per thread held in registers.
+// Negacyclic NTT / INTT for n = 8192 over one 54-bit prime: one CTA of 512
+// threads per polynomial, 16 coefficients per thread in registers.
 //
-// Semantics (must match the reference bit-for-bit after canonicalisation):
-//   forward  = NttContext.fwd  (bgv.py:178-199): Cooley-Tukey, natural-order
-//              input, bit-reversed output, twiddle tbl[m+i] = psi^bitrev(m+i);
-//   inverse  = NttContext.inv  (bgv.py:201-225): Gentleman-Sande with
-//              inv_tbl[h+i] = psi^-bitrev(h+i), then * n^-1.
+// Semantics (bit-for-bit after canonicalisation):
+//   forward = NttContext.fwd (bgv.py:178-199): Cooley-Tukey, natural-order
+//             input, bit-reversed output, twiddle tbl[m+i] = psi^bitrev(m+i);
+//   inverse = NttContext.inv (bgv.py:201-225): Gentleman-Sande with
+//             inv_tbl[h+i] = psi^-bitrev(h+i), then * n^-1.
 // Modular arithmetic is exact, so any schedule of the same butterflies gives
-// the reference's values; the schedule here is radix-32/16/16 in registers
-// with two swizzled shared-memory transposes between register passes.
+// the reference's values.  Schedule (13 stages = 4 + 4 + 4 + 1):
+//   three radix-16 register passes over coefficient index bits 12..9, 8..5
+//   and 4..1 -- ONE inlined radix-16 routine run in a rolled loop, because
+//   each pass's index pattern is affine, j(v) = base + v*stride -- and the
+//   bit-0 stage across lane pairs with a warp shuffle.  Between passes the
+//   data goes through a swizzled 64 KiB shared-memory tile.  Compact code is
+//   deliberate: the fully unrolled first version (468 KiB of SASS) stalled
+//   on instruction fetch.
 //
-// Register layout in and out of both transforms ("canonical layout"):
-//   thread tid holds x[i] = a[tid + 256*i], i = 0..31   (coalesced in HBM).
+// Register layout in/out of both transforms ("canonical layout"):
+//   thread t holds x[v] = a[t + 512*v], v = 0..15  (coalesced in HBM).
 //
-// Every pass is a __host__ __device__ function of (tid, registers, smem) so
-// the CPU self-test can run the exact device schedule thread by thread
-// (passes are separated by __syncthreads on the device, by a loop over all
-// 256 tids on the host).
+// The passes are __host__ __device__ functions of (tid, registers, smem), so
+// the CPU self-test runs this exact schedule thread by thread.
 #pragma once
 #include "arith.cuh"
 
 #if defined(__CUDACC__)
 #define HC_UNROLL _Pragma("unroll")
+#define HC_NOUNROLL _Pragma("unroll 1")
 #else
 #define HC_UNROLL
+#define HC_NOUNROLL
 #endif
 
 namespace hc {
 
 constexpr int LOGN = 13;
 constexpr int NPOLY = 1 << LOGN;  // ring degree n
-constexpr int NT = 256;           // threads per transform CTA
-constexpr int EPT = NPOLY / NT;   // 32 coefficients per thread
+constexpr int NT = 512;           // threads per transform CTA
+constexpr int EPT = NPOLY / NT;   // 16 coefficients per thread
 
 struct alignas(16) Tw {
     u64 w, ws;  // twiddle and its Shoup constant
@@ -58,237 +64,235 @@ HD Tw ldtw(const Tw* t, int i) {
 #endif
 }
 
-// shared-memory swizzle: conflict-free for all four access patterns below
-HD int swz(int j) { return j ^ ((j >> 4) & 15); }
+// shared-memory swizzle (XOR index bits 1..4 with bits 5..8): conflict-free
+// for the three affine patterns below (64-bit accesses, 16 lanes per phase)
+HD int swz(int j) { return j ^ (((j >> 5) & 15) << 1); }
 
-// ---------------- forward -------------------------------------------------
+// Forward pass p covers index bits 12-4p .. 9-4p; thread t's 16 coefficients
+// are j(v) = base + v*stride, "hi" = the index bits above the pass.
+struct PassIdx {
+    int base, stride, hi, s0;
+};
+HD PassIdx pass_idx(int p, int t) {
+    PassIdx r;
+    if (p == 0) {
+        r.base = t; r.stride = 512; r.hi = 0; r.s0 = 0;
+    } else if (p == 1) {
+        r.base = ((t >> 5) << 9) | (t & 31); r.stride = 32; r.hi = t >> 5; r.s0 = 4;
+    } else {
+        r.base = ((t >> 1) << 5) | (t & 1); r.stride = 2; r.hi = t >> 1; r.s0 = 8;
+    }
+    return r;
+}
 
-// stages 0..4 (bits 12..8), registers only
-HD void fwd_p1(u64 (&x)[EPT], const Tw* tw, u64 q, u64 q2) {
+HD void sm_load(u64 (&x)[EPT], const u64* sm, int base, int stride) {
     HC_UNROLL
-    for (int s = 0; s < 5; s++) {
-        const int half = 16 >> s;
+    for (int v = 0; v < EPT; v++) x[v] = sm[swz(base + v * stride)];
+}
+HD void sm_store(const u64 (&x)[EPT], u64* sm, int base, int stride) {
+    HC_UNROLL
+    for (int v = 0; v < EPT; v++) sm[swz(base + v * stride)] = x[v];
+}
+
+// 4 Cooley-Tukey stages s0..s0+3 on a 16-point group: stage s0+u pairs v and
+// v + (8 >> u), twiddle tbl[2^(s0+u) + (hi << u | v >> (4-u))].
+HD void r16_ct(u64 (&x)[EPT], const Tw* tw, int s0, int hi, u64 q, u64 q2) {
+    HC_UNROLL
+    for (int u = 0; u < 4; u++) {
+        const int half = 8 >> u;
+        const int tbase = (1 << (s0 + u)) + (hi << u);
         HC_UNROLL
-        for (int i = 0; i < 32; i++) {
-            if (!(i & half)) {
-                Tw w = ldtw(tw, (1 << s) + (i >> (5 - s)));
-                bf_ct(x[i], x[i + half], w.w, w.ws, q, q2);
+        for (int v = 0; v < EPT; v++) {
+            if (!(v & half)) {
+                Tw w = ldtw(tw, tbase + (v >> (4 - u)));
+                bf_ct(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
     }
 }
 
-HD void st_canon(int tid, const u64 (&x)[EPT], u64* sm) {
+// 4 Gentleman-Sande stages b0..b0+3 on a 16-point group: stage b0+u pairs v
+// and v + (1 << u), twiddle inv_tbl[2^(12-b0-u) + (hi << (3-u) | v >> (u+1))].
+HD void r16_gs(u64 (&x)[EPT], const Tw* tw, int b0, int hi, u64 q, u64 q2) {
     HC_UNROLL
-    for (int i = 0; i < 32; i++) sm[swz(tid + NT * i)] = x[i];
-}
-HD void ld_canon(int tid, u64 (&x)[EPT], const u64* sm) {
-    HC_UNROLL
-    for (int i = 0; i < 32; i++) x[i] = sm[swz(tid + NT * i)];
-}
-
-// "mid" groups: fixed bits 12..8 and 3..0, v = bits 7..4
-HD int mid_index(int G, int v) { return ((G >> 4) << 8) | (v << 4) | (G & 15); }
-HD void ld_mid(int tid, u64 (&x)[EPT], const u64* sm) {
-    HC_UNROLL
-    for (int g = 0; g < 2; g++) {
+    for (int u = 0; u < 4; u++) {
+        const int half = 1 << u;
+        const int tbase = (1 << (12 - b0 - u)) + (hi << (3 - u));
         HC_UNROLL
-        for (int v = 0; v < 16; v++) x[g * 16 + v] = sm[swz(mid_index(tid + NT * g, v))];
-    }
-}
-HD void st_mid(int tid, const u64 (&x)[EPT], u64* sm) {
-    HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        HC_UNROLL
-        for (int v = 0; v < 16; v++) sm[swz(mid_index(tid + NT * g, v))] = x[g * 16 + v];
-    }
-}
-// "low" groups: fixed bits 12..4, v = bits 3..0
-HD void ld_low(int tid, u64 (&x)[EPT], const u64* sm) {
-    HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        HC_UNROLL
-        for (int v = 0; v < 16; v++) x[g * 16 + v] = sm[swz(((tid + NT * g) << 4) | v)];
-    }
-}
-HD void st_low(int tid, const u64 (&x)[EPT], u64* sm) {
-    HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        HC_UNROLL
-        for (int v = 0; v < 16; v++) sm[swz(((tid + NT * g) << 4) | v)] = x[g * 16 + v];
-    }
-}
-
-// stages 5..8 (bits 7..4)
-HD void fwd_p2(int tid, u64 (&x)[EPT], const Tw* tw, u64 q, u64 q2) {
-    HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        const int hi5 = (tid + NT * g) >> 4;
-        HC_UNROLL
-        for (int s = 5; s < 9; s++) {
-            const int half = 8 >> (s - 5);
-            HC_UNROLL
-            for (int v = 0; v < 16; v++) {
-                if (!(v & half)) {
-                    Tw w = ldtw(tw, (1 << s) + ((hi5 << (s - 5)) | (v >> (9 - s))));
-                    bf_ct(x[g * 16 + v], x[g * 16 + v + half], w.w, w.ws, q, q2);
-                }
+        for (int v = 0; v < EPT; v++) {
+            if (!(v & half)) {
+                Tw w = ldtw(tw, tbase + (v >> (u + 1)));
+                bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
     }
 }
 
-// stages 9..12 (bits 3..0); leaves values canonical in [0, q)
-HD void fwd_p3(int tid, u64 (&x)[EPT], const Tw* tw, u64 q, u64 q2) {
+// Forward stage 12 (index bit 0) across the lane pair (t, t^1): even lane
+// keeps X + w*Y, odd lane X - w*Y, w = tbl[4096 + ((t >> 1) << 4 | v)].
+// Inputs [0,4q), outputs canonical.  `other` = the partner lane's registers.
+HD void st12_ct(int t, u64 (&x)[EPT], const u64 (&other)[EPT], const Tw* tw, u64 q, u64 q2) {
+    const int odd = t & 1;
+    const int tb = 4096 + ((t >> 1) << 4);
     HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        const int G = tid + NT * g;
-        HC_UNROLL
-        for (int s = 9; s < 13; s++) {
-            const int half = 8 >> (s - 9);
-            HC_UNROLL
-            for (int v = 0; v < 16; v++) {
-                if (!(v & half)) {
-                    Tw w = ldtw(tw, (1 << s) + ((G << (s - 9)) | (v >> (13 - s))));
-                    bf_ct(x[g * 16 + v], x[g * 16 + v + half], w.w, w.ws, q, q2);
-                }
-            }
-        }
+    for (int v = 0; v < EPT; v++) {
+        u64 X = odd ? other[v] : x[v];
+        u64 Y = odd ? x[v] : other[v];
+        Tw w = ldtw(tw, tb + v);
+        bf_ct(X, Y, w.w, w.ws, q, q2);
+        x[v] = canon4(odd ? Y : X, q, q2);
     }
-    HC_UNROLL
-    for (int i = 0; i < 32; i++) x[i] = canon4(x[i], q, q2);
 }
 
-// ---------------- inverse -------------------------------------------------
-
-// bits 0..3; input in [0, 2q)
-HD void inv_pa(int tid, u64 (&x)[EPT], const Tw* tw, u64 q, u64 q2) {
+// First inverse stage (bit 0) across the lane pair: even lane X + Y, odd
+// lane (X - Y) * w, w = inv_tbl[4096 + ((t >> 1) << 4 | v)].  [0,2q) in/out.
+HD void st0_gs(int t, u64 (&x)[EPT], const u64 (&other)[EPT], const Tw* tw, u64 q, u64 q2) {
+    const int odd = t & 1;
+    const int tb = 4096 + ((t >> 1) << 4);
     HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        const int G = tid + NT * g;
-        HC_UNROLL
-        for (int b = 0; b < 4; b++) {
-            const int half = 1 << b;
-            HC_UNROLL
-            for (int v = 0; v < 16; v++) {
-                if (!(v & half)) {
-                    Tw w = ldtw(tw, (1 << (12 - b)) + ((G << (3 - b)) | (v >> (b + 1))));
-                    bf_gs(x[g * 16 + v], x[g * 16 + v + half], w.w, w.ws, q, q2);
-                }
-            }
+    for (int v = 0; v < EPT; v++) {
+        const u64 X = odd ? other[v] : x[v];
+        const u64 Y = odd ? x[v] : other[v];
+        if (odd) {
+            Tw w = ldtw(tw, tb + v);
+            x[v] = mul_shoup_lazy(X - Y + q2, w.w, w.ws, q);
+        } else {
+            u64 s = X + Y;
+            x[v] = s >= q2 ? s - q2 : s;
         }
     }
 }
 
-// bits 4..7
-HD void inv_pb(int tid, u64 (&x)[EPT], const Tw* tw, u64 q, u64 q2) {
-    HC_UNROLL
-    for (int g = 0; g < 2; g++) {
-        const int hi5 = (tid + NT * g) >> 4;
-        HC_UNROLL
-        for (int b = 4; b < 8; b++) {
-            const int half = 1 << (b - 4);
-            HC_UNROLL
-            for (int v = 0; v < 16; v++) {
-                if (!(v & half)) {
-                    Tw w = ldtw(tw, (1 << (12 - b)) + ((hi5 << (7 - b)) | (v >> (b - 3))));
-                    bf_gs(x[g * 16 + v], x[g * 16 + v + half], w.w, w.ws, q, q2);
-                }
-            }
-        }
-    }
-}
-
-// bits 8..12 in canonical layout; the last stage folds in n^-1.
-// Output canonical in [0, q).
-HD void inv_pc(u64 (&x)[EPT], const Tw* tw, const PrimeC& P) {
+// Inverse stages 9..11 in the canonical layout, then the bit-12 stage folded
+// with n^-1.  Output canonical.
+HD void inv_tail(u64 (&x)[EPT], const Tw* tw, const PrimeC& P) {
     const u64 q = P.q, q2 = P.q2;
     HC_UNROLL
-    for (int b = 8; b < 12; b++) {
-        const int half = 1 << (b - 8);
+    for (int u = 0; u < 3; u++) {
+        const int half = 1 << u;
+        const int tbase = 1 << (3 - u);
         HC_UNROLL
-        for (int i = 0; i < 32; i++) {
-            if (!(i & half)) {
-                Tw w = ldtw(tw, (1 << (12 - b)) + (i >> (b - 7)));
-                bf_gs(x[i], x[i + half], w.w, w.ws, q, q2);
+        for (int v = 0; v < EPT; v++) {
+            if (!(v & half)) {
+                Tw w = ldtw(tw, tbase + (v >> (u + 1)));
+                bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
     }
     HC_UNROLL
-    for (int i = 0; i < 16; i++) {
-        u64 u = x[i], v = x[i + 16];
-        x[i] = reduce_once(mul_shoup_lazy(u + v, P.ninv, P.ninv_s, q), q);
-        x[i + 16] = reduce_once(mul_shoup_lazy(u - v + q2, P.ninvw, P.ninvw_s, q), q);
+    for (int v = 0; v < 8; v++) {
+        u64 a = x[v], b = x[v + 8];
+        x[v] = reduce_once(mul_shoup_lazy(a + b, P.ninv, P.ninv_s, q), q);
+        x[v + 8] = reduce_once(mul_shoup_lazy(a - b + q2, P.ninvw, P.ninvw_s, q), q);
     }
 }
 
 #if defined(__CUDACC__)
-// Device CTA transforms (blockDim.x == 256).  `sm` = 8192 u64 of shared memory.
-// In/out in canonical layout.  fwd input < 4q; inv input < 2q.  Output < q.
-__device__ __forceinline__ void cta_ntt_fwd(u64 (&x)[EPT], const Tw* tw, const PrimeC& P, u64* sm) {
-    const int tid = threadIdx.x;
-    fwd_p1(x, tw, P.q, P.q2);
-    st_canon(tid, x, sm);
-    __syncthreads();
-    ld_mid(tid, x, sm);
-    fwd_p2(tid, x, tw, P.q, P.q2);
-    st_mid(tid, x, sm);
-    __syncthreads();
-    ld_low(tid, x, sm);
-    fwd_p3(tid, x, tw, P.q, P.q2);
-    st_low(tid, x, sm);
-    __syncthreads();
-    ld_canon(tid, x, sm);
-    __syncthreads();  // smem reusable by the caller
+__device__ __forceinline__ void shfl_pair(const u64 (&x)[EPT], u64 (&o)[EPT]) {
+    HC_UNROLL
+    for (int v = 0; v < EPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
 }
 
-__device__ __forceinline__ void cta_ntt_inv(u64 (&x)[EPT], const Tw* tw, const PrimeC& P, u64* sm) {
-    const int tid = threadIdx.x;
-    st_canon(tid, x, sm);
-    __syncthreads();
-    ld_low(tid, x, sm);
-    inv_pa(tid, x, tw, P.q, P.q2);
-    st_low(tid, x, sm);
-    __syncthreads();
-    ld_mid(tid, x, sm);
-    inv_pb(tid, x, tw, P.q, P.q2);
-    st_mid(tid, x, sm);
-    __syncthreads();
-    ld_canon(tid, x, sm);
-    inv_pc(x, tw, P);
+// Device CTA transforms (blockDim.x == 512) on a 64 KiB smem tile holding
+// coefficient j at sm[swz(j)] (natural index order in and out; the caller
+// writes/reads it with rolled per-coefficient loops).  fwd input < 4q,
+// inv input < 2q; output canonical < q.  The caller must __syncthreads()
+// after filling the tile; the functions end with a barrier.
+// In any one access pattern every smem word belongs to exactly one thread,
+// so one barrier between a store pattern and the next load pattern suffices.
+__device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* sm) {
+    const int t = threadIdx.x;
+    u64 x[EPT];
+    HC_NOUNROLL
+    for (int p = 0; p < 3; p++) {
+        const PassIdx I = pass_idx(p, t);
+        sm_load(x, sm, I.base, I.stride);
+        r16_ct(x, tw, I.s0, I.hi, P.q, P.q2);
+        if (p == 2) {
+            u64 o[EPT];
+            shfl_pair(x, o);
+            st12_ct(t, x, o, tw, P.q, P.q2);
+        }
+        sm_store(x, sm, I.base, I.stride);
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* sm) {
+    const int t = threadIdx.x;
+    u64 x[EPT];
+    HC_NOUNROLL
+    for (int p = 0; p < 3; p++) {
+        const PassIdx I = pass_idx(2 - p, t);
+        sm_load(x, sm, I.base, I.stride);
+        if (p == 0) {
+            u64 o[EPT];
+            shfl_pair(x, o);
+            st0_gs(t, x, o, tw, P.q, P.q2);
+        }
+        if (p < 2) {
+            r16_gs(x, tw, 1 + 4 * p, I.hi, P.q, P.q2);
+            sm_store(x, sm, I.base, I.stride);
+            __syncthreads();
+        }
+    }
+    inv_tail(x, tw, P);
+    sm_store(x, sm, t, NT);
     __syncthreads();
 }
 #endif
 
-// Host emulation of the device schedule (CPU self-test only): a[n] in/out.
+// ---- host emulation of the device schedule (CPU self-test only) ----------
 inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
-    static u64 regs[NT][EPT];
+    static u64 regs[NT][EPT], other[NT][EPT];
     static u64 sm[NPOLY];
-    for (int t = 0; t < NT; t++)
-        for (int i = 0; i < EPT; i++) regs[t][i] = a[t + NT * i];
-    for (int t = 0; t < NT; t++) { fwd_p1(regs[t], tw, P.q, P.q2); st_canon(t, regs[t], sm); }
-    for (int t = 0; t < NT; t++) { ld_mid(t, regs[t], sm); fwd_p2(t, regs[t], tw, P.q, P.q2); }
-    for (int t = 0; t < NT; t++) st_mid(t, regs[t], sm);
-    for (int t = 0; t < NT; t++) { ld_low(t, regs[t], sm); fwd_p3(t, regs[t], tw, P.q, P.q2); }
-    for (int t = 0; t < NT; t++) st_low(t, regs[t], sm);
-    for (int t = 0; t < NT; t++) ld_canon(t, regs[t], sm);
-    for (int t = 0; t < NT; t++)
-        for (int i = 0; i < EPT; i++) a[t + NT * i] = regs[t][i];
+    for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
+    for (int p = 0; p < 3; p++) {
+        for (int t = 0; t < NT; t++) {
+            PassIdx I = pass_idx(p, t);
+            sm_load(regs[t], sm, I.base, I.stride);
+            r16_ct(regs[t], tw, I.s0, I.hi, P.q, P.q2);
+        }
+        if (p == 2) {
+            for (int t = 0; t < NT; t++)
+                for (int v = 0; v < EPT; v++) other[t][v] = regs[t ^ 1][v];
+            for (int t = 0; t < NT; t++) st12_ct(t, regs[t], other[t], tw, P.q, P.q2);
+        }
+        for (int t = 0; t < NT; t++) {
+            PassIdx I = pass_idx(p, t);
+            sm_store(regs[t], sm, I.base, I.stride);
+        }
+    }
+    for (int j = 0; j < NPOLY; j++) a[j] = sm[swz(j)];
 }
 
 inline void host_emulate_inv(u64* a, const Tw* tw, const PrimeC& P) {
-    static u64 regs[NT][EPT];
+    static u64 regs[NT][EPT], other[NT][EPT];
     static u64 sm[NPOLY];
-    for (int t = 0; t < NT; t++)
-        for (int i = 0; i < EPT; i++) regs[t][i] = a[t + NT * i];
-    for (int t = 0; t < NT; t++) st_canon(t, regs[t], sm);
-    for (int t = 0; t < NT; t++) { ld_low(t, regs[t], sm); inv_pa(t, regs[t], tw, P.q, P.q2); }
-    for (int t = 0; t < NT; t++) st_low(t, regs[t], sm);
-    for (int t = 0; t < NT; t++) { ld_mid(t, regs[t], sm); inv_pb(t, regs[t], tw, P.q, P.q2); }
-    for (int t = 0; t < NT; t++) st_mid(t, regs[t], sm);
-    for (int t = 0; t < NT; t++) { ld_canon(t, regs[t], sm); inv_pc(regs[t], tw, P); }
-    for (int t = 0; t < NT; t++)
-        for (int i = 0; i < EPT; i++) a[t + NT * i] = regs[t][i];
+    for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
+    for (int p = 0; p < 3; p++) {
+        for (int t = 0; t < NT; t++) {
+            PassIdx I = pass_idx(2 - p, t);
+            sm_load(regs[t], sm, I.base, I.stride);
+        }
+        if (p == 0) {
+            for (int t = 0; t < NT; t++)
+                for (int v = 0; v < EPT; v++) other[t][v] = regs[t ^ 1][v];
+            for (int t = 0; t < NT; t++) st0_gs(t, regs[t], other[t], tw, P.q, P.q2);
+        }
+        if (p < 2) {
+            for (int t = 0; t < NT; t++) {
+                PassIdx I = pass_idx(2 - p, t);
+                r16_gs(regs[t], tw, 1 + 4 * p, I.hi, P.q, P.q2);
+                sm_store(regs[t], sm, I.base, I.stride);
+            }
+        }
+    }
+    for (int t = 0; t < NT; t++) {
+        inv_tail(regs[t], tw, P);
+        sm_store(regs[t], sm, t, NT);
+    }
+    for (int j = 0; j < NPOLY; j++) a[j] = sm[swz(j)];
 }
 
 }  // namespace hc

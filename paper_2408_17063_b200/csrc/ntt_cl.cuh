@@ -1,0 +1,225 @@
+// Cluster NTT: one 8192-point transform per thread-block CLUSTER of 8 CTAs
+// (8 SMs), 128 threads x 8 coefficients per CTA.  Latency path of the Comp
+// (giant steps, folds, output mask) runs chains of 1-14 transforms; a
+// single-CTA transform occupies one SM for ~18 us, the cluster form spreads
+// it over 8 SMs.  Same arithmetic and semantics as ntt.cuh (bgv.py:178-225).
+//
+// Index j = a*1024 + b, a = bits 12..10 (CTA "row"), b = bits 9..0.
+// Forward (CT, natural in, bit-reversed out):
+//   phase A  CTA c, thread t owns column b = 128c + t, rows a = 0..7
+//            (global loads coalesced); stages 0..2 (bits 12..10) in registers;
+//            element (a, b) is stored into CTA a's shared tile at b (DSMEM);
+//   cluster barrier;
+//   phase B  CTA c owns j = c*1024 + b, b = 0..1023: three radix-8 register
+//            passes over bits 9..7, 6..4, 3..1 through the local tile, then
+//            bit 0 across lane pairs (shuffle); output coalesced.
+// Inverse (GS): phase B' on CTA c's own rows (bit 0, then bits 1..9), DSMEM
+// all-to-all into column layout, cluster barrier, phase A' = bits 10..12 in
+// registers with n^-1 folded into the last stage.
+#pragma once
+#include "ntt.cuh"
+
+namespace hc {
+
+constexpr int CL = 8;       // CTAs per transform
+constexpr int CNT = 128;    // threads per CTA
+constexpr int CEPT = 8;     // coefficients per thread
+constexpr int CTILE = 1024; // coefficients per CTA
+
+// local tile swizzle for the three radix-8 patterns (64-bit, 16 lanes/phase):
+// XOR bits 1..3 with bits 4..6
+HD int cswz(int b) { return b ^ (((b >> 4) & 7) << 1); }
+
+// phase-B pass p (0: bits 9..7, 1: bits 6..4, 2: bits 3..1) of CTA c:
+// b(v) = base + v*stride; G = all index bits of j above the pass.
+struct CPass {
+    int base, stride, G, s0;
+};
+HD CPass cpass(int p, int c, int t) {
+    CPass r;
+    if (p == 0) {
+        r.base = t; r.stride = 128; r.G = c; r.s0 = 3;
+    } else if (p == 1) {
+        r.base = ((t >> 4) << 7) | (t & 15); r.stride = 16; r.G = (c << 3) | (t >> 4); r.s0 = 6;
+    } else {
+        r.base = ((t >> 1) << 4) | (t & 1); r.stride = 2; r.G = (c << 6) | (t >> 1); r.s0 = 9;
+    }
+    return r;
+}
+
+HD void c_load(u64 (&x)[CEPT], const u64* sm, const CPass& I) {
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) x[v] = sm[cswz(I.base + v * I.stride)];
+}
+HD void c_store(const u64 (&x)[CEPT], u64* sm, const CPass& I) {
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) sm[cswz(I.base + v * I.stride)] = x[v];
+}
+
+// 3 CT stages s0..s0+2 on 8 points: stage s0+u pairs v, v + (4 >> u),
+// twiddle tbl[2^(s0+u) + (G << u | v >> (3-u))]
+HD void r8_ct(u64 (&x)[CEPT], const Tw* tw, int s0, int G, u64 q, u64 q2) {
+    HC_UNROLL
+    for (int u = 0; u < 3; u++) {
+        const int half = 4 >> u;
+        const int tb = (1 << (s0 + u)) + (G << u);
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) {
+            if (!(v & half)) {
+                Tw w = ldtw(tw, tb + (v >> (3 - u)));
+                bf_ct(x[v], x[v + half], w.w, w.ws, q, q2);
+            }
+        }
+    }
+}
+
+// 3 GS stages b0..b0+2 on 8 points: stage b0+u pairs v, v + (1 << u),
+// twiddle inv_tbl[2^(12-b0-u) + (G << (2-u) | v >> (u+1))]
+HD void r8_gs(u64 (&x)[CEPT], const Tw* tw, int b0, int G, u64 q, u64 q2) {
+    HC_UNROLL
+    for (int u = 0; u < 3; u++) {
+        const int half = 1 << u;
+        const int tb = (1 << (12 - b0 - u)) + (G << (2 - u));
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) {
+            if (!(v & half)) {
+                Tw w = ldtw(tw, tb + (v >> (u + 1)));
+                bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
+            }
+        }
+    }
+}
+
+// forward bit-0 stage across lanes (t, t^1) in pass-2 layout:
+// w = tbl[4096 + (j >> 1)], j >> 1 = (c << 9) | ((t >> 1) << 3) | v
+HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const Tw* tw, u64 q, u64 q2) {
+    const int odd = t & 1;
+    const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) {
+        u64 X = odd ? o[v] : x[v];
+        u64 Y = odd ? x[v] : o[v];
+        Tw w = ldtw(tw, tb + v);
+        bf_ct(X, Y, w.w, w.ws, q, q2);
+        x[v] = canon4(odd ? Y : X, q, q2);
+    }
+}
+
+// inverse bit-0 stage across lanes: even X + Y, odd (X - Y) w
+HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const Tw* tw, u64 q, u64 q2) {
+    const int odd = t & 1;
+    const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) {
+        const u64 X = odd ? o[v] : x[v];
+        const u64 Y = odd ? x[v] : o[v];
+        if (odd) {
+            Tw w = ldtw(tw, tb + v);
+            x[v] = mul_shoup_lazy(X - Y + q2, w.w, w.ws, q);
+        } else {
+            u64 s = X + Y;
+            x[v] = s >= q2 ? s - q2 : s;
+        }
+    }
+}
+
+// forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
+HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q2) { r8_ct(x, tw, 0, 0, q, q2); }
+
+// inverse phase A': GS stages 10, 11 on the column, then bit 12 folded with n^-1
+HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
+    const u64 q = P.q, q2 = P.q2;
+    HC_UNROLL
+    for (int u = 0; u < 2; u++) {
+        const int half = 1 << u;
+        const int tb = 1 << (2 - u);
+        HC_UNROLL
+        for (int v = 0; v < CEPT; v++) {
+            if (!(v & half)) {
+                Tw w = ldtw(tw, tb + (v >> (u + 1)));
+                bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
+            }
+        }
+    }
+    HC_UNROLL
+    for (int v = 0; v < 4; v++) {
+        u64 a = x[v], b = x[v + 4];
+        x[v] = reduce_once(mul_shoup_lazy(a + b, P.ninv, P.ninv_s, q), q);
+        x[v + 4] = reduce_once(mul_shoup_lazy(a - b + q2, P.ninvw, P.ninvw_s, q), q);
+    }
+}
+
+// ---- host emulation of the cluster schedule (CPU self-test only) ----------
+inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
+    static u64 tile[CL][CTILE];
+    static u64 regs[CL][CNT][CEPT], oth[CL][CNT][CEPT];
+    for (int c = 0; c < CL; c++)
+        for (int t = 0; t < CNT; t++) {
+            u64 x[CEPT];
+            const int b = 128 * c + t;
+            for (int r = 0; r < CEPT; r++) x[r] = a[r * CTILE + b];
+            c_phaseA_fwd(x, tw, P.q, P.q2);
+            for (int r = 0; r < CEPT; r++) tile[r][cswz(b)] = x[r];
+        }
+    for (int p = 0; p < 3; p++) {
+        for (int c = 0; c < CL; c++)
+            for (int t = 0; t < CNT; t++) {
+                CPass I = cpass(p, c, t);
+                c_load(regs[c][t], tile[c], I);
+                r8_ct(regs[c][t], tw, I.s0, I.G, P.q, P.q2);
+            }
+        if (p == 2) {
+            for (int c = 0; c < CL; c++)
+                for (int t = 0; t < CNT; t++)
+                    for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
+            for (int c = 0; c < CL; c++)
+                for (int t = 0; t < CNT; t++) c_st12(c, t, regs[c][t], oth[c][t], tw, P.q, P.q2);
+        }
+        for (int c = 0; c < CL; c++)
+            for (int t = 0; t < CNT; t++) c_store(regs[c][t], tile[c], cpass(p, c, t));
+    }
+    for (int c = 0; c < CL; c++)
+        for (int b = 0; b < CTILE; b++) a[c * CTILE + b] = tile[c][cswz(b)];
+}
+
+inline void host_emulate_cl_inv(u64* a, const Tw* tw, const PrimeC& P) {
+    static u64 tile[CL][CTILE], recv[CL][CTILE];
+    static u64 regs[CL][CNT][CEPT], oth[CL][CNT][CEPT];
+    for (int c = 0; c < CL; c++)
+        for (int b = 0; b < CTILE; b++) tile[c][cswz(b)] = a[c * CTILE + b];
+    for (int p = 0; p < 3; p++) {
+        for (int c = 0; c < CL; c++)
+            for (int t = 0; t < CNT; t++) c_load(regs[c][t], tile[c], cpass(2 - p, c, t));
+        if (p == 0) {
+            for (int c = 0; c < CL; c++)
+                for (int t = 0; t < CNT; t++)
+                    for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
+            for (int c = 0; c < CL; c++)
+                for (int t = 0; t < CNT; t++) c_st0(c, t, regs[c][t], oth[c][t], tw, P.q, P.q2);
+        }
+        for (int c = 0; c < CL; c++)
+            for (int t = 0; t < CNT; t++) {
+                CPass I = cpass(2 - p, c, t);
+                r8_gs(regs[c][t], tw, 1 + 3 * p, I.G, P.q, P.q2);
+                if (p < 2) c_store(regs[c][t], tile[c], I);
+            }
+    }
+    // all-to-all: element (a=c, b) -> CTA b>>7, slot a*128 + (b & 127)
+    for (int c = 0; c < CL; c++)
+        for (int t = 0; t < CNT; t++) {
+            CPass I = cpass(0, c, t);
+            for (int v = 0; v < CEPT; v++) {
+                const int b = I.base + v * I.stride;
+                recv[b >> 7][c * 128 + (b & 127)] = regs[c][t][v];
+            }
+        }
+    for (int c = 0; c < CL; c++)
+        for (int t = 0; t < CNT; t++) {
+            u64 x[CEPT];
+            for (int r = 0; r < CEPT; r++) x[r] = recv[c][r * 128 + t];
+            c_phaseA_inv(x, tw, P);
+            for (int r = 0; r < CEPT; r++) a[r * CTILE + 128 * c + t] = x[r];
+        }
+}
+
+}  // namespace hc

@@ -21,6 +21,7 @@ def ht():
     P = ctypes.c_void_p
     L.ht_init.argtypes = [P, ctypes.c_int, ctypes.c_uint64]
     L.ht_ntt.argtypes = [ctypes.c_int, P, ctypes.c_int]
+    L.ht_ntt_cl.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_compose.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P]
     L.ht_rescale_corr.argtypes = [ctypes.c_int, P, P]
     L.ht_modops.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
@@ -62,6 +63,13 @@ def test_ntt_schedule_matches_reference_transform(setup):
         got = a.copy()
         ht.ht_ntt(k, p_(got), 1)
         assert np.array_equal(got, want_i), f"inverse NTT mismatch for prime {k}"
+        # cluster schedule (8 CTAs, DSMEM exchange) on the same data
+        got = a.copy()
+        ht.ht_ntt_cl(k, p_(got), 0)
+        assert np.array_equal(got, want_f), f"cluster forward NTT mismatch for prime {k}"
+        got = a.copy()
+        ht.ht_ntt_cl(k, p_(got), 1)
+        assert np.array_equal(got, want_i), f"cluster inverse NTT mismatch for prime {k}"
     # lazy-range inputs up to 4q (forward) are accepted
     q = be.q[0]
     a = rand_res(rng, q)
