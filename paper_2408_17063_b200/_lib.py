@@ -16,7 +16,7 @@ import numpy as np
 from .params import BackendMismatch, LevelExhausted, MissingRotationKey
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhcomp.so")
+LIB_PATH = os.environ.get("HCOMP_LIB") or os.path.join(_HERE, "libhcomp.so")
 
 HC_OK = 0
 HC_ERR_ARG = 1
@@ -64,6 +64,8 @@ _SIGS = [
     ("hc_bf_peak", _I, [_P, ctypes.POINTER(ctypes.c_double)]),
     ("hc_bench_xform", _I, [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_double)]),
     ("hc_set_cluster_threshold", _I, [_I]),
+    ("hc_trace_reset", _I, []),
+    ("hc_trace_read", _I, [_P]),
     ("hc_galois_tables", _I, [_I, _U32, _P, _P]),
     ("hc_prim_root_2n", _U64, [_U64, _I]),
 ]

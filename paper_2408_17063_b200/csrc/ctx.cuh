@@ -34,6 +34,7 @@ struct DevCtx {
     PrimeC pc[NPR];
     u64 p, half_p;
     double pinv;
+    u64 pbar;  // floor(2^64 / p): integer Barrett for r mod p
     int L;  // max level
     int pad;
     LevelC lv[MAXL + 1];

@@ -102,7 +102,9 @@ HD void neg_mod_Q(const LevelC& C, u64 (&X)[NLIMB]) {
 }
 
 HD uint16_t digit16(const u64 (&X)[NLIMB], int j) {
-    return (uint16_t)(X[j >> 2] >> (16 * (j & 3)));
+    const int l = j >> 2;  // select chain: keeps X in registers for runtime j
+    const u64 w = l == 0 ? X[0] : l == 1 ? X[1] : l == 2 ? X[2] : X[3];
+    return (uint16_t)(w >> (16 * (j & 3)));
 }
 
 // Modulus-switch correction (see file header).  x = canonical residue of the
@@ -112,7 +114,8 @@ HD void rescale_corr(const DevCtx& D, int l, u64 x, u64* e) {
     const u64 ql = D.pc[l].q;
     const int neg = x > C.half_qd;
     const u64 mag = neg ? ql - x : x;  // |r|
-    u64 rm = mod_small(mag, D.p, D.pinv);
+    u64 rm = mag - mulhi(mag, D.pbar) * D.p;  // Barrett: [0, 2p)
+    if (rm >= D.p) rm -= D.p;
     if (neg && rm) rm = D.p - rm;       // r mod p in [0, p)
     const int dneg = rm > D.half_p;
     const u64 dmag = dneg ? D.p - rm : rm;  // |d|

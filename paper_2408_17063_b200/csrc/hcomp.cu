@@ -58,7 +58,8 @@ struct DevKey {
 };
 
 // transform launches with at most this many jobs use the cluster kernel
-static int CL_MAX_JOBS = 16;
+static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters (split by CL_MAX)
+static const int CL_SPREAD_SMEM = 120 * 1024;
 
 enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET };
 struct Step {
@@ -72,6 +73,9 @@ struct Step {
     long long rows = 0, cstride = 0;
     int period = 0, copies = 0;
     size_t bytes = 0;
+    std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
+    int group = 0;            // consecutive steps with the same nonzero group run concurrently
+    int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
 };
 
 struct Schedule {
@@ -79,6 +83,11 @@ struct Schedule {
     std::vector<void*> allocs;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
+    int cur_group = 0, next_group = 1;
+    // steps added between par_begin() and par_end() are independent: they are
+    // captured on forked streams (parallel graph branches)
+    void par_begin() { cur_group = next_group++; }
+    void par_end() { cur_group = 0; }
     ~Schedule() {
         if (exec) cudaGraphExecDestroy(exec);
         for (void* p : allocs) cudaFree(p);
@@ -96,6 +105,8 @@ struct hc_ctx {
     Tw* d_twi = nullptr;
     uint16_t* d_slot_of = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
     std::map<uint32_t, DevKey> keys;
     std::unique_ptr<Plan> plan;
     int digits[MAXL + 1] = {0, 0, 0, 0};
@@ -107,11 +118,36 @@ static void release_key(DevKey& k) {
     cudaFree(k.perm);
 }
 
+// (direction, loader, epilogue) combinations the schedules use; each gets a
+// single-CTA (k_xf) and an 8-CTA cluster (k_xf_cl) instantiation.
+#define XF_COMBOS(X)                  \
+    X(0, LD_U64, EP_STORE)            \
+    X(1, LD_U64, EP_STORE)            \
+    X(0, LD_RED, EP_STORE)            \
+    X(1, LD_RED, EP_STORE)            \
+    X(1, LD_MONT, EP_RESCALE)         \
+    X(1, LD_MONT, EP_STORE)           \
+    X(1, LD_MONT, EP_RESCALE_ATOMIC)  \
+    X(0, LD_U64, EP_ADDMONT)          \
+    X(0, LD_DIG, EP_STORE)            \
+    X(0, LD_DIGGAL, EP_STORE)         \
+    X(0, LD_RED, EP_ADDRED)           \
+    X(1, LD_RED, EP_ADDRED)           \
+    X(0, LD_COMPOSE, EP_KSACC)        \
+    X(1, LD_KSFIN, EP_STORE)          \
+    X(1, LD_KSFIN, EP_RESCALE)
+
 static int kernels_configured = 0;
 static int configure_kernels() {
     if (kernels_configured) return HC_OK;
-    CU(cudaFuncSetAttribute(k_xform<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));
-    CU(cudaFuncSetAttribute(k_xform<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));
+    // cluster transforms: reserve enough (unused) dynamic smem that each CTA
+    // of a cluster lands on its own SM -- otherwise the scheduler packs all 8
+    // small CTAs onto one or two SMs and nothing is gained
+#define XF_CFG(D, L, E)                                                                                    \
+    CU(cudaFuncSetAttribute(k_xf<D, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));      \
+    CU(cudaFuncSetAttribute(k_xf_cl<D, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    XF_COMBOS(XF_CFG)
+#undef XF_CFG
     CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
     kernels_configured = 1;
     return HC_OK;
@@ -140,6 +176,11 @@ extern "C" int hc_ctx_create(int n, int max_level, const uint64_t* primes, uint6
     // blocking stream: ordered after legacy-stream copies (pageable cudaMemcpy
     // may return before its DMA lands)
     CU(cudaStreamCreate(&h->stream));
+    for (int i = 0; i < 4; i++) {
+        CU(cudaStreamCreateWithFlags(&h->side[i], cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->ev_join[i], cudaEventDisableTiming));
+    }
+    CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
 
     DevCtx& D = h->hctx;
     std::vector<Tw> twf, twi;
@@ -188,7 +229,7 @@ extern "C" int hc_load_ksk(hc_ctx* h, uint32_t t, const uint64_t* ksk) {
     const size_t rows = (size_t)D * 2 * L1;
     CU(cudaMalloc(&k.key, rows * NPOLY * 8));
     CU(cudaMemcpyAsync(k.key, ksk, rows * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
-    k_to_mont<<<592, 256, 0, h->stream>>>(h->d_ctx, k.key, (long long)rows, L1);
+    k_to_mont<<<592, 256, 0, h->stream>>>(h->hctx, k.key, (long long)rows, L1);
     CU(cudaGetLastError());
     std::vector<uint16_t> gal(NPOLY), perm(NPOLY);
     int rc = hc_galois_tables(NPOLY, t, gal.data(), perm.data());
@@ -215,20 +256,41 @@ static int upload_jobs(Schedule& S, Step& st, const void* host, size_t bytes) {
     return HC_OK;
 }
 
-// one step per transform direction (k_xform<0> / k_xform<1>)
+// one step (launch) per (direction, loader, epilogue, transform-less) group,
+// in first-appearance order
+static int g_trace_seq = 0;
 static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
-    for (int dir = 0; dir < 2; dir++) {
+    std::vector<int> taken(jobs.size(), 0);
+    for (size_t i = 0; i < jobs.size(); i++) {
+        if (taken[i]) continue;
         std::vector<XJob> sel;
-        for (const XJob& j : jobs)
-            if (j.dir == dir) sel.push_back(j);
-        if (sel.empty()) continue;
-        Step st;
-        st.kind = ST_XF;
-        st.gy = dir;
-        st.njobs = (int)sel.size();
-        int rc = upload_jobs(S, st, sel.data(), sel.size() * sizeof(XJob));
-        if (rc) return rc;
-        S.steps.push_back(st);
+        for (size_t k = i; k < jobs.size(); k++) {
+            const XJob &a = jobs[i], &b = jobs[k];
+            if (!taken[k] && a.dir == b.dir && a.ld == b.ld && a.ep == b.ep && a.noxf == b.noxf) {
+                sel.push_back(b);
+                taken[k] = 1;
+            }
+        }
+        const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS;
+        const size_t chunk = clu ? (size_t)CL_MAX : sel.size();
+        const int saved = S.cur_group;
+        if (clu && sel.size() > chunk && !S.cur_group) S.par_begin();
+        for (size_t c0 = 0; c0 < sel.size(); c0 += chunk) {
+            std::vector<XJob> part(sel.begin() + c0, sel.begin() + std::min(sel.size(), c0 + chunk));
+            for (XJob& j : part) j.trace = g_trace_seq;
+            g_trace_seq++;
+            Step st;
+            st.kind = ST_XF;
+            st.gy = part[0].dir;
+            st.cl = clu;
+            st.njobs = (int)part.size();
+            st.hjobs = part;
+            st.group = S.cur_group;
+            int rc = upload_jobs(S, st, part.data(), part.size() * sizeof(XJob));
+            if (rc) return rc;
+            S.steps.push_back(st);
+        }
+        if (!saved) S.par_end();
     }
     return HC_OK;
 }
@@ -236,6 +298,7 @@ static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
     if (jobs.empty()) return HC_OK;
     Step st;
     st.kind = ST_CO;
+    st.group = S.cur_group;
     st.njobs = (int)jobs.size();
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(CJob));
     if (rc) return rc;
@@ -246,6 +309,7 @@ static int add_ma(Schedule& S, const std::vector<MJob>& jobs, int nprime) {
     if (jobs.empty()) return HC_OK;
     Step st;
     st.kind = ST_MA;
+    st.group = S.cur_group;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(MJob));
@@ -257,6 +321,7 @@ static int add_dx(Schedule& S, const std::vector<DXJob>& jobs, int nprime) {
     if (jobs.empty()) return HC_OK;
     Step st;
     st.kind = ST_DX;
+    st.group = S.cur_group;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(DXJob));
@@ -272,35 +337,80 @@ static void add_memset(Schedule& S, void* p, size_t bytes) {
     S.steps.push_back(st);
 }
 
-static int enqueue(const hc_ctx* h, const Schedule& S, cudaStream_t s) {
-    for (const Step& st : S.steps) {
+static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
+    {
         switch (st.kind) {
-            case ST_XF:
-                if (st.njobs <= CL_MAX_JOBS) {  // latency path: one 8-CTA cluster per transform
-                    if (st.gy == 0) k_xform_cl<0><<<st.njobs * CL, CNT, 0, s>>>(h->d_ctx, (const XJob*)st.djobs);
-                    else k_xform_cl<1><<<st.njobs * CL, CNT, 0, s>>>(h->d_ctx, (const XJob*)st.djobs);
-                } else {
-                    if (st.gy == 0) k_xform<0><<<st.njobs, NT, NPOLY * 8, s>>>(h->d_ctx, (const XJob*)st.djobs);
-                    else k_xform<1><<<st.njobs, NT, NPOLY * 8, s>>>(h->d_ctx, (const XJob*)st.djobs);
+            case ST_XF: {
+                const XJob& j0 = st.hjobs[0];
+                if (j0.noxf) {
+                    if (j0.ld != LD_KSFIN) return fail(HC_ERR_STATE, "transform-less job needs LD_KSFIN");
+                    k_elem<LD_KSFIN><<<dim3(NPOLY / 256, st.njobs), 128, 0, s>>>(h->hctx, (const XJob*)st.djobs);
+                    break;
                 }
+                const bool clu = st.cl && st.njobs <= CL_MAX;  // latency path: one 8-CTA cluster per transform
+                ClJobs cj;
+                if (clu) {
+                    memset(&cj, 0, sizeof cj);
+                    memcpy(cj.j, st.hjobs.data(), st.njobs * sizeof(XJob));
+                }
+                bool done = false;
+#define XF_LAUNCH(D, L, E)                                                                               \
+    if (!done && j0.dir == D && j0.ld == L && j0.ep == E) {                                              \
+        if (clu) k_xf_cl<D, L, E><<<st.njobs * CL, CNT, CL_SPREAD_SMEM, s>>>(h->hctx, cj);              \
+        else k_xf<D, L, E><<<st.njobs, NT, NPOLY * 8, s>>>(h->hctx, (const XJob*)st.djobs);              \
+        done = true;                                                                                     \
+    }
+                XF_COMBOS(XF_LAUNCH)
+#undef XF_LAUNCH
+                if (!done) return fail(HC_ERR_STATE, "transform job combination not instantiated");
                 break;
+            }
             case ST_CO:
-                k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->d_ctx, (const CJob*)st.djobs);
+                k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->hctx, (const CJob*)st.djobs);
                 break;
             case ST_MA:
-                k_ksmac<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->d_ctx, (const MJob*)st.djobs);
+                k_ksmac<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
                 break;
             case ST_DX:
-                k_diagx<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->d_ctx, (const DXJob*)st.djobs);
+                k_diagx<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);
                 break;
             case ST_SUMC:
-                k_sum_copies<<<592, 256, 0, s>>>(h->d_ctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride);
+                k_sum_copies<<<592, 256, 0, s>>>(h->hctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride);
                 break;
             case ST_MEMSET:
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
                 break;
         }
         CU(cudaGetLastError());
+    }
+    return HC_OK;
+}
+
+// Steps of one nonzero group are independent: fork them onto side streams
+// (parallel branches under graph capture) and join back on `s`.
+static int enqueue(const hc_ctx* h, const Schedule& S, cudaStream_t s) {
+    const size_t n = S.steps.size();
+    for (size_t i = 0; i < n;) {
+        size_t e = i + 1;
+        if (S.steps[i].group)
+            while (e < n && S.steps[e].group == S.steps[i].group) e++;
+        if (e - i == 1) {
+            int rc = enqueue_step(h, S.steps[i], s);
+            if (rc) return rc;
+        } else {
+            CU(cudaEventRecord(h->ev_fork, s));
+            const size_t nb = std::min<size_t>(e - i, 4);
+            for (size_t b = 0; b < nb; b++) CU(cudaStreamWaitEvent(h->side[b], h->ev_fork, 0));
+            for (size_t k = i; k < e; k++) {
+                int rc = enqueue_step(h, S.steps[k], h->side[(k - i) % 4]);
+                if (rc) return rc;
+            }
+            for (size_t b = 0; b < nb; b++) {
+                CU(cudaEventRecord(h->ev_join[b], h->side[b]));
+                CU(cudaStreamWaitEvent(s, h->ev_join[b], 0));
+            }
+        }
+        i = e;
     }
     return HC_OK;
 }
@@ -359,7 +469,7 @@ struct Plan {
     uint16_t *digR = nullptr, *digU = nullptr;
     u64 *Ecp = nullptr, *PX = nullptr;
     u64 *A0 = nullptr, *A1 = nullptr, *A1coef = nullptr, *dnttG = nullptr, *RES = nullptr;
-    u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr;
+    u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr, *ACC = nullptr;
     uint16_t *digG = nullptr, *digF = nullptr;
     std::unique_ptr<Schedule> full, fin;
     std::map<std::pair<long long, long long>, std::unique_ptr<Schedule>> partials;
@@ -518,6 +628,7 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
     PA(P->dnttF, (size_t)P->D1 * 2 * NB);
     PA(P->corr, (size_t)2 * NB);
     PA(P->OUT, (size_t)2 * NB);
+    PA(P->ACC, (size_t)2 * 2 * NB);
 #undef PA
 
     // ---- plaintexts on device (K6) ----
@@ -544,7 +655,7 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
         CU(cudaMemcpy(dj, pj.data(), pj.size() * sizeof(PJob), cudaMemcpyHostToDevice));
         for (size_t off = 0; off < pj.size(); off += maxb) {
             int cnt = (int)std::min(maxb, pj.size() - off);
-            k_plain<<<cnt, NT, 2 * NPOLY * 8, h->stream>>>(h->d_ctx, dj + off, S);
+            k_plain<<<cnt, NT, 2 * NPOLY * 8, h->stream>>>(h->hctx, dj + off, S);
         }
         cudaError_t e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
@@ -722,15 +833,20 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     }
                 }
         }
+        S.par_begin();
         rc = add_xf(S, s1); if (rc) return rc;
+        S.par_end();
+        S.par_begin();
         rc = add_xf(S, s2); if (rc) return rc;
         rc = add_co(S, s2c); if (rc) return rc;
+        S.par_end();
         rc = add_xf(S, s3); if (rc) return rc;
         rc = add_ma(S, s4, 3); if (rc) return rc;
         rc = add_xf(S, s5); if (rc) return rc;
         rc = add_co(S, s6); if (rc) return rc;
         rc = add_xf(S, s7); if (rc) return rc;
         rc = add_ma(S, s8, 3); if (rc) return rc;
+        S.par_begin();  // S9 and S10 both only read the rotated inputs
         rc = add_xf(S, s9); if (rc) return rc;
         // S10: kept-prime half of the diagonal products, X[g] += sum src * diag * q^-1
         {
@@ -775,6 +891,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                 if (rc) return rc;
             }
         }
+        S.par_end();
     }
     // fold E copies into PX[0]
     Step st;
@@ -789,7 +906,32 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
     return HC_OK;
 }
 
-// T1..T4, folds F1..F4 and the output mask D1..D2 (compress.py:298-310).
+static const KsSpec* upload_spec(Schedule& S, const KsSpec& spec, int* rc) {
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(KsSpec));
+    if (e == cudaSuccess) e = cudaMemcpy(d, &spec, sizeof(KsSpec), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        *rc = fail(HC_ERR_CUDA, std::string("spec upload: ") + cudaGetErrorString(e));
+        return nullptr;
+    }
+    S.allocs.push_back(d);
+    *rc = HC_OK;
+    return (const KsSpec*)d;
+}
+
+// Tail: giant steps, folds and the output mask (compress.py:298-310), level 1.
+// Key switches finish in the digit-NTT epilogue: each digit transform
+// multiplies its output by its key digit and red.add's it into ACC (u64;
+// at most (giant-1)*D_1 = 49 addends < 2^60, exact); the consumer's loader
+// (LD_KSFIN) adds base + permuted c0 terms + red(ACC) and re-zeroes ACC.
+//   T1   acc[g] = X[g] + NTT(E[g]) (c1 of g >= 1 in coefficient domain)
+//   T3   giant digit NTTs (CRT/digit split in the loader, KSACC epilogue)
+//   per fold f:
+//     F1 INTT of res_f.c1 (LD_KSFIN, side-stores res_f.c1) + two
+//        transform-less jobs materialising res_f.c0
+//     F3 fold digit NTTs (LD_COMPOSE -> EP_KSACC)
+//   D1   INTT of res_F * mask at the dropped prime (LD_KSFIN * mask) + rescale
+//   D2   NTT of the correction + res_F * mask * q^-1 at the kept prime
 static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     const size_t NB = NPOLY;
     const int G = P.giant, D1 = P.D1;
@@ -797,7 +939,8 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     const u64* X = P.PX + (size_t)G * 2 * 2 * NB;
     auto ex = [&](const u64* base, int g, int poly, int k) { return base + (((size_t)g * 2 + poly) * 2 + k) * NB; };
     int rc;
-    // T1: acc[g] = X[g] + NTT(E[g]); c1 of g >= 1 in coefficient domain
+    add_memset(S, P.ACC, (size_t)2 * 2 * NB * 8);
+    // T1
     std::vector<XJob> t1;
     for (int g = 0; g < G; g++) {
         if (!P.acc_live[g]) continue;
@@ -824,112 +967,121 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
             }
         }
     }
+    S.par_begin();
     rc = add_xf(S, t1); if (rc) return rc;
-    // T2/T3/T4: giant-step rotations summed into res (level 1)
-    std::vector<CJob> t2;
-    std::vector<XJob> t3;
-    MJob t4{};
-    t4.level = 1;
-    t4.nterm = 0;
+    S.par_end();
+    auto digit_jobs = [&](std::vector<XJob>& out, const u64* coef, const DevKey* key) {
+        for (int d = 0; d < D1; d++)
+            for (int k = 0; k < 2; k++) {
+                XJob j{};
+                j.dir = 0; j.k = k; j.ld = LD_COMPOSE; j.ep = EP_KSACC;
+                j.a = coef;
+                j.gal = key->gal;
+                j.clevel = 1;
+                j.dig = d;
+                j.ea = key->key + ((size_t)(d * 2 + 0) * 4 + k) * NB;  // b_d at prime k
+                j.eb = key->key + ((size_t)(d * 2 + 1) * 4 + k) * NB;  // a_d at prime k
+                j.out = P.ACC + (size_t)k * NB;                         // c0 row; c1 row at +2n
+                j.ostride = 2 * NB;
+                out.push_back(j);
+            }
+    };
+    // T3 + the specs of res_0 = acc[0] + sum_g rot(acc[g], g*baby)
+    KsSpec s0{}, s1{};
+    s0.level = s1.level = 1;
+    s0.D = s1.D = D1;
+    s0.ab = 0;
+    s1.ab = 1;
+    s0.acc = P.ACC;
+    s1.acc = P.ACC + 2 * NB;
     if (P.acc_live[0]) {
-        t4.add0 = P.A0;
-        t4.add1 = P.A1;
+        s0.base = P.A0;
+        s1.base = P.A1;
     }
-    std::vector<MJob> t4extra;  // more than MAXTERM terms: chain extra jobs
+    std::vector<XJob> t3;
     for (int g = 1; g < G; g++) {
         if (!P.acc_live[g]) continue;
         const DevKey* kg = need_key(h, P.t_giant[g]);
-        CJob c{};
-        c.level = 1; c.mode = 0;
-        c.x = P.A1coef + (size_t)g * 2 * NB;
-        c.xstride = NB;
-        c.gal = kg->gal;
-        c.dig = P.digG + (size_t)g * D1 * NB;
-        t2.push_back(c);
-        for (int jj = 0; jj < D1; jj++)
-            for (int k = 0; k < 2; k++) {
-                XJob j{};
-                j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
-                j.a = (const u64*)(P.digG + ((size_t)g * D1 + jj) * NB);
-                j.out = P.dnttG + (((size_t)g * D1 + jj) * 2 + k) * NB;
-                t3.push_back(j);
-            }
-        if (t4.nterm == MAXTERM) return fail(HC_ERR_ARG, "too many giant steps");
-        MTerm& T = t4.t[t4.nterm++];
-        T.dntt = P.dnttG + (size_t)g * D1 * 2 * NB;
-        T.key = kg->key;
+        digit_jobs(t3, P.A1coef + (size_t)g * 2 * NB, kg);
+        if (s0.nterm == MAXTERM_KS) return fail(HC_ERR_ARG, "too many giant steps");
+        KsTerm T{};
         T.c0src = P.A0 + (size_t)g * 2 * NB;
         T.perm = kg->perm;
+        s0.t[s0.nterm++] = T;
     }
-    rc = add_co(S, t2); if (rc) return rc;
     rc = add_xf(S, t3); if (rc) return rc;
-    u64* res[2] = {P.RES, P.RES + (size_t)2 * 2 * NB};
-    t4.out0 = res[0];
-    t4.out1 = res[0] + 2 * NB;
-    rc = add_ma(S, std::vector<MJob>{t4}, 2); if (rc) return rc;
-    // folds: res += rot_row(res, a)
+    u64* res[2] = {P.RES, P.RES + (size_t)2 * 2 * NB};  // [poly][prime][n] each
     for (int f = 0; f < P.F; f++) {
         u64* cur = res[f % 2];
-        u64* nxt = res[(f + 1) % 2];
         const DevKey* ka = need_key(h, P.t_fold[f]);
+        const KsSpec* d0 = upload_spec(S, s0, &rc); if (rc) return rc;
+        const KsSpec* d1 = upload_spec(S, s1, &rc); if (rc) return rc;
         std::vector<XJob> f1, f3;
         for (int k = 0; k < 2; k++) {
             XJob j{};
-            j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
-            j.a = cur + (size_t)(2 + k) * NB;
+            j.dir = 1; j.k = k; j.ld = LD_KSFIN; j.ep = EP_STORE;
+            j.ks = d1;
+            j.aux = cur + (size_t)(2 + k) * NB;  // res_f.c1
             j.out = P.rc1coef + (size_t)k * NB;
             f1.push_back(j);
+            XJob e{};
+            e.dir = 1; e.k = k; e.ld = LD_KSFIN; e.noxf = 1;
+            e.ks = d0;
+            e.aux = cur + (size_t)k * NB;  // res_f.c0
+            f1.push_back(e);
         }
-        CJob c{};
-        c.level = 1; c.mode = 0;
-        c.x = P.rc1coef;
-        c.xstride = NB;
-        c.gal = ka->gal;
-        c.dig = P.digF;
-        for (int jj = 0; jj < D1; jj++)
-            for (int k = 0; k < 2; k++) {
-                XJob j{};
-                j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
-                j.a = (const u64*)(P.digF + (size_t)jj * NB);
-                j.out = P.dnttF + ((size_t)jj * 2 + k) * NB;
-                f3.push_back(j);
-            }
-        MJob mj{};
-        mj.level = 1; mj.nterm = 1;
-        mj.t[0].dntt = P.dnttF;
-        mj.t[0].key = ka->key;
-        mj.t[0].c0src = cur;
-        mj.t[0].perm = ka->perm;
-        mj.add0 = cur;
-        mj.add1 = cur + 2 * NB;
-        mj.out0 = nxt;
-        mj.out1 = nxt + 2 * NB;
+        digit_jobs(f3, P.rc1coef, ka);
+        S.par_begin();  // res_f.c1 INTT and the res_f.c0 finish are independent
         rc = add_xf(S, f1); if (rc) return rc;
-        rc = add_co(S, std::vector<CJob>{c}); if (rc) return rc;
+        S.par_end();
         rc = add_xf(S, f3); if (rc) return rc;
-        rc = add_ma(S, std::vector<MJob>{mj}, 2); if (rc) return rc;
+        // res_{f+1} = res_f + rot(res_f, a)
+        s0 = KsSpec{};
+        s1 = KsSpec{};
+        s0.level = s1.level = 1;
+        s0.D = s1.D = D1;
+        s0.ab = 0;
+        s1.ab = 1;
+        s0.acc = P.ACC;
+        s1.acc = P.ACC + 2 * NB;
+        s0.base = cur;
+        s1.base = cur + 2 * NB;
+        s0.nterm = 1;
+        s0.t[0].c0src = cur;
+        s0.t[0].perm = ka->perm;
     }
-    // D1/D2: mul_plain(res, output_mask) level 1 -> 0
+    // D1/D2: mul_plain(res_F, output_mask) level 1 -> 0
     u64* fin = res[P.F % 2];
-    std::vector<XJob> d1, d2;
+    const KsSpec* d0 = upload_spec(S, s0, &rc); if (rc) return rc;
+    const KsSpec* d1 = upload_spec(S, s1, &rc); if (rc) return rc;
+    std::vector<XJob> dd1, dd2;
     for (int poly = 0; poly < 2; poly++) {
+        const KsSpec* sp = poly == 0 ? d0 : d1;
         XJob j{};
-        j.dir = 1; j.k = 1; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 1;
-        j.a = fin + ((size_t)poly * 2 + 1) * NB;
+        j.dir = 1; j.k = 1; j.ld = LD_KSFIN; j.ep = EP_RESCALE; j.level = 1;
+        j.ks = sp;
         j.b = P.omask + NB;
+        j.aux = fin + ((size_t)poly * 2 + 1) * NB;
         j.out = P.corr + (size_t)poly * NB;
         j.ostride = NB;
-        d1.push_back(j);
+        dd1.push_back(j);
+        XJob e{};
+        e.dir = 1; e.k = 0; e.ld = LD_KSFIN; e.noxf = 1;
+        e.ks = sp;
+        e.aux = fin + ((size_t)poly * 2 + 0) * NB;
+        dd1.push_back(e);
         XJob o{};
         o.dir = 0; o.k = 0; o.ld = LD_U64; o.ep = EP_ADDMONT;
         o.a = P.corr + (size_t)poly * NB;
         o.ea = fin + ((size_t)poly * 2 + 0) * NB;
         o.eb = P.omask;
         o.out = P.OUT + (size_t)poly * NB;
-        d2.push_back(o);
+        dd2.push_back(o);
     }
-    rc = add_xf(S, d1); if (rc) return rc;
-    rc = add_xf(S, d2); if (rc) return rc;
+    S.par_begin();
+    rc = add_xf(S, dd1); if (rc) return rc;
+    S.par_end();
+    rc = add_xf(S, dd2); if (rc) return rc;
     return HC_OK;
 }
 
@@ -1100,7 +1252,7 @@ extern "C" int hc_pointwise(hc_ctx* h, const uint64_t* a, const uint64_t* b, uin
     CU(cudaMemcpy(da.p, a, bytes, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(dp.p, pidx, rows * sizeof(int), cudaMemcpyHostToDevice));
-    k_pointwise<<<592, 256, 0, h->stream>>>(h->d_ctx, (u64*)da.p, (u64*)db.p, (u64*)da.p, rows, (int*)dp.p, op);
+    k_pointwise<<<592, 256, 0, h->stream>>>(h->hctx, (u64*)da.p, (u64*)db.p, (u64*)da.p, rows, (int*)dp.p, op);
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaMemcpy(out, da.p, bytes, cudaMemcpyDeviceToHost));
@@ -1258,11 +1410,11 @@ extern "C" int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* st
 // (Harvey lazy Shoup, bf_ct) in registers at full occupancy, no memory
 // traffic.  Returns butterflies per second; the integer-ALU roofline
 // denominator for k_xform.
-__global__ void __launch_bounds__(256) k_bf_peak(const DevCtx* __restrict__ C, int iters, u64* sink) {
-    const PrimeC P = C->pc[0];
+__global__ void __launch_bounds__(256) k_bf_peak(const __grid_constant__ DevCtx C, int iters, u64* sink) {
+    const PrimeC P = C.pc[0];
     u64 x[16];
     for (int i = 0; i < 16; i++) x[i] = (threadIdx.x * 977 + i * 131 + blockIdx.x) % P.q;
-    u64 w = C->twf[5].w, ws = C->twf[5].ws;
+    u64 w = C.twf[5].w, ws = C.twf[5].ws;
     for (int it = 0; it < iters; it++) {
         HC_UNROLL
         for (int i = 0; i < 8; i++) bf_ct(x[i], x[i + 8], w, ws, P.q, P.q2);
@@ -1282,12 +1434,12 @@ extern "C" int hc_bf_peak(hc_ctx* h, double* bfly_per_s) {
     DevBuf sink;
     CU(cudaMalloc(&sink.p, 8));
     const int blocks = nsm * 8, iters = 4096;
-    k_bf_peak<<<blocks, 256, 0, h->stream>>>(h->d_ctx, 64, (u64*)sink.p);  // warm-up
+    k_bf_peak<<<blocks, 256, 0, h->stream>>>(h->hctx, 64, (u64*)sink.p);  // warm-up
     cudaEvent_t a, b;
     CU(cudaEventCreate(&a));
     CU(cudaEventCreate(&b));
     CU(cudaEventRecord(a, h->stream));
-    k_bf_peak<<<blocks, 256, 0, h->stream>>>(h->d_ctx, iters, (u64*)sink.p);
+    k_bf_peak<<<blocks, 256, 0, h->stream>>>(h->hctx, iters, (u64*)sink.p);
     CU(cudaEventRecord(b, h->stream));
     CU(cudaEventSynchronize(b));
     float ms = 0;
@@ -1344,6 +1496,26 @@ extern "C" int hc_bench_xform(hc_ctx* h, int njobs, int dir, int iters, double* 
     return HC_OK;
 }
 
+// HC_TRACE builds: reset the launch numbering / read back the per-CTA
+// %globaltimer stamps [launch][block][point] (128 x 512 x 8 u64).
+extern "C" int hc_trace_reset(void) {
+    g_trace_seq = 0;
+#ifdef HC_TRACE
+    static unsigned long long zero[TR_LAUNCH][TR_BLK][TR_PT];
+    CU(cudaMemcpyToSymbol(g_trace, zero, sizeof(zero)));
+#endif
+    return HC_OK;
+}
+extern "C" int hc_trace_read(uint64_t* out) {
+#ifdef HC_TRACE
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace)));
+    return HC_OK;
+#else
+    return fail(HC_ERR_STATE, "library built without HC_TRACE");
+#endif
+}
+
 extern "C" void hc_ctx_destroy(hc_ctx* h) {
     if (!h) return;
     cudaSetDevice(h->dev);
@@ -1355,5 +1527,10 @@ extern "C" void hc_ctx_destroy(hc_ctx* h) {
     cudaFree(h->d_slot_of);
     cudaFree(h->d_ctx);
     if (h->stream) cudaStreamDestroy(h->stream);
+    for (int i = 0; i < 4; i++) {
+        if (h->side[i]) cudaStreamDestroy(h->side[i]);
+        if (h->ev_join[i]) cudaEventDestroy(h->ev_join[i]);
+    }
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     delete h;
 }

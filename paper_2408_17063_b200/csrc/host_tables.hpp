@@ -110,6 +110,7 @@ static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<T
     D.p = p;
     D.half_p = p >> 1;
     D.pinv = 1.0 / (double)p;
+    D.pbar = (u64)(((u128)1 << 64) / p);
     twf.assign((size_t)NPR * n, Tw{});
     twi.assign((size_t)NPR * n, Tw{});
     // chain primes at RNS rows 0..L; unused rows (L < 3) get a copy of prime 0

@@ -33,6 +33,27 @@ enum : int {
     LD_RED = 3,    // a[j] reduced from any u64 (+ b[j] likewise if b)
     LD_DIG = 4,    // u16 digit a[j]
     LD_DIGGAL = 5, // u16 digit gathered: gal[j] -> (neg ? b : a)[src]
+    LD_COMPOSE = 6,// base-2^16 digit J.dig of CRT(a[k][src]) at level J.clevel, through gal
+    LD_KSMAC = 7,  // key-switch finish (KsSpec) [* b Montgomery], side-stored to aux
+    LD_KSFIN = 8,  // base + sum_t c0src_t[perm_t] + red(acc) (KsSpec.acc, zeroed) [* b], aux
+};
+
+// Key-switch finish for one output poly (c0: ab = 0, c1: ab = 1) at prime k:
+//   v = base[k][j] + sum_t ( c0src_t[k][perm_t[j]] (ab = 0 only)
+//                            + REDC(sum_d dntt_t[d][k][j] * key_t[d][ab][k][j]) )
+// = the k_ksmac computation, fused into the consumer's loader.
+constexpr int MAXTERM_KS = 8;
+struct KsTerm {
+    const u64* dntt;  // [D][P][n]
+    const u64* key;   // [D_L][2][L+1][n] Montgomery
+    const u64* c0src; // [P][n] (ab = 0)
+    const uint16_t* perm;
+};
+struct KsSpec {
+    int level, nterm, ab, D;  // D = digits at `level`
+    const u64* base;  // [P][n] or null
+    KsTerm t[MAXTERM_KS];
+    u64* acc;         // LD_KSFIN: [P][n] digit-product accumulator (EP_KSACC), zeroed after use
 };
 enum : int {
     EP_STORE = 0,          // out[j] = x
@@ -41,6 +62,7 @@ enum : int {
     EP_ADDRED = 3,         // out[j] = x + red(ea[j])
     EP_RESCALE = 4,        // out[k*ostride + j] = e_k (k < level)
     EP_RESCALE_ATOMIC = 5, // atomic += e_k
+    EP_KSACC = 6,          // key-switch digit product: out[j] += x*ea[j], out[ostride+j] += x*eb[j]
 };
 
 struct XJob {
@@ -48,7 +70,11 @@ struct XJob {
     int k;      // RNS prime index of the transform
     int ld, ep;
     int level;  // EP_RESCALE*: level switched from (k == level)
-    int pad;
+    int noxf;   // 1: loader + side store only (no transform, no epilogue)
+    int trace;  // HC_TRACE builds: launch sequence number
+    int dig, clevel;     // LD_COMPOSE: digit index, CRT level
+    const KsSpec* ks;    // LD_KSMAC
+    u64* aux;            // LD_KSMAC side store of the pre-transform value
     const u64* a;
     const u64* b;
     const uint16_t* gal;
@@ -58,180 +84,215 @@ struct XJob {
     long long ostride;
 };
 
-// Loader: fill the smem tile (coefficient j at sm[swz(j)], thread t owns
-// j = t + 512 v).  Global loads are issued 16-wide per thread before any use
-// (latency overlap); each loader kind is its own unrolled loop.
-__device__ __forceinline__ void xf_load(const XJob& J, const PrimeC& P, u64* sm, int tid) {
-    u64 a[EPT];
-    switch (J.ld) {
-        case LD_MONT: {
-            u64 b[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) { a[v] = J.a[tid + NT * v]; b[v] = J.b[tid + NT * v]; }
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = mul_mont(a[v], b[v], P.q, P.qneg);
-            break;
-        }
-        case LD_ADD: {
-            u64 b[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) { a[v] = J.a[tid + NT * v]; b[v] = J.b[tid + NT * v]; }
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = add_mod(a[v], b[v], P.q);
-            break;
-        }
-        case LD_RED: {
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = J.a[tid + NT * v];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = red64(a[v], P.q, P.one_s);
-            if (J.b) {
-                u64 b[EPT];
-                HC_UNROLL
-                for (int v = 0; v < EPT; v++) b[v] = J.b[tid + NT * v];
-                HC_UNROLL
-                for (int v = 0; v < EPT; v++) a[v] = add_mod(a[v], red64(b[v], P.q, P.one_s), P.q);
-            }
-            break;
-        }
-        case LD_DIG: {
-            const uint16_t* d = reinterpret_cast<const uint16_t*>(J.a);
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = d[tid + NT * v];
-            break;
-        }
-        case LD_DIGGAL: {
-            unsigned e[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) e[v] = J.gal[tid + NT * v];
-            const uint16_t* dp = reinterpret_cast<const uint16_t*>(J.a);
-            const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = ((e[v] >> 15) ? dn : dp)[e[v] & 0x7FFF];
-            break;
-        }
-        default:  // LD_U64
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = J.a[tid + NT * v];
-    }
-    sm_store(a, sm, tid, NT);
-}
-
-// Epilogue: consume the canonical transform output (smem tile).
-__device__ __forceinline__ void xf_store(const XJob& J, const DevCtx& D, const PrimeC& P, const u64* sm, int tid) {
-    u64 x[EPT];
-    sm_load(x, sm, tid, NT);
-    switch (J.ep) {
-        case EP_ADDMONT: {
-            u64 a[EPT], b[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) { a[v] = J.ea[tid + NT * v]; b[v] = J.eb[tid + NT * v]; }
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = add_mod(x[v], mul_mont(a[v], b[v], P.q, P.qneg), P.q);
-            break;
-        }
-        case EP_ADD: {
-            u64 a[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = J.ea[tid + NT * v];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = add_mod(x[v], a[v], P.q);
-            break;
-        }
-        case EP_ADDRED: {
-            u64 a[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) a[v] = J.ea[tid + NT * v];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = add_mod(x[v], red64(a[v], P.q, P.one_s), P.q);
-            break;
-        }
-        case EP_RESCALE:
-        case EP_RESCALE_ATOMIC: {
-            const int l = J.level;
-            const bool atom = J.ep == EP_RESCALE_ATOMIC;
-            HC_NOUNROLL
-            for (int v = 0; v < EPT; v++) {
-                u64 xv = sm[swz(tid + NT * v)];
-                u64 e[MAXL];
-                rescale_corr(D, l, xv, e);
-                HC_UNROLL
-                for (int k = 0; k < MAXL; k++) {
-                    if (k >= l) break;
-                    u64* o = J.out + (size_t)k * J.ostride + tid + NT * v;
-                    if (!atom) *o = e[k];
-                    else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)e[k]);
-                }
-            }
-            break;
-        }
-        default:  // EP_STORE
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) J.out[tid + NT * v] = x[v];
-    }
-}
-
-// One transform job per CTA: loader -> smem tile -> NTT/INTT -> epilogue.
-// DIR 0 = forward, 1 = inverse (J.dir must match).
-template <int DIR>
-__global__ void __launch_bounds__(NT, 1) k_xform(const DevCtx* __restrict__ C, const XJob* __restrict__ jobs) {
-    extern __shared__ u64 sm[];
-    const XJob J = jobs[blockIdx.x];
-    const int tid = threadIdx.x;
-    const PrimeC P = C->pc[J.k];
-    xf_load(J, P, sm, tid);
-    __syncthreads();
-    if (DIR == 0) cta_ntt_fwd(C->twf + (size_t)J.k * NPOLY, P, sm);
-    else cta_ntt_inv(C->twi + (size_t)J.k * NPOLY, P, sm);
-    xf_store(J, *C, P, sm, tid);
-}
+#ifdef HC_TRACE
+constexpr int TR_LAUNCH = 128, TR_BLK = 512, TR_PT = 8;
+__device__ unsigned long long g_trace[TR_LAUNCH][TR_BLK][TR_PT];
+#define TRACE(pt)                                                                    \
+    do {                                                                             \
+        if (threadIdx.x == 0 && J.trace < TR_LAUNCH && blockIdx.x < TR_BLK) {       \
+            unsigned long long tnow;                                                 \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));                 \
+            g_trace[J.trace][blockIdx.x][pt] = tnow;                                 \
+        }                                                                            \
+    } while (0)
+#else
+#define TRACE(pt) \
+    do {          \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
-// k_xform_cl: the same jobs on the latency path, one job per 8-CTA cluster
-// (ntt_cl.cuh).  Loads/stores go through per-coefficient loader/epilogue
-// helpers (8 independent accesses per thread, unrolled).
+// Loaders and epilogues, compile-time specialised (one kernel instantiation
+// per (direction, loader, epilogue) used by the schedule -- no unused code
+// paths, no register spills).  Each handles N coefficients j0 + e*stride per
+// thread and issues every round of global loads for all N before any use.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ u64 ld_elem(const XJob& J, const PrimeC& P, int j) {
-    switch (J.ld) {
-        case LD_MONT: return mul_mont(J.a[j], J.b[j], P.q, P.qneg);
-        case LD_ADD: return add_mod(J.a[j], J.b[j], P.q);
-        case LD_RED: {
-            u64 v = red64(J.a[j], P.q, P.one_s);
-            if (J.b) v = add_mod(v, red64(J.b[j], P.q, P.one_s), P.q);
-            return v;
-        }
-        case LD_DIG: return reinterpret_cast<const uint16_t*>(J.a)[j];
-        case LD_DIGGAL: {
-            const unsigned e = J.gal[j];
-            return reinterpret_cast<const uint16_t*>((e >> 15) ? J.b : J.a)[e & 0x7FFF];
-        }
-        default: return J.a[j];
+
+template <int N, int L>
+__device__ __forceinline__ void ld_compose(const DevCtx& C, const XJob& J, int j0, int stride, u64 (&x)[N]) {
+    unsigned src[N];
+    HC_UNROLL
+    for (int e = 0; e < N; e++) src[e] = J.gal ? (unsigned)J.gal[j0 + e * stride] : (unsigned)(j0 + e * stride);
+    u64 xr[N][L + 1];
+    HC_UNROLL
+    for (int e = 0; e < N; e++) {
+        HC_UNROLL
+        for (int k = 0; k <= L; k++) xr[e][k] = J.a[(size_t)k * NPOLY + (src[e] & 0x7FFF)];
+    }
+    HC_UNROLL
+    for (int e = 0; e < N; e++) {
+        u64 X[NLIMB];
+        crt_compose<L>(C.lv[L], C.pc, xr[e], X);
+        if (J.gal && (src[e] >> 15)) neg_mod_Q<L>(C.lv[L], X);
+        x[e] = digit16(X, J.dig);
     }
 }
 
-__device__ __forceinline__ void st_elem(const XJob& J, const DevCtx& D, const PrimeC& P, int j, u64 x) {
-    switch (J.ep) {
-        case EP_ADDMONT: J.out[j] = add_mod(x, mul_mont(J.ea[j], J.eb[j], P.q, P.qneg), P.q); break;
-        case EP_ADD: J.out[j] = add_mod(x, J.ea[j], P.q); break;
-        case EP_ADDRED: J.out[j] = add_mod(x, red64(J.ea[j], P.q, P.one_s), P.q); break;
-        case EP_RESCALE:
-        case EP_RESCALE_ATOMIC: {
-            const int l = J.level;
-            u64 e[MAXL];
-            rescale_corr(D, l, x, e);
+template <int N>
+__device__ __forceinline__ void ld_ksfin(const XJob& J, const PrimeC& P, int j0, int stride, u64 (&x)[N]) {
+    const KsSpec& S = *J.ks;
+    const size_t kofs = (size_t)J.k * NPOLY;
+    u64 acc[N];
+    HC_UNROLL
+    for (int e = 0; e < N; e++) {
+        x[e] = S.base ? S.base[kofs + j0 + e * stride] : 0;
+        acc[e] = S.acc ? S.acc[kofs + j0 + e * stride] : 0;
+    }
+    for (int t = 0; t < S.nterm; t++) {
+        const KsTerm T = S.t[t];
+        if (!T.c0src) continue;
+        unsigned pe[N];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) pe[e] = T.perm[j0 + e * stride];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = add_mod(x[e], T.c0src[kofs + pe[e]], P.q);
+    }
+    HC_UNROLL
+    for (int e = 0; e < N; e++) x[e] = add_mod(x[e], red64(acc[e], P.q, P.one_s), P.q);
+    if (S.acc) {
+        HC_UNROLL
+        for (int e = 0; e < N; e++) S.acc[kofs + j0 + e * stride] = 0;
+    }
+    if (J.aux) {
+        HC_UNROLL
+        for (int e = 0; e < N; e++) J.aux[j0 + e * stride] = x[e];
+    }
+    if (J.b) {
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = mul_mont(x[e], J.b[j0 + e * stride], P.q, P.qneg);
+    }
+}
+
+template <int LD, int N>
+__device__ __forceinline__ void load_n(const DevCtx& C, const XJob& J, const PrimeC& P, int j0, int stride, u64 (&x)[N]) {
+    if constexpr (LD == LD_MONT || LD == LD_ADD) {
+        u64 b[N];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) { x[e] = J.a[j0 + e * stride]; b[e] = J.b[j0 + e * stride]; }
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = LD == LD_MONT ? mul_mont(x[e], b[e], P.q, P.qneg) : add_mod(x[e], b[e], P.q);
+    } else if constexpr (LD == LD_RED) {
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = J.a[j0 + e * stride];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = red64(x[e], P.q, P.one_s);
+    } else if constexpr (LD == LD_DIG) {
+        const uint16_t* d = reinterpret_cast<const uint16_t*>(J.a);
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = d[j0 + e * stride];
+    } else if constexpr (LD == LD_DIGGAL) {
+        unsigned g[N];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) g[e] = J.gal[j0 + e * stride];
+        const uint16_t* dp = reinterpret_cast<const uint16_t*>(J.a);
+        const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = ((g[e] >> 15) ? dn : dp)[g[e] & 0x7FFF];
+    } else if constexpr (LD == LD_COMPOSE) {
+        switch (J.clevel) {
+            case 1: ld_compose<N, 1>(C, J, j0, stride, x); break;
+            case 2: ld_compose<N, 2>(C, J, j0, stride, x); break;
+            default: ld_compose<N, 3>(C, J, j0, stride, x); break;
+        }
+    } else if constexpr (LD == LD_KSFIN) {
+        ld_ksfin<N>(J, P, j0, stride, x);
+    } else {  // LD_U64
+        HC_UNROLL
+        for (int e = 0; e < N; e++) x[e] = J.a[j0 + e * stride];
+    }
+}
+
+template <int EP, int N>
+__device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const PrimeC& P, int j0, int stride,
+                                        const u64 (&x)[N]) {
+    if constexpr (EP == EP_ADDMONT || EP == EP_KSACC) {
+        u64 a[N], b[N];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) { a[e] = J.ea[j0 + e * stride]; b[e] = J.eb[j0 + e * stride]; }
+        HC_UNROLL
+        for (int e = 0; e < N; e++) {
+            const int j = j0 + e * stride;
+            if constexpr (EP == EP_ADDMONT) {
+                J.out[j] = add_mod(x[e], mul_mont(a[e], b[e], P.q, P.qneg), P.q);
+            } else {
+                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + j), (unsigned long long)mul_mont(x[e], a[e], P.q, P.qneg));
+                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + J.ostride + j), (unsigned long long)mul_mont(x[e], b[e], P.q, P.qneg));
+            }
+        }
+    } else if constexpr (EP == EP_ADD || EP == EP_ADDRED) {
+        u64 a[N];
+        HC_UNROLL
+        for (int e = 0; e < N; e++) a[e] = J.ea[j0 + e * stride];
+        HC_UNROLL
+        for (int e = 0; e < N; e++)
+            J.out[j0 + e * stride] = add_mod(x[e], EP == EP_ADD ? a[e] : red64(a[e], P.q, P.one_s), P.q);
+    } else if constexpr (EP == EP_RESCALE || EP == EP_RESCALE_ATOMIC) {
+        const int l = J.level;
+        HC_UNROLL
+        for (int e = 0; e < N; e++) {
+            u64 ek[MAXL];
+            rescale_corr(D, l, x[e], ek);
             HC_UNROLL
             for (int k = 0; k < MAXL; k++) {
                 if (k >= l) break;
-                u64* o = J.out + (size_t)k * J.ostride + j;
-                if (J.ep == EP_RESCALE) *o = e[k];
-                else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)e[k]);
+                u64* o = J.out + (size_t)k * J.ostride + j0 + e * stride;
+                if constexpr (EP == EP_RESCALE) *o = ek[k];
+                else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)ek[k]);
             }
-            break;
         }
-        default: J.out[j] = x;
+    } else {  // EP_STORE
+        HC_UNROLL
+        for (int e = 0; e < N; e++) J.out[j0 + e * stride] = x[e];
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_xf: one transform job per CTA (512 threads, 64 KiB smem tile), throughput path
+// ---------------------------------------------------------------------------
+template <int DIR, int LD, int EP>
+__global__ void __launch_bounds__(NT, 1) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
+    extern __shared__ u64 sm[];
+    const XJob J = jobs[blockIdx.x];
+    const int t = threadIdx.x;
+    const PrimeC& P = C.pc[J.k];
+    TRACE(0);
+    HC_UNROLL
+    for (int h = 0; h < 2; h++) {  // two halves of 8 coefficients: t + 512 v
+        u64 x[8];
+        load_n<LD, 8>(C, J, P, t + 8 * NT * h, NT, x);
+        HC_UNROLL
+        for (int v = 0; v < 8; v++) sm[swz(t + NT * (8 * h + v))] = x[v];
+    }
+    __syncthreads();
+    TRACE(1);
+    if (DIR == 0) cta_ntt_fwd(C.twf + (size_t)J.k * NPOLY, P, sm);
+    else cta_ntt_inv(C.twi + (size_t)J.k * NPOLY, P, sm);
+    TRACE(4);
+    HC_UNROLL
+    for (int h = 0; h < 2; h++) {
+        u64 x[8];
+        HC_UNROLL
+        for (int v = 0; v < 8; v++) x[v] = sm[swz(t + NT * (8 * h + v))];
+        store_n<EP, 8>(C, J, P, t + 8 * NT * h, NT, x);
+    }
+    TRACE(5);
+}
+
+// ---------------------------------------------------------------------------
+// k_elem: transform-less jobs (loader with side store only), e.g. the c0
+// half of a key-switch finish.  grid (NPOLY / 256, njobs), 128 threads x 2.
+// ---------------------------------------------------------------------------
+template <int LD>
+__global__ void __launch_bounds__(128) k_elem(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
+    const XJob J = jobs[blockIdx.y];
+    const PrimeC& P = C.pc[J.k];
+    u64 x[2];
+    load_n<LD, 2>(C, J, P, blockIdx.x * 256 + threadIdx.x, 128, x);
+}
+
+// ---------------------------------------------------------------------------
+// k_xf_cl: latency path, one job per 8-CTA cluster (ntt_cl.cuh)
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ void cluster_arrive_relaxed() {
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
 }
@@ -242,60 +303,92 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-template <int DIR>
+constexpr int CL_MAX = 16;  // jobs per cluster launch (passed by value)
+struct ClJobs {
+    XJob j[CL_MAX];
+};
+
+// prefetch this CTA's 1023-entry twiddle slice (TwL) into shared memory;
+// all 8 loads per thread are issued before the first shared store
+__device__ __forceinline__ void tw_prefetch(Tw* sl, const Tw* tw, int c, int t) {
+    ulonglong2 v[8];
+    HC_UNROLL
+    for (int i = 0; i < 8; i++) {
+        const int L = t + CNT * i;
+        const int Lc = L < 1023 ? L : 1022;
+        const int e = 31 - __clz(Lc + 1);
+        const int m8 = 1 << e;
+        v[i] = __ldg(reinterpret_cast<const ulonglong2*>(tw) + ((m8 << 3) + c * m8 + (Lc - (m8 - 1))));
+    }
+    HC_UNROLL
+    for (int i = 0; i < 8; i++) {
+        const int L = t + CNT * i;
+        if (L < 1023) reinterpret_cast<ulonglong2*>(sl)[L] = v[i];
+    }
+}
+
+template <int DIR, int LD, int EP>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
-    k_xform_cl(const DevCtx* __restrict__ C, const XJob* __restrict__ jobs) {
+    k_xf_cl(const __grid_constant__ DevCtx C, const __grid_constant__ ClJobs jobs) {
     __shared__ u64 tile[CTILE];
     __shared__ u64 recv[DIR ? CTILE : 1];
+    __shared__ Tw twsl[1023];
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     const int c = (int)cl.block_rank();
     const int t = threadIdx.x;
     cluster_arrive_relaxed();  // "this CTA has started" (waited on before DSMEM stores)
-    const XJob J = jobs[blockIdx.x / CL];
-    const PrimeC P = C->pc[J.k];
-    const DevCtx& D = *C;
+    const XJob& J = jobs.j[blockIdx.x / CL];
+    TRACE(0);
+    const PrimeC& P = C.pc[J.k];
+    const TwL twl{twsl, c};
+    u64 x[CEPT];
     if (DIR == 0) {
-        const Tw* tw = C->twf + (size_t)J.k * NPOLY;
-        u64 x[CEPT];
-        const int b = 128 * c + t;
+        const Tw* tw = C.twf + (size_t)J.k * NPOLY;
+        Tw wa[8];
         HC_UNROLL
-        for (int r = 0; r < CEPT; r++) x[r] = ld_elem(J, P, r * CTILE + b);
-        c_phaseA_fwd(x, tw, P.q, P.q2);
+        for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);  // phase-A twiddles tbl[1..7]
+        const int b = 128 * c + t;
+        load_n<LD, CEPT>(C, J, P, b, CTILE, x);
+        tw_prefetch(twsl, tw, c, t);
+        r8_ct(x, TwR{wa}, 0, 0, P.q, P.q2);
+        TRACE(1);
         cluster_wait();
+        TRACE(2);
         HC_UNROLL
         for (int r = 0; r < CEPT; r++) {
             u64* peer = cl.map_shared_rank(tile, r);
             peer[cswz(b)] = x[r];
         }
         cluster_arrive_release();
-        cluster_wait();
+        cluster_wait();  // also orders this CTA's twiddle-slice stores
+        TRACE(3);
         HC_NOUNROLL
         for (int p = 0; p < 3; p++) {
             const CPass I = cpass(p, c, t);
             c_load(x, tile, I);
-            r8_ct(x, tw, I.s0, I.G, P.q, P.q2);
+            r8_ct(x, twl, I.s0, I.G, P.q, P.q2);
             if (p == 2) {
                 u64 o[CEPT];
                 HC_UNROLL
                 for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-                c_st12(c, t, x, o, tw, P.q, P.q2);
+                c_st12(c, t, x, o, twl, P.q, P.q2);
             }
             c_store(x, tile, I);
             __syncthreads();
         }
+        TRACE(4);
         HC_UNROLL
-        for (int v = 0; v < CEPT; v++) {
-            const int bb = t + 128 * v;
-            st_elem(J, D, P, c * CTILE + bb, tile[cswz(bb)]);
-        }
+        for (int v = 0; v < CEPT; v++) x[v] = tile[cswz(t + 128 * v)];
+        store_n<EP, CEPT>(C, J, P, c * CTILE + t, 128, x);
+        TRACE(5);
     } else {
-        const Tw* tw = C->twi + (size_t)J.k * NPOLY;
-        u64 x[CEPT];
-        HC_UNROLL
-        for (int v = 0; v < CEPT; v++) x[v] = ld_elem(J, P, c * CTILE + t + 128 * v);
+        const Tw* tw = C.twi + (size_t)J.k * NPOLY;
+        load_n<LD, CEPT>(C, J, P, c * CTILE + t, 128, x);
+        tw_prefetch(twsl, tw, c, t);
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
         __syncthreads();
+        TRACE(1);
         HC_NOUNROLL
         for (int p = 0; p < 3; p++) {
             const CPass I = cpass(2 - p, c, t);
@@ -304,16 +397,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
                 u64 o[CEPT];
                 HC_UNROLL
                 for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-                c_st0(c, t, x, o, tw, P.q, P.q2);
+                c_st0(c, t, x, o, twl, P.q, P.q2);
             }
-            r8_gs(x, tw, 1 + 3 * p, I.G, P.q, P.q2);
+            r8_gs(x, twl, 1 + 3 * p, I.G, P.q, P.q2);
             if (p < 2) {
                 c_store(x, tile, I);
                 __syncthreads();
             }
         }
         // all-to-all: element (row c, column t + 128 v) -> CTA v, slot c*128 + t
+        TRACE(4);
         cluster_wait();
+        TRACE(2);
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) {
             u64* peer = cl.map_shared_rank(recv, v);
@@ -321,11 +416,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         }
         cluster_arrive_release();
         cluster_wait();
+        TRACE(3);
         HC_UNROLL
         for (int r = 0; r < CEPT; r++) x[r] = recv[r * 128 + t];
         c_phaseA_inv(x, tw, P);
-        HC_UNROLL
-        for (int r = 0; r < CEPT; r++) st_elem(J, D, P, r * CTILE + 128 * c + t, x[r]);
+        store_n<EP, CEPT>(C, J, P, 128 * c + t, CTILE, x);
+        TRACE(5);
     }
 }
 
@@ -343,8 +439,8 @@ struct CJob {
 };
 
 template <int L>
-__device__ __forceinline__ void compose_one(const DevCtx* __restrict__ C, const CJob& J, int pos) {
-    const LevelC& LV = C->lv[L];
+__device__ __forceinline__ void compose_one(const DevCtx& C, const CJob& J, int pos) {
+    const LevelC& LV = C.lv[L];
     constexpr int P = L + 1;
     const int D = LV.D;
     int src = pos, neg = 0;
@@ -357,11 +453,11 @@ __device__ __forceinline__ void compose_one(const DevCtx* __restrict__ C, const 
     HC_UNROLL
     for (int k = 0; k < P; k++) {
         u64 v = J.x[(size_t)k * J.xstride + src];
-        if (J.xadd) v = add_mod(v, J.xadd[(size_t)k * J.xstride + src], C->pc[k].q);
+        if (J.xadd) v = add_mod(v, J.xadd[(size_t)k * J.xstride + src], C.pc[k].q);
         xr[k] = v;
     }
     u64 X[NLIMB];
-    crt_compose<L>(LV, C->pc, xr, X);
+    crt_compose<L>(LV, C.pc, xr, X);
     constexpr int DMAX = 4 * (L + 1);
     if (J.mode == 0) {
         if (neg) neg_mod_Q<L>(LV, X);
@@ -379,7 +475,7 @@ __device__ __forceinline__ void compose_one(const DevCtx* __restrict__ C, const 
     }
 }
 
-__global__ void __launch_bounds__(256) k_compose(const DevCtx* __restrict__ C, const CJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(256) k_compose(const __grid_constant__ DevCtx C, const CJob* __restrict__ jobs) {
     const CJob J = jobs[blockIdx.y];
     const int pos = blockIdx.x * blockDim.x + threadIdx.x;
     switch (J.level) {
@@ -412,13 +508,13 @@ struct MJob {
     u64* out1;
 };
 
-__global__ void __launch_bounds__(256) k_ksmac(const DevCtx* __restrict__ C, const MJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
     const int k = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const LevelC& LV = C->lv[J.level];
-    const int P = LV.P, D = LV.D, L1 = C->L + 1;
-    const PrimeC pc = C->pc[k];
+    const LevelC& LV = C.lv[J.level];
+    const int P = LV.P, D = LV.D, L1 = C.L + 1;
+    const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
     u64 o0 = J.add0 ? J.add0[kn] : 0;
     u64 o1 = J.add1 ? J.add1[kn] : 0;
@@ -453,11 +549,11 @@ struct DXJob {
     u64* X;                 // [nprime][n], canonical, updated in place
 };
 
-__global__ void __launch_bounds__(256) k_diagx(const DevCtx* __restrict__ C, const DXJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
     const DXJob& J = jobs[blockIdx.z];
     const int k = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const PrimeC pc = C->pc[k];
+    const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
     u64 h = 0, l = 0;
     for (int t = 0; t < J.nterm; t++) mac128(h, l, J.src[t][kn], J.dg[t][kn]);
@@ -507,28 +603,28 @@ HD u64 plain_slot_value(const PJob& J, const PlanShape& S, int r, int c, u64 p, 
     }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_plain(const DevCtx* __restrict__ C, const PJob* __restrict__ jobs, PlanShape S) {
+__global__ void __launch_bounds__(NT, 1) k_plain(const __grid_constant__ DevCtx C, const PJob* __restrict__ jobs, PlanShape S) {
     extern __shared__ u64 sm[];
     u64* coef = sm + NPOLY;
     const PJob J = jobs[blockIdx.x];
     const int tid = threadIdx.x;
     HC_NOUNROLL
     for (int j = tid; j < NPOLY; j += NT) {
-        const unsigned so = C->slot_of[j];
-        sm[swz(j)] = plain_slot_value(J, S, so >> 12, so & 4095, C->p, C->pinv);
+        const unsigned so = C.slot_of[j];
+        sm[swz(j)] = plain_slot_value(J, S, so >> 12, so & 4095, C.p, C.pinv);
     }
     __syncthreads();
-    cta_ntt_inv(C->twi + (size_t)PIDX * NPOLY, C->pc[PIDX], sm);
+    cta_ntt_inv(C.twi + (size_t)PIDX * NPOLY, C.pc[PIDX], sm);
     HC_NOUNROLL
     for (int j = tid; j < NPOLY; j += NT) coef[j] = sm[swz(j)];
-    const LevelC& LV = C->lv[J.level];
+    const LevelC& LV = C.lv[J.level];
     for (int k = 0; k <= J.level; k++) {
-        const PrimeC P = C->pc[k];
+        const PrimeC P = C.pc[k];
         __syncthreads();
         HC_NOUNROLL
         for (int j = tid; j < NPOLY; j += NT) sm[swz(j)] = coef[j];
         __syncthreads();
-        cta_ntt_fwd(C->twf + (size_t)k * NPOLY, P, sm);
+        cta_ntt_fwd(C.twf + (size_t)k * NPOLY, P, sm);
         const u64 w = (k == J.level) ? P.rmod : LV.qinv_r[k];
         const u64 ws = (k == J.level) ? P.rmod_s : LV.qinv_rs[k];
         HC_NOUNROLL
@@ -541,24 +637,24 @@ __global__ void __launch_bounds__(NT, 1) k_plain(const DevCtx* __restrict__ C, c
 // ---------------------------------------------------------------------------
 
 // in-place x -> x*R mod q (Montgomery form); prime of row r = r % period
-__global__ void k_to_mont(const DevCtx* __restrict__ C, u64* data, long long rows, int period) {
+__global__ void k_to_mont(const __grid_constant__ DevCtx C, u64* data, long long rows, int period) {
     const long long total = rows * NPOLY;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const int k = (int)((i / NPOLY) % period);
-        const PrimeC P = C->pc[k];
+        const PrimeC P = C.pc[k];
         data[i] = mul_shoup(data[i], P.rmod, P.rmod_s, P.q);
     }
 }
 
 // out[r][j] = sum_c red(in[c][r][j]) mod q_{r % period}
-__global__ void k_sum_copies(const DevCtx* __restrict__ C, const u64* in, u64* out, long long rows,
+__global__ void k_sum_copies(const __grid_constant__ DevCtx C, const u64* in, u64* out, long long rows,
                              int period, int copies, long long cstride) {
     const long long total = rows * NPOLY;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
         const int k = (int)((i / NPOLY) % period);
-        const PrimeC P = C->pc[k];
+        const PrimeC P = C.pc[k];
         u64 s = 0;
         for (int c = 0; c < copies; c++) s = add_mod(s, red64(in[c * cstride + i], P.q, P.one_s), P.q);
         out[i] = s;
@@ -566,12 +662,12 @@ __global__ void k_sum_copies(const DevCtx* __restrict__ C, const u64* in, u64* o
 }
 
 // pointwise op over rows; prime of row r = pidx[r]
-__global__ void k_pointwise(const DevCtx* __restrict__ C, const u64* a, const u64* b, u64* out, int rows,
+__global__ void k_pointwise(const __grid_constant__ DevCtx C, const u64* a, const u64* b, u64* out, int rows,
                             const int* pidx, int op) {
     const long long total = (long long)rows * NPOLY;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const PrimeC P = C->pc[pidx[i / NPOLY]];
+        const PrimeC P = C.pc[pidx[i / NPOLY]];
         const u64 x = a[i], y = b[i];
         u64 r;
         if (op == 0) {

@@ -26,6 +26,44 @@ constexpr int CNT = 128;    // threads per CTA
 constexpr int CEPT = 8;     // coefficients per thread
 constexpr int CTILE = 1024; // coefficients per CTA
 
+// Twiddle access for stage "level" M (M = 2^s for CT stage s, 2^(12-b) for
+// GS stage b).  TwG reads the global table; TwL reads the CTA's prefetched
+// slice: for M >= 8, CTA c only touches indices [M + c*M/8, M + (c+1)*M/8),
+// stored at local offset (M/8 - 1) + (idx - M - c*M/8): 1023 entries.
+struct TwG {
+    const Tw* t;
+    HD Tw operator()(int idx, int M) const { return ldtw(t, idx); }
+};
+struct TwL {
+    const Tw* sm;  // 1023 entries
+    int c;
+    HD Tw operator()(int idx, int M) const {
+        const int m8 = M >> 3;
+        const Tw* p = sm + (idx - M - c * m8 + m8 - 1);
+#if defined(__CUDA_ARCH__)
+        ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+        Tw r;
+        r.w = v.x;
+        r.ws = v.y;
+        return r;
+#else
+        return *p;
+#endif
+    }
+};
+// register-held twiddles tbl[1..7] (forward phase A)
+struct TwR {
+    const Tw* r;
+    HD Tw operator()(int idx, int M) const { return r[idx]; }
+};
+// global index of local slice entry L (0..1022) of CTA c
+HD int tw_slice_index(int L, int c) {
+    int e = 0;
+    while ((2 << e) - 1 <= L) e++;  // level with M/8 = 2^e entries: offsets [2^e - 1, 2^(e+1) - 1)
+    const int m8 = 1 << e, M = m8 << 3;
+    return M + c * m8 + (L - (m8 - 1));
+}
+
 // local tile swizzle for the three radix-8 patterns (64-bit, 16 lanes/phase):
 // XOR bits 1..3 with bits 4..6
 HD int cswz(int b) { return b ^ (((b >> 4) & 7) << 1); }
@@ -58,7 +96,8 @@ HD void c_store(const u64 (&x)[CEPT], u64* sm, const CPass& I) {
 
 // 3 CT stages s0..s0+2 on 8 points: stage s0+u pairs v, v + (4 >> u),
 // twiddle tbl[2^(s0+u) + (G << u | v >> (3-u))]
-HD void r8_ct(u64 (&x)[CEPT], const Tw* tw, int s0, int G, u64 q, u64 q2) {
+template <class TW>
+HD void r8_ct(u64 (&x)[CEPT], const TW& tw, int s0, int G, u64 q, u64 q2) {
     HC_UNROLL
     for (int u = 0; u < 3; u++) {
         const int half = 4 >> u;
@@ -66,7 +105,7 @@ HD void r8_ct(u64 (&x)[CEPT], const Tw* tw, int s0, int G, u64 q, u64 q2) {
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
-                Tw w = ldtw(tw, tb + (v >> (3 - u)));
+                Tw w = tw(tb + (v >> (3 - u)), 1 << (s0 + u));
                 bf_ct(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
@@ -75,7 +114,8 @@ HD void r8_ct(u64 (&x)[CEPT], const Tw* tw, int s0, int G, u64 q, u64 q2) {
 
 // 3 GS stages b0..b0+2 on 8 points: stage b0+u pairs v, v + (1 << u),
 // twiddle inv_tbl[2^(12-b0-u) + (G << (2-u) | v >> (u+1))]
-HD void r8_gs(u64 (&x)[CEPT], const Tw* tw, int b0, int G, u64 q, u64 q2) {
+template <class TW>
+HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q2) {
     HC_UNROLL
     for (int u = 0; u < 3; u++) {
         const int half = 1 << u;
@@ -83,7 +123,7 @@ HD void r8_gs(u64 (&x)[CEPT], const Tw* tw, int b0, int G, u64 q, u64 q2) {
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
-                Tw w = ldtw(tw, tb + (v >> (u + 1)));
+                Tw w = tw(tb + (v >> (u + 1)), 1 << (12 - b0 - u));
                 bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
@@ -92,21 +132,23 @@ HD void r8_gs(u64 (&x)[CEPT], const Tw* tw, int b0, int G, u64 q, u64 q2) {
 
 // forward bit-0 stage across lanes (t, t^1) in pass-2 layout:
 // w = tbl[4096 + (j >> 1)], j >> 1 = (c << 9) | ((t >> 1) << 3) | v
-HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const Tw* tw, u64 q, u64 q2) {
+template <class TW>
+HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2) {
     const int odd = t & 1;
     const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
     HC_UNROLL
     for (int v = 0; v < CEPT; v++) {
         u64 X = odd ? o[v] : x[v];
         u64 Y = odd ? x[v] : o[v];
-        Tw w = ldtw(tw, tb + v);
+        Tw w = tw(tb + v, 4096);
         bf_ct(X, Y, w.w, w.ws, q, q2);
         x[v] = canon4(odd ? Y : X, q, q2);
     }
 }
 
 // inverse bit-0 stage across lanes: even X + Y, odd (X - Y) w
-HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const Tw* tw, u64 q, u64 q2) {
+template <class TW>
+HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2) {
     const int odd = t & 1;
     const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
     HC_UNROLL
@@ -114,7 +156,7 @@ HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const Tw* tw, 
         const u64 X = odd ? o[v] : x[v];
         const u64 Y = odd ? x[v] : o[v];
         if (odd) {
-            Tw w = ldtw(tw, tb + v);
+            Tw w = tw(tb + v, 4096);
             x[v] = mul_shoup_lazy(X - Y + q2, w.w, w.ws, q);
         } else {
             u64 s = X + Y;
@@ -124,11 +166,14 @@ HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const Tw* tw, 
 }
 
 // forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
-HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q2) { r8_ct(x, tw, 0, 0, q, q2); }
+HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q2) { r8_ct(x, TwG{tw}, 0, 0, q, q2); }
 
 // inverse phase A': GS stages 10, 11 on the column, then bit 12 folded with n^-1
 HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
     const u64 q = P.q, q2 = P.q2;
+    Tw wa[8];  // inv_tbl[1..7] (stages 10, 11 use indices 2..7)
+    HC_UNROLL
+    for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);
     HC_UNROLL
     for (int u = 0; u < 2; u++) {
         const int half = 1 << u;
@@ -136,7 +181,7 @@ HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
-                Tw w = ldtw(tw, tb + (v >> (u + 1)));
+                Tw w = wa[tb + (v >> (u + 1))];
                 bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
@@ -150,7 +195,14 @@ HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
 }
 
 // ---- host emulation of the cluster schedule (CPU self-test only) ----------
+inline void host_tw_slices(const Tw* tw, Tw (*sl)[1023]) {
+    for (int c = 0; c < CL; c++)
+        for (int L = 0; L < 1023; L++) sl[c][L] = tw[tw_slice_index(L, c)];
+}
+
 inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
+    static Tw sl[CL][1023];
+    host_tw_slices(tw, sl);
     static u64 tile[CL][CTILE];
     static u64 regs[CL][CNT][CEPT], oth[CL][CNT][CEPT];
     for (int c = 0; c < CL; c++)
@@ -166,14 +218,14 @@ inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
             for (int t = 0; t < CNT; t++) {
                 CPass I = cpass(p, c, t);
                 c_load(regs[c][t], tile[c], I);
-                r8_ct(regs[c][t], tw, I.s0, I.G, P.q, P.q2);
+                r8_ct(regs[c][t], TwL{sl[c], c}, I.s0, I.G, P.q, P.q2);
             }
         if (p == 2) {
             for (int c = 0; c < CL; c++)
                 for (int t = 0; t < CNT; t++)
                     for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
             for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++) c_st12(c, t, regs[c][t], oth[c][t], tw, P.q, P.q2);
+                for (int t = 0; t < CNT; t++) c_st12(c, t, regs[c][t], oth[c][t], TwL{sl[c], c}, P.q, P.q2);
         }
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) c_store(regs[c][t], tile[c], cpass(p, c, t));
@@ -183,6 +235,8 @@ inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
 }
 
 inline void host_emulate_cl_inv(u64* a, const Tw* tw, const PrimeC& P) {
+    static Tw sl[CL][1023];
+    host_tw_slices(tw, sl);
     static u64 tile[CL][CTILE], recv[CL][CTILE];
     static u64 regs[CL][CNT][CEPT], oth[CL][CNT][CEPT];
     for (int c = 0; c < CL; c++)
@@ -195,12 +249,12 @@ inline void host_emulate_cl_inv(u64* a, const Tw* tw, const PrimeC& P) {
                 for (int t = 0; t < CNT; t++)
                     for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
             for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++) c_st0(c, t, regs[c][t], oth[c][t], tw, P.q, P.q2);
+                for (int t = 0; t < CNT; t++) c_st0(c, t, regs[c][t], oth[c][t], TwL{sl[c], c}, P.q, P.q2);
         }
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) {
                 CPass I = cpass(2 - p, c, t);
-                r8_gs(regs[c][t], tw, 1 + 3 * p, I.G, P.q, P.q2);
+                r8_gs(regs[c][t], TwL{sl[c], c}, 1 + 3 * p, I.G, P.q, P.q2);
                 if (p < 2) c_store(regs[c][t], tile[c], I);
             }
     }
