@@ -120,6 +120,35 @@ HD void bf_gs(u64& X, u64& Y, u64 w, u64 ws, u64 q, u64 q2) {
     Y = mul_shoup_lazy(x - y + q2, w, ws, q);
 }
 
+// Lazy forward butterfly used by the transforms: no reduction of X and a
+// 3-product approximate Shoup quotient.  mulhi_approx(a, b) drops the
+// lo x lo product and the low halves of the cross products, so it returns
+// floor(a*b / 2^64) - {0, 1, 2}; hence t = Y*w - qhat*q lies in [0, 4q) for
+// any 64-bit Y.  Each stage adds < 4q to the value range: from inputs < 4q,
+// 13 stages stay below 56q < 2^60, and the caller canonicalises once.
+HD u64 mulhi_approx(u64 a, u64 b) {
+#if defined(__CUDA_ARCH__)
+    const u32 al = (u32)a, ah = (u32)(a >> 32), bl = (u32)b, bh = (u32)(b >> 32);
+    u64 r = (u64)ah * bh;
+    r += __umulhi(ah, bl);
+    r += __umulhi(al, bh);
+    return r;
+#else
+    const u64 al = (u32)a, ah = a >> 32, bl = (u32)b, bh = b >> 32;
+    return ah * bh + ((ah * bl) >> 32) + ((al * bh) >> 32);
+#endif
+}
+
+HD void bf_ct_lazy(u64& X, u64& Y, u64 w, u64 ws, u64 q, u64 q4) {
+    const u64 t = Y * w - mulhi_approx(Y, ws) * q;  // [0, 4q)
+    const u64 x = X;
+    X = x + t;
+    Y = x - t + q4;
+}
+
+// any value < 2^64 -> [0, q) (final canonicalisation of lazy transforms)
+HD u64 canon_any(u64 x, u64 q, u64 one_s) { return reduce_once(x - mulhi(x, one_s) * q, q); }
+
 // [0, 4q) -> [0, q)
 HD u64 canon4(u64 x, u64 q, u64 q2) {
     x = x >= q2 ? x - q2 : x;

@@ -107,28 +107,53 @@ HD uint16_t digit16(const u64 (&X)[NLIMB], int j) {
     return (uint16_t)(w >> (16 * (j & 3)));
 }
 
-// Modulus-switch correction (see file header).  x = canonical residue of the
-// coefficient modulo the dropped prime q_l.  Writes e_k for k < l.
-HD void rescale_corr(const DevCtx& D, int l, u64 x, u64* e) {
-    const LevelC& C = D.lv[l];
-    const u64 ql = D.pc[l].q;
-    const int neg = x > C.half_qd;
-    const u64 mag = neg ? ql - x : x;  // |r|
-    u64 rm = mag - mulhi(mag, D.pbar) * D.p;  // Barrett: [0, 2p)
-    if (rm >= D.p) rm -= D.p;
-    if (neg && rm) rm = D.p - rm;       // r mod p in [0, p)
-    const int dneg = rm > D.half_p;
-    const u64 dmag = dneg ? D.p - rm : rm;  // |d|
+// Modulus-switch correction (see file header).  The constants of the
+// switch from level l are gathered once (RescaleK) so the per-coefficient
+// path touches registers only.
+struct RescaleK {
+    int l;
+    u64 ql, half_qd, p, half_p, pbar;
+    u64 q[MAXL], qinv[MAXL], qinv_s[MAXL];
+};
+HD RescaleK rescale_consts(const DevCtx& D, int l) {
+    RescaleK R;
+    R.l = l;
+    R.ql = D.pc[l].q;
+    R.half_qd = D.lv[l].half_qd;
+    R.p = D.p;
+    R.half_p = D.half_p;
+    R.pbar = D.pbar;
     HC_UNROLL
     for (int k = 0; k < MAXL; k++) {
-        if (k >= l) break;
-        const u64 q = D.pc[k].q;
-        u64 rk = neg ? (mag ? q - mag : 0) : mag;  // r mod q_k (|r| < q_k)
-        u64 t = mul_shoup(rk, C.qinv[k], C.qinv_s[k], q);
-        u64 dk = dneg ? (dmag ? q - dmag : 0) : dmag;
+        R.q[k] = D.pc[k].q;
+        R.qinv[k] = D.lv[l].qinv[k];
+        R.qinv_s[k] = D.lv[l].qinv_s[k];
+    }
+    return R;
+}
+
+// x = canonical residue of the coefficient modulo the dropped prime q_l;
+// writes e_k for k < l.
+HD void rescale_corr(const RescaleK& R, u64 x, u64* e) {
+    const int neg = x > R.half_qd;
+    const u64 mag = neg ? R.ql - x : x;  // |r|
+    u64 rm = mag - mulhi(mag, R.pbar) * R.p;  // Barrett: [0, 2p)
+    if (rm >= R.p) rm -= R.p;
+    if (neg && rm) rm = R.p - rm;  // r mod p in [0, p)
+    const int dneg = rm > R.half_p;
+    const u64 dmag = dneg ? R.p - rm : rm;  // |d|
+    HC_UNROLL
+    for (int k = 0; k < MAXL; k++) {
+        if (k >= R.l) break;
+        const u64 q = R.q[k];
+        const u64 rk = neg ? (mag ? q - mag : 0) : mag;  // r mod q_k (|r| < q_k)
+        const u64 t = mul_shoup(rk, R.qinv[k], R.qinv_s[k], q);
+        const u64 dk = dneg ? (dmag ? q - dmag : 0) : dmag;
         e[k] = sub_mod(dk, t, q);
     }
 }
+
+HD void rescale_corr(const DevCtx& D, int l, u64 x, u64* e) { rescale_corr(rescale_consts(D, l), x, e); }
 
 // any 64-bit value -> [0, q)
 HD u64 red64(u64 a, u64 q, u64 one_s) { return reduce_once(mul_shoup_lazy(a, 1, one_s, q), q); }

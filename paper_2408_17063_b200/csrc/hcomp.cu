@@ -76,6 +76,7 @@ struct Step {
     std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
     int group = 0;            // consecutive steps with the same nonzero group run concurrently
     int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
+    int lane = -1;            // in a group: steps of one lane run in order on one branch
 };
 
 struct Schedule {
@@ -83,7 +84,7 @@ struct Schedule {
     std::vector<void*> allocs;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
-    int cur_group = 0, next_group = 1;
+    int cur_group = 0, next_group = 1, cur_lane = -1;
     // steps added between par_begin() and par_end() are independent: they are
     // captured on forked streams (parallel graph branches)
     void par_begin() { cur_group = next_group++; }
@@ -271,7 +272,9 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
                 taken[k] = 1;
             }
         }
-        const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS;
+        // clusters only for small batches outside parallel lanes (lanes
+        // already fill the GPU; single-CTA transforms are more efficient there)
+        const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS && S.cur_lane < 0;
         const size_t chunk = clu ? (size_t)CL_MAX : sel.size();
         const int saved = S.cur_group;
         if (clu && sel.size() > chunk && !S.cur_group) S.par_begin();
@@ -286,6 +289,7 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
             st.njobs = (int)part.size();
             st.hjobs = part;
             st.group = S.cur_group;
+            st.lane = S.cur_lane;
             int rc = upload_jobs(S, st, part.data(), part.size() * sizeof(XJob));
             if (rc) return rc;
             S.steps.push_back(st);
@@ -299,6 +303,7 @@ static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
     Step st;
     st.kind = ST_CO;
     st.group = S.cur_group;
+    st.lane = S.cur_lane;
     st.njobs = (int)jobs.size();
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(CJob));
     if (rc) return rc;
@@ -310,6 +315,7 @@ static int add_ma(Schedule& S, const std::vector<MJob>& jobs, int nprime) {
     Step st;
     st.kind = ST_MA;
     st.group = S.cur_group;
+    st.lane = S.cur_lane;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(MJob));
@@ -322,6 +328,7 @@ static int add_dx(Schedule& S, const std::vector<DXJob>& jobs, int nprime) {
     Step st;
     st.kind = ST_DX;
     st.group = S.cur_group;
+    st.lane = S.cur_lane;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(DXJob));
@@ -399,10 +406,13 @@ static int enqueue(const hc_ctx* h, const Schedule& S, cudaStream_t s) {
             if (rc) return rc;
         } else {
             CU(cudaEventRecord(h->ev_fork, s));
-            const size_t nb = std::min<size_t>(e - i, 4);
+            size_t nb = std::min<size_t>(e - i, 4);
+            for (size_t k = i; k < e; k++)
+                if (S.steps[k].lane >= 0) nb = std::max<size_t>(nb, std::min(4, S.steps[k].lane + 1));
             for (size_t b = 0; b < nb; b++) CU(cudaStreamWaitEvent(h->side[b], h->ev_fork, 0));
             for (size_t k = i; k < e; k++) {
-                int rc = enqueue_step(h, S.steps[k], h->side[(k - i) % 4]);
+                const int lane = S.steps[k].lane >= 0 ? S.steps[k].lane : (int)(k - i);
+                int rc = enqueue_step(h, S.steps[k], h->side[lane % 4]);
                 if (rc) return rc;
             }
             for (size_t b = 0; b < nb; b++) {
@@ -467,7 +477,7 @@ struct Plan {
     u64 *ecor = nullptr, *rc1raw = nullptr, *pn = nullptr, *rc0n = nullptr, *dnttR = nullptr;
     u64 *U = nullptr, *Ucoef = nullptr, *dnttB = nullptr, *ROT = nullptr;
     uint16_t *digR = nullptr, *digU = nullptr;
-    u64 *Ecp = nullptr, *PX = nullptr;
+    u64 *Eslot = nullptr, *PX = nullptr;
     u64 *A0 = nullptr, *A1 = nullptr, *A1coef = nullptr, *dnttG = nullptr, *RES = nullptr;
     u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr, *ACC = nullptr;
     uint16_t *digG = nullptr, *digF = nullptr;
@@ -615,7 +625,7 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
     PA(P->digU, (size_t)CB * 2 * P->D2 * NB);
     PA(P->dnttB, (size_t)std::max(1, CB * bm1) * P->D2 * 3 * NB);
     PA(P->ROT, (size_t)std::max(1, CB * bm1) * 2 * 3 * NB);
-    PA(P->Ecp, (size_t)P->ncopy * G * 2 * 2 * NB);
+    PA(P->Eslot, (size_t)CB * P->baby * G * 2 * 2 * NB);
     PA(P->PX, P->px_words());
     PA(P->A0, (size_t)G * 2 * NB);
     PA(P->A1, (size_t)2 * NB);
@@ -685,173 +695,195 @@ extern "C" int64_t hc_partial_words(const hc_ctx* h) {
     return (int64_t)h->plan->px_words();
 }
 
+// the level-2 ciphertext multiplied by diagonal (t, g, b): u_t for b = 0,
+// the baby rotation ROT[t][b] otherwise
+static const u64* rot_src(const Plan& P, int tl, int b, int poly) {
+    const size_t NB = NPOLY;
+    return b == 0 ? P.U + ((size_t)tl * 2 + poly) * 3 * NB
+                  : P.ROT + (((size_t)tl * (P.baby - 1) + (b - 1)) * 2 + poly) * 3 * NB;
+}
+// correction slot of product (tl, b) for accumulator (g, poly): [2 primes][n]
+static u64* eslot(const Plan& P, int tl, int b, int g, int poly) {
+    const size_t NB = NPOLY;
+    return P.Eslot + ((((size_t)tl * P.baby + b) * P.giant + g) * 2 + poly) * 2 * NB;
+}
+
 // Steps S1..S10 for blocks [b0, b1): pack_pair (compress.py:338-367), baby
 // rotations and the diagonal products (compress.py:286-297), accumulated
-// into the partial PX = [E | X].
+// into the partial PX = [E | X].  Blocks are independent until the
+// accumulation, so each chunk runs as up to 4 parallel lanes (graph
+// branches) of per-block pipelines S1..S9, joined by S10.
 static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedule& S) {
     const size_t NB = NPOLY;
     const int D2 = P.D2, baby = P.baby, G = P.giant, sp = P.s_pad;
     const DevKey* kcol = need_key(h, P.t_col);
     int rc;
-    add_memset(S, P.Ecp, (size_t)P.ncopy * G * 2 * 2 * NB * 8);
     add_memset(S, P.PX, P.px_words() * 8);
     for (long long c0 = b0; c0 < b1; c0 += P.CB) {
         const int cb = (int)std::min<long long>(P.CB, b1 - c0);
-        std::vector<XJob> s1, s2, s3, s5, s7, s9;
-        std::vector<CJob> s2c, s6;
-        std::vector<MJob> s4, s8;
-        for (int tl = 0; tl < cb; tl++) {
-            const long long t = c0 + tl;
-            const long long src = t / 2;
-            const int par = (int)(t % 2);
-            const u64* mk = P.mask + (size_t)par * 4 * NB;
-            const u64* cv = P.cv + (size_t)src * 2 * 4 * NB;
-            const u64* cd = P.cd + (size_t)src * 2 * 4 * NB;
-            // even block: u = mp(cv, top) + rot_col(mp(cd, top)); odd: rot_col(mp(cv, bot)) + mp(cd, bot)
-            const u64* ctP = par == 0 ? cv : cd;
-            const u64* ctR = par == 0 ? cd : cv;
-            u64* ecor = P.ecor + (size_t)tl * 4 * 3 * NB;  // [P0,P1,R0,R1][3][n]
-            for (int mm = 0; mm < 2; mm++)
-                for (int poly = 0; poly < 2; poly++) {
-                    const u64* ct = mm == 0 ? ctP : ctR;
+        // lanes only while every lane's levels stay wide enough to fill the GPU
+        // (>= 8 blocks per lane); small chunks run as one stream so the
+        // narrow levels can use the low-latency cluster transforms
+        const int nl = std::max(1, std::min(4, cb / 8));
+        if (nl > 1) S.par_begin();
+        for (int lane = 0; lane < nl; lane++) {
+            S.cur_lane = nl > 1 ? lane : -1;
+            std::vector<XJob> s1, s2, s3, s5, s7, s9;
+            std::vector<CJob> s2c, s6;
+            std::vector<MJob> s4, s8;
+            for (int tl = lane; tl < cb; tl += nl) {
+                const long long t = c0 + tl;
+                const long long src = t / 2;
+                const int par = (int)(t % 2);
+                const u64* mk = P.mask + (size_t)par * 4 * NB;
+                const u64* cv = P.cv + (size_t)src * 2 * 4 * NB;
+                const u64* cd = P.cd + (size_t)src * 2 * 4 * NB;
+                // even block: u = mp(cv, top) + rot_col(mp(cd, top)); odd: rot_col(mp(cv, bot)) + mp(cd, bot)
+                const u64* ctP = par == 0 ? cv : cd;
+                const u64* ctR = par == 0 ? cd : cv;
+                u64* ecor = P.ecor + (size_t)tl * 4 * 3 * NB;  // [P0,P1,R0,R1][3][n]
+                // S1: the pack mul_plains' dropped-prime INTTs (+ modulus-switch
+                //     correction) and R.c1's kept-prime INTTs
+                for (int mm = 0; mm < 2; mm++)
+                    for (int poly = 0; poly < 2; poly++) {
+                        const u64* ct = mm == 0 ? ctP : ctR;
+                        XJob j{};
+                        j.dir = 1; j.k = 3; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 3;
+                        j.a = ct + ((size_t)poly * 4 + 3) * NB;
+                        j.b = mk + 3 * NB;
+                        j.out = ecor + (size_t)(mm * 2 + poly) * 3 * NB;
+                        j.ostride = NB;
+                        s1.push_back(j);
+                    }
+                for (int k = 0; k < 3; k++) {
                     XJob j{};
-                    j.dir = 1; j.k = 3; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 3;
-                    j.a = ct + ((size_t)poly * 4 + 3) * NB;
-                    j.b = mk + 3 * NB;
-                    j.out = ecor + (size_t)(mm * 2 + poly) * 3 * NB;
-                    j.ostride = NB;
+                    j.dir = 1; j.k = k; j.ld = LD_MONT; j.ep = EP_STORE;
+                    j.a = ctR + ((size_t)1 * 4 + k) * NB;
+                    j.b = mk + (size_t)k * NB;
+                    j.out = P.rc1raw + ((size_t)tl * 3 + k) * NB;
                     s1.push_back(j);
                 }
-            for (int k = 0; k < 3; k++) {
-                XJob j{};
-                j.dir = 1; j.k = k; j.ld = LD_MONT; j.ep = EP_STORE;
-                j.a = ctR + ((size_t)1 * 4 + k) * NB;
-                j.b = mk + (size_t)k * NB;
-                j.out = P.rc1raw + ((size_t)tl * 3 + k) * NB;
-                s1.push_back(j);
-            }
-            // S2: NTT of corrections + plaintext-product combine
-            for (int which = 0; which < 3; which++) {  // P.c0, P.c1, R.c0
-                const int mm = which < 2 ? 0 : 1, poly = which < 2 ? which : 0;
-                const u64* ct = mm == 0 ? ctP : ctR;
-                for (int k = 0; k < 3; k++) {
-                    XJob j{};
-                    j.dir = 0; j.k = k; j.ld = LD_U64; j.ep = EP_ADDMONT;
-                    j.a = ecor + ((size_t)(mm * 2 + poly) * 3 + k) * NB;
-                    j.ea = ct + ((size_t)poly * 4 + k) * NB;
-                    j.eb = mk + (size_t)k * NB;
-                    j.out = which < 2 ? P.pn + (((size_t)tl * 2 + poly) * 3 + k) * NB : P.rc0n + ((size_t)tl * 3 + k) * NB;
-                    s2.push_back(j);
-                }
-            }
-            {
-                CJob c{};
-                c.level = 2; c.mode = 0;
-                c.x = P.rc1raw + (size_t)tl * 3 * NB;
-                c.xadd = ecor + (size_t)3 * 3 * NB;
-                c.xstride = NB;
-                c.gal = kcol->gal;
-                c.dig = P.digR + (size_t)tl * D2 * NB;
-                s2c.push_back(c);
-            }
-            for (int jj = 0; jj < D2; jj++)
-                for (int k = 0; k < 3; k++) {
-                    XJob j{};
-                    j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
-                    j.a = (const u64*)(P.digR + ((size_t)tl * D2 + jj) * NB);
-                    j.out = P.dnttR + (((size_t)tl * D2 + jj) * 3 + k) * NB;
-                    s3.push_back(j);
-                }
-            {
-                MJob mj{};
-                mj.level = 2; mj.nterm = 1;
-                mj.t[0].dntt = P.dnttR + (size_t)tl * D2 * 3 * NB;
-                mj.t[0].key = kcol->key;
-                mj.t[0].c0src = P.rc0n + (size_t)tl * 3 * NB;
-                mj.t[0].perm = kcol->perm;
-                mj.add0 = P.pn + ((size_t)tl * 2 + 0) * 3 * NB;
-                mj.add1 = P.pn + ((size_t)tl * 2 + 1) * 3 * NB;
-                mj.out0 = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
-                mj.out1 = P.U + ((size_t)tl * 2 + 1) * 3 * NB;
-                s4.push_back(mj);
-            }
-            if (baby > 1) {
-                for (int k = 0; k < 3; k++) {
-                    XJob j{};
-                    j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
-                    j.a = P.U + (((size_t)tl * 2 + 1) * 3 + k) * NB;
-                    j.out = P.Ucoef + ((size_t)tl * 3 + k) * NB;
-                    s5.push_back(j);
-                }
-                CJob c{};
-                c.level = 2; c.mode = 1;
-                c.x = P.Ucoef + (size_t)tl * 3 * NB;
-                c.xstride = NB;
-                c.dig = P.digU + (size_t)tl * 2 * D2 * NB;
-                s6.push_back(c);
-                for (int b = 1; b < baby; b++) {
-                    const DevKey* kb = need_key(h, P.t_baby[b]);
-                    const size_t rb = (size_t)tl * (baby - 1) + (b - 1);
-                    for (int jj = 0; jj < D2; jj++)
-                        for (int k = 0; k < 3; k++) {
-                            XJob j{};
-                            j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_STORE;
-                            j.a = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + jj) * NB);
-                            j.b = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
-                            j.gal = kb->gal;
-                            j.out = P.dnttB + ((rb * D2 + jj) * 3 + k) * NB;
-                            s7.push_back(j);
-                        }
-                    MJob mj{};
-                    mj.level = 2; mj.nterm = 1;
-                    mj.t[0].dntt = P.dnttB + rb * D2 * 3 * NB;
-                    mj.t[0].key = kb->key;
-                    mj.t[0].c0src = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
-                    mj.t[0].perm = kb->perm;
-                    mj.out0 = P.ROT + (rb * 2 + 0) * 3 * NB;
-                    mj.out1 = P.ROT + (rb * 2 + 1) * 3 * NB;
-                    s8.push_back(mj);
-                }
-            }
-            // S9: dropped-prime half of each diagonal product (INTT + rescale correction)
-            for (int g = 0; g < G; g++)
-                for (int b = 0; b < baby; b++) {
-                    const int i = g * baby + b;
-                    if (!P.live[(size_t)t * sp + i]) continue;
-                    const u64* dg = P.diag + ((size_t)t * sp + i) * 3 * NB;
-                    const int copy = (int)((t * baby + b) % P.ncopy);
-                    for (int poly = 0; poly < 2; poly++) {
-                        const u64* srcp = b == 0 ? P.U + ((size_t)tl * 2 + poly) * 3 * NB
-                                                 : P.ROT + (((size_t)tl * (baby - 1) + (b - 1)) * 2 + poly) * 3 * NB;
+                // S2: NTT of corrections + plaintext-product combine
+                for (int which = 0; which < 3; which++) {  // P.c0, P.c1, R.c0
+                    const int mm = which < 2 ? 0 : 1, poly = which < 2 ? which : 0;
+                    const u64* ct = mm == 0 ? ctP : ctR;
+                    for (int k = 0; k < 3; k++) {
                         XJob j{};
-                        j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE_ATOMIC; j.level = 2;
-                        j.a = srcp + 2 * NB;
-                        j.b = dg + 2 * NB;
-                        j.out = P.Ecp + ((((size_t)copy * G + g) * 2 + poly) * 2) * NB;
-                        j.ostride = NB;
-                        s9.push_back(j);
+                        j.dir = 0; j.k = k; j.ld = LD_U64; j.ep = EP_ADDMONT;
+                        j.a = ecor + ((size_t)(mm * 2 + poly) * 3 + k) * NB;
+                        j.ea = ct + ((size_t)poly * 4 + k) * NB;
+                        j.eb = mk + (size_t)k * NB;
+                        j.out = which < 2 ? P.pn + (((size_t)tl * 2 + poly) * 3 + k) * NB : P.rc0n + ((size_t)tl * 3 + k) * NB;
+                        s2.push_back(j);
                     }
                 }
+                {
+                    CJob c{};
+                    c.level = 2; c.mode = 0;
+                    c.x = P.rc1raw + (size_t)tl * 3 * NB;
+                    c.xadd = ecor + (size_t)3 * 3 * NB;
+                    c.xstride = NB;
+                    c.gal = kcol->gal;
+                    c.dig = P.digR + (size_t)tl * D2 * NB;
+                    s2c.push_back(c);
+                }
+                // S3/S4: column-swap key switch of R, u = P + rot_col(R)
+                for (int jj = 0; jj < D2; jj++)
+                    for (int k = 0; k < 3; k++) {
+                        XJob j{};
+                        j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+                        j.a = (const u64*)(P.digR + ((size_t)tl * D2 + jj) * NB);
+                        j.out = P.dnttR + (((size_t)tl * D2 + jj) * 3 + k) * NB;
+                        s3.push_back(j);
+                    }
+                {
+                    MJob mj{};
+                    mj.level = 2; mj.nterm = 1;
+                    mj.t[0].dntt = P.dnttR + (size_t)tl * D2 * 3 * NB;
+                    mj.t[0].key = kcol->key;
+                    mj.t[0].c0src = P.rc0n + (size_t)tl * 3 * NB;
+                    mj.t[0].perm = kcol->perm;
+                    mj.add0 = P.pn + ((size_t)tl * 2 + 0) * 3 * NB;
+                    mj.add1 = P.pn + ((size_t)tl * 2 + 1) * 3 * NB;
+                    mj.out0 = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
+                    mj.out1 = P.U + ((size_t)tl * 2 + 1) * 3 * NB;
+                    s4.push_back(mj);
+                }
+                // S5..S8: baby-step rotations of u (hoisted INTT + CRT digits)
+                if (baby > 1) {
+                    for (int k = 0; k < 3; k++) {
+                        XJob j{};
+                        j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+                        j.a = P.U + (((size_t)tl * 2 + 1) * 3 + k) * NB;
+                        j.out = P.Ucoef + ((size_t)tl * 3 + k) * NB;
+                        s5.push_back(j);
+                    }
+                    CJob c{};
+                    c.level = 2; c.mode = 1;
+                    c.x = P.Ucoef + (size_t)tl * 3 * NB;
+                    c.xstride = NB;
+                    c.dig = P.digU + (size_t)tl * 2 * D2 * NB;
+                    s6.push_back(c);
+                    for (int b = 1; b < baby; b++) {
+                        const DevKey* kb = need_key(h, P.t_baby[b]);
+                        const size_t rb = (size_t)tl * (baby - 1) + (b - 1);
+                        for (int jj = 0; jj < D2; jj++)
+                            for (int k = 0; k < 3; k++) {
+                                XJob j{};
+                                j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_STORE;
+                                j.a = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + jj) * NB);
+                                j.b = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
+                                j.gal = kb->gal;
+                                j.out = P.dnttB + ((rb * D2 + jj) * 3 + k) * NB;
+                                s7.push_back(j);
+                            }
+                        MJob mj{};
+                        mj.level = 2; mj.nterm = 1;
+                        mj.t[0].dntt = P.dnttB + rb * D2 * 3 * NB;
+                        mj.t[0].key = kb->key;
+                        mj.t[0].c0src = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
+                        mj.t[0].perm = kb->perm;
+                        mj.out0 = P.ROT + (rb * 2 + 0) * 3 * NB;
+                        mj.out1 = P.ROT + (rb * 2 + 1) * 3 * NB;
+                        s8.push_back(mj);
+                    }
+                }
+                // S9: dropped-prime half of each diagonal product: INTT + rescale
+                //     correction into the block's slot of Eslot
+                for (int g = 0; g < G; g++)
+                    for (int b = 0; b < baby; b++) {
+                        const int i = g * baby + b;
+                        if (!P.live[(size_t)t * sp + i]) continue;
+                        const u64* dg = P.diag + ((size_t)t * sp + i) * 3 * NB;
+                        for (int poly = 0; poly < 2; poly++) {
+                            XJob j{};
+                            j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 2;
+                            j.a = rot_src(P, tl, b, poly) + 2 * NB;
+                            j.b = dg + 2 * NB;
+                            j.out = eslot(P, tl, b, g, poly);
+                            j.ostride = NB;
+                            s9.push_back(j);
+                        }
+                    }
+            }
+            rc = add_xf(S, s1); if (rc) return rc;
+            rc = add_xf(S, s2); if (rc) return rc;
+            rc = add_co(S, s2c); if (rc) return rc;
+            rc = add_xf(S, s3); if (rc) return rc;
+            rc = add_ma(S, s4, 3); if (rc) return rc;
+            rc = add_xf(S, s5); if (rc) return rc;
+            rc = add_co(S, s6); if (rc) return rc;
+            rc = add_xf(S, s7); if (rc) return rc;
+            rc = add_ma(S, s8, 3); if (rc) return rc;
+            rc = add_xf(S, s9); if (rc) return rc;
         }
-        S.par_begin();
-        rc = add_xf(S, s1); if (rc) return rc;
-        S.par_end();
-        S.par_begin();
-        rc = add_xf(S, s2); if (rc) return rc;
-        rc = add_co(S, s2c); if (rc) return rc;
-        S.par_end();
-        rc = add_xf(S, s3); if (rc) return rc;
-        rc = add_ma(S, s4, 3); if (rc) return rc;
-        rc = add_xf(S, s5); if (rc) return rc;
-        rc = add_co(S, s6); if (rc) return rc;
-        rc = add_xf(S, s7); if (rc) return rc;
-        rc = add_ma(S, s8, 3); if (rc) return rc;
-        S.par_begin();  // S9 and S10 both only read the rotated inputs
-        rc = add_xf(S, s9); if (rc) return rc;
-        // S10: kept-prime half of the diagonal products, X[g] += sum src * diag * q^-1
+        S.cur_lane = -1;
+        if (nl > 1) S.par_end();
+        // S10: per (g, poly): X += sum src * diag * q^-1 (kept primes) and
+        //      E += sum of the chunk's correction slots
         {
             std::vector<DXJob> dx;
-            std::vector<const u64*> srcs, dgs;
+            std::vector<const u64*> srcs, dgs, ess;
             struct Rng { size_t off, cnt; int g, poly; };
             std::vector<Rng> rngs;
             for (int g = 0; g < G; g++)
@@ -862,9 +894,9 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         for (int b = 0; b < baby; b++) {
                             const int i = g * baby + b;
                             if (!P.live[(size_t)t * sp + i]) continue;
-                            srcs.push_back(b == 0 ? P.U + ((size_t)tl * 2 + poly) * 3 * NB
-                                                  : P.ROT + (((size_t)tl * (baby - 1) + (b - 1)) * 2 + poly) * 3 * NB);
+                            srcs.push_back(rot_src(P, tl, b, poly));
                             dgs.push_back(P.diag + ((size_t)t * sp + i) * 3 * NB);
+                            ess.push_back(eslot(P, tl, b, g, poly));
                         }
                     }
                     rngs.push_back({off, srcs.size() - off, g, poly});
@@ -872,37 +904,32 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
             if (!srcs.empty()) {
                 const u64** dsrc = nullptr;
                 const u64** ddg = nullptr;
+                const u64** des = nullptr;
                 CU(cudaMalloc(&dsrc, srcs.size() * sizeof(u64*)));
                 S.allocs.push_back(dsrc);
                 CU(cudaMalloc(&ddg, dgs.size() * sizeof(u64*)));
                 S.allocs.push_back(ddg);
+                CU(cudaMalloc(&des, ess.size() * sizeof(u64*)));
+                S.allocs.push_back(des);
                 CU(cudaMemcpy(dsrc, srcs.data(), srcs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
                 CU(cudaMemcpy(ddg, dgs.data(), dgs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+                CU(cudaMemcpy(des, ess.data(), ess.size() * sizeof(u64*), cudaMemcpyHostToDevice));
                 for (const Rng& r : rngs) {
                     if (!r.cnt) continue;
                     DXJob d{};
                     d.nterm = (int)r.cnt;
                     d.src = dsrc + r.off;
                     d.dg = ddg + r.off;
+                    d.es = des + r.off;
                     d.X = P.PX + (size_t)1 * G * 2 * 2 * NB + (((size_t)r.g * 2 + r.poly) * 2) * NB;
+                    d.E = P.PX + (((size_t)r.g * 2 + r.poly) * 2) * NB;
                     dx.push_back(d);
                 }
                 rc = add_dx(S, dx, 2);
                 if (rc) return rc;
             }
         }
-        S.par_end();
     }
-    // fold E copies into PX[0]
-    Step st;
-    st.kind = ST_SUMC;
-    st.in = P.Ecp;
-    st.out = P.PX;
-    st.rows = (long long)G * 2 * 2;
-    st.period = 2;
-    st.copies = P.ncopy;
-    st.cstride = (long long)G * 2 * 2 * NB;
-    S.steps.push_back(st);
     return HC_OK;
 }
 
@@ -1417,9 +1444,9 @@ __global__ void __launch_bounds__(256) k_bf_peak(const __grid_constant__ DevCtx 
     u64 w = C.twf[5].w, ws = C.twf[5].ws;
     for (int it = 0; it < iters; it++) {
         HC_UNROLL
-        for (int i = 0; i < 8; i++) bf_ct(x[i], x[i + 8], w, ws, P.q, P.q2);
+        for (int i = 0; i < 8; i++) bf_ct_lazy(x[i], x[i + 8], w, ws, P.q, 2 * P.q2);
         HC_UNROLL
-        for (int i = 0; i < 16; i += 2) bf_ct(x[i], x[i + 1], w, ws, P.q, P.q2);
+        for (int i = 0; i < 16; i += 2) bf_ct_lazy(x[i], x[i + 1], w, ws, P.q, 2 * P.q2);
     }
     u64 acc = 0;
     for (int i = 0; i < 16; i++) acc ^= x[i];

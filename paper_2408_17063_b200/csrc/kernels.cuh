@@ -228,10 +228,11 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
             J.out[j0 + e * stride] = add_mod(x[e], EP == EP_ADD ? a[e] : red64(a[e], P.q, P.one_s), P.q);
     } else if constexpr (EP == EP_RESCALE || EP == EP_RESCALE_ATOMIC) {
         const int l = J.level;
+        const RescaleK R = rescale_consts(D, l);
         HC_UNROLL
         for (int e = 0; e < N; e++) {
             u64 ek[MAXL];
-            rescale_corr(D, l, x[e], ek);
+            rescale_corr(R, x[e], ek);
             HC_UNROLL
             for (int k = 0; k < MAXL; k++) {
                 if (k >= l) break;
@@ -350,7 +351,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         const int b = 128 * c + t;
         load_n<LD, CEPT>(C, J, P, b, CTILE, x);
         tw_prefetch(twsl, tw, c, t);
-        r8_ct(x, TwR{wa}, 0, 0, P.q, P.q2);
+        r8_ct(x, TwR{wa}, 0, 0, P.q, 2 * P.q2);
         TRACE(1);
         cluster_wait();
         TRACE(2);
@@ -366,12 +367,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         for (int p = 0; p < 3; p++) {
             const CPass I = cpass(p, c, t);
             c_load(x, tile, I);
-            r8_ct(x, twl, I.s0, I.G, P.q, P.q2);
+            r8_ct(x, twl, I.s0, I.G, P.q, 2 * P.q2);
             if (p == 2) {
                 u64 o[CEPT];
                 HC_UNROLL
                 for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-                c_st12(c, t, x, o, twl, P.q, P.q2);
+                c_st12(c, t, x, o, twl, P.q, 2 * P.q2, P.one_s);
             }
             c_store(x, tile, I);
             __syncthreads();
@@ -546,7 +547,9 @@ struct DXJob {
     int nterm, pad;
     const u64* const* src;  // nterm pointers, each [>=nprime][n]
     const u64* const* dg;   // nterm pointers, each [>=nprime][n]
+    const u64* const* es;   // nterm correction slots [nprime][n] (or null)
     u64* X;                 // [nprime][n], canonical, updated in place
+    u64* E;                 // [nprime][n], += sum of the slots (mod q)
 };
 
 __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
@@ -555,9 +558,13 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
-    u64 h = 0, l = 0;
-    for (int t = 0; t < J.nterm; t++) mac128(h, l, J.src[t][kn], J.dg[t][kn]);
+    u64 h = 0, l = 0, es = 0;
+    for (int t = 0; t < J.nterm; t++) {
+        mac128(h, l, J.src[t][kn], J.dg[t][kn]);
+        if (J.es) es += J.es[t][kn];  // < 2^54 each, nterm <= 1023
+    }
     J.X[kn] = add_mod(J.X[kn], redc(h, l, pc.q, pc.qneg), pc.q);
+    if (J.es) J.E[kn] = add_mod(J.E[kn], red64(es, pc.q, pc.one_s), pc.q);
 }
 
 // ---------------------------------------------------------------------------

@@ -95,7 +95,8 @@ HD void sm_store(const u64 (&x)[EPT], u64* sm, int base, int stride) {
 }
 
 // 4 Cooley-Tukey stages s0..s0+3 on a 16-point group: stage s0+u pairs v and
-// v + (8 >> u), twiddle tbl[2^(s0+u) + (hi << u | v >> (4-u))].
+// v + (8 >> u), twiddle tbl[2^(s0+u) + (hi << u | v >> (4-u))].  Lazy
+// (bf_ct_lazy): q2 here carries 4q.
 HD void r16_ct(u64 (&x)[EPT], const Tw* tw, int s0, int hi, u64 q, u64 q2) {
     HC_UNROLL
     for (int u = 0; u < 4; u++) {
@@ -105,7 +106,7 @@ HD void r16_ct(u64 (&x)[EPT], const Tw* tw, int s0, int hi, u64 q, u64 q2) {
         for (int v = 0; v < EPT; v++) {
             if (!(v & half)) {
                 Tw w = ldtw(tw, tbase + (v >> (4 - u)));
-                bf_ct(x[v], x[v + half], w.w, w.ws, q, q2);
+                bf_ct_lazy(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
     }
@@ -130,8 +131,9 @@ HD void r16_gs(u64 (&x)[EPT], const Tw* tw, int b0, int hi, u64 q, u64 q2) {
 
 // Forward stage 12 (index bit 0) across the lane pair (t, t^1): even lane
 // keeps X + w*Y, odd lane X - w*Y, w = tbl[4096 + ((t >> 1) << 4 | v)].
-// Inputs [0,4q), outputs canonical.  `other` = the partner lane's registers.
-HD void st12_ct(int t, u64 (&x)[EPT], const u64 (&other)[EPT], const Tw* tw, u64 q, u64 q2) {
+// Lazy inputs (< 52q), outputs canonical.  `other` = the partner lane's
+// registers; q2 carries 4q, one_s the full-reduction constant.
+HD void st12_ct(int t, u64 (&x)[EPT], const u64 (&other)[EPT], const Tw* tw, u64 q, u64 q2, u64 one_s) {
     const int odd = t & 1;
     const int tb = 4096 + ((t >> 1) << 4);
     HC_UNROLL
@@ -139,8 +141,8 @@ HD void st12_ct(int t, u64 (&x)[EPT], const u64 (&other)[EPT], const Tw* tw, u64
         u64 X = odd ? other[v] : x[v];
         u64 Y = odd ? x[v] : other[v];
         Tw w = ldtw(tw, tb + v);
-        bf_ct(X, Y, w.w, w.ws, q, q2);
-        x[v] = canon4(odd ? Y : X, q, q2);
+        bf_ct_lazy(X, Y, w.w, w.ws, q, q2);
+        x[v] = canon_any(odd ? Y : X, q, one_s);
     }
 }
 
@@ -207,11 +209,11 @@ __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* 
     for (int p = 0; p < 3; p++) {
         const PassIdx I = pass_idx(p, t);
         sm_load(x, sm, I.base, I.stride);
-        r16_ct(x, tw, I.s0, I.hi, P.q, P.q2);
+        r16_ct(x, tw, I.s0, I.hi, P.q, 2 * P.q2);
         if (p == 2) {
             u64 o[EPT];
             shfl_pair(x, o);
-            st12_ct(t, x, o, tw, P.q, P.q2);
+            st12_ct(t, x, o, tw, P.q, 2 * P.q2, P.one_s);
         }
         sm_store(x, sm, I.base, I.stride);
         __syncthreads();
@@ -251,12 +253,12 @@ inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
         for (int t = 0; t < NT; t++) {
             PassIdx I = pass_idx(p, t);
             sm_load(regs[t], sm, I.base, I.stride);
-            r16_ct(regs[t], tw, I.s0, I.hi, P.q, P.q2);
+            r16_ct(regs[t], tw, I.s0, I.hi, P.q, 2 * P.q2);
         }
         if (p == 2) {
             for (int t = 0; t < NT; t++)
                 for (int v = 0; v < EPT; v++) other[t][v] = regs[t ^ 1][v];
-            for (int t = 0; t < NT; t++) st12_ct(t, regs[t], other[t], tw, P.q, P.q2);
+            for (int t = 0; t < NT; t++) st12_ct(t, regs[t], other[t], tw, P.q, 2 * P.q2, P.one_s);
         }
         for (int t = 0; t < NT; t++) {
             PassIdx I = pass_idx(p, t);

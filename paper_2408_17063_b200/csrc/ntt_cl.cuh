@@ -106,7 +106,7 @@ HD void r8_ct(u64 (&x)[CEPT], const TW& tw, int s0, int G, u64 q, u64 q2) {
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
                 Tw w = tw(tb + (v >> (3 - u)), 1 << (s0 + u));
-                bf_ct(x[v], x[v + half], w.w, w.ws, q, q2);
+                bf_ct_lazy(x[v], x[v + half], w.w, w.ws, q, q2);
             }
         }
     }
@@ -133,7 +133,7 @@ HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q2) {
 // forward bit-0 stage across lanes (t, t^1) in pass-2 layout:
 // w = tbl[4096 + (j >> 1)], j >> 1 = (c << 9) | ((t >> 1) << 3) | v
 template <class TW>
-HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2) {
+HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2, u64 one_s) {
     const int odd = t & 1;
     const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
     HC_UNROLL
@@ -141,8 +141,8 @@ HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw,
         u64 X = odd ? o[v] : x[v];
         u64 Y = odd ? x[v] : o[v];
         Tw w = tw(tb + v, 4096);
-        bf_ct(X, Y, w.w, w.ws, q, q2);
-        x[v] = canon4(odd ? Y : X, q, q2);
+        bf_ct_lazy(X, Y, w.w, w.ws, q, q2);
+        x[v] = canon_any(odd ? Y : X, q, one_s);
     }
 }
 
@@ -166,7 +166,7 @@ HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, 
 }
 
 // forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
-HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q2) { r8_ct(x, TwG{tw}, 0, 0, q, q2); }
+HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q4) { r8_ct(x, TwG{tw}, 0, 0, q, q4); }
 
 // inverse phase A': GS stages 10, 11 on the column, then bit 12 folded with n^-1
 HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
@@ -210,7 +210,7 @@ inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
             u64 x[CEPT];
             const int b = 128 * c + t;
             for (int r = 0; r < CEPT; r++) x[r] = a[r * CTILE + b];
-            c_phaseA_fwd(x, tw, P.q, P.q2);
+            c_phaseA_fwd(x, tw, P.q, 2 * P.q2);
             for (int r = 0; r < CEPT; r++) tile[r][cswz(b)] = x[r];
         }
     for (int p = 0; p < 3; p++) {
@@ -218,14 +218,14 @@ inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
             for (int t = 0; t < CNT; t++) {
                 CPass I = cpass(p, c, t);
                 c_load(regs[c][t], tile[c], I);
-                r8_ct(regs[c][t], TwL{sl[c], c}, I.s0, I.G, P.q, P.q2);
+                r8_ct(regs[c][t], TwL{sl[c], c}, I.s0, I.G, P.q, 2 * P.q2);
             }
         if (p == 2) {
             for (int c = 0; c < CL; c++)
                 for (int t = 0; t < CNT; t++)
                     for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
             for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++) c_st12(c, t, regs[c][t], oth[c][t], TwL{sl[c], c}, P.q, P.q2);
+                for (int t = 0; t < CNT; t++) c_st12(c, t, regs[c][t], oth[c][t], TwL{sl[c], c}, P.q, 2 * P.q2, P.one_s);
         }
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) c_store(regs[c][t], tile[c], cpass(p, c, t));
