@@ -260,7 +260,6 @@ def main():
     cd = np.ascontiguousarray(np.stack([c.payload.res for c in cts]))
     cv = np.ascontiguousarray(np.stack([c.payload.res for c in hint]))
     dc.set_inputs(cd, cv)
-    info = be.plan_info()
 
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
@@ -323,6 +322,7 @@ def main():
     clk = clocks.stop()
     assert np.array_equal(out_h.numpy().view(np.uint64), out), "e2e output differs from the device-resident run"
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
+    info = be.plan_info()  # kernel launches per Comp (graph built by now)
 
     if dist:
         tt = torch.tensor([t_ms, e2e_ms], dtype=torch.float64, device="cuda")
@@ -348,8 +348,11 @@ def main():
     peak = ctypes.c_double()
     _lib.check(L.hc_bf_peak(h, ctypes.byref(peak)))
     bfly_per_ntt = (RING // 2) * 13
+    # dominant kernel family = the transform launches (k_xf / k_xf_cl):
+    # algorithmic butterflies per launch / that launch's event-timed duration
     achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
     peak_g = peak.value / 1e9
+    comp_level = xf_jobs * bfly_per_ntt / (per_step_ms_pre := (t_ms / args.steps)) / 1e6
 
     per_step_ms = t_ms / args.steps
     value = args.N * world / (per_step_ms * 1e-3)
@@ -379,14 +382,17 @@ def main():
         "gpu_launches": int(info["kernel_launches"]) * args.steps * 2,
         "kernel_launches_per_comp": int(info["kernel_launches"]),
         "roofline": {
-            "kernel": "k_xform (8192-point NTT/INTT, 1 CTA per transform, fused loaders/epilogues)",
+            "kernel": "k_xf / k_xf_cl: 8192-point NTT/INTT launches (1 CTA or one 8-CTA cluster per transform, fused loaders/epilogues)",
             "bound": "int-modmul (IMAD pipe; SURVEY 8(d))",
             "achieved": achieved,
             "peak": peak_g,
             "unit": "Gbutterfly/s",
             "frac": achieved / peak_g if peak_g else None,
-            "peak_source": "measured live: hc_bf_peak register-only microbenchmark of the same butterfly (MEASURED_PEAKS.json has no integer peak)",
+            "peak_source": "measured live: hc_bf_peak, register-only microbenchmark of the kernels' own lazy CT butterfly at full occupancy (MEASURED_PEAKS.json has no integer peak)",
+            "work_unit": "one radix-2 butterfly = one 54-bit modmul + 2 modadds; 4096*13 per 8192-point transform",
             "traffic": None,
+            "comp_level_gbfly_s": comp_level,
+            "comp_level_frac": comp_level / peak_g if peak_g else None,
             "xform_share_of_step": xf_ms / prof_total if prof_total else None,
             "xform_jobs_per_comp": xf_jobs,
             "xform_launches_per_comp": xf_launch,

@@ -124,6 +124,11 @@ int hc_bench_xform(hc_ctx* h, int njobs, int dir, int iters, double* us_per_laun
  * (latency path); larger launches use one CTA per transform.  Default 16. */
 int hc_set_cluster_threshold(int max_jobs);
 
+/* Debug builds compiled with -DHC_TRACE: reset the launch numbering and read
+ * per-CTA %globaltimer stamps [128 launches][512 CTAs][8 points]. */
+int hc_trace_reset(void);
+int hc_trace_read(uint64_t* out);
+
 /* Pure host helpers (no GPU needed): Galois tables for element t.
  * coef: uint16[n] (source index | negate << 15) realising X -> X^t on
  * coefficients (coeff_automorphism, bgv.py:273-284, as a gather);

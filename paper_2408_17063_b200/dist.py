@@ -1,0 +1,79 @@
+"""Block-sharded Comp over torch.distributed.
+
+The BSGS matvec is a sum over width-4096 blocks (compress.py:286-297): every
+block's pack, baby rotations and diagonal products are independent until
+they are added into the giant-step accumulators acc[g] at level 1.  Each
+rank runs those for a contiguous block range (libhcomp hc_comp_partial) and
+leaves partial accumulators whose words are all < 2^54; one uint64 SUM
+reduce to the root (NCCL over NVLink on GPUs; < 2^57 for <= 8 ranks, no
+overflow) combines them, and the root alone runs the giant-step and fold
+key switches and the output mask (hc_comp_finish), which do not shard:
+key switching is not additive bit-for-bit.
+
+This is the only collective on the path.  Batched independent queries
+(config 5) need none: one query per rank.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .compress import CompressedAnswer, _check_inputs, comp_noise, live_diagonals
+from .backend import Ciphertext, RnsPayload
+
+
+def shard_blocks(B: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced block range [b0, b1) of `rank` (first B % world
+    ranks take one extra block).  Ranges tile [0, B) exactly."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    base, extra = divmod(B, world)
+    b0 = rank * base + min(rank, extra)
+    return b0, b0 + base + (1 if rank < extra else 0)
+
+
+def reduce_partials(t, dist, group=None, root: int = 0):
+    """Sum the ranks' partial accumulators on `root` (int64 view of uint64 words,
+    each < 2^54: the sum over <= 1023 ranks stays exact)."""
+    dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def comp_sharded(cd, params, backend, keys, index_hint, dist, group=None, root: int = 0):
+    """compress.comp (hint path, packed) with the blocks sharded over the ranks
+    of `group`.  Every rank holds the full standard-layout inputs; the
+    CompressedAnswer is returned on `root` (None elsewhere)."""
+    import torch
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    cv = list(index_hint)
+    cd = list(cd)
+    _check_inputs(cd, cv, params, backend, keys)
+    live = live_diagonals(params)
+    bits, sim = comp_noise(backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live)
+    backend.plan(params.N, params.s, keys)
+    L = _lib.lib()
+    h = backend._ctx()
+    cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd]), dtype=np.uint64)
+    cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv]), dtype=np.uint64)
+    _lib.check(L.hc_comp_set_inputs(h, _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd)))
+    words = L.hc_partial_words(h)
+    b0, b1 = shard_blocks(params.num_blocks, world, rank)
+    part = torch.zeros(words, dtype=torch.int64, device="cuda")
+    _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(part.data_ptr()), None))
+    torch.cuda.synchronize()
+    reduce_partials(part, dist, group, root)
+    if rank != root:
+        return None
+    _lib.check(L.hc_comp_finish(h, ctypes.c_void_p(part.data_ptr()), None))
+    out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
+    _lib.check(L.hc_comp_get_output(h, _lib.ptr(out)))
+    backend.counters.keyswitches += sim.ks
+    backend.counters.pt_mults += sim.pt
+    backend.counters.adds += sim.adds
+    ct = Ciphertext(backend.backend_id, keys.key_id, 0, RnsPayload(out, bits, (backend.q[0],)))
+    return CompressedAnswer((ct,), params.s, True)
