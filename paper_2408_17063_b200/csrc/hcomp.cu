@@ -721,17 +721,17 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
     add_memset(S, P.PX, P.px_words() * 8);
     for (long long c0 = b0; c0 < b1; c0 += P.CB) {
         const int cb = (int)std::min<long long>(P.CB, b1 - c0);
-        // lanes only while every lane's levels stay wide enough to fill the GPU
-        // (>= 8 blocks per lane); small chunks run as one stream so the
-        // narrow levels can use the low-latency cluster transforms
-        const int nl = std::max(1, std::min(4, cb / 8));
-        if (nl > 1) S.par_begin();
-        for (int lane = 0; lane < nl; lane++) {
-            S.cur_lane = nl > 1 ? lane : -1;
-            std::vector<XJob> s1, s2, s3, s5, s7, s9;
-            std::vector<CJob> s2c, s6;
-            std::vector<MJob> s4, s8;
-            for (int tl = lane; tl < cb; tl += nl) {
+        // S1..S6 (pack, u = P + rot_col(R), hoisted baby INTT + digits) run as
+        // one stream over the chunk (narrow levels may use cluster transforms);
+        // the wide baby segment S7 (digit NTTs) -> S8 (MAC) -> S9 (diagonal
+        // INTTs) runs as up to 4 parallel lanes of blocks so the memory-bound
+        // MAC of one block overlaps the NTTs of the next.
+        std::vector<XJob> s1, s2, s3, s5;
+        std::vector<CJob> s2c, s6;
+        std::vector<MJob> s4;
+        std::vector<std::vector<XJob>> s7(cb), s9(cb);
+        std::vector<std::vector<MJob>> s8(cb);
+        for (int tl = 0; tl < cb; tl++) {
                 const long long t = c0 + tl;
                 const long long src = t / 2;
                 const int par = (int)(t % 2);
@@ -835,7 +835,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                                 j.b = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
                                 j.gal = kb->gal;
                                 j.out = P.dnttB + ((rb * D2 + jj) * 3 + k) * NB;
-                                s7.push_back(j);
+                                s7[tl].push_back(j);
                             }
                         MJob mj{};
                         mj.level = 2; mj.nterm = 1;
@@ -845,7 +845,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         mj.t[0].perm = kb->perm;
                         mj.out0 = P.ROT + (rb * 2 + 0) * 3 * NB;
                         mj.out1 = P.ROT + (rb * 2 + 1) * 3 * NB;
-                        s8.push_back(mj);
+                        s8[tl].push_back(mj);
                     }
                 }
                 // S9: dropped-prime half of each diagonal product: INTT + rescale
@@ -862,20 +862,26 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                             j.b = dg + 2 * NB;
                             j.out = eslot(P, tl, b, g, poly);
                             j.ostride = NB;
-                            s9.push_back(j);
+                            s9[tl].push_back(j);
                         }
                     }
+        }
+        rc = add_xf(S, s1); if (rc) return rc;
+        rc = add_xf(S, s2); if (rc) return rc;
+        rc = add_co(S, s2c); if (rc) return rc;
+        rc = add_xf(S, s3); if (rc) return rc;
+        rc = add_ma(S, s4, 3); if (rc) return rc;
+        rc = add_xf(S, s5); if (rc) return rc;
+        rc = add_co(S, s6); if (rc) return rc;
+        const int nl = std::min(4, cb);
+        if (nl > 1) S.par_begin();
+        for (int lane = 0; lane < nl; lane++) {
+            S.cur_lane = nl > 1 ? lane : -1;
+            for (int tl = lane; tl < cb; tl += nl) {
+                rc = add_xf(S, s7[tl]); if (rc) return rc;
+                rc = add_ma(S, s8[tl], 3); if (rc) return rc;
+                rc = add_xf(S, s9[tl]); if (rc) return rc;
             }
-            rc = add_xf(S, s1); if (rc) return rc;
-            rc = add_xf(S, s2); if (rc) return rc;
-            rc = add_co(S, s2c); if (rc) return rc;
-            rc = add_xf(S, s3); if (rc) return rc;
-            rc = add_ma(S, s4, 3); if (rc) return rc;
-            rc = add_xf(S, s5); if (rc) return rc;
-            rc = add_co(S, s6); if (rc) return rc;
-            rc = add_xf(S, s7); if (rc) return rc;
-            rc = add_ma(S, s8, 3); if (rc) return rc;
-            rc = add_xf(S, s9); if (rc) return rc;
         }
         S.cur_lane = -1;
         if (nl > 1) S.par_end();

@@ -7,7 +7,7 @@
 #include <vector>
 
 #include "elem.cuh"
-#include "ntt_cl.cuh"
+#include "ntt1k.cuh"
 #include "host_tables.hpp"
 
 using namespace hc;

@@ -19,7 +19,7 @@
 #include <cooperative_groups.h>
 
 #include "elem.cuh"
-#include "ntt_cl.cuh"
+#include "ntt1k.cuh"
 
 namespace hc {
 
@@ -257,24 +257,22 @@ __global__ void __launch_bounds__(NT, 1) k_xf(const __grid_constant__ DevCtx C, 
     const int t = threadIdx.x;
     const PrimeC& P = C.pc[J.k];
     TRACE(0);
-    HC_UNROLL
-    for (int h = 0; h < 2; h++) {  // two halves of 8 coefficients: t + 512 v
-        u64 x[8];
-        load_n<LD, 8>(C, J, P, t + 8 * NT * h, NT, x);
+    {
+        u64 x[EPT];  // coefficients t + 1024 v
+        load_n<LD, EPT>(C, J, P, t, NT, x);
         HC_UNROLL
-        for (int v = 0; v < 8; v++) sm[swz(t + NT * (8 * h + v))] = x[v];
+        for (int v = 0; v < EPT; v++) sm[swz(t + NT * v)] = x[v];
     }
     __syncthreads();
     TRACE(1);
     if (DIR == 0) cta_ntt_fwd(C.twf + (size_t)J.k * NPOLY, P, sm);
     else cta_ntt_inv(C.twi + (size_t)J.k * NPOLY, P, sm);
     TRACE(4);
-    HC_UNROLL
-    for (int h = 0; h < 2; h++) {
-        u64 x[8];
+    {
+        u64 x[EPT];
         HC_UNROLL
-        for (int v = 0; v < 8; v++) x[v] = sm[swz(t + NT * (8 * h + v))];
-        store_n<EP, 8>(C, J, P, t + 8 * NT * h, NT, x);
+        for (int v = 0; v < EPT; v++) x[v] = sm[swz(t + NT * v)];
+        store_n<EP, EPT>(C, J, P, t, NT, x);
     }
     TRACE(5);
 }

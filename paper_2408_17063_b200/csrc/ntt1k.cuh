@@ -1,0 +1,144 @@
+// Single-CTA negacyclic NTT / INTT for n = 8192 (throughput path): one CTA
+// of 1024 threads per transform, 8 coefficients per thread, radix-8
+// register passes (the building blocks of ntt_cl.cuh) through a swizzled
+// 64 KiB shared-memory tile.  13 stages = 3 + 3 + 3 + 3 + 1 (the bit-0 stage
+// across lane pairs by warp shuffle).  At <= 64 registers per thread this
+// keeps 32 warps per SM resident (the 512-thread radix-16 version had 16 and
+// was latency-bound: ncu issue-active 42%).
+//
+// Tile convention: coefficient j at sm[swz(j)]; the caller fills the tile
+// (natural order), syncs, calls the transform, and reads the result back in
+// natural order.  Forward input < 4q (lazy CT, output canonical); inverse
+// input < 2q (GS, output canonical).  Semantics: NttContext.fwd/inv
+// (bgv.py:178-225).
+#pragma once
+#include "ntt_cl.cuh"
+
+namespace hc {
+
+// 64-bit, 16-lane phases: XOR index bits 1..3 with bits 4..6 (conflict-free
+// for the four affine layouts below)
+HD int swz(int j) { return cswz(j); }
+
+// forward pass p covers bits 12-3p .. 10-3p: thread t's coefficients are
+// j(v) = base + v*stride, G = index bits above the pass
+HD CPass pass1k(int p, int t) {
+    CPass r;
+    if (p == 0) {
+        r.base = t; r.stride = 1024; r.G = 0; r.s0 = 0;
+    } else if (p == 1) {
+        r.base = ((t >> 7) << 10) | (t & 127); r.stride = 128; r.G = t >> 7; r.s0 = 3;
+    } else if (p == 2) {
+        r.base = ((t >> 4) << 7) | (t & 15); r.stride = 16; r.G = t >> 4; r.s0 = 6;
+    } else {
+        r.base = ((t >> 1) << 4) | (t & 1); r.stride = 2; r.G = t >> 1; r.s0 = 9;
+    }
+    return r;
+}
+
+HD void t_load(u64 (&x)[EPT], const u64* sm, const CPass& I) {
+    HC_UNROLL
+    for (int v = 0; v < EPT; v++) x[v] = sm[swz(I.base + v * I.stride)];
+}
+HD void t_store(const u64 (&x)[EPT], u64* sm, const CPass& I) {
+    HC_UNROLL
+    for (int v = 0; v < EPT; v++) sm[swz(I.base + v * I.stride)] = x[v];
+}
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* sm) {
+    const int t = threadIdx.x;
+    const TwG tg{tw};
+    u64 x[EPT];
+    HC_NOUNROLL
+    for (int p = 0; p < 4; p++) {
+        const CPass I = pass1k(p, t);
+        t_load(x, sm, I);
+        r8_ct(x, tg, I.s0, I.G, P.q, 2 * P.q2);
+        if (p == 3) {
+            u64 o[EPT];
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
+            c_st12(0, t, x, o, tg, P.q, 2 * P.q2, P.one_s);
+        }
+        t_store(x, sm, I);
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* sm) {
+    const int t = threadIdx.x;
+    const TwG tg{tw};
+    u64 x[EPT];
+    HC_NOUNROLL
+    for (int p = 0; p < 3; p++) {
+        const CPass I = pass1k(3 - p, t);
+        t_load(x, sm, I);
+        if (p == 0) {
+            u64 o[EPT];
+            HC_UNROLL
+            for (int v = 0; v < EPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
+            c_st0(0, t, x, o, tg, P.q, P.q2);
+        }
+        r8_gs(x, tg, 1 + 3 * p, I.G, P.q, P.q2);
+        t_store(x, sm, I);
+        __syncthreads();
+    }
+    const CPass I = pass1k(0, t);
+    t_load(x, sm, I);
+    c_phaseA_inv(x, tw, P);  // bits 10..12 (element v*1024 + t), n^-1 folded
+    t_store(x, sm, I);
+    __syncthreads();
+}
+#endif
+
+// ---- host emulation of the 1024-thread schedule (CPU self-test only) ------
+inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
+    static u64 regs[NT][EPT], oth[NT][EPT];
+    static u64 sm[NPOLY];
+    const TwG tg{tw};
+    for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
+    for (int p = 0; p < 4; p++) {
+        for (int t = 0; t < NT; t++) {
+            CPass I = pass1k(p, t);
+            t_load(regs[t], sm, I);
+            r8_ct(regs[t], tg, I.s0, I.G, P.q, 2 * P.q2);
+        }
+        if (p == 3) {
+            for (int t = 0; t < NT; t++)
+                for (int v = 0; v < EPT; v++) oth[t][v] = regs[t ^ 1][v];
+            for (int t = 0; t < NT; t++) c_st12(0, t, regs[t], oth[t], tg, P.q, 2 * P.q2, P.one_s);
+        }
+        for (int t = 0; t < NT; t++) t_store(regs[t], sm, pass1k(p, t));
+    }
+    for (int j = 0; j < NPOLY; j++) a[j] = sm[swz(j)];
+}
+
+inline void host_emulate_inv(u64* a, const Tw* tw, const PrimeC& P) {
+    static u64 regs[NT][EPT], oth[NT][EPT];
+    static u64 sm[NPOLY];
+    const TwG tg{tw};
+    for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
+    for (int p = 0; p < 3; p++) {
+        for (int t = 0; t < NT; t++) t_load(regs[t], sm, pass1k(3 - p, t));
+        if (p == 0) {
+            for (int t = 0; t < NT; t++)
+                for (int v = 0; v < EPT; v++) oth[t][v] = regs[t ^ 1][v];
+            for (int t = 0; t < NT; t++) c_st0(0, t, regs[t], oth[t], tg, P.q, P.q2);
+        }
+        for (int t = 0; t < NT; t++) {
+            CPass I = pass1k(3 - p, t);
+            r8_gs(regs[t], tg, 1 + 3 * p, I.G, P.q, P.q2);
+            t_store(regs[t], sm, I);
+        }
+    }
+    for (int t = 0; t < NT; t++) {
+        CPass I = pass1k(0, t);
+        t_load(regs[t], sm, I);
+        c_phaseA_inv(regs[t], tw, P);
+        t_store(regs[t], sm, I);
+    }
+    for (int j = 0; j < NPOLY; j++) a[j] = sm[swz(j)];
+}
+
+}  // namespace hc
