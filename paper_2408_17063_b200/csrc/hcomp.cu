@@ -61,7 +61,7 @@ struct DevKey {
 static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters (split by CL_MAX)
 static const int CL_SPREAD_SMEM = 120 * 1024;
 
-enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET };
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET, ST_I2 };
 struct Step {
     int kind = 0;
     int njobs = 0;
@@ -74,6 +74,7 @@ struct Step {
     int period = 0, copies = 0;
     size_t bytes = 0;
     std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
+    std::vector<Intt2Job> i2jobs;  // ST_I2
     int group = 0;            // consecutive steps with the same nonzero group run concurrently
     int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
     int lane = -1;            // in a group: steps of one lane run in order on one branch
@@ -135,6 +136,7 @@ static void release_key(DevKey& k) {
     X(0, LD_RED, EP_ADDRED)           \
     X(1, LD_RED, EP_ADDRED)           \
     X(0, LD_COMPOSE, EP_KSACC)        \
+    X(0, LD_DIGGAL, EP_KSACC)         \
     X(1, LD_KSFIN, EP_STORE)          \
     X(1, LD_KSFIN, EP_RESCALE)
 
@@ -150,6 +152,8 @@ static int configure_kernels() {
     XF_COMBOS(XF_CFG)
 #undef XF_CFG
     CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
+    CU(cudaFuncSetAttribute(k_cl_intt2<LD_KSFIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaFuncSetAttribute(k_cl_intt2<LD_RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
     kernels_configured = 1;
     return HC_OK;
 }
@@ -336,6 +340,22 @@ static int add_dx(Schedule& S, const std::vector<DXJob>& jobs, int nprime) {
     S.steps.push_back(st);
     return HC_OK;
 }
+// two-prime INTT + CRT digits (k_cl_intt2), <= I2_MAX jobs per launch
+static int add_i2(Schedule& S, std::vector<Intt2Job> jobs) {
+    for (size_t c0 = 0; c0 < jobs.size(); c0 += I2_MAX) {
+        Step st;
+        st.kind = ST_I2;
+        st.group = S.cur_group;
+        st.lane = S.cur_lane;
+        st.i2jobs.assign(jobs.begin() + c0, jobs.begin() + std::min(jobs.size(), c0 + (size_t)I2_MAX));
+        for (Intt2Job& j : st.i2jobs) j.j[0].trace = j.j[1].trace = g_trace_seq;
+        g_trace_seq++;
+        st.njobs = (int)st.i2jobs.size();
+        S.steps.push_back(st);
+    }
+    return HC_OK;
+}
+
 static void add_memset(Schedule& S, void* p, size_t bytes) {
     Step st;
     st.kind = ST_MEMSET;
@@ -387,6 +407,17 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
             case ST_MEMSET:
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
                 break;
+            case ST_I2: {
+                Intt2Jobs jj;
+                memset(&jj, 0, sizeof jj);
+                memcpy(jj.j, st.i2jobs.data(), st.i2jobs.size() * sizeof(Intt2Job));
+                const int n = (int)st.i2jobs.size();
+                if (st.i2jobs[0].j[0].ld == LD_KSFIN)
+                    k_cl_intt2<LD_KSFIN><<<n * CL, 2 * CNT, CL_SPREAD_SMEM, s>>>(h->hctx, jj);
+                else
+                    k_cl_intt2<LD_RED><<<n * CL, 2 * CNT, CL_SPREAD_SMEM, s>>>(h->hctx, jj);
+                break;
+            }
         }
         CU(cudaGetLastError());
     }
@@ -630,11 +661,11 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
     PA(P->A0, (size_t)G * 2 * NB);
     PA(P->A1, (size_t)2 * NB);
     PA(P->A1coef, (size_t)G * 2 * NB);
-    PA(P->digG, (size_t)G * P->D1 * NB);
+    PA(P->digG, (size_t)G * 2 * P->D1 * NB);
     PA(P->dnttG, (size_t)G * P->D1 * 2 * NB);
     PA(P->RES, (size_t)2 * 2 * 2 * NB);
     PA(P->rc1coef, (size_t)2 * NB);
-    PA(P->digF, (size_t)P->D1 * NB);
+    PA(P->digF, (size_t)2 * P->D1 * NB);
     PA(P->dnttF, (size_t)P->D1 * 2 * NB);
     PA(P->corr, (size_t)2 * NB);
     PA(P->OUT, (size_t)2 * NB);
@@ -973,8 +1004,10 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     auto ex = [&](const u64* base, int g, int poly, int k) { return base + (((size_t)g * 2 + poly) * 2 + k) * NB; };
     int rc;
     add_memset(S, P.ACC, (size_t)2 * 2 * NB * 8);
-    // T1
+    // T1 (acc[g] c0 transforms; c1 of g >= 1 inverted on both primes with the
+    // CRT digit split fused: k_cl_intt2)
     std::vector<XJob> t1;
+    std::vector<Intt2Job> t1i;
     for (int g = 0; g < G; g++) {
         if (!P.acc_live[g]) continue;
         for (int k = 0; k < 2; k++) {
@@ -990,28 +1023,31 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
                 c.ea = ex(X, g, 1, k);
                 c.out = P.A1 + (size_t)k * NB;
                 t1.push_back(c);
-            } else {
-                XJob c{};
-                c.dir = 1; c.k = k; c.ld = LD_RED; c.ep = EP_ADDRED;
-                c.a = ex(X, g, 1, k);
-                c.ea = ex(E, g, 1, k);
-                c.out = P.A1coef + ((size_t)g * 2 + k) * NB;
-                t1.push_back(c);
             }
+        }
+        if (g > 0) {
+            Intt2Job ij{};
+            for (int k = 0; k < 2; k++) {
+                ij.j[k].dir = 1; ij.j[k].k = k; ij.j[k].ld = LD_RED; ij.j[k].ep = EP_STORE;
+                ij.j[k].a = ex(X, g, 1, k);
+            }
+            ij.E = ex(E, g, 1, 0);
+            ij.dig = P.digG + (size_t)g * 2 * D1 * NB;
+            t1i.push_back(ij);
         }
     }
     S.par_begin();
     rc = add_xf(S, t1); if (rc) return rc;
+    rc = add_i2(S, t1i); if (rc) return rc;
     S.par_end();
-    auto digit_jobs = [&](std::vector<XJob>& out, const u64* coef, const DevKey* key) {
+    auto digit_jobs = [&](std::vector<XJob>& out, const uint16_t* dig, const DevKey* key) {
         for (int d = 0; d < D1; d++)
             for (int k = 0; k < 2; k++) {
                 XJob j{};
-                j.dir = 0; j.k = k; j.ld = LD_COMPOSE; j.ep = EP_KSACC;
-                j.a = coef;
+                j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_KSACC;
+                j.a = (const u64*)(dig + (size_t)d * NB);
+                j.b = (const u64*)(dig + (size_t)(D1 + d) * NB);
                 j.gal = key->gal;
-                j.clevel = 1;
-                j.dig = d;
                 j.ea = key->key + ((size_t)(d * 2 + 0) * 4 + k) * NB;  // b_d at prime k
                 j.eb = key->key + ((size_t)(d * 2 + 1) * 4 + k) * NB;  // a_d at prime k
                 j.out = P.ACC + (size_t)k * NB;                         // c0 row; c1 row at +2n
@@ -1035,7 +1071,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     for (int g = 1; g < G; g++) {
         if (!P.acc_live[g]) continue;
         const DevKey* kg = need_key(h, P.t_giant[g]);
-        digit_jobs(t3, P.A1coef + (size_t)g * 2 * NB, kg);
+        digit_jobs(t3, P.digG + (size_t)g * 2 * D1 * NB, kg);
         if (s0.nterm == MAXTERM_KS) return fail(HC_ERR_ARG, "too many giant steps");
         KsTerm T{};
         T.c0src = P.A0 + (size_t)g * 2 * NB;
@@ -1050,21 +1086,21 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
         const KsSpec* d0 = upload_spec(S, s0, &rc); if (rc) return rc;
         const KsSpec* d1 = upload_spec(S, s1, &rc); if (rc) return rc;
         std::vector<XJob> f1, f3;
+        Intt2Job ij{};
         for (int k = 0; k < 2; k++) {
-            XJob j{};
-            j.dir = 1; j.k = k; j.ld = LD_KSFIN; j.ep = EP_STORE;
-            j.ks = d1;
-            j.aux = cur + (size_t)(2 + k) * NB;  // res_f.c1
-            j.out = P.rc1coef + (size_t)k * NB;
-            f1.push_back(j);
+            ij.j[k].dir = 1; ij.j[k].k = k; ij.j[k].ld = LD_KSFIN; ij.j[k].ep = EP_STORE;
+            ij.j[k].ks = d1;
+            ij.j[k].aux = cur + (size_t)(2 + k) * NB;  // res_f.c1
             XJob e{};
             e.dir = 1; e.k = k; e.ld = LD_KSFIN; e.noxf = 1;
             e.ks = d0;
             e.aux = cur + (size_t)k * NB;  // res_f.c0
             f1.push_back(e);
         }
-        digit_jobs(f3, P.rc1coef, ka);
-        S.par_begin();  // res_f.c1 INTT and the res_f.c0 finish are independent
+        ij.dig = P.digF;
+        digit_jobs(f3, P.digF, ka);
+        S.par_begin();  // res_f.c1 INTT (+ CRT digits) and the res_f.c0 finish are independent
+        rc = add_i2(S, std::vector<Intt2Job>{ij}); if (rc) return rc;
         rc = add_xf(S, f1); if (rc) return rc;
         S.par_end();
         rc = add_xf(S, f3); if (rc) return rc;

@@ -425,6 +425,121 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
 }
 
 // ---------------------------------------------------------------------------
+// k_cl_intt2: level-1 key-switch front end on one 8-CTA cluster.  Inverts
+// BOTH primes of a c1 polynomial (the two INTTs of a tail key switch,
+// interleaved per thread for ILP), then splits each coefficient's CRT
+// integer into base-2^16 digits of X and of Q - X (k_compose mode 1) in the
+// epilogue, so the following digit NTTs only gather u16 digits (LD_DIGGAL)
+// instead of re-composing every coefficient 14 times.
+//   j[0] / j[1]: the two primes' loader jobs (k = 0, 1; LD_KSFIN or LD_RED,
+//   optional aux side store); E: optional coefficient-domain addend
+//   ([2][n], reduced with red64) applied before the split (T1 of the tail:
+//   acc[g].c1 = INTT(X) + E).
+// ---------------------------------------------------------------------------
+struct Intt2Job {
+    XJob j[2];
+    const u64* E;
+    uint16_t* dig;  // [2 * D_1][n]: digits of X, then of Q - X
+};
+constexpr int I2_MAX = 8;
+struct Intt2Jobs {
+    Intt2Job j[I2_MAX];
+};
+
+template <int LD>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
+    k_cl_intt2(const __grid_constant__ DevCtx C, const __grid_constant__ Intt2Jobs jobs) {
+    // threads [0,128) invert prime 0, [128,256) prime 1 (one INTT chain per
+    // thread, as in k_xf_cl); the CRT/digit split is then shared by all 256
+    extern __shared__ u64 dsm[];  // 2 tiles, 2 receive buffers, 2 twiddle slices
+    const int pr = threadIdx.x >> 7;
+    const int t = threadIdx.x & 127;
+    u64* tile = dsm + pr * CTILE;
+    u64* recvb = dsm + (2 + pr) * CTILE;
+    Tw* twsl = reinterpret_cast<Tw*>(dsm + 4 * CTILE) + pr * 1024;
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    const int c = (int)cl.block_rank();
+    cluster_arrive_relaxed();
+    const Intt2Job& JJ = jobs.j[blockIdx.x / CL];
+    const XJob& J = JJ.j[pr];
+    TRACE(0);
+    const PrimeC& P = C.pc[pr];
+    const Tw* tw = C.twi + (size_t)pr * NPOLY;
+    u64 x[CEPT];
+    load_n<LD, CEPT>(C, J, P, c * CTILE + t, 128, x);
+    tw_prefetch(twsl, tw, c, t);
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+    __syncthreads();
+    TRACE(1);
+    const TwL twl{twsl, c};
+    HC_NOUNROLL
+    for (int p = 0; p < 3; p++) {
+        const CPass I = cpass(2 - p, c, t);
+        c_load(x, tile, I);
+        if (p == 0) {
+            u64 o[CEPT];
+            HC_UNROLL
+            for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
+            c_st0(c, t, x, o, twl, P.q, P.q2);
+        }
+        r8_gs(x, twl, 1 + 3 * p, I.G, P.q, P.q2);
+        if (p < 2) {
+            c_store(x, tile, I);
+            __syncthreads();
+        }
+    }
+    TRACE(4);
+    cluster_wait();
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) cl.map_shared_rank(recvb, v)[c * 128 + t] = x[v];
+    cluster_arrive_release();
+    cluster_wait();
+    TRACE(3);
+    HC_UNROLL
+    for (int r = 0; r < CEPT; r++) x[r] = recvb[r * 128 + t];
+    c_phaseA_inv(x, tw, P);
+    // x[r] = coefficient r*1024 + 128c + t mod q_pr; park it (local index r*128 + t)
+    HC_UNROLL
+    for (int r = 0; r < CEPT; r++) tile[r * 128 + t] = x[r];
+    __syncthreads();
+    const LevelC& LV = C.lv[1];
+    const int D = LV.D;
+    const u64* E = JJ.E;
+    uint16_t* dig = JJ.dig;
+    u64* out0 = JJ.j[0].out;
+    u64* out1 = JJ.j[1].out;
+    const u64* tile0 = dsm;
+    const u64* tile1 = dsm + CTILE;
+    const int tt = threadIdx.x;
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) {
+        const int L = tt + 256 * i;
+        const int j = (L >> 7) * CTILE + 128 * c + (L & 127);
+        u64 a = tile0[L], b = tile1[L];
+        if (E) {
+            a = add_mod(a, red64(E[j], C.pc[0].q, C.pc[0].one_s), C.pc[0].q);
+            b = add_mod(b, red64(E[NPOLY + j], C.pc[1].q, C.pc[1].one_s), C.pc[1].q);
+        }
+        if (out0) {  // optional coefficient side store
+            out0[j] = a;
+            out1[j] = b;
+        }
+        u64 xr[2] = {a, b};
+        u64 X[NLIMB];
+        crt_compose<1>(LV, C.pc, xr, X);
+        HC_UNROLL
+        for (int d = 0; d < 8; d++)
+            if (d < D) dig[(size_t)d * NPOLY + j] = digit16(X, d);
+        neg_mod_Q<1>(LV, X);
+        HC_UNROLL
+        for (int d = 0; d < 8; d++)
+            if (d < D) dig[(size_t)(D + d) * NPOLY + j] = digit16(X, d);
+    }
+    TRACE(5);
+}
+
+// ---------------------------------------------------------------------------
 // k_compose: grid (n/256, njobs)
 // ---------------------------------------------------------------------------
 struct CJob {

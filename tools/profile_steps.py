@@ -25,7 +25,7 @@ for _ in range(3):
     dc.launch()
 dc.output()
 ms = np.zeros(4096, np.float32); kind = np.zeros(4096, np.int32); jobs = np.zeros(4096, np.int32)
-names = {0: "xform", 1: "compose", 2: "ksmac", 3: "diagx", 4: "sumcopies", 5: "memset"}
+names = {0: "xform", 1: "compose", 2: "ksmac", 3: "diagx", 4: "sumcopies", 5: "memset", 6: "intt2"}
 for r in range(reps):
     n = L.hc_comp_profile(h, None, 4096, _lib.ptr(ms), _lib.ptr(kind), _lib.ptr(jobs))
 print("plan", be.plan_info())
