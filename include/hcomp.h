@@ -123,6 +123,10 @@ int hc_bench_xform(hc_ctx* h, int njobs, int dir, int iters, double* us_per_laun
 /* Transform launches with <= max_jobs jobs use the 8-CTA cluster kernel
  * (latency path); larger launches use one CTA per transform.  Default 16. */
 int hc_set_cluster_threshold(int max_jobs);
+/* Tuning: chunks of up to `max_blocks` blocks run the baby-step segment as
+ * parallel per-block lanes (latency regime); larger chunks use one wide launch
+ * per segment (throughput regime). Applies to plans built afterwards. */
+int hc_set_lane_blocks(int max_blocks);
 
 /* Debug builds compiled with -DHC_TRACE: reset the launch numbering and read
  * per-CTA %globaltimer stamps [128 launches][512 CTAs][8 points]. */

@@ -59,6 +59,7 @@ struct DevKey {
 
 // transform launches with at most this many jobs use the cluster kernel
 static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters (split by CL_MAX)
+static int g_lane_max_blocks = 4;  // chunks up to this many blocks run the baby segment as lanes
 static const int CL_SPREAD_SMEM = 120 * 1024;
 
 enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET, ST_I2 };
@@ -396,10 +397,10 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->hctx, (const CJob*)st.djobs);
                 break;
             case ST_MA:
-                k_ksmac<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
+                k_ksmac<<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
                 break;
             case ST_DX:
-                k_diagx<<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);
+                k_diagx<<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);
                 break;
             case ST_SUMC:
                 k_sum_copies<<<592, 256, 0, s>>>(h->hctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride);
@@ -582,7 +583,10 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
     P->F = (int)P->fold.size();
     P->D1 = h->digits[1];
     P->D2 = h->digits[2];
-    P->CB = chunk_blocks > 0 ? chunk_blocks : (int)std::min<long long>(P->B, P->baby >= 8 ? 16 : 32);
+    P->CB = chunk_blocks > 0 ? chunk_blocks : (int)std::min<long long>(P->B, 64);
+    // k_diagx sums CB*baby Montgomery products (each < q^2) before one REDC,
+    // which needs the sum < q * 2^64, i.e. at most 1024 terms for 54-bit q
+    P->CB = std::max(1, std::min(P->CB, 1024 / std::max(1, P->baby)));
     P->ncopy = (int)std::max<long long>(1, (P->B * P->baby + 999) / 1000);
     // live diagonals: only the last block can have all-zero diagonals
     P->live.assign((size_t)P->B * P->s_pad, 1);
@@ -904,6 +908,19 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         rc = add_ma(S, s4, 3); if (rc) return rc;
         rc = add_xf(S, s5); if (rc) return rc;
         rc = add_co(S, s6); if (rc) return rc;
+        if (cb > g_lane_max_blocks) {
+            // throughput regime: one wide launch per segment over the chunk
+            std::vector<XJob> w7, w9;
+            std::vector<MJob> w8;
+            for (int tl = 0; tl < cb; tl++) {
+                w7.insert(w7.end(), s7[tl].begin(), s7[tl].end());
+                w8.insert(w8.end(), s8[tl].begin(), s8[tl].end());
+                w9.insert(w9.end(), s9[tl].begin(), s9[tl].end());
+            }
+            rc = add_xf(S, w7); if (rc) return rc;
+            rc = add_ma(S, w8, 3); if (rc) return rc;
+            rc = add_xf(S, w9); if (rc) return rc;
+        } else {
         const int nl = std::min(4, cb);
         if (nl > 1) S.par_begin();
         for (int lane = 0; lane < nl; lane++) {
@@ -916,6 +933,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         }
         S.cur_lane = -1;
         if (nl > 1) S.par_end();
+        }
         // S10: per (g, poly): X += sum src * diag * q^-1 (kept primes) and
         //      E += sum of the chunk's correction slots
         {
@@ -1523,6 +1541,11 @@ extern "C" int hc_bf_peak(hc_ctx* h, double* bfly_per_s) {
 // EP_STORE) per launch, `iters` back-to-back launches; returns us/launch.
 extern "C" int hc_set_cluster_threshold(int max_jobs) {
     CL_MAX_JOBS = max_jobs;
+    return HC_OK;
+}
+
+extern "C" int hc_set_lane_blocks(int max_blocks) {
+    g_lane_max_blocks = max_blocks;
     return HC_OK;
 }
 

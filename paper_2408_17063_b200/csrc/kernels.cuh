@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256) k_compose(const __grid_constant__ DevCtx 
 }
 
 // ---------------------------------------------------------------------------
-// k_ksmac: grid (n/256, P, njobs)
+// k_ksmac: grid (n/512, P, njobs), two coefficients per thread
 //   out0 = add0 + sum_t ( c0src_t[perm_t[j]] + sum_j dntt_t[j] * b_t[j] )
 //   out1 = add1 + sum_t ( sum_j dntt_t[j] * a_t[j] )
 // dntt: [D][P][n]; key: [D_L][2][L+1][n] (Montgomery form).
@@ -622,37 +622,49 @@ struct MJob {
     u64* out1;
 };
 
+// two adjacent coefficients per thread (128-bit loads)
 __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
     const int k = blockIdx.y;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     const LevelC& LV = C.lv[J.level];
     const int P = LV.P, D = LV.D, L1 = C.L + 1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
-    u64 o0 = J.add0 ? J.add0[kn] : 0;
-    u64 o1 = J.add1 ? J.add1[kn] : 0;
+    ulonglong2 o0 = J.add0 ? *reinterpret_cast<const ulonglong2*>(J.add0 + kn) : make_ulonglong2(0, 0);
+    ulonglong2 o1 = J.add1 ? *reinterpret_cast<const ulonglong2*>(J.add1 + kn) : make_ulonglong2(0, 0);
     const int nt = J.nterm;
     for (int t = 0; t < nt; t++) {
         const MTerm T = J.t[t];
-        u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+        u64 h0x = 0, l0x = 0, h1x = 0, l1x = 0, h0y = 0, l0y = 0, h1y = 0, l1y = 0;
+        const u64* vp = T.dntt + (size_t)k * NPOLY + j;
+        const u64* bp = T.key + (size_t)k * NPOLY + j;
+        const size_t vstep = (size_t)P * NPOLY, kstep = (size_t)2 * L1 * NPOLY, astep = (size_t)L1 * NPOLY;
         for (int d = 0; d < D; d++) {
-            const u64 v = T.dntt[((size_t)d * P + k) * NPOLY + j];
-            const u64 kb = T.key[((size_t)(d * 2 + 0) * L1 + k) * NPOLY + j];
-            const u64 ka = T.key[((size_t)(d * 2 + 1) * L1 + k) * NPOLY + j];
-            mac128(h0, l0, v, kb);
-            mac128(h1, l1, v, ka);
+            const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(vp + d * vstep));
+            const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep));
+            const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep + astep));
+            mac128(h0x, l0x, v.x, kb.x);
+            mac128(h0y, l0y, v.y, kb.y);
+            mac128(h1x, l1x, v.x, ka.x);
+            mac128(h1y, l1y, v.y, ka.y);
         }
-        o0 = add_mod(o0, redc(h0, l0, pc.q, pc.qneg), pc.q);
-        o1 = add_mod(o1, redc(h1, l1, pc.q, pc.qneg), pc.q);
-        if (T.c0src) o0 = add_mod(o0, T.c0src[(size_t)k * NPOLY + T.perm[j]], pc.q);
+        o0.x = add_mod(o0.x, redc(h0x, l0x, pc.q, pc.qneg), pc.q);
+        o0.y = add_mod(o0.y, redc(h0y, l0y, pc.q, pc.qneg), pc.q);
+        o1.x = add_mod(o1.x, redc(h1x, l1x, pc.q, pc.qneg), pc.q);
+        o1.y = add_mod(o1.y, redc(h1y, l1y, pc.q, pc.qneg), pc.q);
+        if (T.c0src) {
+            const u64* c0 = T.c0src + (size_t)k * NPOLY;
+            o0.x = add_mod(o0.x, c0[T.perm[j]], pc.q);
+            o0.y = add_mod(o0.y, c0[T.perm[j + 1]], pc.q);
+        }
     }
-    J.out0[kn] = o0;
-    J.out1[kn] = o1;
+    *reinterpret_cast<ulonglong2*>(J.out0 + kn) = o0;
+    *reinterpret_cast<ulonglong2*>(J.out1 + kn) = o1;
 }
 
 // ---------------------------------------------------------------------------
-// k_diagx: grid (n/256, nprime, njobs).  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
+// k_diagx: grid (n/512, nprime, njobs), two coefficients per thread.  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
 // (dg Montgomery with q^-1 folded in) -- the kept-prime half of each
 // plaintext product; the dropped-prime half goes through k_xform/EP_RESCALE*.
 // ---------------------------------------------------------------------------
@@ -668,16 +680,43 @@ struct DXJob {
 __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
     const DXJob& J = jobs[blockIdx.z];
     const int k = blockIdx.y;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
-    u64 h = 0, l = 0, es = 0;
-    for (int t = 0; t < J.nterm; t++) {
-        mac128(h, l, J.src[t][kn], J.dg[t][kn]);
-        if (J.es) es += J.es[t][kn];  // < 2^54 each, nterm <= 1023
+    u64 hx = 0, lx = 0, hy = 0, ly = 0, ex = 0, ey = 0;
+    const int nt = J.nterm;
+    const u64* const* src = J.src;
+    const u64* const* dg = J.dg;
+    const u64* const* es = J.es;
+    // batches of 8 terms: pointers, then all data loads, then the MACs
+    for (int t0 = 0; t0 < nt; t0 += 8) {
+        ulonglong2 a[8], b[8], e[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (t0 + i < nt) {
+                a[i] = __ldcs(reinterpret_cast<const ulonglong2*>(src[t0 + i] + kn));
+                b[i] = __ldg(reinterpret_cast<const ulonglong2*>(dg[t0 + i] + kn));
+                e[i] = es ? __ldcs(reinterpret_cast<const ulonglong2*>(es[t0 + i] + kn)) : make_ulonglong2(0, 0);
+            }
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (t0 + i < nt) {
+                mac128(hx, lx, a[i].x, b[i].x);
+                mac128(hy, ly, a[i].y, b[i].y);
+                ex += e[i].x;  // < 2^54 each, nterm <= 1024
+                ey += e[i].y;
+            }
     }
-    J.X[kn] = add_mod(J.X[kn], redc(h, l, pc.q, pc.qneg), pc.q);
-    if (J.es) J.E[kn] = add_mod(J.E[kn], red64(es, pc.q, pc.one_s), pc.q);
+    ulonglong2 X = *reinterpret_cast<const ulonglong2*>(J.X + kn);
+    X.x = add_mod(X.x, redc(hx, lx, pc.q, pc.qneg), pc.q);
+    X.y = add_mod(X.y, redc(hy, ly, pc.q, pc.qneg), pc.q);
+    *reinterpret_cast<ulonglong2*>(J.X + kn) = X;
+    if (es) {
+        ulonglong2 E = *reinterpret_cast<const ulonglong2*>(J.E + kn);
+        E.x = add_mod(E.x, red64(ex, pc.q, pc.one_s), pc.q);
+        E.y = add_mod(E.y, red64(ey, pc.q, pc.one_s), pc.q);
+        *reinterpret_cast<ulonglong2*>(J.E + kn) = E;
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -41,3 +41,11 @@ for _ in range(50):
     dc.launch()
 dc.output()
 print("graph ms/comp", (time.perf_counter() - t0) / 50 * 1e3)
+agg = {}
+for i in range(n):
+    k = (names[int(kind[i])], int(jobs[i]))
+    c, t = agg.get(k, (0, 0.0))
+    agg[k] = (c + 1, t + float(ms[i]))
+print("by (kind, jobs): count, total us, us/job")
+for (nm, j), (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+    print(f"  {nm:9s} jobs={j:5d} x{c:4d} {t*1e3:9.1f} us  {t*1e3/max(1,c*j):7.2f} us/job")
