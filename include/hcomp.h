@@ -62,6 +62,12 @@ int hc_clear_keys(hc_ctx* h);
  * chunk_blocks: blocks processed per pass (0 = automatic).
  * Fails with HC_ERR_KEY if a needed rotation key is not loaded. */
 int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks);
+/* Replaces _plan(params, "packed", masked) for comp_masked (compress.py:
+ * 154-157, 521-530): as hc_plan, but the bottom lane evaluates
+ * D = C diag(DB) (VandermondeTable with db_values, compress.py:107-135).
+ * db_mod_p = uint64[N], the cleartext database reduced mod p (int(v) % p).
+ * Run it with hc_comp(h, cv, cv, ...): the index vector is both inputs. */
+int hc_plan_masked(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db_mod_p);
 /* schedule facts: [B, C, baby, giant, F, s_pad, live_diagonals, kernel_launches] */
 int hc_plan_info(const hc_ctx* h, int64_t* info8);
 

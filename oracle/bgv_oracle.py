@@ -607,9 +607,10 @@ def plan_rotation_amounts(s: int, n: int) -> tuple[list[int], bool]:
     return sorted(amounts), True
 
 
-def vandermonde_block(N: int, s: int, p: int, m: int, k: int) -> np.ndarray:
-    """compress.py:120-141 (no database scaling): rows j=0..s-1 hold
-    col^(j+1) mod p for the block's columns k*m+1..(k+1)*m, zero past N."""
+def vandermonde_block(N: int, s: int, p: int, m: int, k: int, db=None) -> np.ndarray:
+    """compress.py:120-141: rows j=0..s-1 hold col^(j+1) mod p for the
+    block's columns k*m+1..(k+1)*m, zero past N; with a cleartext database
+    (compress.py:107-116,131-135) each column is scaled by db[col-1] mod p."""
     cols = np.arange(k * m + 1, (k + 1) * m + 1, dtype=np.int64)
     valid = cols <= N
     base = np.where(valid, cols % p, 0).astype(object if p >= (1 << 31) else np.int64)
@@ -618,6 +619,11 @@ def vandermonde_block(N: int, s: int, p: int, m: int, k: int) -> np.ndarray:
     for j in range(s):
         table[j] = row
         row = row * base % p
+    if db is not None:
+        scale = np.zeros(m, dtype=table.dtype)
+        nv = int(valid.sum())
+        scale[:nv] = [int(v) % p for v in db[k * m : k * m + nv]]
+        table = table * scale[None, :] % p
     return table
 
 
@@ -641,8 +647,9 @@ class OPlan:
     output_mask: np.ndarray
 
 
-def build_plan(N: int, s: int, n: int, p: int) -> OPlan:
-    """compress.py:198-255, mode "packed", no cleartext database."""
+def build_plan(N: int, s: int, n: int, p: int, db=None) -> OPlan:
+    """compress.py:198-255, mode "packed"; `db` = the cleartext database of
+    precompute_masked_matrix (bottom lane evaluates D = C diag(DB))."""
     m = n // 2
     s_pad = 1 << (s - 1).bit_length()
     baby, giant = bsgs_shape(s)
@@ -650,14 +657,16 @@ def build_plan(N: int, s: int, n: int, p: int) -> OPlan:
     diagonals = []
     for t in range(B):
         tab = vandermonde_block(N, s, p, m, t)
+        tab_d = tab if db is None else vandermonde_block(N, s, p, m, t, db)
         per = []
         for g in range(giant):
             for b in range(baby):
                 r0 = diag_vector(tab, g, b, baby, s_pad, m)
-                if not np.any(r0):
+                r1 = r0 if db is None else diag_vector(tab_d, g, b, baby, s_pad, m)
+                if not np.any(r0) and not np.any(r1):
                     per.append(None)
                 else:
-                    per.append(np.stack([r0, r0]) % p)
+                    per.append(np.stack([r0, r1]) % p)
         diagonals.append(per)
     fold = []
     step = s_pad
@@ -730,10 +739,12 @@ def bsgs_matvec(plan: OPlan, inputs, be: OracleBgv, keys: OKeys) -> OCt:
     return be.mul_plain(res, plan.output_mask)
 
 
-def comp(cd, N: int, s: int, be: OracleBgv, keys: OKeys, index_hint) -> OCt:
-    """compress.py:488-514 with an index hint, packed."""
-    u = pack_pair(list(index_hint), cd, N, be, keys)
-    plan = build_plan(N, s, be.n, be.p)
+def comp(cd, N: int, s: int, be: OracleBgv, keys: OKeys, index_hint=None, masked_db=None) -> OCt:
+    """compress.py:488-514, packed: with an index hint, or (comp_masked,
+    compress.py:521-530) with masked_db, where cd is the index vector."""
+    cv = list(cd) if masked_db is not None else list(index_hint)
+    u = pack_pair(cv, cd, N, be, keys)
+    plan = build_plan(N, s, be.n, be.p, masked_db)
     return bsgs_matvec(plan, u, be, keys)
 
 
@@ -751,6 +762,18 @@ def plant_sparse(rng: random.Random, N: int, s: int, p: int) -> list[int]:
     for i in support:
         d[i - 1] = rng.randrange(1, p)
     return d
+
+
+def masked_payload(N: int, s: int, p: int, seed: int):
+    """comp_masked fixture recipe (oracle/make_golden.py): the encrypted index
+    vector's support and a cleartext database value on every position."""
+    rng = random.Random(seed)
+    support = sorted(rng.sample(range(1, N + 1), s))
+    db = [rng.randrange(1, p) for _ in range(N)]
+    dense = [0] * N
+    for i in support:
+        dense[i - 1] = db[i - 1]
+    return support, db, dense
 
 
 def expected_slots(dense, s: int, p: int) -> tuple[list[int], list[int]]:

@@ -46,7 +46,21 @@ CASES = {
     "c2_N16384_s16": (8192, 65537, 16384, 16, 0, False),
     "odd_N10000_s5": (8192, 65537, 10000, 5, 3, True),
     "c2_N16384_s32": (8192, 65537, 16384, 32, 0, True),
+    # comp_masked (compress.py:521-530): cleartext DB on every position,
+    # encrypted 0/1 index vector on the support (masked_payload below)
+    "masked_small_n64_N200_s5": (64, 257, 200, 5, 13, True),
+    "masked_c1_N8192_s8": (8192, 65537, 8192, 8, 4, False),
+    "masked_c2_N16384_s16": (8192, 65537, 16384, 16, 5, False),
 }
+
+
+def masked_payload(N, s, p, seed):
+    """support = sorted(rng.sample(range(1, N+1), s)); db[i] = rng.randrange(1, p)
+    for every position i (the server's cleartext database)."""
+    rng = random.Random(seed)
+    support = sorted(rng.sample(range(1, N + 1), s))
+    db = [rng.randrange(1, p) for _ in range(N)]
+    return support, db
 
 
 def residues_of(vals, primes_rns):
@@ -92,9 +106,11 @@ def run_case(name):
     from hcpdq.compress import (
         CompressionParams,
         comp,
+        comp_masked,
         decomp,
         encrypt_vector,
         plan_rotation_amounts,
+        precompute_masked_matrix,
     )
     from hcpdq.heiface import HeParams
 
@@ -104,20 +120,36 @@ def run_case(name):
     amounts, col = plan_rotation_amounts(s, n)
     t0 = time.time()
     keys = be.keygen(amounts, col_swap=col)
-    rng = random.Random(seed)
-    support = sorted(rng.sample(range(1, N + 1), s))
-    dense = [0] * N
-    for i in support:
-        dense[i - 1] = rng.randrange(1, p)
-    cts = encrypt_vector(dense, params, be, keys)
-    hint = encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    masked = name.startswith("masked_")
+    if masked:
+        support, db = masked_payload(N, s, p, seed)
+        dense = [0] * N
+        for i in support:
+            dense[i - 1] = db[i - 1]
+        table = precompute_masked_matrix(db, params)
+        hint = encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+        cts = hint
+
+        def run():
+            return comp_masked(hint, table, params, be, keys)
+    else:
+        rng = random.Random(seed)
+        support = sorted(rng.sample(range(1, N + 1), s))
+        dense = [0] * N
+        for i in support:
+            dense[i - 1] = rng.randrange(1, p)
+        cts = encrypt_vector(dense, params, be, keys)
+        hint = encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+
+        def run():
+            return comp(cts, params, be, keys, index_hint=hint)
     t1 = time.time()
     before = be.counters.snapshot()
     if guard_off:
         with refimport.noise_guard_disabled():
-            ans = comp(cts, params, be, keys, index_hint=hint)
+            ans = run()
     else:
-        ans = comp(cts, params, be, keys, index_hint=hint)
+        ans = run()
     t2 = time.time()
     delta = be.counters.delta(before)
     blob = ans.serialize(be)
@@ -136,6 +168,7 @@ def run_case(name):
         "s": s,
         "seed": seed,
         "noise_guard_disabled": guard_off,
+        "masked": masked,
         "chain_primes_desc": list(be.chain.primes),
         "key_id": keys.key_id.hex(),
         "support": support,

@@ -15,7 +15,16 @@ from .backend import (
     RnsPayload,
     SlotMatrix,
 )
-from .compress import CompressedAnswer, DeviceComp, comp, encode_vector, encrypt_vector
+from .compress import (
+    CompressedAnswer,
+    DeviceComp,
+    MaskedMatrix,
+    comp,
+    comp_masked,
+    encode_vector,
+    encrypt_vector,
+    precompute_masked_matrix,
+)
 from .params import (
     BackendMismatch,
     CompressionParams,

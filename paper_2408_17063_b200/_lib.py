@@ -47,6 +47,7 @@ _SIGS = [
     ("hc_load_ksk", _I, [_P, _U32, _P]),
     ("hc_clear_keys", _I, [_P]),
     ("hc_plan", _I, [_P, _I64, _I, _I]),
+    ("hc_plan_masked", _I, [_P, ctypes.c_int64, _I, _I, _P]),
     ("hc_plan_info", _I, [_P, _P]),
     ("hc_comp", _I, [_P, _P, _P, _I, _P]),
     ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),

@@ -17,6 +17,7 @@ reference's composite-modulus integer lists on demand.
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import math
 import random
 import struct
@@ -638,11 +639,17 @@ class B200BgvBackend:
 
     # -- the fused Comp (compress.py:488-514) ------------------------------------------
 
-    def plan(self, N: int, s: int, keys: KeySet, chunk_blocks: int = 0) -> None:
+    def plan(self, N: int, s: int, keys: KeySet, chunk_blocks: int = 0, db: np.ndarray | None = None) -> None:
+        """Device plan for (N, s); `db` (uint64[N], mod p) selects comp_masked's D = C diag(DB)."""
         self._load_keys(keys)
-        if self._planned != (N, s, chunk_blocks):
-            _lib.check(_lib.lib().hc_plan(self._ctx(), N, s, chunk_blocks))
-            self._planned = (N, s, chunk_blocks)
+        tag = (N, s, chunk_blocks, None if db is None else hashlib.sha256(db.tobytes()).digest())
+        if self._planned != tag:
+            if db is None:
+                _lib.check(_lib.lib().hc_plan(self._ctx(), N, s, chunk_blocks))
+            else:
+                db = np.ascontiguousarray(db, dtype=np.uint64)
+                _lib.check(_lib.lib().hc_plan_masked(self._ctx(), N, s, chunk_blocks, _lib.ptr(db)))
+            self._planned = tag
 
     def plan_info(self) -> dict:
         info = np.zeros(8, dtype=np.int64)

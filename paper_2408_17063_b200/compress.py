@@ -162,6 +162,24 @@ def comp_noise(be: B200BgvBackend, params: CompressionParams, cv_bits, cd_bits, 
     return out, sim
 
 
+class MaskedMatrix:
+    """The cleartext-database matrix D = C diag(DB) of comp_masked
+    (VandermondeTable(params, db_values), compress.py:107-135): held as the
+    database reduced mod p; the device generates the scaled diagonals."""
+
+    def __init__(self, params: CompressionParams, db_values: Sequence[int]):
+        if len(db_values) != params.N:
+            raise ValueError("database length must equal N")
+        p = params.he.p
+        self.params = params
+        self.db_mod_p = np.ascontiguousarray([int(v) % p for v in db_values], dtype=np.uint64)
+
+
+def precompute_masked_matrix(db_values: Sequence[int], params: CompressionParams) -> MaskedMatrix:
+    """compress.py:154-157."""
+    return MaskedMatrix(params, db_values)
+
+
 def _stack_level3(cts: Sequence[Ciphertext], L: int) -> np.ndarray:
     return np.ascontiguousarray(np.stack([c.payload.res for c in cts]), dtype=np.uint64)
 
@@ -186,27 +204,34 @@ def comp(
     pack: bool = True,
     masked=None,
 ) -> CompressedAnswer:
-    """Compress ciphertexts of an s-sparse vector d into (w, e) (compress.py:488-518)."""
+    """Compress ciphertexts of an s-sparse vector d into (w, e) (compress.py:488-518).
+
+    With `masked` (comp_masked), cd is the index vector and the bottom lane
+    evaluates D = C diag(DB) instead of C (compress.py:507-510)."""
     if not isinstance(backend, B200BgvBackend):
         raise BackendMismatch("paper_2408_17063_b200.comp needs a B200BgvBackend")
-    if masked is not None or index_hint is None or not pack:
+    if (masked is None and index_hint is None) or not pack:
         raise NotImplementedError(
-            "the B200 path implements comp with an index hint in the packed layout "
-            "(the reference's hint path); comp_masked / power_fermat / pack=False are not built"
+            "the B200 path implements comp with an index hint or a masked matrix in the packed "
+            "layout; power_fermat / pack=False are not built"
         )
+    if masked is not None and not isinstance(masked, MaskedMatrix):
+        raise TypeError("masked must come from precompute_masked_matrix")
     if backend.params != params.he:
         raise BackendMismatch("compression parameters do not match the backend")
-    cv = list(index_hint)
     cd = list(cd)
+    cv = list(cd) if masked is not None else list(index_hint)
     _check_inputs(cd, cv, params, backend, keys)
     live = live_diagonals(params)
     bits, sim = comp_noise(
         backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live
     )
-    backend.plan(params.N, params.s, keys)
+    if masked is not None and masked.params != params:
+        raise ValueError("masked matrix was built for different compression parameters")
+    backend.plan(params.N, params.s, keys, db=None if masked is None else masked.db_mod_p)
     L = backend.params.max_level
     cd_arr = _stack_level3(cd, L)
-    cv_arr = _stack_level3(cv, L)
+    cv_arr = cd_arr if masked is not None else _stack_level3(cv, L)
     out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
     _lib.check(
         _lib.lib().hc_comp(backend._ctx(), _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd), _lib.ptr(out))
@@ -216,6 +241,13 @@ def comp(
     backend.counters.adds += sim.adds
     ct = Ciphertext(backend.backend_id, keys.key_id, 0, RnsPayload(out, bits, (backend.q[0],)))
     return CompressedAnswer((ct,), params.s, True)
+
+
+def comp_masked(
+    cv: Sequence[Ciphertext], masked: MaskedMatrix, params: CompressionParams, backend, keys: KeySet
+) -> CompressedAnswer:
+    """compress.py:521-530: one [C; D].v pass on the index vector."""
+    return comp(cv, params, backend, keys, masked=masked)
 
 
 class DeviceComp:

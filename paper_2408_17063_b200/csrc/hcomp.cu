@@ -496,6 +496,7 @@ struct Plan {
     int s = 0, s_pad = 0, baby = 0, giant = 0, m = 0, F = 0, CB = 0, ncopy = 1;
     long long B = 0, C = 0;
     int D1 = 0, D2 = 0;
+    bool masked = false;  // comp_masked plan (row-1 diagonals scaled by the DB)
     std::vector<int> fold;
     std::vector<uint8_t> live;      // [B][s_pad]
     std::vector<uint8_t> acc_live;  // [giant]
@@ -563,7 +564,7 @@ static const DevKey* need_key(hc_ctx* h, uint32_t t) {
     return it == h->keys.end() ? nullptr : &it->second;
 }
 
-extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
+static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db) {
     if (!h) return fail(HC_ERR_ARG, "null context");
     if (h->L != 3) return fail(HC_ERR_ARG, "Comp needs max_level = 3 (SURVEY F3)");
     const int n = NPOLY, m = n / 2;
@@ -693,7 +694,20 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
                     d.out = P->diag + ((size_t)t * P->s_pad + i) * 3 * NB;
                     pj.push_back(d);
                 }
-        PlanShape S{N, s, P->s_pad, P->baby, m};
+        PlanShape S{N, s, P->s_pad, P->baby, m, nullptr};
+        if (db) {
+            std::vector<uint32_t> dbv((size_t)N);
+            for (long long i = 0; i < N; i++) {
+                if (db[i] >= h->p) return fail(HC_ERR_ARG, "database values must be reduced mod p");
+                dbv[i] = (uint32_t)db[i];
+            }
+            uint32_t* ddb = nullptr;
+            rc = palloc(*P, &ddb, (size_t)N);
+            if (rc) return rc;
+            CU(cudaMemcpy(ddb, dbv.data(), (size_t)N * 4, cudaMemcpyHostToDevice));
+            S.db = ddb;
+            P->masked = true;
+        }
         PJob* dj = nullptr;
         const size_t maxb = 65535;
         CU(cudaMalloc(&dj, pj.size() * sizeof(PJob)));
@@ -709,6 +723,13 @@ extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) {
     }
     h->plan = std::move(P);
     return HC_OK;
+}
+
+extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) { return plan_impl(h, N, s, chunk_blocks, nullptr); }
+
+extern "C" int hc_plan_masked(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db_mod_p) {
+    if (!db_mod_p) return fail(HC_ERR_ARG, "null database");
+    return plan_impl(h, N, s, chunk_blocks, db_mod_p);
 }
 
 extern "C" int hc_plan_info(const hc_ctx* h, int64_t* info) {

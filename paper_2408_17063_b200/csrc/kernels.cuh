@@ -734,6 +734,7 @@ struct PJob {
 struct PlanShape {
     long long N;
     int s, s_pad, baby, m;
+    const uint32_t* db;  // comp_masked: cleartext DB mod p scaling row 1 (D = C diag(DB)), or null
 };
 
 HD u64 powmod_small(u64 b, int e, u64 p, double pinv) {
@@ -754,7 +755,10 @@ HD u64 plain_slot_value(const PJob& J, const PlanShape& S, int r, int c, u64 p, 
             int col = (c + J.b) % S.m;
             long long idx = (long long)J.t * S.m + col + 1;
             if (row >= S.s || idx > S.N) return 0;
-            return powmod_small((u64)(idx % (long long)p), row + 1, p, pinv);
+            const u64 v = powmod_small((u64)(idx % (long long)p), row + 1, p, pinv);
+            // precompute_masked_matrix (compress.py:154-157,131-135): the bottom
+            // lane's table is column-scaled by the cleartext database
+            return (r == 1 && S.db) ? mod_small(v * S.db[idx - 1], p, pinv) : v;
         }
         case PT_TOP: return r == 0 ? 1 : 0;
         case PT_BOT: return r == 1 ? 1 : 0;

@@ -130,7 +130,8 @@ def test_decrypt_roundtrip(c1):
     assert [int(x) for x in m.rows[1]] == dense[4096:8192]
 
 
-GOLDEN_8K = [g for g in golden_names() if not g.startswith("small_")]
+GOLDEN_8K = [g for g in golden_names() if not g.startswith(("small_", "masked_"))]
+MASKED_8K = [g for g in golden_names("masked_") if not g.startswith("masked_small_")]
 
 
 @pytest.mark.parametrize("name", GOLDEN_8K)
@@ -153,6 +154,37 @@ def test_comp_matches_reference_golden(pkg, oracle, name):
     assert delta.as_dict() == g["counters"]
     w, e = ans.payload_slots(be, keys)
     assert (w, e) == (g["w"], g["e"])
+
+
+@pytest.mark.parametrize("name", MASKED_8K)
+def test_comp_masked_matches_reference_golden(pkg, oracle, name):
+    """comp_masked (compress.py:521-530): encrypted 0/1 index vector against
+    the cleartext-DB matrix D = C diag(DB); byte-identical to the reference."""
+    P, O = pkg, oracle
+    g = load_golden(name)
+    n, p, N, s, seed = g["n"], g["p"], g["N"], g["s"], g["seed"]
+    he = P.HeParams(n, p, 3)
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed, noise_guard=not g["noise_guard_disabled"])
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    assert keys.key_id.hex() == g["key_id"]
+    support, db, dense = O.masked_payload(N, s, p, seed)
+    assert support == g["support"]
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    table = P.precompute_masked_matrix(db, params)
+    before = be.counters.snapshot()
+    ans = P.comp_masked(hint, table, params, be, keys)
+    delta = be.counters.delta(before)
+    blob = ans.serialize(be)
+    assert O.sha256(blob) == g["answer_sha256"], "comp_masked output differs from the reference"
+    assert ans.cts[0].payload.noise_bits == g["noise_bits"]
+    assert delta.as_dict() == g["counters"]
+    w, e = ans.payload_slots(be, keys)
+    assert (w, e) == (g["w"], g["e"]) == O.expected_slots(dense, s, p)
+    # the same backend then runs the plain hint path again (plan switches back)
+    cts = P.encrypt_vector(dense, params, be, keys)
+    ans2 = P.comp(cts, params, be, keys, index_hint=hint)
+    assert ans2.payload_slots(be, keys) == (w, e)
 
 
 def test_comp_p786433_N2_17_vs_oracle(pkg, oracle):
