@@ -39,7 +39,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_DEFAULT, S_DEFAULT, P_DEFAULT, RING = 1 << 14, 16, 65537, 8192
-METRIC = "Comp encrypted entries/sec (N=2^14, s=16)"
+
+
+def metric_name(N: int, s: int) -> str:
+    n = f"2^{N.bit_length() - 1}" if N & (N - 1) == 0 else str(N)
+    return f"Comp encrypted entries/sec (N={n}, s={s})"
 
 
 def parse():
@@ -53,6 +57,8 @@ def parse():
     ap.add_argument("--p", type=int, default=0, help="plaintext prime (default: 65537, or per SURVEY F4 for N >= p)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="auto", choices=["auto", "on", "off"],
+                    help="block-sharded Comp over the ranks (SURVEY 8(e)); auto = on for N >= 2^20 with >1 rank")
     return ap.parse_args()
 
 
@@ -77,7 +83,8 @@ def workload(args, p):
         "max_level": 3,
         "seeded_synthetic": "bench.run_point recipe: random.Random(seed) s-sparse payload, encrypted d + index hint",
         "l2": "flushed between timed steps (256 MiB write, untimed)",
-        "parallelism": "replicas" if args.gpus > 1 else "single",
+        "parallelism": (f"blocks sharded over {args.gpus} GPU(s) + NCCL uint64 reduce (SURVEY 8(e))" if args.shard_on
+                        else ("replicas (independent queries)" if args.gpus > 1 else "single")),
     }
 
 
@@ -168,7 +175,7 @@ def run_reference(args, p, rank):
     total = sum(times)
     value = args.N * args.steps / total
     line = {
-        "metric": METRIC,
+        "metric": metric_name(args.N, args.s),
         "impl": "reference",
         "value": value,
         "unit": "entries/s",
@@ -177,7 +184,7 @@ def run_reference(args, p, rank):
         "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.shard_on else "weak",
         "vs_baseline": None,
         "dtype": "u64 (RNS, 54-bit primes)",
         "data": "synthetic (seeded; bench.run_point recipe)",
@@ -228,6 +235,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
+    args.shard_on = args.shard == "on" or (args.shard == "auto" and world > 1 and args.N >= (1 << 20))
+    args.gpus = world
     if args.impl == "reference":
         line = run_reference(args, p, rank)
         if line is not None:
@@ -249,38 +258,81 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    shard = args.shard_on
     he = P.HeParams(RING, p, 3)
     params = P.CompressionParams(args.N, args.s, he)
-    be = P.B200BgvBackend(he, seed=rank, device=local, noise_guard=False)
+    seed = 0 if shard else rank  # sharded: one query split over the ranks; replicas: one query per rank
+    be = P.B200BgvBackend(he, seed=seed, device=local, noise_guard=False)
     keys = be.keygen(*P.plan_rotation_amounts(args.s, RING))
-    dense = plant(args.N, args.s, p, rank)
+    dense = plant(args.N, args.s, p, seed)
     cts = P.encrypt_vector(dense, params, be, keys)
     hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
     dc = P.DeviceComp(be, params, keys)
     cd = np.ascontiguousarray(np.stack([c.payload.res for c in cts]))
     cv = np.ascontiguousarray(np.stack([c.payload.res for c in hint]))
-    dc.set_inputs(cd, cv)
 
     stream = torch.cuda.Stream()
     sh = stream.cuda_stream
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     L = _lib.lib()
     h = be._ctx()
+    out_h = torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()
+
+    if shard:
+        from paper_2408_17063_b200.dist import shard_blocks
+
+        b0, b1 = shard_blocks(params.num_blocks, world, rank)
+        c0, c1 = b0 // 2, (b1 + 1) // 2
+        cd_h = torch.from_numpy(np.ascontiguousarray(cd[c0:c1])).pin_memory()
+        cv_h = torch.from_numpy(np.ascontiguousarray(cv[c0:c1])).pin_memory()
+        part = torch.zeros(L.hc_partial_words(h), dtype=torch.int64, device="cuda")
+        _lib.check(L.hc_comp_set_inputs_range(h, cd_h.data_ptr(), cv_h.data_ptr(), c0, c1, sh))
+        torch.cuda.synchronize()
+
+        def step(e2e: bool):
+            if e2e:
+                _lib.check(L.hc_comp_set_inputs_range(h, cd_h.data_ptr(), cv_h.data_ptr(), c0, c1, sh))
+            _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(part.data_ptr()), sh))
+            if dist:
+                dist.reduce(part, dst=0, op=dist.ReduceOp.SUM)  # joins the current stream
+            if rank == 0:
+                _lib.check(L.hc_comp_finish(h, ctypes.c_void_p(part.data_ptr()), sh))
+                if e2e:
+                    _lib.check(L.hc_comp_get_output_async(h, out_h.data_ptr(), sh))
+
+        h2d_bytes = int(cd_h.numel() * 8 + cv_h.numel() * 8)
+    else:
+        dc.set_inputs(cd, cv)
+        cd_h = torch.from_numpy(cd).pin_memory()
+        cv_h = torch.from_numpy(cv).pin_memory()
+
+        def step(e2e: bool):
+            if e2e:
+                _lib.check(L.hc_comp_async(h, cd_h.data_ptr(), cv_h.data_ptr(), cd.shape[0], out_h.data_ptr(), sh))
+            else:
+                dc.launch(sh)
+
+        h2d_bytes = int(cd.nbytes + cv.nbytes)
+
+    def output():
+        torch.cuda.synchronize()
+        return dc.output() if rank == 0 else None
 
     # correctness gate: the timed Comp must decrypt to the payload's power sums
-    dc.launch(sh)
-    torch.cuda.synchronize()
-    out = dc.output()
-    ct = P.Ciphertext(be.backend_id, keys.key_id, 0, P.RnsPayload(out, 0.0, (be.q[0],)))
-    m = be.decrypt(ct, keys)
-    w = [int(x) for x in m.rows[0][: args.s]]
-    want_w = [sum(pow(i + 1, j + 1, p) for i, v in enumerate(dense) if v) % p for j in range(args.s)]
-    assert w == want_w, "Comp output does not decrypt to the expected power sums"
+    with torch.cuda.stream(stream):
+        step(False)
+    out = output()
+    if rank == 0:
+        ct = P.Ciphertext(be.backend_id, keys.key_id, 0, P.RnsPayload(out, 0.0, (be.q[0],)))
+        m = be.decrypt(ct, keys)
+        w = [int(x) for x in m.rows[0][: args.s]]
+        want_w = [sum(pow(i + 1, j + 1, p) for i, v in enumerate(dense) if v) % p for j in range(args.s)]
+        assert w == want_w, "Comp output does not decrypt to the expected power sums"
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             flush.zero_()
-            dc.launch(sh)
+            step(False)
     torch.cuda.synchronize()
 
     # ---- device-resident timed region ----
@@ -295,7 +347,7 @@ def main():
         for a, b in evs:
             flush.zero_()
             a.record(stream)
-            dc.launch(sh)
+            step(False)
             b.record(stream)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
@@ -304,25 +356,23 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_ms = sum(step_ms)
 
-    # ---- end-to-end through the public C-ABI with pinned host buffers ----
-    cd_h = torch.from_numpy(cd).pin_memory()
-    cv_h = torch.from_numpy(cv).pin_memory()
-    out_h = torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()
+    # ---- end to end through the public C-ABI: pinned host inputs in, result out ----
     e2e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with torch.cuda.stream(stream):
         for _ in range(2):
-            _lib.check(L.hc_comp_async(h, cd_h.data_ptr(), cv_h.data_ptr(), cd.shape[0], out_h.data_ptr(), sh))
+            step(True)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         for a, b in e2e_evs:
             flush.zero_()
             a.record(stream)
-            _lib.check(L.hc_comp_async(h, cd_h.data_ptr(), cv_h.data_ptr(), cd.shape[0], out_h.data_ptr(), sh))
+            step(True)
             b.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    assert np.array_equal(out_h.numpy().view(np.uint64), out), "e2e output differs from the device-resident run"
+    if rank == 0:
+        assert np.array_equal(out_h.numpy().view(np.uint64), out), "e2e output differs from the device-resident run"
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
     info = be.plan_info()  # kernel launches per Comp (graph built by now)
 
@@ -357,10 +407,11 @@ def main():
     comp_level = xf_jobs * bfly_per_ntt / (per_step_ms_pre := (t_ms / args.steps)) / 1e6
 
     per_step_ms = t_ms / args.steps
-    value = args.N * world / (per_step_ms * 1e-3)
-    e2e_value = args.N * world / (e2e_ms / args.steps * 1e-3)
+    units = args.N if shard else args.N * world  # sharded: one Comp per step; replicas: one per rank
+    value = units / (per_step_ms * 1e-3)
+    e2e_value = units / (e2e_ms / args.steps * 1e-3)
     line = {
-        "metric": METRIC,
+        "metric": metric_name(args.N, args.s),
         "value": value,
         "unit": "entries/s",
         "n_gpus": world,
@@ -369,7 +420,7 @@ def main():
         "ms_per_step": per_step_ms,
         "latency_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if shard else "weak",
         "vs_baseline": None,
         "dtype": "u64 (RNS, 54-bit primes)",
         "data": "synthetic (seeded; bench.run_point recipe; real keygen + encryption)",
@@ -378,8 +429,8 @@ def main():
             "value": e2e_value,
             "unit": "entries/s",
             "ms_per_step": e2e_ms / args.steps,
-            "h2d_bytes_per_step": int(cd.nbytes + cv.nbytes),
-            "d2h_bytes_per_step": int(out.nbytes),
+            "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": 2 * RING * 8,
         },
         "gpu_launches": int(info["kernel_launches"]) * args.steps * 2,
         "kernel_launches_per_comp": int(info["kernel_launches"]),

@@ -80,8 +80,15 @@ int hc_comp(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* 
  * hc_comp_set_inputs; hc_comp_launch enqueues the whole Comp (one graph
  * launch) on `stream` (a cudaStream_t, NULL = legacy default stream). */
 int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C);
+/* Sharded use: upload only input ciphertexts [c0, c1) (host buffers hold
+ * exactly those c1 - c0 ciphertexts, layout as above), asynchronously on
+ * `stream` (pinned host memory for a true async copy).  A rank running
+ * blocks [b0, b1) needs ciphertexts [b0/2, (b1+1)/2). */
+int hc_comp_set_inputs_range(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int c0, int c1, void* stream);
 int hc_comp_launch(hc_ctx* h, void* stream);
 int hc_comp_get_output(hc_ctx* h, uint64_t* out);
+/* Enqueue the device->host read of the output on `stream` (pinned `out`). */
+int hc_comp_get_output_async(hc_ctx* h, uint64_t* out, void* stream);
 /* Asynchronous end-to-end Comp on `stream`: H2D of cd/cv, the Comp graph and
  * D2H of the output, all stream-ordered (pass pinned host buffers for
  * overlap; the caller synchronises). */

@@ -52,8 +52,10 @@ _SIGS = [
     ("hc_comp", _I, [_P, _P, _P, _I, _P]),
     ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),
     ("hc_comp_set_inputs", _I, [_P, _P, _P, _I]),
+    ("hc_comp_set_inputs_range", _I, [_P, _P, _P, _I, _I, _P]),
     ("hc_comp_launch", _I, [_P, _P]),
     ("hc_comp_get_output", _I, [_P, _P]),
+    ("hc_comp_get_output_async", _I, [_P, _P, _P]),
     ("hc_partial_words", _I64, [_P]),
     ("hc_comp_partial", _I, [_P, _I64, _I64, _P, _P]),
     ("hc_comp_finish", _I, [_P, _P, _P]),

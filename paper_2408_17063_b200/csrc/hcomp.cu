@@ -1219,6 +1219,20 @@ extern "C" int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t*
     return HC_OK;
 }
 
+extern "C" int hc_comp_set_inputs_range(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int c0, int c1,
+                                        void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (c0 < 0 || c1 > P.C || c0 > c1) return fail(HC_ERR_ARG, "ciphertext range out of bounds");
+    CU(cudaSetDevice(h->dev));
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    const size_t ct = (size_t)2 * 4 * NPOLY;
+    const size_t bytes = (size_t)(c1 - c0) * ct * 8;
+    CU(cudaMemcpyAsync(P.cd + (size_t)c0 * ct, cd, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(P.cv + (size_t)c0 * ct, cv, bytes, cudaMemcpyHostToDevice, s));
+    return HC_OK;
+}
+
 extern "C" int hc_comp_launch(hc_ctx* h, void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     CU(cudaSetDevice(h->dev));
@@ -1234,6 +1248,14 @@ extern "C" int hc_comp_get_output(hc_ctx* h, uint64_t* out) {
     CU(cudaSetDevice(h->dev));
     CU(cudaDeviceSynchronize());
     CU(cudaMemcpy(out, h->plan->OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost));
+    return HC_OK;
+}
+
+extern "C" int hc_comp_get_output_async(hc_ctx* h, uint64_t* out, void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    CU(cudaSetDevice(h->dev));
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    CU(cudaMemcpyAsync(out, h->plan->OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, s));
     return HC_OK;
 }
 

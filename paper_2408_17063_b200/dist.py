@@ -58,11 +58,12 @@ def comp_sharded(cd, params, backend, keys, index_hint, dist, group=None, root: 
     backend.plan(params.N, params.s, keys)
     L = _lib.lib()
     h = backend._ctx()
-    cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd]), dtype=np.uint64)
-    cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv]), dtype=np.uint64)
-    _lib.check(L.hc_comp_set_inputs(h, _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd)))
-    words = L.hc_partial_words(h)
     b0, b1 = shard_blocks(params.num_blocks, world, rank)
+    c0, c1 = b0 // 2, (b1 + 1) // 2  # the input ciphertexts this rank's blocks read
+    cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd[c0:c1]]), dtype=np.uint64)
+    cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv[c0:c1]]), dtype=np.uint64)
+    _lib.check(L.hc_comp_set_inputs_range(h, _lib.ptr(cd_arr), _lib.ptr(cv_arr), c0, c1, None))
+    words = L.hc_partial_words(h)
     part = torch.zeros(words, dtype=torch.int64, device="cuda")
     _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(part.data_ptr()), None))
     torch.cuda.synchronize()
