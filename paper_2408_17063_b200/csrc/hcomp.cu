@@ -130,13 +130,11 @@ static void release_key(DevKey& k) {
     X(1, LD_RED, EP_STORE)            \
     X(1, LD_MONT, EP_RESCALE)         \
     X(1, LD_MONT, EP_STORE)           \
-    X(1, LD_MONT, EP_RESCALE_ATOMIC)  \
     X(0, LD_U64, EP_ADDMONT)          \
     X(0, LD_DIG, EP_STORE)            \
     X(0, LD_DIGGAL, EP_STORE)         \
     X(0, LD_RED, EP_ADDRED)           \
     X(1, LD_RED, EP_ADDRED)           \
-    X(0, LD_COMPOSE, EP_KSACC)        \
     X(0, LD_DIGGAL, EP_KSACC)         \
     X(1, LD_KSFIN, EP_STORE)          \
     X(1, LD_KSFIN, EP_RESCALE)
@@ -1030,9 +1028,10 @@ static const KsSpec* upload_spec(Schedule& S, const KsSpec& spec, int* rc) {
 //   T1   acc[g] = X[g] + NTT(E[g]) (c1 of g >= 1 in coefficient domain)
 //   T3   giant digit NTTs (CRT/digit split in the loader, KSACC epilogue)
 //   per fold f:
-//     F1 INTT of res_f.c1 (LD_KSFIN, side-stores res_f.c1) + two
-//        transform-less jobs materialising res_f.c0
-//     F3 fold digit NTTs (LD_COMPOSE -> EP_KSACC)
+//     F1 two-prime INTT of res_f.c1 (k_cl_intt2: LD_KSFIN, side-stores
+//        res_f.c1, CRT/digit split fused) + transform-less jobs
+//        materialising res_f.c0
+//     F3 fold digit NTTs (LD_DIGGAL -> EP_KSACC)
 //   D1   INTT of res_F * mask at the dropped prime (LD_KSFIN * mask) + rescale
 //   D2   NTT of the correction + res_F * mask * q^-1 at the kept prime
 static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {

@@ -33,8 +33,6 @@ enum : int {
     LD_RED = 3,    // a[j] reduced from any u64 (+ b[j] likewise if b)
     LD_DIG = 4,    // u16 digit a[j]
     LD_DIGGAL = 5, // u16 digit gathered: gal[j] -> (neg ? b : a)[src]
-    LD_COMPOSE = 6,// base-2^16 digit J.dig of CRT(a[k][src]) at level J.clevel, through gal
-    LD_KSMAC = 7,  // key-switch finish (KsSpec) [* b Montgomery], side-stored to aux
     LD_KSFIN = 8,  // base + sum_t c0src_t[perm_t] + red(acc) (KsSpec.acc, zeroed) [* b], aux
 };
 
@@ -61,7 +59,6 @@ enum : int {
     EP_ADD = 2,            // out[j] = x + ea[j]
     EP_ADDRED = 3,         // out[j] = x + red(ea[j])
     EP_RESCALE = 4,        // out[k*ostride + j] = e_k (k < level)
-    EP_RESCALE_ATOMIC = 5, // atomic += e_k
     EP_KSACC = 6,          // key-switch digit product: out[j] += x*ea[j], out[ostride+j] += x*eb[j]
 };
 
@@ -72,9 +69,8 @@ struct XJob {
     int level;  // EP_RESCALE*: level switched from (k == level)
     int noxf;   // 1: loader + side store only (no transform, no epilogue)
     int trace;  // HC_TRACE builds: launch sequence number
-    int dig, clevel;     // LD_COMPOSE: digit index, CRT level
-    const KsSpec* ks;    // LD_KSMAC
-    u64* aux;            // LD_KSMAC side store of the pre-transform value
+    const KsSpec* ks;    // LD_KSFIN
+    u64* aux;            // LD_KSFIN side store of the pre-transform value
     const u64* a;
     const u64* b;
     const uint16_t* gal;
@@ -107,26 +103,6 @@ __device__ unsigned long long g_trace[TR_LAUNCH][TR_BLK][TR_PT];
 // paths, no register spills).  Each handles N coefficients j0 + e*stride per
 // thread and issues every round of global loads for all N before any use.
 // ---------------------------------------------------------------------------
-
-template <int N, int L>
-__device__ __forceinline__ void ld_compose(const DevCtx& C, const XJob& J, int j0, int stride, u64 (&x)[N]) {
-    unsigned src[N];
-    HC_UNROLL
-    for (int e = 0; e < N; e++) src[e] = J.gal ? (unsigned)J.gal[j0 + e * stride] : (unsigned)(j0 + e * stride);
-    u64 xr[N][L + 1];
-    HC_UNROLL
-    for (int e = 0; e < N; e++) {
-        HC_UNROLL
-        for (int k = 0; k <= L; k++) xr[e][k] = J.a[(size_t)k * NPOLY + (src[e] & 0x7FFF)];
-    }
-    HC_UNROLL
-    for (int e = 0; e < N; e++) {
-        u64 X[NLIMB];
-        crt_compose<L>(C.lv[L], C.pc, xr[e], X);
-        if (J.gal && (src[e] >> 15)) neg_mod_Q<L>(C.lv[L], X);
-        x[e] = digit16(X, J.dig);
-    }
-}
 
 template <int N>
 __device__ __forceinline__ void ld_ksfin(const XJob& J, const PrimeC& P, int j0, int stride, u64 (&x)[N]) {
@@ -188,12 +164,6 @@ __device__ __forceinline__ void load_n(const DevCtx& C, const XJob& J, const Pri
         const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
         HC_UNROLL
         for (int e = 0; e < N; e++) x[e] = ((g[e] >> 15) ? dn : dp)[g[e] & 0x7FFF];
-    } else if constexpr (LD == LD_COMPOSE) {
-        switch (J.clevel) {
-            case 1: ld_compose<N, 1>(C, J, j0, stride, x); break;
-            case 2: ld_compose<N, 2>(C, J, j0, stride, x); break;
-            default: ld_compose<N, 3>(C, J, j0, stride, x); break;
-        }
     } else if constexpr (LD == LD_KSFIN) {
         ld_ksfin<N>(J, P, j0, stride, x);
     } else {  // LD_U64
@@ -226,7 +196,7 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
         HC_UNROLL
         for (int e = 0; e < N; e++)
             J.out[j0 + e * stride] = add_mod(x[e], EP == EP_ADD ? a[e] : red64(a[e], P.q, P.one_s), P.q);
-    } else if constexpr (EP == EP_RESCALE || EP == EP_RESCALE_ATOMIC) {
+    } else if constexpr (EP == EP_RESCALE) {
         const int l = J.level;
         const RescaleK R = rescale_consts(D, l);
         HC_UNROLL
@@ -236,9 +206,7 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
             HC_UNROLL
             for (int k = 0; k < MAXL; k++) {
                 if (k >= l) break;
-                u64* o = J.out + (size_t)k * J.ostride + j0 + e * stride;
-                if constexpr (EP == EP_RESCALE) *o = ek[k];
-                else atomicAdd(reinterpret_cast<unsigned long long*>(o), (unsigned long long)ek[k]);
+                J.out[(size_t)k * J.ostride + j0 + e * stride] = ek[k];
             }
         }
     } else {  // EP_STORE
@@ -309,20 +277,26 @@ struct ClJobs {
 
 // prefetch this CTA's 1023-entry twiddle slice (TwL) into shared memory;
 // all 8 loads per thread are issued before the first shared store
-__device__ __forceinline__ void tw_prefetch(Tw* sl, const Tw* tw, int c, int t) {
+// the CTA's twiddle slice: loads issued first (tw_issue, constant tables, so
+// they overlap the data loads), stored to smem afterwards (tw_commit)
+struct TwPre {
     ulonglong2 v[8];
+};
+__device__ __forceinline__ void tw_issue(TwPre& pre, const Tw* tw, int c, int t) {
     HC_UNROLL
     for (int i = 0; i < 8; i++) {
         const int L = t + CNT * i;
         const int Lc = L < 1023 ? L : 1022;
         const int e = 31 - __clz(Lc + 1);
         const int m8 = 1 << e;
-        v[i] = __ldg(reinterpret_cast<const ulonglong2*>(tw) + ((m8 << 3) + c * m8 + (Lc - (m8 - 1))));
+        pre.v[i] = __ldg(reinterpret_cast<const ulonglong2*>(tw) + ((m8 << 3) + c * m8 + (Lc - (m8 - 1))));
     }
+}
+__device__ __forceinline__ void tw_commit(Tw* sl, const TwPre& pre, int t) {
     HC_UNROLL
     for (int i = 0; i < 8; i++) {
         const int L = t + CNT * i;
-        if (L < 1023) reinterpret_cast<ulonglong2*>(sl)[L] = v[i];
+        if (L < 1023) reinterpret_cast<ulonglong2*>(sl)[L] = pre.v[i];
     }
 }
 
@@ -343,12 +317,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
     u64 x[CEPT];
     if (DIR == 0) {
         const Tw* tw = C.twf + (size_t)J.k * NPOLY;
+        TwPre pre;
+        tw_issue(pre, tw, c, t);
         Tw wa[8];
         HC_UNROLL
         for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);  // phase-A twiddles tbl[1..7]
         const int b = 128 * c + t;
         load_n<LD, CEPT>(C, J, P, b, CTILE, x);
-        tw_prefetch(twsl, tw, c, t);
+        TRACE(6);
+        tw_commit(twsl, pre, t);
+        TRACE(7);
         r8_ct(x, TwR{wa}, 0, 0, P.q, 2 * P.q2);
         TRACE(1);
         cluster_wait();
@@ -382,8 +360,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         TRACE(5);
     } else {
         const Tw* tw = C.twi + (size_t)J.k * NPOLY;
+        TwPre pre;
+        tw_issue(pre, tw, c, t);
         load_n<LD, CEPT>(C, J, P, c * CTILE + t, 128, x);
-        tw_prefetch(twsl, tw, c, t);
+        tw_commit(twsl, pre, t);
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
         __syncthreads();
@@ -466,8 +446,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     const PrimeC& P = C.pc[pr];
     const Tw* tw = C.twi + (size_t)pr * NPOLY;
     u64 x[CEPT];
+    TwPre pre;
+    tw_issue(pre, tw, c, t);
     load_n<LD, CEPT>(C, J, P, c * CTILE + t, 128, x);
-    tw_prefetch(twsl, tw, c, t);
+    tw_commit(twsl, pre, t);
     HC_UNROLL
     for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
     __syncthreads();
