@@ -112,14 +112,6 @@ HD void bf_ct(u64& X, u64& Y, u64 w, u64 ws, u64 q, u64 q2) {
     Y = x - t + q2;
 }
 
-// Gentleman-Sande inverse butterfly, bgv.py:217-220.  In/out in [0, 2q).
-HD void bf_gs(u64& X, u64& Y, u64 w, u64 ws, u64 q, u64 q2) {
-    u64 x = X, y = Y;
-    u64 s = x + y;
-    X = s >= q2 ? s - q2 : s;
-    Y = mul_shoup_lazy(x - y + q2, w, ws, q);
-}
-
 // Lazy forward butterfly used by the transforms: no reduction of X and a
 // 3-product approximate Shoup quotient.  mulhi_approx(a, b) drops the
 // lo x lo product and the low halves of the cross products, so it returns
@@ -144,6 +136,17 @@ HD void bf_ct_lazy(u64& X, u64& Y, u64 w, u64 ws, u64 q, u64 q4) {
     const u64 x = X;
     X = x + t;
     Y = x - t + q4;
+}
+
+// Lazy Gentleman-Sande inverse butterfly (bgv.py:217-220): X + Y and
+// (X - Y) * w with the 3-product quotient; in/out in [0, 4q) (q4 = 4q < 2^56,
+// so X + Y and X - Y + 4q stay below 2^57).
+HD void bf_gs_lazy(u64& X, u64& Y, u64 w, u64 ws, u64 q, u64 q4) {
+    const u64 x = X, y = Y;
+    const u64 s = x + y;
+    X = s >= q4 ? s - q4 : s;
+    const u64 d = x - y + q4;
+    Y = d * w - mulhi_approx(d, ws) * q;  // [0, 4q)
 }
 
 // any value < 2^64 -> [0, q) (final canonicalisation of lazy transforms)

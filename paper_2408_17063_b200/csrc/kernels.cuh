@@ -378,7 +378,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
                 for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
                 c_st0(c, t, x, o, twl, P.q, P.q2);
             }
-            r8_gs(x, twl, 1 + 3 * p, I.G, P.q, P.q2);
+            r8_gs(x, twl, 1 + 3 * p, I.G, P.q, 2 * P.q2);
             if (p < 2) {
                 c_store(x, tile, I);
                 __syncthreads();
@@ -465,7 +465,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
             for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
             c_st0(c, t, x, o, twl, P.q, P.q2);
         }
-        r8_gs(x, twl, 1 + 3 * p, I.G, P.q, P.q2);
+        r8_gs(x, twl, 1 + 3 * p, I.G, P.q, 2 * P.q2);
         if (p < 2) {
             c_store(x, tile, I);
             __syncthreads();

@@ -80,7 +80,7 @@ __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* 
             for (int v = 0; v < EPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
             c_st0(0, t, x, o, tg, P.q, P.q2);
         }
-        r8_gs(x, tg, 1 + 3 * p, I.G, P.q, P.q2);
+        r8_gs(x, tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
         t_store(x, sm, I);
         __syncthreads();
     }
@@ -128,7 +128,7 @@ inline void host_emulate_inv(u64* a, const Tw* tw, const PrimeC& P) {
         }
         for (int t = 0; t < NT; t++) {
             CPass I = pass1k(3 - p, t);
-            r8_gs(regs[t], tg, 1 + 3 * p, I.G, P.q, P.q2);
+            r8_gs(regs[t], tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
             t_store(regs[t], sm, I);
         }
     }

@@ -115,7 +115,7 @@ HD void r8_ct(u64 (&x)[CEPT], const TW& tw, int s0, int G, u64 q, u64 q2) {
 // 3 GS stages b0..b0+2 on 8 points: stage b0+u pairs v, v + (1 << u),
 // twiddle inv_tbl[2^(12-b0-u) + (G << (2-u) | v >> (u+1))]
 template <class TW>
-HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q2) {
+HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q4) {
     HC_UNROLL
     for (int u = 0; u < 3; u++) {
         const int half = 1 << u;
@@ -124,7 +124,7 @@ HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q2) {
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
                 Tw w = tw(tb + (v >> (u + 1)), 1 << (12 - b0 - u));
-                bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
+                bf_gs_lazy(x[v], x[v + half], w.w, w.ws, q, q4);
             }
         }
     }
@@ -146,7 +146,8 @@ HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw,
     }
 }
 
-// inverse bit-0 stage across lanes: even X + Y, odd (X - Y) w
+// inverse bit-0 stage across lanes: even X + Y, odd (X - Y) w.  Inputs
+// (loader output) in [0, 2q), outputs in [0, 4q).
 template <class TW>
 HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2) {
     const int odd = t & 1;
@@ -157,10 +158,10 @@ HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, 
         const u64 Y = odd ? x[v] : o[v];
         if (odd) {
             Tw w = tw(tb + v, 4096);
-            x[v] = mul_shoup_lazy(X - Y + q2, w.w, w.ws, q);
+            const u64 d = X - Y + q2;
+            x[v] = d * w.w - mulhi_approx(d, w.ws) * q;
         } else {
-            u64 s = X + Y;
-            x[v] = s >= q2 ? s - q2 : s;
+            x[v] = X + Y;
         }
     }
 }
@@ -170,7 +171,7 @@ HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q4) { r8_ct(x, TwG
 
 // inverse phase A': GS stages 10, 11 on the column, then bit 12 folded with n^-1
 HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
-    const u64 q = P.q, q2 = P.q2;
+    const u64 q = P.q, q4 = 2 * P.q2;
     Tw wa[8];  // inv_tbl[1..7] (stages 10, 11 use indices 2..7)
     HC_UNROLL
     for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);
@@ -182,15 +183,16 @@ HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
                 Tw w = wa[tb + (v >> (u + 1))];
-                bf_gs(x[v], x[v + half], w.w, w.ws, q, q2);
+                bf_gs_lazy(x[v], x[v + half], w.w, w.ws, q, q4);
             }
         }
     }
+    // bit 12 with n^-1 folded in: exact Shoup takes any 64-bit input (< 8q here)
     HC_UNROLL
     for (int v = 0; v < 4; v++) {
         u64 a = x[v], b = x[v + 4];
         x[v] = reduce_once(mul_shoup_lazy(a + b, P.ninv, P.ninv_s, q), q);
-        x[v + 4] = reduce_once(mul_shoup_lazy(a - b + q2, P.ninvw, P.ninvw_s, q), q);
+        x[v + 4] = reduce_once(mul_shoup_lazy(a - b + q4, P.ninvw, P.ninvw_s, q), q);
     }
 }
 
@@ -254,7 +256,7 @@ inline void host_emulate_cl_inv(u64* a, const Tw* tw, const PrimeC& P) {
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) {
                 CPass I = cpass(2 - p, c, t);
-                r8_gs(regs[c][t], TwL{sl[c], c}, 1 + 3 * p, I.G, P.q, P.q2);
+                r8_gs(regs[c][t], TwL{sl[c], c}, 1 + 3 * p, I.G, P.q, 2 * P.q2);
                 if (p < 2) c_store(regs[c][t], tile[c], I);
             }
     }
