@@ -339,7 +339,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         cluster_arrive_release();
         cluster_wait();  // also orders this CTA's twiddle-slice stores
         TRACE(3);
-        HC_NOUNROLL
+        HC_UNROLL
         for (int p = 0; p < 3; p++) {
             const CPass I = cpass(p, c, t);
             c_load(x, tile, I);
@@ -368,7 +368,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
         __syncthreads();
         TRACE(1);
-        HC_NOUNROLL
+        HC_UNROLL
         for (int p = 0; p < 3; p++) {
             const CPass I = cpass(2 - p, c, t);
             c_load(x, tile, I);
@@ -455,7 +455,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     __syncthreads();
     TRACE(1);
     const TwL twl{twsl, c};
-    HC_NOUNROLL
+    HC_UNROLL
     for (int p = 0; p < 3; p++) {
         const CPass I = cpass(2 - p, c, t);
         c_load(x, tile, I);

@@ -50,7 +50,7 @@ __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* 
     const int t = threadIdx.x;
     const TwG tg{tw};
     u64 x[EPT];
-    HC_NOUNROLL
+    HC_UNROLL
     for (int p = 0; p < 4; p++) {
         const CPass I = pass1k(p, t);
         t_load(x, sm, I);
@@ -70,7 +70,7 @@ __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* 
     const int t = threadIdx.x;
     const TwG tg{tw};
     u64 x[EPT];
-    HC_NOUNROLL
+    HC_UNROLL
     for (int p = 0; p < 3; p++) {
         const CPass I = pass1k(3 - p, t);
         t_load(x, sm, I);
