@@ -344,12 +344,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
             const CPass I = cpass(p, c, t);
             c_load(x, tile, I);
             r8_ct(x, twl, I.s0, I.G, P.q, 2 * P.q2);
-            if (p == 2) {
-                u64 o[CEPT];
-                HC_UNROLL
-                for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-                c_st12(c, t, x, o, twl, P.q, 2 * P.q2, P.one_s);
-            }
+            if (p == 2) c_st12(c, t, x, twl, P.q, 2 * P.q2, P.one_s);
             c_store(x, tile, I);
             __syncthreads();
         }

@@ -55,12 +55,7 @@ __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* 
         const CPass I = pass1k(p, t);
         t_load(x, sm, I);
         r8_ct(x, tg, I.s0, I.G, P.q, 2 * P.q2);
-        if (p == 3) {
-            u64 o[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-            c_st12(0, t, x, o, tg, P.q, 2 * P.q2, P.one_s);
-        }
+        if (p == 3) c_st12(0, t, x, tg, P.q, 2 * P.q2, P.one_s);
         t_store(x, sm, I);
         __syncthreads();
     }
@@ -94,7 +89,7 @@ __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* 
 
 // ---- host emulation of the 1024-thread schedule (CPU self-test only) ------
 inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
-    static u64 regs[NT][EPT], oth[NT][EPT];
+    static u64 regs[NT][EPT];
     static u64 sm[NPOLY];
     const TwG tg{tw};
     for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
@@ -104,11 +99,7 @@ inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
             t_load(regs[t], sm, I);
             r8_ct(regs[t], tg, I.s0, I.G, P.q, 2 * P.q2);
         }
-        if (p == 3) {
-            for (int t = 0; t < NT; t++)
-                for (int v = 0; v < EPT; v++) oth[t][v] = regs[t ^ 1][v];
-            for (int t = 0; t < NT; t++) c_st12(0, t, regs[t], oth[t], tg, P.q, 2 * P.q2, P.one_s);
-        }
+        if (p == 3) host_st12(0, NT, regs, tg, P.q, 2 * P.q2, P.one_s);
         for (int t = 0; t < NT; t++) t_store(regs[t], sm, pass1k(p, t));
     }
     for (int j = 0; j < NPOLY; j++) a[j] = sm[swz(j)];

@@ -131,19 +131,65 @@ HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q4) {
 }
 
 // forward bit-0 stage across lanes (t, t^1) in pass-2 layout:
-// w = tbl[4096 + (j >> 1)], j >> 1 = (c << 9) | ((t >> 1) << 3) | v
+// w = tbl[4096 + (j >> 1)], j >> 1 = (c << 9) | ((t >> 1) << 3) | v.
+// The even lane holds X_v, the odd lane Y_v of 8 butterflies; each lane
+// computes 4 of them (even: v = 4..7, odd: v = 0..3), so the stage costs
+// half a pass of modmuls, with two exchanges of 4 values:
+//   st12_send1 -> exchange -> st12_compute (-> 4 sends) -> exchange -> st12_recv2.
+// Outputs canonical.
+HD void st12_send1(int odd, const u64 (&x)[CEPT], u64 (&s)[4]) {
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) s[i] = odd ? x[4 + i] : x[i];
+}
 template <class TW>
-HD void c_st12(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2, u64 one_s) {
+HD void st12_compute(int c, int t, const u64 (&x)[CEPT], const u64 (&r)[4], const TW& tw, u64 q, u64 q4,
+                     u64 one_s, u64 (&A)[4], u64 (&B)[4], u64 (&s)[4]) {
     const int odd = t & 1;
     const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) {
-        u64 X = odd ? o[v] : x[v];
-        u64 Y = odd ? x[v] : o[v];
-        Tw w = tw(tb + v, 4096);
-        bf_ct_lazy(X, Y, w.w, w.ws, q, q2);
-        x[v] = canon_any(odd ? Y : X, q, one_s);
+    for (int i = 0; i < 4; i++) {
+        u64 X = odd ? r[i] : x[4 + i];
+        u64 Y = odd ? x[i] : r[i];
+        Tw w = tw(tb + (odd ? i : 4 + i), 4096);
+        bf_ct_lazy(X, Y, w.w, w.ws, q, q4);
+        A[i] = canon_any(X, q, one_s);
+        B[i] = canon_any(Y, q, one_s);
+        s[i] = odd ? A[i] : B[i];  // the partner's outputs
     }
+}
+HD void st12_recv2(int odd, u64 (&x)[CEPT], const u64 (&r)[4], const u64 (&A)[4], const u64 (&B)[4]) {
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) {
+        x[i] = odd ? B[i] : r[i];
+        x[4 + i] = odd ? r[i] : A[i];
+    }
+}
+#if defined(__CUDACC__)
+template <class TW>
+__device__ __forceinline__ void c_st12(int c, int t, u64 (&x)[CEPT], const TW& tw, u64 q, u64 q4, u64 one_s) {
+    const int odd = t & 1;
+    u64 s[4], r[4], A[4], B[4];
+    st12_send1(odd, x, s);
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) r[i] = __shfl_xor_sync(0xffffffffu, s[i], 1);
+    st12_compute(c, t, x, r, tw, q, q4, one_s, A, B, s);
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) r[i] = __shfl_xor_sync(0xffffffffu, s[i], 1);
+    st12_recv2(odd, x, r, A, B);
+}
+#endif
+// host emulation of c_st12 over lane pairs: regs[t] for t in [0, n)
+template <class TW>
+inline void host_st12(int c, int n, u64 (*regs)[CEPT], const TW& tw, u64 q, u64 q4, u64 one_s) {
+    static u64 snd[1024][4], A[1024][4], B[1024][4];
+    for (int t = 0; t < n; t++) st12_send1(t & 1, regs[t], snd[t]);
+    static u64 rcv[1024][4];
+    for (int t = 0; t < n; t++)
+        for (int i = 0; i < 4; i++) rcv[t][i] = snd[t ^ 1][i];
+    for (int t = 0; t < n; t++) st12_compute(c, t, regs[t], rcv[t], tw, q, q4, one_s, A[t], B[t], snd[t]);
+    for (int t = 0; t < n; t++)
+        for (int i = 0; i < 4; i++) rcv[t][i] = snd[t ^ 1][i];
+    for (int t = 0; t < n; t++) st12_recv2(t & 1, regs[t], rcv[t], A[t], B[t]);
 }
 
 // inverse bit-0 stage across lanes: even X + Y, odd (X - Y) w.  Inputs
@@ -206,7 +252,7 @@ inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
     static Tw sl[CL][1023];
     host_tw_slices(tw, sl);
     static u64 tile[CL][CTILE];
-    static u64 regs[CL][CNT][CEPT], oth[CL][CNT][CEPT];
+    static u64 regs[CL][CNT][CEPT];
     for (int c = 0; c < CL; c++)
         for (int t = 0; t < CNT; t++) {
             u64 x[CEPT];
@@ -222,13 +268,8 @@ inline void host_emulate_cl_fwd(u64* a, const Tw* tw, const PrimeC& P) {
                 c_load(regs[c][t], tile[c], I);
                 r8_ct(regs[c][t], TwL{sl[c], c}, I.s0, I.G, P.q, 2 * P.q2);
             }
-        if (p == 2) {
-            for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++)
-                    for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
-            for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++) c_st12(c, t, regs[c][t], oth[c][t], TwL{sl[c], c}, P.q, 2 * P.q2, P.one_s);
-        }
+        if (p == 2)
+            for (int c = 0; c < CL; c++) host_st12(c, CNT, regs[c], TwL{sl[c], c}, P.q, 2 * P.q2, P.one_s);
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) c_store(regs[c][t], tile[c], cpass(p, c, t));
     }
