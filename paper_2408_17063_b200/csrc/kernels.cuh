@@ -367,12 +367,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         for (int p = 0; p < 3; p++) {
             const CPass I = cpass(2 - p, c, t);
             c_load(x, tile, I);
-            if (p == 0) {
-                u64 o[CEPT];
-                HC_UNROLL
-                for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-                c_st0(c, t, x, o, twl, P.q, P.q2);
-            }
+            if (p == 0) c_st0(c, t, x, twl, P.q, P.q2);
             r8_gs(x, twl, 1 + 3 * p, I.G, P.q, 2 * P.q2);
             if (p < 2) {
                 c_store(x, tile, I);
@@ -454,12 +449,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     for (int p = 0; p < 3; p++) {
         const CPass I = cpass(2 - p, c, t);
         c_load(x, tile, I);
-        if (p == 0) {
-            u64 o[CEPT];
-            HC_UNROLL
-            for (int v = 0; v < CEPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-            c_st0(c, t, x, o, twl, P.q, P.q2);
-        }
+        if (p == 0) c_st0(c, t, x, twl, P.q, P.q2);
         r8_gs(x, twl, 1 + 3 * p, I.G, P.q, 2 * P.q2);
         if (p < 2) {
             c_store(x, tile, I);

@@ -69,12 +69,7 @@ __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* 
     for (int p = 0; p < 3; p++) {
         const CPass I = pass1k(3 - p, t);
         t_load(x, sm, I);
-        if (p == 0) {
-            u64 o[EPT];
-            HC_UNROLL
-            for (int v = 0; v < EPT; v++) o[v] = __shfl_xor_sync(0xffffffffu, x[v], 1);
-            c_st0(0, t, x, o, tg, P.q, P.q2);
-        }
+        if (p == 0) c_st0(0, t, x, tg, P.q, P.q2);
         r8_gs(x, tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
         t_store(x, sm, I);
         __syncthreads();
@@ -106,17 +101,13 @@ inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
 }
 
 inline void host_emulate_inv(u64* a, const Tw* tw, const PrimeC& P) {
-    static u64 regs[NT][EPT], oth[NT][EPT];
+    static u64 regs[NT][EPT];
     static u64 sm[NPOLY];
     const TwG tg{tw};
     for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
     for (int p = 0; p < 3; p++) {
         for (int t = 0; t < NT; t++) t_load(regs[t], sm, pass1k(3 - p, t));
-        if (p == 0) {
-            for (int t = 0; t < NT; t++)
-                for (int v = 0; v < EPT; v++) oth[t][v] = regs[t ^ 1][v];
-            for (int t = 0; t < NT; t++) c_st0(0, t, regs[t], oth[t], tg, P.q, P.q2);
-        }
+        if (p == 0) host_st0(0, NT, regs, tg, P.q, P.q2);
         for (int t = 0; t < NT; t++) {
             CPass I = pass1k(3 - p, t);
             r8_gs(regs[t], tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);

@@ -192,24 +192,50 @@ inline void host_st12(int c, int n, u64 (*regs)[CEPT], const TW& tw, u64 q, u64 
     for (int t = 0; t < n; t++) st12_recv2(t & 1, regs[t], rcv[t], A[t], B[t]);
 }
 
-// inverse bit-0 stage across lanes: even X + Y, odd (X - Y) w.  Inputs
-// (loader output) in [0, 2q), outputs in [0, 4q).
+// inverse bit-0 stage across lanes: the even lane keeps X + Y, the odd lane
+// (X - Y) w; as for the forward stage each lane computes 4 butterflies
+// (st12_send1 -> exchange -> st0_compute -> exchange -> st12_recv2).
+// Inputs (loader output) in [0, 2q), outputs in [0, 4q).
 template <class TW>
-HD void c_st0(int c, int t, u64 (&x)[CEPT], const u64 (&o)[CEPT], const TW& tw, u64 q, u64 q2) {
+HD void st0_compute(int c, int t, const u64 (&x)[CEPT], const u64 (&r)[4], const TW& tw, u64 q, u64 q2,
+                    u64 (&A)[4], u64 (&B)[4], u64 (&s)[4]) {
     const int odd = t & 1;
     const int tb = 4096 + (c << 9) + ((t >> 1) << 3);
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) {
-        const u64 X = odd ? o[v] : x[v];
-        const u64 Y = odd ? x[v] : o[v];
-        if (odd) {
-            Tw w = tw(tb + v, 4096);
-            const u64 d = X - Y + q2;
-            x[v] = d * w.w - mulhi_approx(d, w.ws) * q;
-        } else {
-            x[v] = X + Y;
-        }
+    for (int i = 0; i < 4; i++) {
+        const u64 X = odd ? r[i] : x[4 + i];
+        const u64 Y = odd ? x[i] : r[i];
+        Tw w = tw(tb + (odd ? i : 4 + i), 4096);
+        const u64 d = X - Y + q2;
+        A[i] = X + Y;
+        B[i] = d * w.w - mulhi_approx(d, w.ws) * q;
+        s[i] = odd ? A[i] : B[i];
     }
+}
+#if defined(__CUDACC__)
+template <class TW>
+__device__ __forceinline__ void c_st0(int c, int t, u64 (&x)[CEPT], const TW& tw, u64 q, u64 q2) {
+    const int odd = t & 1;
+    u64 s[4], r[4], A[4], B[4];
+    st12_send1(odd, x, s);
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) r[i] = __shfl_xor_sync(0xffffffffu, s[i], 1);
+    st0_compute(c, t, x, r, tw, q, q2, A, B, s);
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) r[i] = __shfl_xor_sync(0xffffffffu, s[i], 1);
+    st12_recv2(odd, x, r, A, B);
+}
+#endif
+template <class TW>
+inline void host_st0(int c, int n, u64 (*regs)[CEPT], const TW& tw, u64 q, u64 q2) {
+    static u64 snd[1024][4], rcv[1024][4], A[1024][4], B[1024][4];
+    for (int t = 0; t < n; t++) st12_send1(t & 1, regs[t], snd[t]);
+    for (int t = 0; t < n; t++)
+        for (int i = 0; i < 4; i++) rcv[t][i] = snd[t ^ 1][i];
+    for (int t = 0; t < n; t++) st0_compute(c, t, regs[t], rcv[t], tw, q, q2, A[t], B[t], snd[t]);
+    for (int t = 0; t < n; t++)
+        for (int i = 0; i < 4; i++) rcv[t][i] = snd[t ^ 1][i];
+    for (int t = 0; t < n; t++) st12_recv2(t & 1, regs[t], rcv[t], A[t], B[t]);
 }
 
 // forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
@@ -281,18 +307,14 @@ inline void host_emulate_cl_inv(u64* a, const Tw* tw, const PrimeC& P) {
     static Tw sl[CL][1023];
     host_tw_slices(tw, sl);
     static u64 tile[CL][CTILE], recv[CL][CTILE];
-    static u64 regs[CL][CNT][CEPT], oth[CL][CNT][CEPT];
+    static u64 regs[CL][CNT][CEPT];
     for (int c = 0; c < CL; c++)
         for (int b = 0; b < CTILE; b++) tile[c][cswz(b)] = a[c * CTILE + b];
     for (int p = 0; p < 3; p++) {
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) c_load(regs[c][t], tile[c], cpass(2 - p, c, t));
         if (p == 0) {
-            for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++)
-                    for (int v = 0; v < CEPT; v++) oth[c][t][v] = regs[c][t ^ 1][v];
-            for (int c = 0; c < CL; c++)
-                for (int t = 0; t < CNT; t++) c_st0(c, t, regs[c][t], oth[c][t], TwL{sl[c], c}, P.q, P.q2);
+            for (int c = 0; c < CL; c++) host_st0(c, CNT, regs[c], TwL{sl[c], c}, P.q, P.q2);
         }
         for (int c = 0; c < CL; c++)
             for (int t = 0; t < CNT; t++) {
