@@ -399,6 +399,13 @@ def main():
     prof_total = float(sm_[:nsteps].sum())
     peak = ctypes.c_double()
     _lib.check(L.hc_bf_peak(h, ctypes.byref(peak)))
+    # the same transform kernel saturated (4 full waves of 148 single-CTA jobs):
+    # what it reaches when the GPU is full, vs the latency-bound launches above
+    sat = {}
+    for dname, dval in (("fwd", 0), ("inv", 1)):
+        us = ctypes.c_double()
+        _lib.check(L.hc_bench_xform(h, 592, dval, 20, ctypes.byref(us)))
+        sat[dname] = 592 * (RING // 2) * 13 / (us.value * 1e-6) / 1e9
     bfly_per_ntt = (RING // 2) * 13
     # dominant kernel family = the transform launches (k_xf / k_xf_cl):
     # algorithmic butterflies per launch / that launch's event-timed duration
@@ -451,6 +458,8 @@ def main():
             "xform_launches_per_comp": xf_launch,
             "profiled_step_ms_ungraphed": prof_total,
             "per_kind_ms": {str(k): round(v[0], 4) for k, v in sorted(kinds.items())},
+            "saturated_592_jobs_gbfly_s": sat,
+            "saturated_frac": {k: v / peak_g for k, v in sat.items()} if peak_g else None,
         },
         "clocks": clk,
         "plan": info,
