@@ -28,6 +28,7 @@ struct LevelC {
     u64 M[MAXL + 1][NLIMB];                // Q_l/q_k
     u64 Q[NLIMB];                          // Q_l
     double qrecip[MAXL + 1];               // 1/q_k
+    u64 g01, g01_s;                        // Garner: q_0^-1 mod q_1 (compose2)
 };
 
 struct DevCtx {

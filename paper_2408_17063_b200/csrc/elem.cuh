@@ -83,6 +83,24 @@ HD void crt_compose(const LevelC& C, const PrimeC* pc, const u64* x, u64 (&X)[NL
     }
 }
 
+// Two-prime CRT by Garner's formula (level 1): X = x0 + q0 * t with
+// t = (x1 - x0) * q0^-1 mod q1, which lands in [0, q0 q1) directly -- one
+// Shoup multiply and one 64x64 product instead of crt_compose<1>'s general
+// sum-and-correct.  x0 < q0, x1 < q1 canonical.
+HD void compose2(const LevelC& C, const PrimeC* pc, u64 x0, u64 x1, u64 (&X)[NLIMB]) {
+    const u64 q0 = pc[0].q, q1 = pc[1].q;
+    const u64 a = x0 >= q1 ? x0 - q1 : x0;  // x0 mod q1
+    const u64 t = mul_shoup(sub_mod(x1, a, q1), C.g01, C.g01_s, q1);
+    u64 hi, lo;
+    mul128(hi, lo, q0, t);
+    lo += x0;
+    hi += lo < x0 ? 1 : 0;
+    X[0] = lo;
+    X[1] = hi;
+    X[2] = 0;
+    X[3] = 0;
+}
+
 // Q - X for X != 0 (0 stays 0): the coefficient a negated automorphism
 // image carries (coeff_automorphism, bgv.py:273-284)
 template <int L>

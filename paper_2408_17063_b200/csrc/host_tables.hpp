@@ -145,6 +145,10 @@ static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<T
             C.Minv_s[k] = shoup_const(mi, primes[k]);
             C.qrecip[k] = 1.0 / (double)primes[k];
         }
+        if (l >= 1) {
+            C.g01 = inv_mod(primes[0] % primes[1], primes[1]);
+            C.g01_s = shoup_const(C.g01, primes[1]);
+        }
     }
     // slot_of: NTT index -> (row << 12 | col)  (bgv.py:367-377)
     slot_of.assign(n, 0);

@@ -3,6 +3,7 @@
 // CRT/digit split and the modulus-switch correction for the host with g++,
 // so the exact code the GPU runs is checked against the oracle on a machine
 // without a GPU.  Not part of the product library.
+#include <cstring>
 #include <cstdint>
 #include <vector>
 
@@ -61,6 +62,20 @@ static void compose_all(const uint64_t* x, const uint16_t* gal, int mode, uint16
             for (int j = 0; j < D; j++) dig[(size_t)(D + j) * NPOLY + pos] = digit16(X, j);
         }
     }
+}
+
+// compose2 (Garner, level 1) against crt_compose<1>: number of mismatches
+extern "C" int ht_compose2_check(const uint64_t* x0, const uint64_t* x1, int count) {
+    const LevelC& LV = g_ctx.lv[1];
+    int bad = 0;
+    for (int i = 0; i < count; i++) {
+        u64 xr[2] = {x0[i], x1[i]};
+        u64 A[NLIMB], B[NLIMB];
+        crt_compose<1>(LV, g_ctx.pc, xr, A);
+        compose2(LV, g_ctx.pc, x0[i], x1[i], B);
+        bad += memcmp(A, B, sizeof A) != 0;
+    }
+    return bad;
 }
 
 extern "C" int ht_compose(int level, const uint64_t* x, const uint16_t* gal, int mode, uint16_t* dig) {

@@ -492,9 +492,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
             out0[j] = a;
             out1[j] = b;
         }
-        u64 xr[2] = {a, b};
         u64 X[NLIMB];
-        crt_compose<1>(LV, C.pc, xr, X);
+        compose2(LV, C.pc, a, b, X);
         HC_UNROLL
         for (int d = 0; d < 8; d++)
             if (d < D) dig[(size_t)d * NPOLY + j] = digit16(X, d);

@@ -23,6 +23,7 @@ def ht():
     L.ht_ntt.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_ntt_cl.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_compose.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P]
+    L.ht_compose2_check.argtypes = [P, P, ctypes.c_int]
     L.ht_rescale_corr.argtypes = [ctypes.c_int, P, P]
     L.ht_modops.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
     L.ht_galois.argtypes = [ctypes.c_uint32, P, P]
@@ -104,6 +105,21 @@ def test_crt_digits_match_reference_digit_split(setup, oracle):
         neg = [(Q - v) % Q for v in ints]
         want_neg = np.array([[(v >> (16 * j)) & 0xFFFF for v in neg] for j in range(D)], dtype=np.uint16)
         assert np.array_equal(got[D:], want_neg)
+
+
+def test_garner_compose2_matches_crt(setup):
+    """compose2 (the level-1 Garner CRT in the fold INTT) == crt_compose<1>,
+    random residues plus 0 / q_k - 1 edges."""
+    ht, be, _ = setup
+    import random
+
+    rng = random.Random(11)
+    n = 4096
+    x0 = np.array([rng.randrange(be.q[0]) for _ in range(n)], dtype=np.uint64)
+    x1 = np.array([rng.randrange(be.q[1]) for _ in range(n)], dtype=np.uint64)
+    x0[:4] = [0, be.q[0] - 1, 0, be.q[0] - 1]
+    x1[:4] = [0, 0, be.q[1] - 1, be.q[1] - 1]
+    assert ht.ht_compose2_check(p_(x0), p_(x1), n) == 0
 
 
 def test_rescale_correction_equals_mod_switch(setup, oracle):

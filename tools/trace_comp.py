@@ -40,6 +40,7 @@ for lid, s0, e, b in rows:
         return np.median(b[m, j] - b[m, i]) / 1e3 if m.any() else float('nan')
     print(f"launch {lid:3d} blocks {len(b):4d} start {(s0-t0)/1e3:8.2f} gap {(s0-prev_end)/1e3:6.2f} dur {(e-s0)/1e3:7.2f} us | "
           f"ld {med(0,1):5.2f} 1->4 {med(1,4):5.2f} 4->5 {med(4,5):5.2f} start-spread {(b[:,0].max()-s0)/1e3:5.2f}"
-          + (f" | 0->6 {med(0,6):5.2f} 6->7 {med(6,7):5.2f} 7->1 {med(7,1):5.2f}" if (b[:, 6] > 0).any() else ""))
+          + (f" | 0->6 {med(0,6):5.2f} 6->7 {med(6,7):5.2f} 7->1 {med(7,1):5.2f}" if (b[:, 6] > 0).any() else "")
+          + (f" | 4->3 {med(4,3):5.2f} 3->5 {med(3,5):5.2f}" if (b[:, 3] > b[:, 4]).all() else ""))
     prev_end = e
 print("total", (prev_end - t0) / 1e3, "us")
