@@ -478,30 +478,45 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     u64* out1 = JJ.j[1].out;
     const u64* tile0 = dsm;
     const u64* tile1 = dsm + CTILE;
-    const int tt = threadIdx.x;
+    // each thread: 4 adjacent coefficients (local L = 4 tt + i), so every
+    // digit index is one 8-byte store of 4 digits (coalesced across the warp)
+    const int L0 = 4 * threadIdx.x;
+    const int j0 = (L0 >> 7) * CTILE + 128 * c + (L0 & 127);
+    u64 a[4], b[4];
     HC_UNROLL
     for (int i = 0; i < 4; i++) {
-        const int L = tt + 256 * i;
-        const int j = (L >> 7) * CTILE + 128 * c + (L & 127);
-        u64 a = tile0[L], b = tile1[L];
-        if (E) {
-            a = add_mod(a, red64(E[j], C.pc[0].q, C.pc[0].one_s), C.pc[0].q);
-            b = add_mod(b, red64(E[NPOLY + j], C.pc[1].q, C.pc[1].one_s), C.pc[1].q);
-        }
-        if (out0) {  // optional coefficient side store
-            out0[j] = a;
-            out1[j] = b;
-        }
-        u64 X[NLIMB];
-        compose2(LV, C.pc, a, b, X);
-        HC_UNROLL
-        for (int d = 0; d < 8; d++)
-            if (d < D) dig[(size_t)d * NPOLY + j] = digit16(X, d);
-        neg_mod_Q<1>(LV, X);
-        HC_UNROLL
-        for (int d = 0; d < 8; d++)
-            if (d < D) dig[(size_t)(D + d) * NPOLY + j] = digit16(X, d);
+        a[i] = tile0[L0 + i];
+        b[i] = tile1[L0 + i];
     }
+    if (E) {
+        HC_UNROLL
+        for (int i = 0; i < 4; i++) {
+            a[i] = add_mod(a[i], red64(E[j0 + i], C.pc[0].q, C.pc[0].one_s), C.pc[0].q);
+            b[i] = add_mod(b[i], red64(E[NPOLY + j0 + i], C.pc[1].q, C.pc[1].one_s), C.pc[1].q);
+        }
+    }
+    if (out0) {  // optional coefficient side store
+        HC_UNROLL
+        for (int i = 0; i < 4; i++) {
+            out0[j0 + i] = a[i];
+            out1[j0 + i] = b[i];
+        }
+    }
+    u64 X[4][NLIMB];
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) compose2(LV, C.pc, a[i], b[i], X[i]);
+    HC_UNROLL
+    for (int d = 0; d < 8; d++)
+        if (d < D)
+            *reinterpret_cast<ushort4*>(dig + (size_t)d * NPOLY + j0) =
+                make_ushort4(digit16(X[0], d), digit16(X[1], d), digit16(X[2], d), digit16(X[3], d));
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) neg_mod_Q<1>(LV, X[i]);
+    HC_UNROLL
+    for (int d = 0; d < 8; d++)
+        if (d < D)
+            *reinterpret_cast<ushort4*>(dig + (size_t)(D + d) * NPOLY + j0) =
+                make_ushort4(digit16(X[0], d), digit16(X[1], d), digit16(X[2], d), digit16(X[3], d));
     TRACE(5);
 }
 
