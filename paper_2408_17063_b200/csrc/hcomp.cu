@@ -927,8 +927,9 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         rc = add_ma(S, s4, 3); if (rc) return rc;
         rc = add_xf(S, s5); if (rc) return rc;
         rc = add_co(S, s6); if (rc) return rc;
-        if (cb > g_lane_max_blocks) {
-            // throughput regime: one wide launch per segment over the chunk
+        if (cb > g_lane_max_blocks || cb < 3) {  // lanes pay off from 3 blocks (measured)
+            // one wide launch per segment over the chunk (throughput regime, or
+            // too few blocks for lanes to overlap anything)
             std::vector<XJob> w7, w9;
             std::vector<MJob> w8;
             for (int tl = 0; tl < cb; tl++) {
