@@ -140,6 +140,8 @@ int hc_set_cluster_threshold(int max_jobs);
  * parallel per-block lanes (latency regime); larger chunks use one wide launch
  * per segment (throughput regime). Applies to plans built afterwards. */
 int hc_set_lane_blocks(int max_blocks);
+/* Diagnostics: co-resident 8-CTA transform clusters on this device. */
+int hc_max_active_clusters(hc_ctx* h, int* clusters);
 
 /* Debug builds compiled with -DHC_TRACE: reset the launch numbering and read
  * per-CTA %globaltimer stamps [128 launches][512 CTAs][8 points]. */

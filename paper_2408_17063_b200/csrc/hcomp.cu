@@ -58,7 +58,8 @@ struct DevKey {
 };
 
 // transform launches with at most this many jobs use the cluster kernel
-static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters (split by CL_MAX)
+static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters
+static int g_cl_chunk = CL_MAX;  // jobs per cluster launch: co-resident 8-CTA clusters (<= CL_MAX)
 static int g_lane_max_blocks = 4;  // chunks up to this many blocks run the baby segment as lanes
 static const int CL_SPREAD_SMEM = 120 * 1024;
 
@@ -140,6 +141,24 @@ static void release_key(DevKey& k) {
     X(1, LD_KSFIN, EP_RESCALE)
 
 static int kernels_configured = 0;
+// co-resident 8-CTA transform clusters (one CTA per SM) on the current device
+static int max_active_clusters(int* clusters) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CL * CL_MAX);
+    cfg.blockDim = dim3(CNT);
+    cfg.dynamicSmemBytes = CL_SPREAD_SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaFuncSetAttribute(k_xf_cl<0, LD_U64, EP_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaOccupancyMaxActiveClusters(clusters, k_xf_cl<0, LD_U64, EP_STORE>, &cfg));
+    return HC_OK;
+}
+
 static int configure_kernels() {
     if (kernels_configured) return HC_OK;
     // cluster transforms: reserve enough (unused) dynamic smem that each CTA
@@ -153,6 +172,10 @@ static int configure_kernels() {
     CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
     CU(cudaFuncSetAttribute(k_cl_intt2<LD_KSFIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
     CU(cudaFuncSetAttribute(k_cl_intt2<LD_RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    {
+        int n = 0;
+        if (max_active_clusters(&n) == HC_OK && n > 0) g_cl_chunk = std::min(n, CL_MAX);
+    }
     kernels_configured = 1;
     return HC_OK;
 }
@@ -263,6 +286,9 @@ static int upload_jobs(Schedule& S, Step& st, const void* host, size_t bytes) {
 // one step (launch) per (direction, loader, epilogue, transform-less) group,
 // in first-appearance order
 static int g_trace_seq = 0;
+// One batch of independent transforms, grouped by (dir, loader, epilogue);
+// a group too big for one cluster launch (g_cl_chunk = co-resident 8-CTA
+// clusters) is split into launches that run as parallel graph branches.
 static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
     std::vector<int> taken(jobs.size(), 0);
     for (size_t i = 0; i < jobs.size(); i++) {
@@ -278,7 +304,7 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
         // clusters only for small batches outside parallel lanes (lanes
         // already fill the GPU; single-CTA transforms are more efficient there)
         const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS && S.cur_lane < 0;
-        const size_t chunk = clu ? (size_t)CL_MAX : sel.size();
+        const size_t chunk = clu ? (size_t)g_cl_chunk : sel.size();
         const int saved = S.cur_group;
         if (clu && sel.size() > chunk && !S.cur_group) S.par_begin();
         for (size_t c0 = 0; c0 < sel.size(); c0 += chunk) {
@@ -1585,6 +1611,12 @@ extern "C" int hc_bf_peak(hc_ctx* h, double* bfly_per_s) {
 extern "C" int hc_set_cluster_threshold(int max_jobs) {
     CL_MAX_JOBS = max_jobs;
     return HC_OK;
+}
+
+extern "C" int hc_max_active_clusters(hc_ctx* h, int* clusters) {
+    if (!h || !clusters) return fail(HC_ERR_ARG, "bad arguments");
+    CU(cudaSetDevice(h->dev));
+    return max_active_clusters(clusters);
 }
 
 extern "C" int hc_set_lane_blocks(int max_blocks) {
