@@ -1,4 +1,4 @@
-"""Warm device-resident Comp latency over (N, s) points with random level-3
+"""Device-resident Comp latency (warm, or median with L2 flushed: --flush) over (N, s) points with random level-3
 residues as inputs (timing only; parity is covered by tests/ and
 tools/large_config.py).  usage: python tools/sweep.py N:s [N:s ...] [--lanes K]"""
 import os, sys, time
@@ -36,12 +36,24 @@ for pt in args:
         torch.cuda.synchronize()
         iters = int(os.environ.get("SWEEP_ITERS", "0")) or max(3, min(50, int(2000 / max(1, N >> 14))))
         st = torch.cuda.Stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        for _ in range(iters):
-            dc.launch(st.cuda_stream)
-        e1.record(st)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / iters
+        if "--flush" in sys.argv:  # L2 flushed (256 MiB write) before every timed Comp, as bench.py
+            flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+            with torch.cuda.stream(st):
+                for a, b in evs:
+                    flush.zero_()
+                    a.record(st)
+                    dc.launch(st.cuda_stream)
+                    b.record(st)
+            torch.cuda.synchronize()
+            ms = sorted(a.elapsed_time(b) for a, b in evs)[iters // 2]
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(iters):
+                dc.launch(st.cuda_stream)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / iters
         print(f"N={N:8d} s={s:4d} cb={cb:3d} lanes<={ln:5d} blocks={params.num_blocks:5d}  {ms:9.3f} ms  {N/ms/1e3:8.1f} M entries/s", flush=True)
 _lib.lib().hc_set_lane_blocks(4)
