@@ -176,4 +176,32 @@ HD void rescale_corr(const DevCtx& D, int l, u64 x, u64* e) { rescale_corr(resca
 // any 64-bit value -> [0, q)
 HD u64 red64(u64 a, u64 q, u64 one_s) { return reduce_once(mul_shoup_lazy(a, 1, one_s, q), q); }
 
+// The integers behind rescale_corr: r = centered(x mod q_l) (|r| < q_l / 2)
+// and d = centered_p(r mod p).  e_k = d - r q_l^-1 (mod q_k) is linear in
+// (r, d), so a sum of corrections is formed from the sums of r and d (exact in
+// int64 for up to 1024 terms) with one multiply per coefficient (k_diagx).
+HD void rescale_rd(const RescaleK& R, u64 x, long long& r, long long& d) {
+    const int neg = x > R.half_qd;
+    const u64 mag = neg ? R.ql - x : x;
+    u64 rm = mag - mulhi(mag, R.pbar) * R.p;  // Barrett: [0, 2p)
+    if (rm >= R.p) rm -= R.p;
+    if (neg && rm) rm = R.p - rm;  // r mod p in [0, p)
+    const int dneg = rm > R.half_p;
+    const u64 dmag = dneg ? R.p - rm : rm;
+    r = neg ? -(long long)mag : (long long)mag;
+    d = dneg ? -(long long)dmag : (long long)dmag;
+}
+
+// signed 64-bit -> [0, q)
+HD u64 smod(long long v, u64 q, u64 one_s) {
+    if (v >= 0) return red64((u64)v, q, one_s);
+    const u64 m = red64((u64)(-(v + 1)) + 1, q, one_s);
+    return m ? q - m : 0;
+}
+
+// e_k of a sum of rescale_rd terms: (sum d) - (sum r) q_l^-1 mod q_k
+HD u64 corr_from_sums(long long sr, long long sd, u64 q, u64 qinv, u64 qinv_s, u64 one_s) {
+    return sub_mod(smod(sd, q, one_s), mul_shoup(smod(sr, q, one_s), qinv, qinv_s, q), q);
+}
+
 }  // namespace hc

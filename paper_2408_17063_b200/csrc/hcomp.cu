@@ -130,6 +130,7 @@ static void release_key(DevKey& k) {
     X(0, LD_RED, EP_STORE)            \
     X(1, LD_RED, EP_STORE)            \
     X(1, LD_MONT, EP_RESCALE)         \
+    X(1, LD_MONT, EP_RESCALE_RD)      \
     X(1, LD_MONT, EP_STORE)           \
     X(0, LD_U64, EP_ADDMONT)          \
     X(0, LD_DIG, EP_STORE)            \
@@ -928,8 +929,9 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         s8[tl].push_back(mj);
                     }
                 }
-                // S9: dropped-prime half of each diagonal product: INTT + rescale
-                //     correction into the block's slot of Eslot
+                // S9: dropped-prime half of each diagonal product: INTT + the
+                //     (r, d) integers of its rescale correction into the
+                //     block's slot of Eslot (summed and multiplied by S10)
                 for (int g = 0; g < G; g++)
                     for (int b = 0; b < baby; b++) {
                         const int i = g * baby + b;
@@ -937,7 +939,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         const u64* dg = P.diag + ((size_t)t * sp + i) * 3 * NB;
                         for (int poly = 0; poly < 2; poly++) {
                             XJob j{};
-                            j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = 2;
+                            j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE_RD; j.level = 2;
                             j.a = rot_src(P, tl, b, poly) + 2 * NB;
                             j.b = dg + 2 * NB;
                             j.out = eslot(P, tl, b, g, poly);
@@ -1019,6 +1021,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     if (!r.cnt) continue;
                     DXJob d{};
                     d.nterm = (int)r.cnt;
+                    d.level = 2;
                     d.src = dsrc + r.off;
                     d.dg = ddg + r.off;
                     d.es = des + r.off;

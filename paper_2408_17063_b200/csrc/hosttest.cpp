@@ -96,6 +96,35 @@ extern "C" void ht_rescale_corr(int level, const uint64_t* x, uint64_t* e) {
     }
 }
 
+// rescale_rd + corr_from_sums (one term) against rescale_corr, and a sum of
+// terms against the sum of corrections: number of mismatches
+extern "C" int ht_rescale_rd_check(int level, const uint64_t* x, int count) {
+    const RescaleK R = rescale_consts(g_ctx, level);
+    int bad = 0;
+    long long sr = 0, sd = 0;
+    u64 se[MAXL] = {0, 0, 0};
+    for (int i = 0; i < count; i++) {
+        u64 e[MAXL];
+        rescale_corr(R, x[i], e);
+        long long r, d;
+        rescale_rd(R, x[i], r, d);
+        sr += r;
+        sd += d;
+        for (int k = 0; k < level; k++) {
+            const PrimeC& P = g_ctx.pc[k];
+            const LevelC& LV = g_ctx.lv[level];
+            bad += corr_from_sums(r, d, P.q, LV.qinv[k], LV.qinv_s[k], P.one_s) != e[k];
+            se[k] = add_mod(se[k], e[k], P.q);
+        }
+    }
+    for (int k = 0; k < level; k++) {
+        const PrimeC& P = g_ctx.pc[k];
+        const LevelC& LV = g_ctx.lv[level];
+        bad += corr_from_sums(sr, sd, P.q, LV.qinv[k], LV.qinv_s[k], P.one_s) != se[k];
+    }
+    return bad;
+}
+
 // Montgomery / Shoup helpers on arrays: op 0 = a*b mod q via mul_mont(a, b*R),
 // op 1 = redc(hi, lo) of 128-bit a*b, op 2 = red64(a)
 extern "C" void ht_modops(int k, int op, const uint64_t* a, const uint64_t* b, uint64_t* out, int count) {

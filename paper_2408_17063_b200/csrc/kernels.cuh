@@ -59,6 +59,7 @@ enum : int {
     EP_ADD = 2,            // out[j] = x + ea[j]
     EP_ADDRED = 3,         // out[j] = x + red(ea[j])
     EP_RESCALE = 4,        // out[k*ostride + j] = e_k (k < level)
+    EP_RESCALE_RD = 5,     // out[j] = r, out[ostride + j] = d (int64; summed by k_diagx)
     EP_KSACC = 6,          // key-switch digit product: out[j] += x*ea[j], out[ostride+j] += x*eb[j]
 };
 
@@ -196,6 +197,15 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
         HC_UNROLL
         for (int e = 0; e < N; e++)
             J.out[j0 + e * stride] = add_mod(x[e], EP == EP_ADD ? a[e] : red64(a[e], P.q, P.one_s), P.q);
+    } else if constexpr (EP == EP_RESCALE_RD) {
+        const RescaleK R = rescale_consts(D, J.level);
+        HC_UNROLL
+        for (int e = 0; e < N; e++) {
+            long long r, d;
+            rescale_rd(R, x[e], r, d);
+            J.out[j0 + e * stride] = (u64)r;
+            J.out[J.ostride + j0 + e * stride] = (u64)d;
+        }
     } else if constexpr (EP == EP_RESCALE) {
         const int l = J.level;
         const RescaleK R = rescale_consts(D, l);
@@ -647,15 +657,16 @@ __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C,
 // ---------------------------------------------------------------------------
 // k_diagx: grid (n/512, nprime, njobs), two coefficients per thread.  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
 // (dg Montgomery with q^-1 folded in) -- the kept-prime half of each
-// plaintext product; the dropped-prime half goes through k_xform/EP_RESCALE*.
+// plaintext product -- and E[k][j] += sum_t d_t - (sum_t r_t) q_l^-1 from the
+// (r, d) slots the dropped-prime INTTs wrote (EP_RESCALE_RD).
 // ---------------------------------------------------------------------------
 struct DXJob {
-    int nterm, pad;
+    int nterm, level;       // level: of the dropped prime behind the (r, d) slots
     const u64* const* src;  // nterm pointers, each [>=nprime][n]
     const u64* const* dg;   // nterm pointers, each [>=nprime][n]
-    const u64* const* es;   // nterm correction slots [nprime][n] (or null)
+    const u64* const* es;   // nterm (r, d) slots [2][n] int64 (EP_RESCALE_RD), or null
     u64* X;                 // [nprime][n], canonical, updated in place
-    u64* E;                 // [nprime][n], += sum of the slots (mod q)
+    u64* E;                 // [nprime][n], += sum of the slots' corrections (mod q)
 };
 
 __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
@@ -664,28 +675,36 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
     const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
-    u64 hx = 0, lx = 0, hy = 0, ly = 0, ex = 0, ey = 0;
+    u64 hx = 0, lx = 0, hy = 0, ly = 0;
+    long long rx = 0, ry = 0, dx = 0, dy = 0;
     const int nt = J.nterm;
     const u64* const* src = J.src;
     const u64* const* dg = J.dg;
     const u64* const* es = J.es;
     // batches of 8 terms: pointers, then all data loads, then the MACs
     for (int t0 = 0; t0 < nt; t0 += 8) {
-        ulonglong2 a[8], b[8], e[8];
-#pragma unroll
+        ulonglong2 a[8], b[8], r[8], d[8];
+        HC_UNROLL
         for (int i = 0; i < 8; i++)
             if (t0 + i < nt) {
                 a[i] = __ldcs(reinterpret_cast<const ulonglong2*>(src[t0 + i] + kn));
                 b[i] = __ldg(reinterpret_cast<const ulonglong2*>(dg[t0 + i] + kn));
-                e[i] = es ? __ldcs(reinterpret_cast<const ulonglong2*>(es[t0 + i] + kn)) : make_ulonglong2(0, 0);
+                if (es) {
+                    r[i] = *reinterpret_cast<const ulonglong2*>(es[t0 + i] + j);
+                    d[i] = *reinterpret_cast<const ulonglong2*>(es[t0 + i] + NPOLY + j);
+                }
             }
-#pragma unroll
+        HC_UNROLL
         for (int i = 0; i < 8; i++)
             if (t0 + i < nt) {
                 mac128(hx, lx, a[i].x, b[i].x);
                 mac128(hy, ly, a[i].y, b[i].y);
-                ex += e[i].x;  // < 2^54 each, nterm <= 1024
-                ey += e[i].y;
+                if (es) {  // |r| < 2^53, nterm <= 1024: exact in int64
+                    rx += (long long)r[i].x;
+                    ry += (long long)r[i].y;
+                    dx += (long long)d[i].x;
+                    dy += (long long)d[i].y;
+                }
             }
     }
     ulonglong2 X = *reinterpret_cast<const ulonglong2*>(J.X + kn);
@@ -693,9 +712,10 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
     X.y = add_mod(X.y, redc(hy, ly, pc.q, pc.qneg), pc.q);
     *reinterpret_cast<ulonglong2*>(J.X + kn) = X;
     if (es) {
+        const u64 qi = C.lv[J.level].qinv[k], qis = C.lv[J.level].qinv_s[k];
         ulonglong2 E = *reinterpret_cast<const ulonglong2*>(J.E + kn);
-        E.x = add_mod(E.x, red64(ex, pc.q, pc.one_s), pc.q);
-        E.y = add_mod(E.y, red64(ey, pc.q, pc.one_s), pc.q);
+        E.x = add_mod(E.x, corr_from_sums(rx, dx, pc.q, qi, qis, pc.one_s), pc.q);
+        E.y = add_mod(E.y, corr_from_sums(ry, dy, pc.q, qi, qis, pc.one_s), pc.q);
         *reinterpret_cast<ulonglong2*>(J.E + kn) = E;
     }
 }

@@ -24,6 +24,7 @@ def ht():
     L.ht_ntt_cl.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_compose.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P]
     L.ht_compose2_check.argtypes = [P, P, ctypes.c_int]
+    L.ht_rescale_rd_check.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_rescale_corr.argtypes = [ctypes.c_int, P, P]
     L.ht_modops.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
     L.ht_galois.argtypes = [ctypes.c_uint32, P, P]
@@ -120,6 +121,26 @@ def test_garner_compose2_matches_crt(setup):
     x0[:4] = [0, be.q[0] - 1, 0, be.q[0] - 1]
     x1[:4] = [0, 0, be.q[1] - 1, be.q[1] - 1]
     assert ht.ht_compose2_check(p_(x0), p_(x1), n) == 0
+
+
+def test_rescale_rd_sums_equal_summed_corrections(setup):
+    """EP_RESCALE_RD + k_diagx: the correction rebuilt from (r, d) equals
+    rescale_corr per term, and from summed (r, d) over 1024 terms (the most a
+    k_diagx job sums) equals the sum of the corrections."""
+    ht, be, _ = setup
+    import random
+
+    rng = random.Random(13)
+    for level in (1, 2, 3):
+        q = be.q[level]
+        x = np.array([rng.randrange(q) for _ in range(1024)], dtype=np.uint64)
+        x[:6] = [0, 1, q // 2, q // 2 + 1, q - 1, q - 2]
+        assert ht.ht_rescale_rd_check(level, p_(x), len(x)) == 0
+        # worst case for the int64 sums: every r near -q/2 or +q/2
+        hi = np.full(1024, q // 2, dtype=np.uint64)
+        lo = np.full(1024, q // 2 + 1, dtype=np.uint64)
+        assert ht.ht_rescale_rd_check(level, p_(hi), 1024) == 0
+        assert ht.ht_rescale_rd_check(level, p_(lo), 1024) == 0
 
 
 def test_rescale_correction_equals_mod_switch(setup, oracle):
