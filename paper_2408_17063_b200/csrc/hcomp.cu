@@ -340,8 +340,10 @@ static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
     S.steps.push_back(st);
     return HC_OK;
 }
-static int add_ma(Schedule& S, const std::vector<MJob>& jobs, int nprime) {
+static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
     if (jobs.empty()) return HC_OK;
+    for (MJob& j : jobs) j.trace = g_trace_seq;
+    g_trace_seq++;
     Step st;
     st.kind = ST_MA;
     st.group = S.cur_group;

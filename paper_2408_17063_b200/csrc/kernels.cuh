@@ -606,6 +606,7 @@ struct MTerm {
 };
 struct MJob {
     int level, nterm;
+    int trace, pad;  // HC_TRACE builds: launch sequence number
     MTerm t[MAXTERM];
     const u64* add0;
     const u64* add1;
@@ -616,6 +617,7 @@ struct MJob {
 // two adjacent coefficients per thread (128-bit loads)
 __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
+    TRACE(0);
     const int k = blockIdx.y;
     const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
     const LevelC& LV = C.lv[J.level];
@@ -644,14 +646,17 @@ __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C,
         o0.y = add_mod(o0.y, redc(h0y, l0y, pc.q, pc.qneg), pc.q);
         o1.x = add_mod(o1.x, redc(h1x, l1x, pc.q, pc.qneg), pc.q);
         o1.y = add_mod(o1.y, redc(h1y, l1y, pc.q, pc.qneg), pc.q);
+        TRACE(1);
         if (T.c0src) {
             const u64* c0 = T.c0src + (size_t)k * NPOLY;
             o0.x = add_mod(o0.x, c0[T.perm[j]], pc.q);
             o0.y = add_mod(o0.y, c0[T.perm[j + 1]], pc.q);
         }
     }
+    TRACE(4);
     *reinterpret_cast<ulonglong2*>(J.out0 + kn) = o0;
     *reinterpret_cast<ulonglong2*>(J.out1 + kn) = o1;
+    TRACE(5);
 }
 
 // ---------------------------------------------------------------------------
