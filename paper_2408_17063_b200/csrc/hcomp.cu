@@ -427,7 +427,7 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 k_ksmac<<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
                 break;
             case ST_DX:
-                k_diagx<<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);
+                k_diagx<<<dim3(NPOLY / 256, 1, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);
                 break;
             case ST_SUMC:
                 k_sum_copies<<<592, 256, 0, s>>>(h->hctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride);

@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C,
 }
 
 // ---------------------------------------------------------------------------
-// k_diagx: grid (n/512, nprime, njobs), two coefficients per thread.  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
+// k_diagx: grid (n/256, 1, njobs), the two kept primes per thread.  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
 // (dg Montgomery with q^-1 folded in) -- the kept-prime half of each
 // plaintext product -- and E[k][j] += sum_t d_t - (sum_t r_t) q_l^-1 from the
 // (r, d) slots the dropped-prime INTTs wrote (EP_RESCALE_RD).
@@ -674,54 +674,52 @@ struct DXJob {
     u64* E;                 // [nprime][n], += sum of the slots' corrections (mod q)
 };
 
+// one coefficient per thread, both kept primes, so every (r, d) slot is read
+// once; terms in batches of DXB (pointers, then all loads, then the MACs)
+constexpr int DXB = 4;
 __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
     const DXJob& J = jobs[blockIdx.z];
-    const int k = blockIdx.y;
-    const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-    const PrimeC pc = C.pc[k];
-    const size_t kn = (size_t)k * NPOLY + j;
-    u64 hx = 0, lx = 0, hy = 0, ly = 0;
-    long long rx = 0, ry = 0, dx = 0, dy = 0;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const u64 q0 = C.pc[0].q, q1 = C.pc[1].q;
+    u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
+    long long sr = 0, sd = 0;
     const int nt = J.nterm;
     const u64* const* src = J.src;
     const u64* const* dg = J.dg;
     const u64* const* es = J.es;
-    // batches of 8 terms: pointers, then all data loads, then the MACs
-    for (int t0 = 0; t0 < nt; t0 += 8) {
-        ulonglong2 a[8], b[8], r[8], d[8];
+    for (int t0 = 0; t0 < nt; t0 += DXB) {
+        u64 a0[DXB], a1[DXB], b0[DXB], b1[DXB], r[DXB], d[DXB];
         HC_UNROLL
-        for (int i = 0; i < 8; i++)
+        for (int i = 0; i < DXB; i++)
             if (t0 + i < nt) {
-                a[i] = __ldcs(reinterpret_cast<const ulonglong2*>(src[t0 + i] + kn));
-                b[i] = __ldg(reinterpret_cast<const ulonglong2*>(dg[t0 + i] + kn));
+                const u64* sp = src[t0 + i];
+                const u64* gp = dg[t0 + i];
+                a0[i] = __ldcs(sp + j);
+                a1[i] = __ldcs(sp + NPOLY + j);
+                b0[i] = __ldg(gp + j);
+                b1[i] = __ldg(gp + NPOLY + j);
                 if (es) {
-                    r[i] = *reinterpret_cast<const ulonglong2*>(es[t0 + i] + j);
-                    d[i] = *reinterpret_cast<const ulonglong2*>(es[t0 + i] + NPOLY + j);
+                    r[i] = __ldcs(es[t0 + i] + j);
+                    d[i] = __ldcs(es[t0 + i] + NPOLY + j);
                 }
             }
         HC_UNROLL
-        for (int i = 0; i < 8; i++)
+        for (int i = 0; i < DXB; i++)
             if (t0 + i < nt) {
-                mac128(hx, lx, a[i].x, b[i].x);
-                mac128(hy, ly, a[i].y, b[i].y);
+                mac128(h0, l0, a0[i], b0[i]);
+                mac128(h1, l1, a1[i], b1[i]);
                 if (es) {  // |r| < 2^53, nterm <= 1024: exact in int64
-                    rx += (long long)r[i].x;
-                    ry += (long long)r[i].y;
-                    dx += (long long)d[i].x;
-                    dy += (long long)d[i].y;
+                    sr += (long long)r[i];
+                    sd += (long long)d[i];
                 }
             }
     }
-    ulonglong2 X = *reinterpret_cast<const ulonglong2*>(J.X + kn);
-    X.x = add_mod(X.x, redc(hx, lx, pc.q, pc.qneg), pc.q);
-    X.y = add_mod(X.y, redc(hy, ly, pc.q, pc.qneg), pc.q);
-    *reinterpret_cast<ulonglong2*>(J.X + kn) = X;
+    J.X[j] = add_mod(J.X[j], redc(h0, l0, q0, C.pc[0].qneg), q0);
+    J.X[NPOLY + j] = add_mod(J.X[NPOLY + j], redc(h1, l1, q1, C.pc[1].qneg), q1);
     if (es) {
-        const u64 qi = C.lv[J.level].qinv[k], qis = C.lv[J.level].qinv_s[k];
-        ulonglong2 E = *reinterpret_cast<const ulonglong2*>(J.E + kn);
-        E.x = add_mod(E.x, corr_from_sums(rx, dx, pc.q, qi, qis, pc.one_s), pc.q);
-        E.y = add_mod(E.y, corr_from_sums(ry, dy, pc.q, qi, qis, pc.one_s), pc.q);
-        *reinterpret_cast<ulonglong2*>(J.E + kn) = E;
+        const LevelC& LV = C.lv[J.level];
+        J.E[j] = add_mod(J.E[j], corr_from_sums(sr, sd, q0, LV.qinv[0], LV.qinv_s[0], C.pc[0].one_s), q0);
+        J.E[NPOLY + j] = add_mod(J.E[NPOLY + j], corr_from_sums(sr, sd, q1, LV.qinv[1], LV.qinv_s[1], C.pc[1].one_s), q1);
     }
 }
 
