@@ -424,7 +424,10 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->hctx, (const CJob*)st.djobs);
                 break;
             case ST_MA:
-                k_ksmac<<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
+                if (st.njobs > 16)  // throughput: occupancy
+                    k_ksmac<1><<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
+                else  // small: fewer CTAs beside the transforms
+                    k_ksmac<2><<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
                 break;
             case ST_DX:
                 k_diagx<<<dim3(NPOLY / 256, 1, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);

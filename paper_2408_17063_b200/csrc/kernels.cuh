@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(256) k_compose(const __grid_constant__ DevCtx 
 }
 
 // ---------------------------------------------------------------------------
-// k_ksmac: grid (n/512, P, njobs), two coefficients per thread
+// k_ksmac<CPT>: grid (n/(256 CPT), P, njobs)
 //   out0 = add0 + sum_t ( c0src_t[perm_t[j]] + sum_j dntt_t[j] * b_t[j] )
 //   out1 = add1 + sum_t ( sum_j dntt_t[j] * a_t[j] )
 // dntt: [D][P][n]; key: [D_L][2][L+1][n] (Montgomery form).
@@ -614,48 +614,70 @@ struct MJob {
     u64* out1;
 };
 
-// two adjacent coefficients per thread (128-bit loads)
+// CPT adjacent coefficients per thread: 1 at scale (low register count, the
+// digit loads of many warps in flight), 2 for small launches that share the
+// SMs with transform CTAs (fewer CTAs).
+template <int CPT>
 __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
     TRACE(0);
     const int k = blockIdx.y;
-    const int j = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+    const int j = CPT * (blockIdx.x * blockDim.x + threadIdx.x);
     const LevelC& LV = C.lv[J.level];
     const int P = LV.P, D = LV.D, L1 = C.L + 1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
-    ulonglong2 o0 = J.add0 ? *reinterpret_cast<const ulonglong2*>(J.add0 + kn) : make_ulonglong2(0, 0);
-    ulonglong2 o1 = J.add1 ? *reinterpret_cast<const ulonglong2*>(J.add1 + kn) : make_ulonglong2(0, 0);
+    u64 o0[CPT], o1[CPT];
+    HC_UNROLL
+    for (int c = 0; c < CPT; c++) {
+        o0[c] = J.add0 ? J.add0[kn + c] : 0;
+        o1[c] = J.add1 ? J.add1[kn + c] : 0;
+    }
     const int nt = J.nterm;
     for (int t = 0; t < nt; t++) {
         const MTerm T = J.t[t];
-        u64 h0x = 0, l0x = 0, h1x = 0, l1x = 0, h0y = 0, l0y = 0, h1y = 0, l1y = 0;
-        const u64* vp = T.dntt + (size_t)k * NPOLY + j;
-        const u64* bp = T.key + (size_t)k * NPOLY + j;
+        u64 h0[CPT], l0[CPT], h1[CPT], l1[CPT];
+        HC_UNROLL
+        for (int c = 0; c < CPT; c++) h0[c] = l0[c] = h1[c] = l1[c] = 0;
+        const u64* vp = T.dntt + kn;
+        const u64* bp = T.key + kn;
         const size_t vstep = (size_t)P * NPOLY, kstep = (size_t)2 * L1 * NPOLY, astep = (size_t)L1 * NPOLY;
         for (int d = 0; d < D; d++) {
-            const ulonglong2 v = __ldcs(reinterpret_cast<const ulonglong2*>(vp + d * vstep));
-            const ulonglong2 kb = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep));
-            const ulonglong2 ka = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep + astep));
-            mac128(h0x, l0x, v.x, kb.x);
-            mac128(h0y, l0y, v.y, kb.y);
-            mac128(h1x, l1x, v.x, ka.x);
-            mac128(h1y, l1y, v.y, ka.y);
+            u64 v[CPT], kb[CPT], ka[CPT];
+            if constexpr (CPT == 2) {
+                const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(vp + d * vstep));
+                const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep));
+                const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep + astep));
+                v[0] = a.x; v[1] = a.y; kb[0] = b.x; kb[1] = b.y; ka[0] = e.x; ka[1] = e.y;
+            } else {
+                v[0] = __ldcs(vp + d * vstep);
+                kb[0] = __ldg(bp + d * kstep);
+                ka[0] = __ldg(bp + d * kstep + astep);
+            }
+            HC_UNROLL
+            for (int c = 0; c < CPT; c++) {
+                mac128(h0[c], l0[c], v[c], kb[c]);
+                mac128(h1[c], l1[c], v[c], ka[c]);
+            }
         }
-        o0.x = add_mod(o0.x, redc(h0x, l0x, pc.q, pc.qneg), pc.q);
-        o0.y = add_mod(o0.y, redc(h0y, l0y, pc.q, pc.qneg), pc.q);
-        o1.x = add_mod(o1.x, redc(h1x, l1x, pc.q, pc.qneg), pc.q);
-        o1.y = add_mod(o1.y, redc(h1y, l1y, pc.q, pc.qneg), pc.q);
+        HC_UNROLL
+        for (int c = 0; c < CPT; c++) {
+            o0[c] = add_mod(o0[c], redc(h0[c], l0[c], pc.q, pc.qneg), pc.q);
+            o1[c] = add_mod(o1[c], redc(h1[c], l1[c], pc.q, pc.qneg), pc.q);
+        }
         TRACE(1);
         if (T.c0src) {
             const u64* c0 = T.c0src + (size_t)k * NPOLY;
-            o0.x = add_mod(o0.x, c0[T.perm[j]], pc.q);
-            o0.y = add_mod(o0.y, c0[T.perm[j + 1]], pc.q);
+            HC_UNROLL
+            for (int c = 0; c < CPT; c++) o0[c] = add_mod(o0[c], c0[T.perm[j + c]], pc.q);
         }
     }
     TRACE(4);
-    *reinterpret_cast<ulonglong2*>(J.out0 + kn) = o0;
-    *reinterpret_cast<ulonglong2*>(J.out1 + kn) = o1;
+    HC_UNROLL
+    for (int c = 0; c < CPT; c++) {
+        J.out0[kn + c] = o0[c];
+        J.out1[kn + c] = o1[c];
+    }
     TRACE(5);
 }
 
