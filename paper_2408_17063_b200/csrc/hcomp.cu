@@ -133,8 +133,8 @@ static void release_key(DevKey& k) {
     X(1, LD_MONT, EP_RESCALE_RD)      \
     X(1, LD_MONT, EP_STORE)           \
     X(0, LD_U64, EP_ADDMONT)          \
-    X(0, LD_DIG, EP_STORE)            \
-    X(0, LD_DIGGAL, EP_STORE)         \
+    X(0, LD_DIG, EP_STORE_LAZY)       \
+    X(0, LD_DIGGAL, EP_STORE_LAZY)    \
     X(0, LD_RED, EP_ADDRED)           \
     X(1, LD_RED, EP_ADDRED)           \
     X(0, LD_DIGGAL, EP_KSACC)         \
@@ -877,7 +877,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                 for (int jj = 0; jj < D2; jj++)
                     for (int k = 0; k < 3; k++) {
                         XJob j{};
-                        j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+                        j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE_LAZY;  // feeds k_ksmac only
                         j.a = (const u64*)(P.digR + ((size_t)tl * D2 + jj) * NB);
                         j.out = P.dnttR + (((size_t)tl * D2 + jj) * 3 + k) * NB;
                         s3.push_back(j);
@@ -916,7 +916,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         for (int jj = 0; jj < D2; jj++)
                             for (int k = 0; k < 3; k++) {
                                 XJob j{};
-                                j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_STORE;
+                                j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_STORE_LAZY;  // feeds k_ksmac only
                                 j.a = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + jj) * NB);
                                 j.b = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
                                 j.gal = kb->gal;
@@ -1510,7 +1510,7 @@ extern "C" int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t t, u
     for (int jj = 0; jj < D; jj++)
         for (int k = 0; k < P1; k++) {
             XJob j{};
-            j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE;
+            j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE_LAZY;  // feeds k_ksmac (<= 14 lazy terms < q 2^64)
             j.a = (const u64*)((uint16_t*)ddig.p + (size_t)jj * NB);
             j.out = (u64*)dntt.p + ((size_t)jj * P1 + k) * NB;
             fwd.push_back(j);

@@ -61,6 +61,7 @@ enum : int {
     EP_RESCALE = 4,        // out[k*ostride + j] = e_k (k < level)
     EP_RESCALE_RD = 5,     // out[j] = r, out[ostride + j] = d (int64; summed by k_diagx)
     EP_KSACC = 6,          // key-switch digit product: out[j] += x*ea[j], out[ostride+j] += x*eb[j]
+    EP_STORE_LAZY = 7,     // out[j] = x, x < 2^60 not canonicalised (forward NTT feeding k_ksmac)
 };
 
 struct XJob {
@@ -219,7 +220,7 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
                 J.out[(size_t)k * J.ostride + j0 + e * stride] = ek[k];
             }
         }
-    } else {  // EP_STORE
+    } else {  // EP_STORE, EP_STORE_LAZY
         HC_UNROLL
         for (int e = 0; e < N; e++) J.out[j0 + e * stride] = x[e];
     }
@@ -243,7 +244,9 @@ __global__ void __launch_bounds__(NT, 1) k_xf(const __grid_constant__ DevCtx C, 
     }
     __syncthreads();
     TRACE(1);
-    if (DIR == 0) cta_ntt_fwd(C.twf + (size_t)J.k * NPOLY, P, sm);
+    // forward outputs that only feed Montgomery products stay lazy (< 2^60)
+    constexpr bool lazy = EP == EP_KSACC || EP == EP_STORE_LAZY;
+    if (DIR == 0) cta_ntt_fwd<lazy>(C.twf + (size_t)J.k * NPOLY, P, sm);
     else cta_ntt_inv(C.twi + (size_t)J.k * NPOLY, P, sm);
     TRACE(4);
     {
@@ -354,7 +357,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
             const CPass I = cpass(p, c, t);
             c_load(x, tile, I);
             r8_ct(x, twl, I.s0, I.G, P.q, 2 * P.q2);
-            if (p == 2) c_st12(c, t, x, twl, P.q, 2 * P.q2, P.one_s);
+            if (p == 2) c_st12<EP == EP_KSACC || EP == EP_STORE_LAZY>(c, t, x, twl, P.q, 2 * P.q2, P.one_s);
             c_store(x, tile, I);
             __syncthreads();
         }

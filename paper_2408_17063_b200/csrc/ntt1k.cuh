@@ -46,6 +46,7 @@ HD void t_store(const u64 (&x)[EPT], u64* sm, const CPass& I) {
 }
 
 #if defined(__CUDACC__)
+template <bool LAZY = false>
 __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* sm) {
     const int t = threadIdx.x;
     const TwG tg{tw};
@@ -55,7 +56,7 @@ __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* 
         const CPass I = pass1k(p, t);
         t_load(x, sm, I);
         r8_ct(x, tg, I.s0, I.G, P.q, 2 * P.q2);
-        if (p == 3) c_st12(0, t, x, tg, P.q, 2 * P.q2, P.one_s);
+        if (p == 3) c_st12<LAZY>(0, t, x, tg, P.q, 2 * P.q2, P.one_s);
         t_store(x, sm, I);
         __syncthreads();
     }

@@ -136,12 +136,13 @@ HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q4) {
 // computes 4 of them (even: v = 4..7, odd: v = 0..3), so the stage costs
 // half a pass of modmuls, with two exchanges of 4 values:
 //   st12_send1 -> exchange -> st12_compute (-> 4 sends) -> exchange -> st12_recv2.
-// Outputs canonical.
+// Outputs canonical, or (LAZY) below 2^60 for consumers that only feed them
+// to Montgomery products.
 HD void st12_send1(int odd, const u64 (&x)[CEPT], u64 (&s)[4]) {
     HC_UNROLL
     for (int i = 0; i < 4; i++) s[i] = odd ? x[4 + i] : x[i];
 }
-template <class TW>
+template <bool LAZY = false, class TW>
 HD void st12_compute(int c, int t, const u64 (&x)[CEPT], const u64 (&r)[4], const TW& tw, u64 q, u64 q4,
                      u64 one_s, u64 (&A)[4], u64 (&B)[4], u64 (&s)[4]) {
     const int odd = t & 1;
@@ -152,8 +153,8 @@ HD void st12_compute(int c, int t, const u64 (&x)[CEPT], const u64 (&r)[4], cons
         u64 Y = odd ? x[i] : r[i];
         Tw w = tw(tb + (odd ? i : 4 + i), 4096);
         bf_ct_lazy(X, Y, w.w, w.ws, q, q4);
-        A[i] = canon_any(X, q, one_s);
-        B[i] = canon_any(Y, q, one_s);
+        A[i] = LAZY ? X : canon_any(X, q, one_s);  // LAZY: < 2^60 (13 stages of < 4q growth)
+        B[i] = LAZY ? Y : canon_any(Y, q, one_s);
         s[i] = odd ? A[i] : B[i];  // the partner's outputs
     }
 }
@@ -165,14 +166,14 @@ HD void st12_recv2(int odd, u64 (&x)[CEPT], const u64 (&r)[4], const u64 (&A)[4]
     }
 }
 #if defined(__CUDACC__)
-template <class TW>
+template <bool LAZY = false, class TW>
 __device__ __forceinline__ void c_st12(int c, int t, u64 (&x)[CEPT], const TW& tw, u64 q, u64 q4, u64 one_s) {
     const int odd = t & 1;
     u64 s[4], r[4], A[4], B[4];
     st12_send1(odd, x, s);
     HC_UNROLL
     for (int i = 0; i < 4; i++) r[i] = __shfl_xor_sync(0xffffffffu, s[i], 1);
-    st12_compute(c, t, x, r, tw, q, q4, one_s, A, B, s);
+    st12_compute<LAZY>(c, t, x, r, tw, q, q4, one_s, A, B, s);
     HC_UNROLL
     for (int i = 0; i < 4; i++) r[i] = __shfl_xor_sync(0xffffffffu, s[i], 1);
     st12_recv2(odd, x, r, A, B);
