@@ -126,3 +126,57 @@ def test_comp_rejects_bad_inputs_like_reference():
         P.comp([ct, ct], params, be, keys, index_hint=[ct])  # wrong count (compress.py:348-349)
     with pytest.raises(P.MissingRotationKey):
         P.comp([ct], params, be, keys, index_hint=[ct])  # no col-swap key (bgv.py:767-768)
+
+
+def test_masked_matrix_mirrors_vandermonde_table_checks():
+    """precompute_masked_matrix (compress.py:154-157 -> VandermondeTable,
+    compress.py:107-116): wrong length raises ValueError; values are reduced
+    with Python's int(v) % p (negatives included)."""
+    he = P.HeParams(8192, 65537, 3)
+    params = P.CompressionParams(200, 5, he)
+    with pytest.raises(ValueError):
+        P.precompute_masked_matrix([1] * 199, params)
+    db = [-1, 65537, 70000, 3] + [0] * 196
+    m = P.precompute_masked_matrix(db, params)
+    assert m.db_mod_p.dtype == np.uint64 and len(m.db_mod_p) == 200
+    assert list(m.db_mod_p[:4]) == [65536, 0, 70000 % 65537, 3]
+
+
+def test_comp_masked_argument_checks():
+    he = P.HeParams(8192, 65537, 3)
+    params = P.CompressionParams(8192, 8, he)
+    be = P.B200BgvBackend(he, seed=0)
+    ct = P.Ciphertext(be.backend_id, b"x" * 16, 3, P.RnsPayload(np.zeros((2, 4, 8192), np.uint64), 0.0))
+    keys = P.KeySet(be.backend_id, he, b"x" * 16, {}, None, None, None, None)
+    with pytest.raises(TypeError):  # only tables from precompute_masked_matrix
+        P.comp([ct], params, be, keys, masked=object())
+    table = P.precompute_masked_matrix([1] * 8192, params)
+    with pytest.raises(P.MissingRotationKey):  # same input checks as the hint path
+        P.comp_masked([ct], table, params, be, keys)
+
+
+def test_shard_input_ranges_cover_the_blocks_sources():
+    """A rank running blocks [b0, b1) reads input ciphertexts b // 2; the
+    range it uploads (hc_comp_set_inputs_range) is [b0 // 2, (b1 + 1) // 2)."""
+    from paper_2408_17063_b200.dist import shard_blocks
+
+    for B in (1, 2, 3, 4, 7, 256, 1023):
+        for world in (1, 2, 3, 8):
+            for rank in range(world):
+                b0, b1 = shard_blocks(B, world, rank)
+                if b1 == b0:
+                    continue
+                c0, c1 = b0 // 2, (b1 + 1) // 2
+                assert {b // 2 for b in range(b0, b1)} == set(range(c0, c1))
+                assert c1 <= (B + 1) // 2
+
+
+def test_bench_helpers():
+    import bench
+
+    assert bench.metric_name(1 << 14, 16) == "Comp encrypted entries/sec (N=2^14, s=16)"
+    assert bench.metric_name(10000, 5) == "Comp encrypted entries/sec (N=10000, s=5)"
+    assert bench.pick_p(1 << 14, 0) == 65537
+    assert bench.pick_p(1 << 17, 0) == 786433
+    assert bench.pick_p(1 << 20, 0) == 1097729
+    assert bench.pick_p(1 << 22, 0) == 4423681
