@@ -68,6 +68,7 @@ _SIGS = [
     ("hc_bench_xform", _I, [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_double)]),
     ("hc_set_cluster_threshold", _I, [_I]),
     ("hc_set_lane_blocks", _I, [_I]),
+    ("hc_set_vt2_jobs", _I, [_I]),
     ("hc_max_active_clusters", _I, [_P, _P]),
     ("hc_trace_reset", _I, []),
     ("hc_trace_read", _I, [_P]),

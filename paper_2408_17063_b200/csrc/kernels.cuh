@@ -229,30 +229,33 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
 // ---------------------------------------------------------------------------
 // k_xf: one transform job per CTA (512 threads, 64 KiB smem tile), throughput path
 // ---------------------------------------------------------------------------
-template <int DIR, int LD, int EP>
-__global__ void __launch_bounds__(NT, 1) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
+template <int DIR, int LD, int EP, int VT = 1>
+__global__ void __launch_bounds__(NT / VT, VT) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
     extern __shared__ u64 sm[];
     const XJob J = jobs[blockIdx.x];
-    const int t = threadIdx.x;
     const PrimeC& P = C.pc[J.k];
     TRACE(0);
-    {
-        u64 x[EPT];  // coefficients t + 1024 v
+    HC_NOUNROLL
+    for (int v = 0; v < VT; v++) {
+        const int t = threadIdx.x + v * (NT / VT);
+        u64 x[EPT];  // coefficients t + 1024 e
         load_n<LD, EPT>(C, J, P, t, NT, x);
         HC_UNROLL
-        for (int v = 0; v < EPT; v++) sm[swz(t + NT * v)] = x[v];
+        for (int e = 0; e < EPT; e++) sm[swz(t + NT * e)] = x[e];
     }
     __syncthreads();
     TRACE(1);
     // forward outputs that only feed Montgomery products stay lazy (< 2^60)
     constexpr bool lazy = EP == EP_KSACC || EP == EP_STORE_LAZY;
-    if (DIR == 0) cta_ntt_fwd<lazy>(C.twf + (size_t)J.k * NPOLY, P, sm);
-    else cta_ntt_inv(C.twi + (size_t)J.k * NPOLY, P, sm);
+    if (DIR == 0) cta_ntt_fwd<lazy, VT>(C.twf + (size_t)J.k * NPOLY, P, sm);
+    else cta_ntt_inv<VT>(C.twi + (size_t)J.k * NPOLY, P, sm);
     TRACE(4);
-    {
+    HC_NOUNROLL
+    for (int v = 0; v < VT; v++) {
+        const int t = threadIdx.x + v * (NT / VT);
         u64 x[EPT];
         HC_UNROLL
-        for (int v = 0; v < EPT; v++) x[v] = sm[swz(t + NT * v)];
+        for (int e = 0; e < EPT; e++) x[e] = sm[swz(t + NT * e)];
         store_n<EP, EPT>(C, J, P, t, NT, x);
     }
     TRACE(5);

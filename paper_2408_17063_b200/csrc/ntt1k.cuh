@@ -46,39 +46,53 @@ HD void t_store(const u64 (&x)[EPT], u64* sm, const CPass& I) {
 }
 
 #if defined(__CUDACC__)
-template <bool LAZY = false>
+// VT virtual threads per thread: a CTA of NT / VT threads runs the 1024-thread
+// schedule, each thread taking threads t and t + NT / VT in turn within every
+// pass (their coefficients are disjoint, so no extra synchronisation).  VT = 2
+// puts two independent transforms (CTAs, barriers) on each SM.
+template <bool LAZY = false, int VT = 1>
 __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* sm) {
-    const int t = threadIdx.x;
     const TwG tg{tw};
     u64 x[EPT];
     HC_UNROLL
     for (int p = 0; p < 4; p++) {
-        const CPass I = pass1k(p, t);
-        t_load(x, sm, I);
-        r8_ct(x, tg, I.s0, I.G, P.q, 2 * P.q2);
-        if (p == 3) c_st12<LAZY>(0, t, x, tg, P.q, 2 * P.q2, P.one_s);
-        t_store(x, sm, I);
+        HC_NOUNROLL
+        for (int v = 0; v < VT; v++) {
+            const int t = threadIdx.x + v * (NT / VT);
+            const CPass I = pass1k(p, t);
+            t_load(x, sm, I);
+            r8_ct(x, tg, I.s0, I.G, P.q, 2 * P.q2);
+            if (p == 3) c_st12<LAZY>(0, t, x, tg, P.q, 2 * P.q2, P.one_s);
+            t_store(x, sm, I);
+        }
         __syncthreads();
     }
 }
 
+template <int VT = 1>
 __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* sm) {
-    const int t = threadIdx.x;
     const TwG tg{tw};
     u64 x[EPT];
     HC_UNROLL
     for (int p = 0; p < 3; p++) {
-        const CPass I = pass1k(3 - p, t);
-        t_load(x, sm, I);
-        if (p == 0) c_st0(0, t, x, tg, P.q, P.q2);
-        r8_gs(x, tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
-        t_store(x, sm, I);
+        HC_NOUNROLL
+        for (int v = 0; v < VT; v++) {
+            const int t = threadIdx.x + v * (NT / VT);
+            const CPass I = pass1k(3 - p, t);
+            t_load(x, sm, I);
+            if (p == 0) c_st0(0, t, x, tg, P.q, P.q2);
+            r8_gs(x, tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
+            t_store(x, sm, I);
+        }
         __syncthreads();
     }
-    const CPass I = pass1k(0, t);
-    t_load(x, sm, I);
-    c_phaseA_inv(x, tw, P);  // bits 10..12 (element v*1024 + t), n^-1 folded
-    t_store(x, sm, I);
+    HC_NOUNROLL
+    for (int v = 0; v < VT; v++) {
+        const CPass I = pass1k(0, threadIdx.x + v * (NT / VT));
+        t_load(x, sm, I);
+        c_phaseA_inv(x, tw, P);  // bits 10..12 (element v*1024 + t), n^-1 folded
+        t_store(x, sm, I);
+    }
     __syncthreads();
 }
 #endif

@@ -10,6 +10,7 @@ from paper_2408_17063_b200 import _lib
 
 args = [a for a in sys.argv[1:] if ":" in a]
 cbs = [int(x) for x in sys.argv[sys.argv.index("--cb") + 1].split(",")] if "--cb" in sys.argv else [0]
+vts = [int(x) for x in sys.argv[sys.argv.index("--vt2") + 1].split(",")] if "--vt2" in sys.argv else [0]
 lanes = [int(x) for x in sys.argv[sys.argv.index("--lanes") + 1].split(",")] if "--lanes" in sys.argv else [4]
 keys_cache = {}
 for pt in args:
@@ -26,8 +27,10 @@ for pt in args:
     qs = np.array(be.q, dtype=np.uint64).reshape(1, 1, 4, 1)
     cd = (rng.integers(0, 2**63, (C, 2, 4, 8192), dtype=np.uint64) % qs).astype(np.uint64)
     cv = (rng.integers(0, 2**63, (C, 2, 4, 8192), dtype=np.uint64) % qs).astype(np.uint64)
-    for ln, cb in [(a, b) for a in lanes for b in cbs]:
+    for ln, cb, vt in [(a, b, c) for a in lanes for b in cbs for c in vts]:
         _lib.lib().hc_set_lane_blocks(ln)
+        if vt:
+            _lib.lib().hc_set_vt2_jobs(vt)
         be._planned = None  # force a re-plan with this setting
         dc = P.DeviceComp(be, params, keys, chunk_blocks=cb)
         dc.set_inputs(cd, cv)
@@ -55,5 +58,5 @@ for pt in args:
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / iters
-        print(f"N={N:8d} s={s:4d} cb={cb:3d} lanes<={ln:5d} blocks={params.num_blocks:5d}  {ms:9.3f} ms  {N/ms/1e3:8.1f} M entries/s", flush=True)
+        print(f"N={N:8d} s={s:4d} cb={cb:3d} vt2>={vt:10d} lanes<={ln:5d} blocks={params.num_blocks:5d}  {ms:9.3f} ms  {N/ms/1e3:8.1f} M entries/s", flush=True)
 _lib.lib().hc_set_lane_blocks(4)
