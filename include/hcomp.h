@@ -140,8 +140,8 @@ int hc_set_cluster_threshold(int max_jobs);
  * parallel per-block lanes (latency regime); larger chunks use one wide launch
  * per segment (throughput regime). Applies to plans built afterwards. */
 int hc_set_lane_blocks(int max_blocks);
-/* Tuning: single-CTA transform launches of >= jobs use the 512-thread
- * two-per-SM variant.  Applies to schedules built afterwards. */
+/* Tuning: single-CTA transform launches of >= jobs (default 200) use the
+ * 256-thread three-per-SM variant.  Applies to schedules built afterwards. */
 int hc_set_vt2_jobs(int jobs);
 /* Diagnostics: co-resident 8-CTA transform clusters on this device. */
 int hc_max_active_clusters(hc_ctx* h, int* clusters);

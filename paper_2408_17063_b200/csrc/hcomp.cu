@@ -61,7 +61,7 @@ struct DevKey {
 static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters
 static int g_cl_chunk = CL_MAX;  // jobs per cluster launch: co-resident 8-CTA clusters (<= CL_MAX)
 static int g_lane_max_blocks = 4;  // chunks up to this many blocks run the baby segment as lanes
-static int g_vt2_jobs = 200;       // single-CTA launches of >= this many jobs: two 512-thread transforms per SM
+static int g_vt2_jobs = 200;       // single-CTA launches of >= this many jobs: three 256-thread transforms per SM
 static const int CL_SPREAD_SMEM = 120 * 1024;
 
 enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET, ST_I2 };
@@ -168,7 +168,7 @@ static int configure_kernels() {
     // small CTAs onto one or two SMs and nothing is gained
 #define XF_CFG(D, L, E)                                                                                    \
     CU(cudaFuncSetAttribute(k_xf<D, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));      \
-    CU(cudaFuncSetAttribute(k_xf<D, L, E, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));   \
+    CU(cudaFuncSetAttribute(k_xf<D, L, E, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));   \
     CU(cudaFuncSetAttribute(k_xf_cl<D, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
     XF_COMBOS(XF_CFG)
 #undef XF_CFG
@@ -415,7 +415,7 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
     if (!done && j0.dir == D && j0.ld == L && j0.ep == E) {                                              \
         if (clu) k_xf_cl<D, L, E><<<st.njobs * CL, CNT, CL_SPREAD_SMEM, s>>>(h->hctx, cj);              \
         else if (st.njobs >= g_vt2_jobs)                                                                 \
-            k_xf<D, L, E, 2><<<st.njobs, NT / 2, NPOLY * 8, s>>>(h->hctx, (const XJob*)st.djobs);         \
+            k_xf<D, L, E, 4><<<st.njobs, NT / 4, NPOLY * 8, s>>>(h->hctx, (const XJob*)st.djobs);         \
         else k_xf<D, L, E><<<st.njobs, NT, NPOLY * 8, s>>>(h->hctx, (const XJob*)st.djobs);              \
         done = true;                                                                                     \
     }

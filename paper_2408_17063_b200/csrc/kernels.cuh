@@ -229,8 +229,11 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
 // ---------------------------------------------------------------------------
 // k_xf: one transform job per CTA (512 threads, 64 KiB smem tile), throughput path
 // ---------------------------------------------------------------------------
+// VT = 1: one 1024-thread transform per SM (latency); VT = 4: 256-thread CTAs,
+// three per SM (64 KiB smem each), whose independent barriers keep the IMAD
+// pipe busy while other transforms load, store or synchronise (throughput).
 template <int DIR, int LD, int EP, int VT = 1>
-__global__ void __launch_bounds__(NT / VT, VT) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(NT / VT, VT == 4 ? 3 : VT) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
     extern __shared__ u64 sm[];
     const XJob J = jobs[blockIdx.x];
     const PrimeC& P = C.pc[J.k];

@@ -47,9 +47,9 @@ HD void t_store(const u64 (&x)[EPT], u64* sm, const CPass& I) {
 
 #if defined(__CUDACC__)
 // VT virtual threads per thread: a CTA of NT / VT threads runs the 1024-thread
-// schedule, each thread taking threads t and t + NT / VT in turn within every
-// pass (their coefficients are disjoint, so no extra synchronisation).  VT = 2
-// puts two independent transforms (CTAs, barriers) on each SM.
+// schedule, each thread taking threads t, t + NT / VT, ... in turn within every
+// pass (their coefficients are disjoint, so no extra synchronisation).  VT = 4
+// puts three independent transforms (CTAs, barriers) on each SM.
 template <bool LAZY = false, int VT = 1>
 __device__ __forceinline__ void cta_ntt_fwd(const Tw* tw, const PrimeC& P, u64* sm) {
     const TwG tg{tw};

@@ -1,5 +1,5 @@
-"""Single-CTA transform throughput: 1024-thread (one per SM) vs 512-thread
-two-per-SM variant (hc_set_vt2_jobs)."""
+"""Single-CTA transform throughput: 1024-thread (one per SM) vs the 256-thread
+three-per-SM variant (hc_set_vt2_jobs)."""
 import os, sys, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2408_17063_b200 as P
