@@ -85,6 +85,10 @@ int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C)
  * `stream` (pinned host memory for a true async copy).  A rank running
  * blocks [b0, b1) needs ciphertexts [b0/2, (b1+1)/2). */
 int hc_comp_set_inputs_range(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int c0, int c1, void* stream);
+/* Streamed use: inputs already in device memory (e.g. uploaded on a copy
+ * stream while the previous query computes) -> the plan's input buffers,
+ * device to device, on `stream`. */
+int hc_comp_set_inputs_device(hc_ctx* h, const uint64_t* cd_dev, const uint64_t* cv_dev, int C, void* stream);
 int hc_comp_launch(hc_ctx* h, void* stream);
 int hc_comp_get_output(hc_ctx* h, uint64_t* out);
 /* Enqueue the device->host read of the output on `stream` (pinned `out`). */

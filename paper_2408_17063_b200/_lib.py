@@ -53,6 +53,7 @@ _SIGS = [
     ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),
     ("hc_comp_set_inputs", _I, [_P, _P, _P, _I]),
     ("hc_comp_set_inputs_range", _I, [_P, _P, _P, _I, _I, _P]),
+    ("hc_comp_set_inputs_device", _I, [_P, _P, _P, _I, _P]),
     ("hc_comp_launch", _I, [_P, _P]),
     ("hc_comp_get_output", _I, [_P, _P]),
     ("hc_comp_get_output_async", _I, [_P, _P, _P]),

@@ -1257,6 +1257,19 @@ extern "C" int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t*
     return HC_OK;
 }
 
+extern "C" int hc_comp_set_inputs_device(hc_ctx* h, const uint64_t* cd_dev, const uint64_t* cv_dev, int C,
+                                         void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    CU(cudaSetDevice(h->dev));
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    const size_t bytes = (size_t)C * 2 * 4 * NPOLY * 8;
+    CU(cudaMemcpyAsync(P.cd, cd_dev, bytes, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(P.cv, cv_dev, bytes, cudaMemcpyDeviceToDevice, s));
+    return HC_OK;
+}
+
 extern "C" int hc_comp_set_inputs_range(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int c0, int c1,
                                         void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
