@@ -37,7 +37,13 @@ def shard_blocks(B: int, world: int, rank: int) -> tuple[int, int]:
 
 def reduce_partials(t, dist, group=None, root: int = 0):
     """Sum the ranks' partial accumulators on `root` (int64 view of uint64 words,
-    each < 2^54: the sum over <= 1023 ranks stays exact)."""
+    each < 2^54: the sum over <= 1023 ranks stays exact).  NCCL reduces device
+    tensors in place; a CPU backend (gloo) goes through a host copy."""
+    if t.is_cuda and dist.get_backend(group) != "nccl":
+        h = t.cpu()
+        dist.reduce(h, dst=root, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+        return t
     dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
     return t
 

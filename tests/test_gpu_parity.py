@@ -255,3 +255,53 @@ def test_missing_rotation_key_raises(c1, pkg):
     be, keys = c1["be"], c1["keys"]
     with pytest.raises(P.MissingRotationKey):
         be.rot_row(c1["cts"][0], 5, keys)
+
+
+def _sharded_worker(rank, world, port, q):
+    """One rank of a two-process sharded Comp on the same GPU (gloo for the
+    uint64 reduce: NCCL needs one GPU per rank)."""
+    import os
+
+    import torch.distributed as dist
+
+    import paper_2408_17063_b200 as P
+    from oracle import bgv_oracle as O
+    from paper_2408_17063_b200.dist import comp_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = load_golden("c2_N16384_s16")
+        n, p, N, s, seed = g["n"], g["p"], g["N"], g["s"], g["seed"]
+        be, params, keys, dense, cts, hint = make_case(P, O, n, p, N, s, seed, guard=not g["noise_guard_disabled"])
+        ans = comp_sharded(cts, params, be, keys, hint, dist)
+        if rank == 0:
+            q.put(O.sha256(ans.serialize(be)) == g["answer_sha256"] and ans.cts[0].payload.noise_bits == g["noise_bits"])
+        else:
+            q.put(ans is None)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_comp_two_processes_matches_reference_golden(pkg):
+    """SURVEY 8(e) end to end with real ranks: blocks [0,2) and [2,4) of the
+    headline Comp on two processes (hc_comp_partial + per-rank input upload),
+    uint64 SUM reduce, hc_comp_finish on rank 0 == the reference's answer."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=600)
+        assert pr.exitcode == 0
+    assert q.get(timeout=5) is True and q.get(timeout=5) is True
