@@ -163,7 +163,27 @@ int hc_galois_tables(int n, uint32_t galois_t, uint16_t* coef, uint16_t* perm);
 /* primitive 2n-th root used by the tables (bgv.py:120-126) */
 uint64_t hc_prim_root_2n(uint64_t q, int n);
 
+/* Host samplers on the reference's random.Random stream (keygen / encrypt,
+ * bgv.py:398-557; CPython's MT19937, Modules/_randommodule.c):
+ * hc_rng_create seeds like random.Random(seed) for an int seed, key = |seed|
+ * as little-endian 32-bit words (at least one).  Each call consumes exactly
+ * what the named Python expression consumes. */
+typedef struct hc_rng hc_rng;
+int hc_rng_create(const uint32_t* key, int len, hc_rng** out);
+void hc_rng_destroy(hc_rng* r);
+/* getrandbits(k) -> little-endian 32-bit words, ceil(k/32) of them */
+int hc_rng_getrandbits(hc_rng* r, int k, uint32_t* words);
+/* [randrange(3) - 1 for _ in range(n)] */
+int hc_rng_ternary(hc_rng* r, int n, int64_t* out);
+/* [getrandbits(k).bit_count() - getrandbits(k).bit_count() for _ in range(n)] */
+int hc_rng_cbd(hc_rng* r, int n, int k, int64_t* out);
+/* [randrange(Q) for _ in range(n)] as residues out[np][n] mod primes[np];
+ * Q = nw little-endian 32-bit words of bit length kbits */
+int hc_rng_uniform(hc_rng* r, int n, const uint32_t* q, int nw, int kbits, const uint64_t* primes, int np,
+                   uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif
+
 #endif

@@ -73,6 +73,12 @@ _SIGS = [
     ("hc_max_active_clusters", _I, [_P, _P]),
     ("hc_trace_reset", _I, []),
     ("hc_trace_read", _I, [_P]),
+    ("hc_rng_create", _I, [_P, _I, _P]),
+    ("hc_rng_destroy", None, [_P]),
+    ("hc_rng_getrandbits", _I, [_P, _I, _P]),
+    ("hc_rng_ternary", _I, [_P, _I, _P]),
+    ("hc_rng_cbd", _I, [_P, _I, _I, _P]),
+    ("hc_rng_uniform", _I, [_P, _I, _P, _I, _I, _P, _I, _P]),
     ("hc_galois_tables", _I, [_I, _U32, _P, _P]),
     ("hc_prim_root_2n", _U64, [_U64, _I]),
 ]

@@ -18,8 +18,8 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import os
 import math
-import random
 import struct
 from dataclasses import dataclass, field, replace
 
@@ -229,6 +229,58 @@ def slot_index(n: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 
+class HostRng:
+    """random.Random(seed) restated natively (csrc/pyrng.hpp, CPython's
+    MT19937): the reference backend's samplers (bgv.py:398-414) consume the
+    same stream, so keys and ciphertexts stay bit-identical, ~100x faster than
+    the Python loops."""
+
+    def __init__(self, seed):
+        if seed is None:  # random.Random(None): fresh entropy
+            seed = int.from_bytes(os.urandom(32), "little")
+        n = abs(int(seed))
+        words = []
+        while n:
+            words.append(n & 0xFFFFFFFF)
+            n >>= 32
+        key = np.array(words or [0], dtype=np.uint32)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().hc_rng_create(_lib.ptr(key), len(key), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().hc_rng_destroy(self._h)
+        except Exception:
+            pass
+
+    def getrandbits(self, k: int) -> int:
+        w = np.zeros(max(1, (k + 31) // 32), dtype=np.uint32)
+        _lib.check(_lib.lib().hc_rng_getrandbits(self._h, k, _lib.ptr(w)))
+        return int.from_bytes(w.tobytes(), "little")
+
+    def ternary(self, n: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.int64)
+        _lib.check(_lib.lib().hc_rng_ternary(self._h, n, _lib.ptr(out)))
+        return out
+
+    def cbd(self, n: int, k: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.int64)
+        _lib.check(_lib.lib().hc_rng_cbd(self._h, n, k, _lib.ptr(out)))
+        return out
+
+    def uniform(self, n: int, modulus: int, primes) -> np.ndarray:
+        """[randrange(modulus) for _ in range(n)] as residues [len(primes)][n]."""
+        kbits = modulus.bit_length()
+        nw = (kbits + 31) // 32
+        q = np.frombuffer(modulus.to_bytes(4 * nw, "little"), dtype=np.uint32).copy()
+        pr = np.ascontiguousarray(primes, dtype=np.uint64)
+        out = np.empty((len(pr), n), dtype=np.uint64)
+        _lib.check(_lib.lib().hc_rng_uniform(self._h, n, _lib.ptr(q), nw, kbits, _lib.ptr(pr), len(pr), _lib.ptr(out)))
+        return out
+
+
 class B200BgvBackend:
     """BGV evaluation session on a B200 (reference: BgvBackend, bgv.py:321)."""
 
@@ -253,7 +305,7 @@ class B200BgvBackend:
             raise ValueError("ksw_base_bits must be 16")
         self.params = params
         self.counters = OpCounters()
-        self._rng = random.Random(seed)
+        self._rng = HostRng(seed)
         self.w = ksw_base_bits
         self.noise_guard = noise_guard
         n, p = params.n, params.p
@@ -372,24 +424,13 @@ class B200BgvBackend:
     # -- sampling (bgv.py:398-414) ---------------------------------------------
 
     def _sample_ternary(self) -> list[int]:
-        rr = self._rng.randrange
-        return [rr(3) - 1 for _ in range(self.params.n)]
+        return [int(v) for v in self._rng.ternary(self.params.n)]
 
     def _sample_cbd(self) -> np.ndarray:
-        g = self._rng.getrandbits
-        k = CBD_HALF_WIDTH
-        out = np.empty(self.params.n, dtype=np.int64)
-        for i in range(self.params.n):
-            a = g(k).bit_count()
-            b = g(k).bit_count()
-            out[i] = a - b
-        return out
+        return self._rng.cbd(self.params.n, CBD_HALF_WIDTH)
 
     def _sample_uniform_ntt(self, level: int) -> np.ndarray:
-        modulus = self.moduli[level]
-        rr = self._rng.randrange
-        vals = [rr(modulus) for _ in range(self.params.n)]
-        return self.big_residues(vals, level)
+        return self._rng.uniform(self.params.n, self.moduli[level], self.q[: level + 1])
 
     # -- keys (bgv.py:464-520) ----------------------------------------------------
 
@@ -421,11 +462,11 @@ class B200BgvBackend:
         def make_ksk(target_res: np.ndarray) -> np.ndarray:
             target_ntt = self.ntt(target_res, L)
             ksk = np.empty((D, 2, L + 1, n), dtype=np.uint64)
-            for j in range(D):
-                a_j = self._sample_uniform_ntt(L)
-                e_j = self._sample_cbd()
-                ksk[j, 0] = self.ntt(self.small_residues(p * e_j, L), L)  # p*e_j, finished below
-                ksk[j, 1] = a_j
+            pe = np.empty((D, L + 1, n), dtype=np.uint64)
+            for j in range(D):  # the reference's sampling order: a_j then e_j
+                ksk[j, 1] = self._sample_uniform_ntt(L)
+                pe[j] = self.small_residues(p * self._sample_cbd(), L)
+            ksk[:, 0] = self.ntt(pe, L)  # p*e_j in one batched transform, finished below
             # b_j = p e_j - a_j s + 2^(16 j) t  (bgv.py:488-493), batched on the GPU
             shifts = np.array(
                 [[pow(2, self.w * j, int(q)) for q in self.q] for j in range(D)], dtype=np.uint64

@@ -17,6 +17,7 @@
 
 #include "../../include/hcomp.h"
 #include "kernels.cuh"
+#include "pyrng.hpp"
 #include "host_tables.hpp"
 
 using namespace hc;
@@ -1730,4 +1731,65 @@ extern "C" void hc_ctx_destroy(hc_ctx* h) {
     }
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     delete h;
+}
+
+// ---------------------------------------------------------------------------
+// Host sampling with the reference's random.Random stream (pyrng.hpp):
+// keygen / encrypt (bgv.py:398-557) run their samplers natively, consuming
+// exactly the values the reference would.
+// ---------------------------------------------------------------------------
+struct hc_rng {
+    PyMT mt;
+};
+
+extern "C" int hc_rng_create(const uint32_t* key, int len, hc_rng** out) {
+    if (!key || len < 1 || !out) return fail(HC_ERR_ARG, "bad seed words");
+    hc_rng* r = new hc_rng();
+    r->mt.init_by_array(key, len);
+    *out = r;
+    return HC_OK;
+}
+
+extern "C" void hc_rng_destroy(hc_rng* r) { delete r; }
+
+extern "C" int hc_rng_getrandbits(hc_rng* r, int k, uint32_t* words) {
+    if (!r || k < 0 || !words) return fail(HC_ERR_ARG, "bad arguments");
+    r->mt.getrandbits(k, words);
+    return HC_OK;
+}
+
+// [randrange(3) - 1 for _ in range(n)]  (bgv.py _sample_ternary)
+extern "C" int hc_rng_ternary(hc_rng* r, int n, int64_t* out) {
+    if (!r || n < 0 || !out) return fail(HC_ERR_ARG, "bad arguments");
+    for (int i = 0; i < n; i++) out[i] = (int64_t)r->mt.randbelow32(3) - 1;
+    return HC_OK;
+}
+
+// getrandbits(k).bit_count() - getrandbits(k).bit_count()  (centered binomial)
+extern "C" int hc_rng_cbd(hc_rng* r, int n, int k, int64_t* out) {
+    if (!r || n < 0 || k < 1 || k > 32 || !out) return fail(HC_ERR_ARG, "bad arguments");
+    for (int i = 0; i < n; i++) {
+        uint32_t a, b;
+        r->mt.getrandbits(k, &a);
+        r->mt.getrandbits(k, &b);
+        out[i] = (int64_t)__builtin_popcount(a) - (int64_t)__builtin_popcount(b);
+    }
+    return HC_OK;
+}
+
+// [randrange(Q) for _ in range(n)] reduced mod each prime: out[np][n]
+extern "C" int hc_rng_uniform(hc_rng* r, int n, const uint32_t* q, int nw, int kbits, const uint64_t* primes, int np,
+                              uint64_t* out) {
+    if (!r || n < 0 || !q || nw < 1 || nw > 16 || kbits < 1 || kbits > 32 * nw || !primes || np < 1 || !out)
+        return fail(HC_ERR_ARG, "bad arguments");
+    uint32_t w[16];
+    for (int i = 0; i < n; i++) {
+        r->mt.randbelow_words(q, nw, kbits, w);
+        for (int k = 0; k < np; k++) {
+            unsigned __int128 acc = 0;
+            for (int j = nw - 1; j >= 0; j--) acc = ((acc << 32) | w[j]) % primes[k];
+            out[(size_t)k * n + i] = (uint64_t)acc;
+        }
+    }
+    return HC_OK;
 }

@@ -180,3 +180,33 @@ def test_bench_helpers():
     assert bench.pick_p(1 << 17, 0) == 786433
     assert bench.pick_p(1 << 20, 0) == 1097729
     assert bench.pick_p(1 << 22, 0) == 4423681
+
+
+@pytest.mark.parametrize("seed", [0, 1, 7, 2**32 - 1, 2**32, 12345678901234567890, -5])
+def test_host_rng_reproduces_python_random(seed):
+    """HostRng (csrc/pyrng.hpp) consumes random.Random(seed)'s stream exactly:
+    interleaved getrandbits of every width class, randrange(3), the CBD
+    sampler and randrange of a 216-bit modulus (the samplers of bgv.py:398-414)."""
+    import random
+
+    from paper_2408_17063_b200.backend import HostRng
+
+    py = random.Random(seed)
+    hr = HostRng(seed)
+    for k in (1, 2, 5, 21, 31, 32, 33, 63, 64, 65, 128, 216):
+        assert hr.getrandbits(k) == py.getrandbits(k), k
+    assert list(hr.ternary(1000)) == [py.randrange(3) - 1 for _ in range(1000)]
+    want = []
+    for _ in range(500):
+        a = py.getrandbits(21).bit_count()
+        b = py.getrandbits(21).bit_count()
+        want.append(a - b)
+    assert list(hr.cbd(500, 21)) == want
+    primes = P.find_chain_primes(8192, 65537, 4)[::-1]  # ascending = level order
+    Q = 1
+    for q in primes:
+        Q *= q
+    got = hr.uniform(300, Q, primes)
+    vals = [py.randrange(Q) for _ in range(300)]
+    assert np.array_equal(got, np.array([[v % q for v in vals] for q in primes], dtype=np.uint64))
+    assert hr.getrandbits(128) == py.getrandbits(128)  # still in lockstep
