@@ -138,9 +138,7 @@ static void release_key(DevKey& k) {
     X(0, LD_DIG, EP_STORE_LAZY)       \
     X(0, LD_DIGGAL, EP_STORE_LAZY)    \
     X(0, LD_RED, EP_ADDRED)           \
-    X(1, LD_RED, EP_ADDRED)           \
     X(0, LD_DIGGAL, EP_KSACC)         \
-    X(1, LD_KSFIN, EP_STORE)          \
     X(1, LD_KSFIN, EP_RESCALE)
 
 static int kernels_configured = 0;
