@@ -698,6 +698,7 @@ __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C,
 // ---------------------------------------------------------------------------
 struct DXJob {
     int nterm, level;       // level: of the dropped prime behind the (r, d) slots
+    int trace, pad;         // HC_TRACE builds: launch sequence number
     const u64* const* src;  // nterm pointers, each [>=nprime][n]
     const u64* const* dg;   // nterm pointers, each [>=nprime][n]
     const u64* const* es;   // nterm (r, d) slots [2][n] int64 (EP_RESCALE_RD), or null
@@ -710,6 +711,7 @@ struct DXJob {
 constexpr int DXB = 4;
 __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
     const DXJob& J = jobs[blockIdx.z];
+    TRACE(0);
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const u64 q0 = C.pc[0].q, q1 = C.pc[1].q;
     u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
@@ -745,6 +747,7 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
                 }
             }
     }
+    TRACE(1);
     J.X[j] = add_mod(J.X[j], redc(h0, l0, q0, C.pc[0].qneg), q0);
     J.X[NPOLY + j] = add_mod(J.X[NPOLY + j], redc(h1, l1, q1, C.pc[1].qneg), q1);
     if (es) {
@@ -752,6 +755,8 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
         J.E[j] = add_mod(J.E[j], corr_from_sums(sr, sd, q0, LV.qinv[0], LV.qinv_s[0], C.pc[0].one_s), q0);
         J.E[NPOLY + j] = add_mod(J.E[NPOLY + j], corr_from_sums(sr, sd, q1, LV.qinv[1], LV.qinv_s[1], C.pc[1].one_s), q1);
     }
+    TRACE(4);
+    TRACE(5);
 }
 
 // ---------------------------------------------------------------------------
