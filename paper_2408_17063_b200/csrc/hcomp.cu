@@ -91,6 +91,7 @@ struct Schedule {
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
     int cur_group = 0, next_group = 1, cur_lane = -1;
+    bool cl_in_lane = false;  // allow cluster launches inside a lane
     // steps added between par_begin() and par_end() are independent: they are
     // captured on forked streams (parallel graph branches)
     void par_begin() { cur_group = next_group++; }
@@ -306,7 +307,7 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
         }
         // clusters only for small batches outside parallel lanes (lanes
         // already fill the GPU; single-CTA transforms are more efficient there)
-        const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS && S.cur_lane < 0;
+        const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS && (S.cur_lane < 0 || S.cl_in_lane);
         const size_t chunk = clu ? (size_t)g_cl_chunk : sel.size();
         const int saved = S.cur_group;
         if (clu && sel.size() > chunk && !S.cur_group) S.par_begin();
@@ -960,9 +961,26 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     }
         }
         rc = add_xf(S, s1); if (rc) return rc;
+        // S2 (P and R.c0 at level 2) is independent of S2c -> S3 (R.c1's
+        // digits and their NTTs): at small chunks (latency regime) they run as
+        // two graph branches joined before S4; wide chunks fill the GPU anyway
+        const bool fork23 = cb <= g_lane_max_blocks;
+        if (fork23) {
+            S.par_begin();
+            S.cur_lane = 0;
+            S.cl_in_lane = true;
+        }
         rc = add_xf(S, s2); if (rc) return rc;
+        if (fork23) {
+            S.cl_in_lane = false;
+            S.cur_lane = 1;
+        }
         rc = add_co(S, s2c); if (rc) return rc;
         rc = add_xf(S, s3); if (rc) return rc;
+        if (fork23) {
+            S.cur_lane = -1;
+            S.par_end();
+        }
         rc = add_ma(S, s4, 3); if (rc) return rc;
         rc = add_xf(S, s5); if (rc) return rc;
         rc = add_co(S, s6); if (rc) return rc;
