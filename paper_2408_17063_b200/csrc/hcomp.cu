@@ -65,6 +65,34 @@ static int g_cl_chunk = CL_MAX;  // jobs per cluster launch: co-resident 8-CTA c
 static int g_lane_max_blocks = 4;  // chunks up to this many blocks run the baby segment as lanes
 static int g_vt2_jobs = 200;       // single-CTA launches of >= this many jobs: three 256-thread transforms per SM
 static const int CL_SPREAD_SMEM = 120 * 1024;
+// schedule kernels launch with programmatic stream serialization (PDL): each
+// starts while its predecessor drains and blocks in pdl_wait() (kernels.cuh)
+// before touching the predecessor's data.  HC_PDL=0 disables it (A/B timing).
+static int g_pdl = -1;
+static bool pdl_on() {
+    if (g_pdl < 0) {
+        const char* e = getenv("HC_PDL");
+        g_pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_pdl == 1;
+}
+// PDL only on the main chain: inside parallel branches (lanes) an early-launched
+// kernel would hold SMs idle that the other branches need
+static thread_local bool g_step_pdl = true;
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl_on() && g_step_pdl) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
 
 enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET, ST_I2 };
 struct Step {
@@ -80,6 +108,7 @@ struct Step {
     size_t bytes = 0;
     std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
     std::vector<Intt2Job> i2jobs;  // ST_I2
+    std::vector<XJob> side;        // ST_XF cluster launch: ClJobs.side (res_f.c0 finish of a fold)
     int group = 0;            // consecutive steps with the same nonzero group run concurrently
     int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
     int lane = -1;            // in a group: steps of one lane run in order on one branch
@@ -398,13 +427,14 @@ static void add_memset(Schedule& S, void* p, size_t bytes) {
 }
 
 static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
+    g_step_pdl = st.group == 0;
     {
         switch (st.kind) {
             case ST_XF: {
                 const XJob& j0 = st.hjobs[0];
                 if (j0.noxf) {
                     if (j0.ld != LD_KSFIN) return fail(HC_ERR_STATE, "transform-less job needs LD_KSFIN");
-                    k_elem<LD_KSFIN><<<dim3(NPOLY / 256, st.njobs), 128, 0, s>>>(h->hctx, (const XJob*)st.djobs);
+                    CU(launch(k_elem<LD_KSFIN>, dim3(NPOLY / 256, st.njobs), 128, 0, s, h->hctx, (const XJob*)st.djobs));
                     break;
                 }
                 const bool clu = st.cl && st.njobs <= CL_MAX;  // latency path: one 8-CTA cluster per transform
@@ -412,14 +442,21 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 if (clu) {
                     memset(&cj, 0, sizeof cj);
                     memcpy(cj.j, st.hjobs.data(), st.njobs * sizeof(XJob));
+                    if (!st.side.empty()) {
+                        if (st.njobs < 8 || st.side.size() != 2 || j0.ep != EP_KSACC)
+                            return fail(HC_ERR_STATE, "side finish needs a KSACC cluster launch of >= 8 jobs");
+                        cj.nside = 2;
+                        cj.side[0] = st.side[0];
+                        cj.side[1] = st.side[1];
+                    }
                 }
                 bool done = false;
 #define XF_LAUNCH(D, L, E)                                                                               \
     if (!done && j0.dir == D && j0.ld == L && j0.ep == E) {                                              \
-        if (clu) k_xf_cl<D, L, E><<<st.njobs * CL, CNT, CL_SPREAD_SMEM, s>>>(h->hctx, cj);              \
+        if (clu) CU(launch(k_xf_cl<D, L, E>, st.njobs * CL, CNT, CL_SPREAD_SMEM, s, h->hctx, cj));       \
         else if (st.njobs >= g_vt2_jobs)                                                                 \
-            k_xf<D, L, E, 4><<<st.njobs, NT / 4, NPOLY * 8, s>>>(h->hctx, (const XJob*)st.djobs);         \
-        else k_xf<D, L, E><<<st.njobs, NT, NPOLY * 8, s>>>(h->hctx, (const XJob*)st.djobs);              \
+            CU(launch(k_xf<D, L, E, 4>, st.njobs, NT / 4, NPOLY * 8, s, h->hctx, (const XJob*)st.djobs)); \
+        else CU(launch(k_xf<D, L, E>, st.njobs, NT, NPOLY * 8, s, h->hctx, (const XJob*)st.djobs));       \
         done = true;                                                                                     \
     }
                 XF_COMBOS(XF_LAUNCH)
@@ -428,19 +465,19 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 break;
             }
             case ST_CO:
-                k_compose<<<dim3(NPOLY / 256, st.njobs), 256, 0, s>>>(h->hctx, (const CJob*)st.djobs);
+                CU(launch(k_compose, dim3(NPOLY / 256, st.njobs), 256, 0, s, h->hctx, (const CJob*)st.djobs));
                 break;
             case ST_MA:
                 if (st.njobs > 16)  // throughput: occupancy
-                    k_ksmac<1><<<dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
+                    CU(launch(k_ksmac<1>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
                 else  // small: fewer CTAs beside the transforms
-                    k_ksmac<2><<<dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s>>>(h->hctx, (const MJob*)st.djobs);
+                    CU(launch(k_ksmac<2>, dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
                 break;
             case ST_DX:
-                k_diagx<<<dim3(NPOLY / 256, 1, st.njobs), 256, 0, s>>>(h->hctx, (const DXJob*)st.djobs);
+                CU(launch(k_diagx, dim3(NPOLY / 256, 1, st.njobs), 256, 0, s, h->hctx, (const DXJob*)st.djobs));
                 break;
             case ST_SUMC:
-                k_sum_copies<<<592, 256, 0, s>>>(h->hctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride);
+                CU(launch(k_sum_copies, 592, 256, 0, s, h->hctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride));
                 break;
             case ST_MEMSET:
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
@@ -451,9 +488,9 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 memcpy(jj.j, st.i2jobs.data(), st.i2jobs.size() * sizeof(Intt2Job));
                 const int n = (int)st.i2jobs.size();
                 if (st.i2jobs[0].j[0].ld == LD_KSFIN)
-                    k_cl_intt2<LD_KSFIN><<<n * CL, 2 * CNT, CL_SPREAD_SMEM, s>>>(h->hctx, jj);
+                    CU(launch(k_cl_intt2<LD_KSFIN>, n * CL, 2 * CNT, CL_SPREAD_SMEM, s, h->hctx, jj));
                 else
-                    k_cl_intt2<LD_RED><<<n * CL, 2 * CNT, CL_SPREAD_SMEM, s>>>(h->hctx, jj);
+                    CU(launch(k_cl_intt2<LD_RED>, n * CL, 2 * CNT, CL_SPREAD_SMEM, s, h->hctx, jj));
                 break;
             }
         }
@@ -711,7 +748,7 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
     PA(P->dnttF, (size_t)P->D1 * 2 * NB);
     PA(P->corr, (size_t)2 * NB);
     PA(P->OUT, (size_t)2 * NB);
-    PA(P->ACC, (size_t)2 * 2 * NB);
+    PA(P->ACC, (size_t)2 * 2 * 2 * NB);  // two [poly][prime][n] buffers (folds alternate)
 #undef PA
 
     // ---- plaintexts on device (K6) ----
@@ -1100,7 +1137,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     const u64* X = P.PX + (size_t)G * 2 * 2 * NB;
     auto ex = [&](const u64* base, int g, int poly, int k) { return base + (((size_t)g * 2 + poly) * 2 + k) * NB; };
     int rc;
-    add_memset(S, P.ACC, (size_t)2 * 2 * NB * 8);
+    add_memset(S, P.ACC, (size_t)2 * 2 * 2 * NB * 8);
     // T1 (acc[g] c0 transforms; c1 of g >= 1 inverted on both primes with the
     // CRT digit split fused: k_cl_intt2)
     std::vector<XJob> t1;
@@ -1137,7 +1174,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     // each other down (measured: 14.6 + 8.0 us in parallel vs 5.0 + 7.4)
     rc = add_xf(S, t1); if (rc) return rc;
     rc = add_i2(S, t1i); if (rc) return rc;
-    auto digit_jobs = [&](std::vector<XJob>& out, const uint16_t* dig, const DevKey* key) {
+    auto digit_jobs = [&](std::vector<XJob>& out, const uint16_t* dig, const DevKey* key, u64* acc) {
         for (int d = 0; d < D1; d++)
             for (int k = 0; k < 2; k++) {
                 XJob j{};
@@ -1147,7 +1184,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
                 j.gal = key->gal;
                 j.ea = key->key + ((size_t)(d * 2 + 0) * 4 + k) * NB;  // b_d at prime k
                 j.eb = key->key + ((size_t)(d * 2 + 1) * 4 + k) * NB;  // a_d at prime k
-                j.out = P.ACC + (size_t)k * NB;                         // c0 row; c1 row at +2n
+                j.out = acc + (size_t)k * NB;                           // c0 row; c1 row at +2n
                 j.ostride = 2 * NB;
                 out.push_back(j);
             }
@@ -1168,7 +1205,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     for (int g = 1; g < G; g++) {
         if (!P.acc_live[g]) continue;
         const DevKey* kg = need_key(h, P.t_giant[g]);
-        digit_jobs(t3, P.digG + (size_t)g * 2 * D1 * NB, kg);
+        digit_jobs(t3, P.digG + (size_t)g * 2 * D1 * NB, kg, P.ACC);
         if (s0.nterm == MAXTERM_KS) return fail(HC_ERR_ARG, "too many giant steps");
         KsTerm T{};
         T.c0src = P.A0 + (size_t)g * 2 * NB;
@@ -1182,7 +1219,11 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
         const DevKey* ka = need_key(h, P.t_fold[f]);
         const KsSpec* d0 = upload_spec(S, s0, &rc); if (rc) return rc;
         const KsSpec* d1 = upload_spec(S, s1, &rc); if (rc) return rc;
-        std::vector<XJob> f1, f3;
+        // the fold's digit products go to the other ACC buffer, so the res_f.c0
+        // finish (which reads and re-zeroes this fold's buffer) can ride in the
+        // digit-NTT launch; the chain is INTT2 -> digit NTTs, one stream
+        u64* acc_next = P.ACC + (size_t)((f + 1) % 2) * 2 * 2 * NB;
+        std::vector<XJob> f3, f1;
         Intt2Job ij{};
         for (int k = 0; k < 2; k++) {
             ij.j[k].dir = 1; ij.j[k].k = k; ij.j[k].ld = LD_KSFIN; ij.j[k].ep = EP_STORE;
@@ -1195,12 +1236,15 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
             f1.push_back(e);
         }
         ij.dig = P.digF;
-        digit_jobs(f3, P.digF, ka);
-        S.par_begin();  // res_f.c1 INTT (+ CRT digits) and the res_f.c0 finish are independent
+        digit_jobs(f3, P.digF, ka, acc_next);
         rc = add_i2(S, std::vector<Intt2Job>{ij}); if (rc) return rc;
-        rc = add_xf(S, f1); if (rc) return rc;
-        S.par_end();
+        const size_t n0 = S.steps.size();
         rc = add_xf(S, f3); if (rc) return rc;
+        if (S.steps[n0].cl && S.steps[n0].njobs >= 8) {
+            S.steps[n0].side = f1;
+        } else {  // no cluster launch to ride in: a separate transform-less launch
+            rc = add_xf(S, f1); if (rc) return rc;
+        }
         // res_{f+1} = res_f + rot(res_f, a)
         s0 = KsSpec{};
         s1 = KsSpec{};
@@ -1208,8 +1252,8 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
         s0.D = s1.D = D1;
         s0.ab = 0;
         s1.ab = 1;
-        s0.acc = P.ACC;
-        s1.acc = P.ACC + 2 * NB;
+        s0.acc = acc_next;
+        s1.acc = acc_next + 2 * NB;
         s0.base = cur;
         s1.base = cur + 2 * NB;
         s0.nterm = 1;

@@ -82,6 +82,28 @@ struct XJob {
     long long ostride;
 };
 
+// Programmatic dependent launch (schedule kernels outside parallel graph
+// branches are launched with cudaLaunchAttributeProgrammaticStreamSerialization):
+// a kernel may start while its predecessor still runs.  pdl_wait() blocks until
+// the predecessor grid has completed and its writes are visible, so it precedes
+// every global access to data another kernel of the Comp writes or reads (job
+// tables, key-switch specs, Galois tables, keys and twiddles are constant for
+// the plan's lifetime and are read before it).  Right after the wait the kernel
+// lets ITS successor launch: the successor's CTAs run their constant-operand
+// prologue on the SMs this kernel leaves free, and at most two kernels of a
+// chain are resident at once (no cascade of idle CTAs).  HC_PDL_LATE moves the
+// trigger to just before the epilogue instead (A/B builds).
+#ifndef HC_PDL_LATE
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {}
+#else
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+#endif
+
 #ifdef HC_TRACE
 constexpr int TR_LAUNCH = 128, TR_BLK = 512, TR_PT = 8;
 __device__ unsigned long long g_trace[TR_LAUNCH][TR_BLK][TR_PT];
@@ -106,30 +128,81 @@ __device__ unsigned long long g_trace[TR_LAUNCH][TR_BLK][TR_PT];
 // thread and issues every round of global loads for all N before any use.
 // ---------------------------------------------------------------------------
 
+// Loaders run in two phases around pdl_wait(): load_pre issues the loads of
+// operands that are constant for the plan's lifetime (Galois gather tables,
+// key-switch specs and their permutations, plaintext multipliers), so they
+// overlap the predecessor kernel's tail; load_post reads the data the
+// predecessor produced.
+template <int LD, int N>
+struct LdPre {};
 template <int N>
-__device__ __forceinline__ void ld_ksfin(const XJob& J, const PrimeC& P, int j0, int stride, u64 (&x)[N]) {
+struct LdPre<LD_DIGGAL, N> {
+    unsigned g[N];
+};
+template <int N>
+struct LdPre<LD_KSFIN, N> {
+    const u64* base;
+    u64* acc;
+    const u64* c0;  // term 0's c0src (null: none)
+    int nterm;
+    unsigned pe[N];  // term 0's permutation
+    u64 b[N];        // J.b multiplier (if J.b)
+};
+
+template <int N>
+__device__ __forceinline__ void ksfin_pre(const XJob& J, int j0, int stride, LdPre<LD_KSFIN, N>& pre) {
     const KsSpec& S = *J.ks;
+    pre.base = S.base;
+    pre.acc = S.acc;
+    pre.nterm = S.nterm;
+    pre.c0 = S.nterm > 0 ? S.t[0].c0src : nullptr;
+    if (pre.c0) {
+        const uint16_t* pm = S.t[0].perm;
+        HC_UNROLL
+        for (int e = 0; e < N; e++) pre.pe[e] = pm[j0 + e * stride];
+    }
+    if (J.b) {
+        HC_UNROLL
+        for (int e = 0; e < N; e++) pre.b[e] = J.b[j0 + e * stride];
+    }
+}
+
+// key-switch finish, loads (no stores: two finishes' loads can be in flight together)
+template <int N>
+struct KsLd {
+    u64 x[N], acc[N], c[N];
+};
+template <int N>
+__device__ __forceinline__ void ksfin_load(const XJob& J, const PrimeC& P, int j0, int stride,
+                                           const LdPre<LD_KSFIN, N>& pre, KsLd<N>& v) {
     const size_t kofs = (size_t)J.k * NPOLY;
-    u64 acc[N];
     HC_UNROLL
     for (int e = 0; e < N; e++) {
-        x[e] = S.base ? S.base[kofs + j0 + e * stride] : 0;
-        acc[e] = S.acc ? S.acc[kofs + j0 + e * stride] : 0;
+        v.x[e] = pre.base ? pre.base[kofs + j0 + e * stride] : 0;
+        v.acc[e] = pre.acc ? pre.acc[kofs + j0 + e * stride] : 0;
+        v.c[e] = pre.c0 ? pre.c0[kofs + pre.pe[e]] : 0;
     }
-    for (int t = 0; t < S.nterm; t++) {
-        const KsTerm T = S.t[t];
+    // further terms (the giant-step sum): permutation, then gather
+    for (int t = 1; t < pre.nterm; t++) {
+        const KsTerm T = J.ks->t[t];
         if (!T.c0src) continue;
         unsigned pe[N];
         HC_UNROLL
         for (int e = 0; e < N; e++) pe[e] = T.perm[j0 + e * stride];
         HC_UNROLL
-        for (int e = 0; e < N; e++) x[e] = add_mod(x[e], T.c0src[kofs + pe[e]], P.q);
+        for (int e = 0; e < N; e++) v.c[e] = add_mod(v.c[e], T.c0src[kofs + pe[e]], P.q);
     }
+}
+// v = base + sum_t c0src_t[perm_t] + red(acc); zero acc; aux store; [* b]
+template <int N>
+__device__ __forceinline__ void ksfin_finish(const XJob& J, const PrimeC& P, int j0, int stride,
+                                             const LdPre<LD_KSFIN, N>& pre, const KsLd<N>& v, u64 (&x)[N]) {
+    const size_t kofs = (size_t)J.k * NPOLY;
     HC_UNROLL
-    for (int e = 0; e < N; e++) x[e] = add_mod(x[e], red64(acc[e], P.q, P.one_s), P.q);
-    if (S.acc) {
+    for (int e = 0; e < N; e++) x[e] = add_mod(add_mod(v.x[e], v.c[e], P.q), red64(v.acc[e], P.q, P.one_s), P.q);
+    if (pre.acc) {
         HC_UNROLL
-        for (int e = 0; e < N; e++) S.acc[kofs + j0 + e * stride] = 0;
+        for (int e = 0; e < N; e++) pre.acc[kofs + j0 + e * stride] = 0;
     }
     if (J.aux) {
         HC_UNROLL
@@ -137,12 +210,23 @@ __device__ __forceinline__ void ld_ksfin(const XJob& J, const PrimeC& P, int j0,
     }
     if (J.b) {
         HC_UNROLL
-        for (int e = 0; e < N; e++) x[e] = mul_mont(x[e], J.b[j0 + e * stride], P.q, P.qneg);
+        for (int e = 0; e < N; e++) x[e] = mul_mont(x[e], pre.b[e], P.q, P.qneg);
     }
 }
 
 template <int LD, int N>
-__device__ __forceinline__ void load_n(const DevCtx& C, const XJob& J, const PrimeC& P, int j0, int stride, u64 (&x)[N]) {
+__device__ __forceinline__ void load_pre(const XJob& J, int j0, int stride, LdPre<LD, N>& pre) {
+    if constexpr (LD == LD_DIGGAL) {
+        HC_UNROLL
+        for (int e = 0; e < N; e++) pre.g[e] = J.gal[j0 + e * stride];
+    } else if constexpr (LD == LD_KSFIN) {
+        ksfin_pre<N>(J, j0, stride, pre);
+    }
+}
+
+template <int LD, int N>
+__device__ __forceinline__ void load_post(const DevCtx& C, const XJob& J, const PrimeC& P, int j0, int stride,
+                                          const LdPre<LD, N>& pre, u64 (&x)[N]) {
     if constexpr (LD == LD_MONT || LD == LD_ADD) {
         u64 b[N];
         HC_UNROLL
@@ -159,19 +243,25 @@ __device__ __forceinline__ void load_n(const DevCtx& C, const XJob& J, const Pri
         HC_UNROLL
         for (int e = 0; e < N; e++) x[e] = d[j0 + e * stride];
     } else if constexpr (LD == LD_DIGGAL) {
-        unsigned g[N];
-        HC_UNROLL
-        for (int e = 0; e < N; e++) g[e] = J.gal[j0 + e * stride];
         const uint16_t* dp = reinterpret_cast<const uint16_t*>(J.a);
         const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
         HC_UNROLL
-        for (int e = 0; e < N; e++) x[e] = ((g[e] >> 15) ? dn : dp)[g[e] & 0x7FFF];
+        for (int e = 0; e < N; e++) x[e] = ((pre.g[e] >> 15) ? dn : dp)[pre.g[e] & 0x7FFF];
     } else if constexpr (LD == LD_KSFIN) {
-        ld_ksfin<N>(J, P, j0, stride, x);
+        KsLd<N> v;
+        ksfin_load<N>(J, P, j0, stride, pre, v);
+        ksfin_finish<N>(J, P, j0, stride, pre, v, x);
     } else {  // LD_U64
         HC_UNROLL
         for (int e = 0; e < N; e++) x[e] = J.a[j0 + e * stride];
     }
+}
+
+template <int LD, int N>
+__device__ __forceinline__ void load_n(const DevCtx& C, const XJob& J, const PrimeC& P, int j0, int stride, u64 (&x)[N]) {
+    LdPre<LD, N> pre;
+    load_pre<LD, N>(J, j0, stride, pre);
+    load_post<LD, N>(C, J, P, j0, stride, pre, x);
 }
 
 template <int EP, int N>
@@ -238,13 +328,25 @@ __global__ void __launch_bounds__(NT / VT, VT == 4 ? 3 : VT) k_xf(const __grid_c
     const XJob J = jobs[blockIdx.x];
     const PrimeC& P = C.pc[J.k];
     TRACE(0);
-    HC_NOUNROLL
-    for (int v = 0; v < VT; v++) {
-        const int t = threadIdx.x + v * (NT / VT);
+    if constexpr (VT == 1) {
+        const int t = threadIdx.x;
         u64 x[EPT];  // coefficients t + 1024 e
-        load_n<LD, EPT>(C, J, P, t, NT, x);
+        LdPre<LD, EPT> pre;
+        load_pre<LD, EPT>(J, t, NT, pre);
+        pdl_wait();
+        load_post<LD, EPT>(C, J, P, t, NT, pre, x);
         HC_UNROLL
         for (int e = 0; e < EPT; e++) sm[swz(t + NT * e)] = x[e];
+    } else {
+        pdl_wait();
+        HC_NOUNROLL
+        for (int v = 0; v < VT; v++) {
+            const int t = threadIdx.x + v * (NT / VT);
+            u64 x[EPT];  // coefficients t + 1024 e
+            load_n<LD, EPT>(C, J, P, t, NT, x);
+            HC_UNROLL
+            for (int e = 0; e < EPT; e++) sm[swz(t + NT * e)] = x[e];
+        }
     }
     __syncthreads();
     TRACE(1);
@@ -253,6 +355,7 @@ __global__ void __launch_bounds__(NT / VT, VT == 4 ? 3 : VT) k_xf(const __grid_c
     if (DIR == 0) cta_ntt_fwd<lazy, VT>(C.twf + (size_t)J.k * NPOLY, P, sm);
     else cta_ntt_inv<VT>(C.twi + (size_t)J.k * NPOLY, P, sm);
     TRACE(4);
+    pdl_trigger();
     HC_NOUNROLL
     for (int v = 0; v < VT; v++) {
         const int t = threadIdx.x + v * (NT / VT);
@@ -272,8 +375,12 @@ template <int LD>
 __global__ void __launch_bounds__(128) k_elem(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
     const XJob J = jobs[blockIdx.y];
     const PrimeC& P = C.pc[J.k];
+    const int j0 = blockIdx.x * 256 + threadIdx.x;
+    LdPre<LD, 2> pre;
+    load_pre<LD, 2>(J, j0, 128, pre);
+    pdl_wait();
     u64 x[2];
-    load_n<LD, 2>(C, J, P, blockIdx.x * 256 + threadIdx.x, 128, x);
+    load_post<LD, 2>(C, J, P, j0, 128, pre, x);
 }
 
 // ---------------------------------------------------------------------------
@@ -292,6 +399,12 @@ __device__ __forceinline__ void cluster_wait() {
 constexpr int CL_MAX = 16;  // jobs per cluster launch (passed by value)
 struct ClJobs {
     XJob j[CL_MAX];
+    // optional transform-less key-switch finishes (LD_KSFIN, noxf; one per
+    // prime) spread over every thread of a forward KSACC launch of >= 8 jobs:
+    // a fold's res_f.c0 finish rides in the fold's digit-NTT launch instead of
+    // a parallel graph branch (the digit products go to the other ACC buffer)
+    int nside;
+    XJob side[2];
 };
 
 // prefetch this CTA's 1023-entry twiddle slice (TwL) into shared memory;
@@ -342,11 +455,58 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         HC_UNROLL
         for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);  // phase-A twiddles tbl[1..7]
         const int b = 128 * c + t;
-        load_n<LD, CEPT>(C, J, P, b, CTILE, x);
+        LdPre<LD, CEPT> lpre;
+        load_pre<LD, CEPT>(J, b, CTILE, lpre);
+        // key digits of the KSACC epilogue: constant, fetched before the wait
+        u64 ka[EP == EP_KSACC ? CEPT : 1], kb[EP == EP_KSACC ? CEPT : 1];
+        if constexpr (EP == EP_KSACC) {
+            HC_UNROLL
+            for (int v = 0; v < CEPT; v++) {
+                ka[v] = J.ea[c * CTILE + t + 128 * v];
+                kb[v] = J.eb[c * CTILE + t + 128 * v];
+            }
+        }
+        constexpr bool SIDE = EP == EP_KSACC;
+        const bool side = SIDE && jobs.nside;
+        const int gt = blockIdx.x * CNT + t, gT = gridDim.x * CNT;  // gT >= n (>= 8 jobs)
+        LdPre<LD_KSFIN, 1> sp[2];
+        KsLd<1> sv[2];
+        if constexpr (SIDE) {
+            if (side) {
+                HC_UNROLL
+                for (int i = 0; i < 2; i++) {
+                    const int e = gt + i * gT;
+                    if (e < 2 * NPOLY) ksfin_pre<1>(jobs.side[e >> 13], e & (NPOLY - 1), 0, sp[i]);
+                }
+            }
+        }
+        pdl_wait();
+        load_post<LD, CEPT>(C, J, P, b, CTILE, lpre, x);
+        if constexpr (SIDE) {
+            if (side) {
+                HC_UNROLL
+                for (int i = 0; i < 2; i++) {
+                    const int e = gt + i * gT;
+                    if (e < 2 * NPOLY) ksfin_load<1>(jobs.side[e >> 13], C.pc[jobs.side[e >> 13].k], e & (NPOLY - 1), 0, sp[i], sv[i]);
+                }
+            }
+        }
         TRACE(6);
         tw_commit(twsl, pre, t);
         TRACE(7);
         r8_ct(x, TwR{wa}, 0, 0, P.q, 2 * P.q2);
+        if constexpr (SIDE) {
+            if (side) {
+                HC_UNROLL
+                for (int i = 0; i < 2; i++) {
+                    const int e = gt + i * gT;
+                    if (e < 2 * NPOLY) {
+                        u64 y[1];
+                        ksfin_finish<1>(jobs.side[e >> 13], C.pc[jobs.side[e >> 13].k], e & (NPOLY - 1), 0, sp[i], sv[i], y);
+                    }
+                }
+            }
+        }
         TRACE(1);
         cluster_wait();
         TRACE(2);
@@ -368,15 +528,28 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
             __syncthreads();
         }
         TRACE(4);
+        pdl_trigger();
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) x[v] = tile[cswz(t + 128 * v)];
-        store_n<EP, CEPT>(C, J, P, c * CTILE + t, 128, x);
+        if constexpr (EP == EP_KSACC) {
+            HC_UNROLL
+            for (int v = 0; v < CEPT; v++) {
+                const int j = c * CTILE + t + 128 * v;
+                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + j), (unsigned long long)mul_mont(x[v], ka[v], P.q, P.qneg));
+                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + J.ostride + j), (unsigned long long)mul_mont(x[v], kb[v], P.q, P.qneg));
+            }
+        } else {
+            store_n<EP, CEPT>(C, J, P, c * CTILE + t, 128, x);
+        }
         TRACE(5);
     } else {
         const Tw* tw = C.twi + (size_t)J.k * NPOLY;
         TwPre pre;
         tw_issue(pre, tw, c, t);
-        load_n<LD, CEPT>(C, J, P, c * CTILE + t, 128, x);
+        LdPre<LD, CEPT> lpre;
+        load_pre<LD, CEPT>(J, c * CTILE + t, 128, lpre);
+        pdl_wait();
+        load_post<LD, CEPT>(C, J, P, c * CTILE + t, 128, lpre, x);
         tw_commit(twsl, pre, t);
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
@@ -395,6 +568,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         }
         // all-to-all: element (row c, column t + 128 v) -> CTA v, slot c*128 + t
         TRACE(4);
+        pdl_trigger();
         cluster_wait();
         TRACE(2);
         HC_UNROLL
@@ -457,7 +631,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     u64 x[CEPT];
     TwPre pre;
     tw_issue(pre, tw, c, t);
-    load_n<LD, CEPT>(C, J, P, c * CTILE + t, 128, x);
+    const int jl = c * CTILE + t;
+    LdPre<LD, CEPT> lpre;
+    load_pre<LD, CEPT>(J, jl, 128, lpre);
+    pdl_wait();
+    load_post<LD, CEPT>(C, J, P, jl, 128, lpre, x);
     tw_commit(twsl, pre, t);
     HC_UNROLL
     for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
@@ -476,6 +654,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
         }
     }
     TRACE(4);
+    pdl_trigger();
     cluster_wait();
     HC_UNROLL
     for (int v = 0; v < CEPT; v++) cl.map_shared_rank(recvb, v)[c * 128 + t] = x[v];
@@ -592,6 +771,7 @@ __device__ __forceinline__ void compose_one(const DevCtx& C, const CJob& J, int 
 __global__ void __launch_bounds__(256) k_compose(const __grid_constant__ DevCtx C, const CJob* __restrict__ jobs) {
     const CJob J = jobs[blockIdx.y];
     const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
     switch (J.level) {
         case 1: compose_one<1>(C, J, pos); break;
         case 2: compose_one<2>(C, J, pos); break;
@@ -630,6 +810,7 @@ template <int CPT>
 __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
     TRACE(0);
+    pdl_wait();
     const int k = blockIdx.y;
     const int j = CPT * (blockIdx.x * blockDim.x + threadIdx.x);
     const LevelC& LV = C.lv[J.level];
@@ -712,6 +893,7 @@ constexpr int DXB = 4;
 __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C, const DXJob* __restrict__ jobs) {
     const DXJob& J = jobs[blockIdx.z];
     TRACE(0);
+    pdl_wait();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const u64 q0 = C.pc[0].q, q1 = C.pc[1].q;
     u64 h0 = 0, l0 = 0, h1 = 0, l1 = 0;
@@ -853,6 +1035,7 @@ __global__ void k_to_mont(const __grid_constant__ DevCtx C, u64* data, long long
 // out[r][j] = sum_c red(in[c][r][j]) mod q_{r % period}
 __global__ void k_sum_copies(const __grid_constant__ DevCtx C, const u64* in, u64* out, long long rows,
                              int period, int copies, long long cstride) {
+    pdl_wait();
     const long long total = rows * NPOLY;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
