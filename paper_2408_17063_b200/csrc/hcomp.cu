@@ -426,8 +426,30 @@ static void add_memset(Schedule& S, void* p, size_t bytes) {
     S.steps.push_back(st);
 }
 
+// PDL for launches of about one wave or less (the latency path); a multi-wave
+// launch gains nothing from an early successor and measured slower with one
+// (its CTAs park on SMs the last wave could use): N=2^20 6.12 -> 6.40 ms.
+static int g_pdl_maxcta = -1;  // HC_PDL_MAXCTA: elementwise-launch CTA bound for PDL
+static bool step_one_wave(const Step& st) {
+    const int sms = 148;
+    if (g_pdl_maxcta < 0) {
+        const char* e = getenv("HC_PDL_MAXCTA");
+        g_pdl_maxcta = e ? atoi(e) : 0;  // measured: PDL on elementwise launches helps nowhere
+    }
+    switch (st.kind) {
+        case ST_XF:
+            if (st.hjobs[0].noxf) return st.njobs * (NPOLY / 256) <= g_pdl_maxcta;
+            if (st.cl && st.njobs <= CL_MAX) return true;
+            return st.njobs < g_vt2_jobs && st.njobs <= std::min(sms, g_pdl_maxcta);
+        case ST_MA: return (NPOLY / 256) * st.gy * st.njobs <= g_pdl_maxcta;
+        case ST_DX:
+        case ST_CO: return (NPOLY / 256) * st.njobs <= g_pdl_maxcta;
+        default: return true;
+    }
+}
+
 static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
-    g_step_pdl = st.group == 0;
+    g_step_pdl = st.group == 0 && step_one_wave(st);
     {
         switch (st.kind) {
             case ST_XF: {
@@ -469,9 +491,9 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 break;
             case ST_MA:
                 if (st.njobs > 16)  // throughput: occupancy
-                    CU(launch(k_ksmac<1>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
-                else  // small: fewer CTAs beside the transforms
-                    CU(launch(k_ksmac<2>, dim3(NPOLY / 512, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
+                    CU(launch(k_ksmac<1, 1>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
+                else  // small (latency path): 4 digits' loads in flight per thread
+                    CU(launch(k_ksmac<1, 4>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
                 break;
             case ST_DX:
                 CU(launch(k_diagx, dim3(NPOLY / 256, 1, st.njobs), 256, 0, s, h->hctx, (const DXJob*)st.djobs));

@@ -805,25 +805,34 @@ struct MJob {
 
 // CPT adjacent coefficients per thread: 1 at scale (low register count, the
 // digit loads of many warps in flight), 2 for small launches that share the
-// SMs with transform CTAs (fewer CTAs).
-template <int CPT>
-__global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
+// SMs with transform CTAs (fewer CTAs).  Digits are loaded KSB at a time
+// (every load of a batch in flight before its MACs: the loop is bound by
+// memory latency, not bandwidth, at the latency-path launch sizes); the
+// Galois permutation of the c0 term is constant and read before pdl_wait().
+template <int CPT, int KSB>
+__global__ void __launch_bounds__(256, KSB == 1 ? 5 : 2) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
     TRACE(0);
-    pdl_wait();
     const int k = blockIdx.y;
     const int j = CPT * (blockIdx.x * blockDim.x + threadIdx.x);
     const LevelC& LV = C.lv[J.level];
     const int P = LV.P, D = LV.D, L1 = C.L + 1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
+    const int nt = J.nterm;
+    unsigned pe0[CPT];  // term 0's c0 permutation (constant)
+    if (J.t[0].c0src) {
+        HC_UNROLL
+        for (int c = 0; c < CPT; c++) pe0[c] = J.t[0].perm[j + c];
+    }
+    pdl_wait();
     u64 o0[CPT], o1[CPT];
     HC_UNROLL
     for (int c = 0; c < CPT; c++) {
         o0[c] = J.add0 ? J.add0[kn + c] : 0;
         o1[c] = J.add1 ? J.add1[kn + c] : 0;
     }
-    const int nt = J.nterm;
+    const size_t vstep = (size_t)P * NPOLY, kstep = (size_t)2 * L1 * NPOLY, astep = (size_t)L1 * NPOLY;
     for (int t = 0; t < nt; t++) {
         const MTerm T = J.t[t];
         u64 h0[CPT], l0[CPT], h1[CPT], l1[CPT];
@@ -831,23 +840,39 @@ __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C,
         for (int c = 0; c < CPT; c++) h0[c] = l0[c] = h1[c] = l1[c] = 0;
         const u64* vp = T.dntt + kn;
         const u64* bp = T.key + kn;
-        const size_t vstep = (size_t)P * NPOLY, kstep = (size_t)2 * L1 * NPOLY, astep = (size_t)L1 * NPOLY;
-        for (int d = 0; d < D; d++) {
-            u64 v[CPT], kb[CPT], ka[CPT];
-            if constexpr (CPT == 2) {
-                const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(vp + d * vstep));
-                const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep));
-                const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep + astep));
-                v[0] = a.x; v[1] = a.y; kb[0] = b.x; kb[1] = b.y; ka[0] = e.x; ka[1] = e.y;
-            } else {
-                v[0] = __ldcs(vp + d * vstep);
-                kb[0] = __ldg(bp + d * kstep);
-                ka[0] = __ldg(bp + d * kstep + astep);
+        u64 c0v[CPT];
+        for (int d0 = 0; d0 < D; d0 += KSB) {
+            u64 v[KSB][CPT], kb[KSB][CPT], ka[KSB][CPT];
+            HC_UNROLL
+            for (int i = 0; i < KSB; i++) {
+                if (d0 + i < D) {
+                    const int d = d0 + i;
+                    if constexpr (CPT == 2) {
+                        const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(vp + d * vstep));
+                        const ulonglong2 b = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep));
+                        const ulonglong2 e = __ldg(reinterpret_cast<const ulonglong2*>(bp + d * kstep + astep));
+                        v[i][0] = a.x; v[i][1] = a.y; kb[i][0] = b.x; kb[i][1] = b.y; ka[i][0] = e.x; ka[i][1] = e.y;
+                    } else {
+                        v[i][0] = __ldcs(vp + d * vstep);
+                        kb[i][0] = __ldg(bp + d * kstep);
+                        ka[i][0] = __ldg(bp + d * kstep + astep);
+                    }
+                }
+            }
+            if (d0 == 0 && T.c0src) {  // the c0 gather, in flight with the first batch
+                const u64* c0 = T.c0src + (size_t)k * NPOLY;
+                HC_UNROLL
+                for (int c = 0; c < CPT; c++) c0v[c] = c0[t == 0 ? pe0[c] : T.perm[j + c]];
             }
             HC_UNROLL
-            for (int c = 0; c < CPT; c++) {
-                mac128(h0[c], l0[c], v[c], kb[c]);
-                mac128(h1[c], l1[c], v[c], ka[c]);
+            for (int i = 0; i < KSB; i++) {
+                if (d0 + i < D) {
+                    HC_UNROLL
+                    for (int c = 0; c < CPT; c++) {
+                        mac128(h0[c], l0[c], v[i][c], kb[i][c]);
+                        mac128(h1[c], l1[c], v[i][c], ka[i][c]);
+                    }
+                }
             }
         }
         HC_UNROLL
@@ -857,9 +882,8 @@ __global__ void __launch_bounds__(256) k_ksmac(const __grid_constant__ DevCtx C,
         }
         TRACE(1);
         if (T.c0src) {
-            const u64* c0 = T.c0src + (size_t)k * NPOLY;
             HC_UNROLL
-            for (int c = 0; c < CPT; c++) o0[c] = add_mod(o0[c], c0[T.perm[j + c]], pc.q);
+            for (int c = 0; c < CPT; c++) o0[c] = add_mod(o0[c], c0v[c], pc.q);
         }
     }
     TRACE(4);
