@@ -61,10 +61,10 @@ struct DevKey {
 
 // transform launches with at most this many jobs use the cluster kernel
 static int CL_MAX_JOBS = 48;  // transform batches up to this size use clusters
-static int g_cl_chunk = CL_MAX;  // jobs per cluster launch: co-resident 8-CTA clusters (<= CL_MAX)
+static int g_cl_chunk = 15;  // co-resident 8-CTA clusters (cudaOccupancyMaxActiveClusters)
 static int g_lane_max_blocks = 4;  // chunks up to this many blocks run the baby segment as lanes
 static int g_vt2_jobs = 200;       // single-CTA launches of >= this many jobs: three 256-thread transforms per SM
-static const int CL_SPREAD_SMEM = 120 * 1024;
+static const int CL_SPREAD_SMEM = 120 * 1024;  // k_cl_intt2 (static smem beside it)
 // schedule kernels launch with programmatic stream serialization (PDL): each
 // starts while its predecessor drains and blocks in pdl_wait() (kernels.cuh)
 // before touching the predecessor's data.  HC_PDL=0 disables it (A/B timing).
@@ -79,6 +79,8 @@ static bool pdl_on() {
 // PDL only on the main chain: inside parallel branches (lanes) an early-launched
 // kernel would hold SMs idle that the other branches need
 static thread_local bool g_step_pdl = true;
+static thread_local int g_step_prio = 0;
+static int g_prio_on = -1;  // HC_PRIO=0 disables launch priorities (A/B)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -86,11 +88,24 @@ static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    if (g_prio_on < 0) {
+        const char* e = getenv("HC_PRIO");
+        g_prio_on = (e && e[0] == '0') ? 0 : 1;
+    }
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl_on() && g_step_pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        na++;
+    }
+    if (g_prio_on && g_step_prio) {
+        at[na].id = cudaLaunchAttributePriority;
+        at[na].val.priority = g_step_prio;
+        na++;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = (pdl_on() && g_step_pdl) ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
@@ -111,7 +126,9 @@ struct Step {
     std::vector<XJob> side;        // ST_XF cluster launch: ClJobs.side (res_f.c0 finish of a fold)
     int group = 0;            // consecutive steps with the same nonzero group run concurrently
     int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
+    int jpc = 1;              // ST_XF cluster launch: transforms per cluster
     int lane = -1;            // in a group: steps of one lane run in order on one branch
+    int prio = 0;             // launch priority (0 = default; lower = more urgent)
 };
 
 struct Schedule {
@@ -119,7 +136,7 @@ struct Schedule {
     std::vector<void*> allocs;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
-    int cur_group = 0, next_group = 1, cur_lane = -1;
+    int cur_group = 0, next_group = 1, cur_lane = -1, cur_prio = 0;
     bool cl_in_lane = false;  // allow cluster launches inside a lane
     // steps added between par_begin() and par_end() are independent: they are
     // captured on forked streams (parallel graph branches)
@@ -176,9 +193,9 @@ static int kernels_configured = 0;
 // co-resident 8-CTA transform clusters (one CTA per SM) on the current device
 static int max_active_clusters(int* clusters) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(CL * CL_MAX);
+    cfg.gridDim = dim3(CL * 16);
     cfg.blockDim = dim3(CNT);
-    cfg.dynamicSmemBytes = CL_SPREAD_SMEM;
+    cfg.dynamicSmemBytes = CL_SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
@@ -186,8 +203,8 @@ static int max_active_clusters(int* clusters) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CU(cudaFuncSetAttribute(k_xf_cl<0, LD_U64, EP_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
-    CU(cudaOccupancyMaxActiveClusters(clusters, k_xf_cl<0, LD_U64, EP_STORE>, &cfg));
+    CU(cudaFuncSetAttribute(k_xf_cl<0, LD_U64, EP_STORE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));
+    CU(cudaOccupancyMaxActiveClusters(clusters, k_xf_cl<0, LD_U64, EP_STORE, 1>, &cfg));
     return HC_OK;
 }
 
@@ -199,7 +216,10 @@ static int configure_kernels() {
 #define XF_CFG(D, L, E)                                                                                    \
     CU(cudaFuncSetAttribute(k_xf<D, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));      \
     CU(cudaFuncSetAttribute(k_xf<D, L, E, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, NPOLY * 8));   \
-    CU(cudaFuncSetAttribute(k_xf_cl<D, L, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaFuncSetAttribute(k_xf_cl<D, L, E, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));  \
+    CU(cudaFuncSetAttribute(k_xf_cl<D, L, E, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));  \
+    CU(cudaFuncSetAttribute(k_xf_cl<D, L, E, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));  \
+    CU(cudaFuncSetAttribute(k_xf_cl<D, L, E, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SMEM));
     XF_COMBOS(XF_CFG)
 #undef XF_CFG
     CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
@@ -207,7 +227,7 @@ static int configure_kernels() {
     CU(cudaFuncSetAttribute(k_cl_intt2<LD_RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
     {
         int n = 0;
-        if (max_active_clusters(&n) == HC_OK && n > 0) g_cl_chunk = std::min(n, CL_MAX);
+        if (max_active_clusters(&n) == HC_OK && n > 0) g_cl_chunk = std::min(n, CL_MAX / CL_JPC_MAX);
     }
     kernels_configured = 1;
     return HC_OK;
@@ -323,6 +343,8 @@ static int g_trace_seq = 0;
 // a group too big for one cluster launch (g_cl_chunk = co-resident 8-CTA
 // clusters) is split into launches that run as parallel graph branches.
 static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
+    // one launch per kernel instantiation (dir, loader, epilogue)
+    std::vector<std::vector<XJob>> sets;
     std::vector<int> taken(jobs.size(), 0);
     for (size_t i = 0; i < jobs.size(); i++) {
         if (taken[i]) continue;
@@ -334,10 +356,35 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
                 taken[k] = 1;
             }
         }
-        // clusters only for small batches outside parallel lanes (lanes
-        // already fill the GPU; single-CTA transforms are more efficient there)
-        const bool clu = !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS && (S.cur_lane < 0 || S.cl_in_lane);
-        const size_t chunk = clu ? (size_t)g_cl_chunk : sel.size();
+        sets.push_back(sel);
+    }
+    // clusters only for small batches outside parallel lanes (lanes
+    // already fill the GPU; single-CTA transforms are more efficient there)
+    auto cl_ok = [&](const std::vector<XJob>& sel) {
+        return !sel[0].noxf && (int)sel.size() <= CL_MAX_JOBS && (S.cur_lane < 0 || S.cl_in_lane);
+    };
+    // several cluster batches of one call are independent: run them side by
+    // side (parallel graph branches) sharing one wave of co-resident clusters
+    int ncl_sets = 0, shared_jpc = 0;
+    for (const auto& sel : sets) ncl_sets += cl_ok(sel);
+    if (ncl_sets > 1 && !S.cur_group && S.cur_lane < 0) {
+        for (int jj = 1; jj <= CL_JPC_MAX && !shared_jpc; jj++) {
+            int need = 0;
+            for (const auto& sel : sets)
+                if (cl_ok(sel)) need += ((int)sel.size() + jj - 1) / jj;
+            if (need <= g_cl_chunk) shared_jpc = jj;
+        }
+    }
+    const bool together = shared_jpc > 0;
+    if (together) S.par_begin();
+    for (const auto& sel : sets) {
+        const bool clu = cl_ok(sel);
+        // cluster launches: up to CL_JPC_MAX transforms per cluster so that the
+        // batch fits one wave of co-resident clusters
+        const int jpc = !clu ? 1
+                        : together ? shared_jpc
+                                   : std::min(CL_JPC_MAX, std::max(1, ((int)sel.size() + g_cl_chunk - 1) / g_cl_chunk));
+        const size_t chunk = clu ? (size_t)g_cl_chunk * jpc : sel.size();
         const int saved = S.cur_group;
         if (clu && sel.size() > chunk && !S.cur_group) S.par_begin();
         for (size_t c0 = 0; c0 < sel.size(); c0 += chunk) {
@@ -348,16 +395,19 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
             st.kind = ST_XF;
             st.gy = part[0].dir;
             st.cl = clu;
+            st.jpc = jpc;
             st.njobs = (int)part.size();
             st.hjobs = part;
             st.group = S.cur_group;
             st.lane = S.cur_lane;
+            st.prio = S.cur_prio;
             int rc = upload_jobs(S, st, part.data(), part.size() * sizeof(XJob));
             if (rc) return rc;
             S.steps.push_back(st);
         }
         if (!saved) S.par_end();
     }
+    if (together) S.par_end();
     return HC_OK;
 }
 static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
@@ -366,6 +416,7 @@ static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
     st.kind = ST_CO;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
+    st.prio = S.cur_prio;
     st.njobs = (int)jobs.size();
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(CJob));
     if (rc) return rc;
@@ -380,6 +431,7 @@ static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
     st.kind = ST_MA;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
+    st.prio = S.cur_prio;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(MJob));
@@ -395,6 +447,7 @@ static int add_dx(Schedule& S, std::vector<DXJob> jobs, int nprime) {
     st.kind = ST_DX;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
+    st.prio = S.cur_prio;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(DXJob));
@@ -409,6 +462,7 @@ static int add_i2(Schedule& S, std::vector<Intt2Job> jobs) {
         st.kind = ST_I2;
         st.group = S.cur_group;
         st.lane = S.cur_lane;
+        st.prio = S.cur_prio;
         st.i2jobs.assign(jobs.begin() + c0, jobs.begin() + std::min(jobs.size(), c0 + (size_t)I2_MAX));
         for (Intt2Job& j : st.i2jobs) j.j[0].trace = j.j[1].trace = g_trace_seq;
         g_trace_seq++;
@@ -450,6 +504,7 @@ static bool step_one_wave(const Step& st) {
 
 static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
     g_step_pdl = st.group == 0 && step_one_wave(st);
+    g_step_prio = st.prio;
     {
         switch (st.kind) {
             case ST_XF: {
@@ -459,14 +514,16 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                     CU(launch(k_elem<LD_KSFIN>, dim3(NPOLY / 256, st.njobs), 128, 0, s, h->hctx, (const XJob*)st.djobs));
                     break;
                 }
-                const bool clu = st.cl && st.njobs <= CL_MAX;  // latency path: one 8-CTA cluster per transform
+                const bool clu = st.cl && st.njobs <= CL_MAX;  // latency path: 8-CTA clusters, jpc transforms each
+                const int ncl = (st.njobs + st.jpc - 1) / st.jpc;
                 ClJobs cj;
                 if (clu) {
                     memset(&cj, 0, sizeof cj);
                     memcpy(cj.j, st.hjobs.data(), st.njobs * sizeof(XJob));
+                    cj.n = st.njobs;
                     if (!st.side.empty()) {
-                        if (st.njobs < 8 || st.side.size() != 2 || j0.ep != EP_KSACC)
-                            return fail(HC_ERR_STATE, "side finish needs a KSACC cluster launch of >= 8 jobs");
+                        if (ncl * st.jpc < 8 || st.side.size() != 2 || j0.ep != EP_KSACC)
+                            return fail(HC_ERR_STATE, "side finish needs a KSACC cluster launch of >= 8 job slots");
                         cj.nside = 2;
                         cj.side[0] = st.side[0];
                         cj.side[1] = st.side[1];
@@ -475,7 +532,14 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 bool done = false;
 #define XF_LAUNCH(D, L, E)                                                                               \
     if (!done && j0.dir == D && j0.ld == L && j0.ep == E) {                                              \
-        if (clu) CU(launch(k_xf_cl<D, L, E>, st.njobs * CL, CNT, CL_SPREAD_SMEM, s, h->hctx, cj));       \
+        if (clu) {                                                                                       \
+            switch (st.jpc) {                                                                            \
+                case 1: CU(launch(k_xf_cl<D, L, E, 1>, ncl * CL, CNT, CL_SMEM, s, h->hctx, cj)); break;     \
+                case 2: CU(launch(k_xf_cl<D, L, E, 2>, ncl * CL, 2 * CNT, CL_SMEM, s, h->hctx, cj)); break; \
+                case 3: CU(launch(k_xf_cl<D, L, E, 3>, ncl * CL, 3 * CNT, CL_SMEM, s, h->hctx, cj)); break; \
+                default: CU(launch(k_xf_cl<D, L, E, 4>, ncl * CL, 4 * CNT, CL_SMEM, s, h->hctx, cj)); break; \
+            }                                                                                            \
+        }                                                                                                \
         else if (st.njobs >= g_vt2_jobs)                                                                 \
             CU(launch(k_xf<D, L, E, 4>, st.njobs, NT / 4, NPOLY * 8, s, h->hctx, (const XJob*)st.djobs)); \
         else CU(launch(k_xf<D, L, E>, st.njobs, NT, NPOLY * 8, s, h->hctx, (const XJob*)st.djobs));       \
@@ -1061,10 +1125,17 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         if (nl > 1) S.par_begin();
         for (int lane = 0; lane < nl; lane++) {
             S.cur_lane = nl > 1 ? lane : -1;
+            // later pipeline stages first: when an SM frees up, a lane's MAC or
+            // diagonal INTTs take it before the other lanes' queued digit NTTs,
+            // so finished lanes drain instead of all meeting in one tail
             for (int tl = lane; tl < cb; tl += nl) {
+                S.cur_prio = 0;
                 rc = add_xf(S, s7[tl]); if (rc) return rc;
+                S.cur_prio = -1;
                 rc = add_ma(S, s8[tl], 3); if (rc) return rc;
+                S.cur_prio = -2;
                 rc = add_xf(S, s9[tl]); if (rc) return rc;
+                S.cur_prio = 0;
             }
         }
         S.cur_lane = -1;

@@ -396,11 +396,18 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-constexpr int CL_MAX = 16;  // jobs per cluster launch (passed by value)
+constexpr int CL_MAX = 60;  // jobs per cluster launch (passed by value): 15 clusters x 4
+constexpr int CL_JPC_MAX = 4;  // transforms per cluster (one per 128-thread group of each CTA)
+// dynamic smem of a cluster-transform CTA: JPC groups of [tile | recv (inverse) |
+// twiddle slice] (<= 4 x 32 KiB), padded so every CTA of a cluster lands on its
+// own SM (the scheduler would otherwise pack small CTAs onto one or two SMs)
+constexpr int CL_GROUP_WORDS_FWD = CTILE + 2048, CL_GROUP_WORDS_INV = 2 * CTILE + 2048;
+constexpr int CL_SMEM = 150 * 1024;
 struct ClJobs {
     XJob j[CL_MAX];
+    int n;  // jobs in this launch (the last cluster's spare groups idle)
     // optional transform-less key-switch finishes (LD_KSFIN, noxf; one per
-    // prime) spread over every thread of a forward KSACC launch of >= 8 jobs:
+    // prime) spread over every thread of a forward KSACC launch of >= 8 job slots:
     // a fold's res_f.c0 finish rides in the fold's digit-NTT launch instead of
     // a parallel graph branch (the digit products go to the other ACC buffer)
     int nside;
@@ -432,17 +439,28 @@ __device__ __forceinline__ void tw_commit(Tw* sl, const TwPre& pre, int t) {
     }
 }
 
-template <int DIR, int LD, int EP>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
+// JPC transforms per cluster: thread group g = threadIdx.x / 128 of every CTA
+// runs job (cluster * JPC + g) with its own tile / receive buffer / twiddle
+// slice; the groups share the CTA and cluster barriers.  A small launch thus
+// fits in one wave of co-resident clusters (e.g. 42 giant-step digit NTTs:
+// 14 clusters of 3 instead of three sequential launches of <= 15), and the
+// extra warps per SM hide the butterflies' latency.
+template <int DIR, int LD, int EP, int JPC>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
     k_xf_cl(const __grid_constant__ DevCtx C, const __grid_constant__ ClJobs jobs) {
-    __shared__ u64 tile[CTILE];
-    __shared__ u64 recv[DIR ? CTILE : 1];
-    __shared__ Tw twsl[1023];
+    extern __shared__ __align__(16) u64 csm[];
+    constexpr int GW = DIR ? CL_GROUP_WORDS_INV : CL_GROUP_WORDS_FWD;
+    const int grp = JPC == 1 ? 0 : (int)(threadIdx.x >> 7);
+    u64* tile = csm + grp * GW;
+    u64* recv = tile + CTILE;  // inverse only
+    Tw* twsl = reinterpret_cast<Tw*>(tile + (DIR ? 2 : 1) * CTILE);
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     const int c = (int)cl.block_rank();
-    const int t = threadIdx.x;
+    const int t = threadIdx.x & (CNT - 1);
     cluster_arrive_relaxed();  // "this CTA has started" (waited on before DSMEM stores)
-    const XJob& J = jobs.j[blockIdx.x / CL];
+    const int jid = (blockIdx.x / CL) * JPC + grp;
+    const bool valid = jid < jobs.n;  // spare group of the last cluster: barriers only
+    const XJob& J = jobs.j[valid ? jid : jobs.n - 1];
     TRACE(0);
     const PrimeC& P = C.pc[J.k];
     const TwL twl{twsl, c};
@@ -456,19 +474,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);  // phase-A twiddles tbl[1..7]
         const int b = 128 * c + t;
         LdPre<LD, CEPT> lpre;
-        load_pre<LD, CEPT>(J, b, CTILE, lpre);
+        if (valid) load_pre<LD, CEPT>(J, b, CTILE, lpre);
         // key digits of the KSACC epilogue: constant, fetched before the wait
         u64 ka[EP == EP_KSACC ? CEPT : 1], kb[EP == EP_KSACC ? CEPT : 1];
         if constexpr (EP == EP_KSACC) {
-            HC_UNROLL
-            for (int v = 0; v < CEPT; v++) {
-                ka[v] = J.ea[c * CTILE + t + 128 * v];
-                kb[v] = J.eb[c * CTILE + t + 128 * v];
+            if (valid) {
+                HC_UNROLL
+                for (int v = 0; v < CEPT; v++) {
+                    ka[v] = J.ea[c * CTILE + t + 128 * v];
+                    kb[v] = J.eb[c * CTILE + t + 128 * v];
+                }
             }
         }
         constexpr bool SIDE = EP == EP_KSACC;
         const bool side = SIDE && jobs.nside;
-        const int gt = blockIdx.x * CNT + t, gT = gridDim.x * CNT;  // gT >= n (>= 8 jobs)
+        const int gt = blockIdx.x * blockDim.x + threadIdx.x, gT = gridDim.x * blockDim.x;  // gT >= n (host-checked)
         LdPre<LD_KSFIN, 1> sp[2];
         KsLd<1> sv[2];
         if constexpr (SIDE) {
@@ -481,7 +501,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
             }
         }
         pdl_wait();
-        load_post<LD, CEPT>(C, J, P, b, CTILE, lpre, x);
+        if (valid) load_post<LD, CEPT>(C, J, P, b, CTILE, lpre, x);
+        else
+            HC_UNROLL
+            for (int v = 0; v < CEPT; v++) x[v] = 0;
         if constexpr (SIDE) {
             if (side) {
                 HC_UNROLL
@@ -531,7 +554,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         pdl_trigger();
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) x[v] = tile[cswz(t + 128 * v)];
-        if constexpr (EP == EP_KSACC) {
+        if (!valid) {
+        } else if constexpr (EP == EP_KSACC) {
             HC_UNROLL
             for (int v = 0; v < CEPT; v++) {
                 const int j = c * CTILE + t + 128 * v;
@@ -547,9 +571,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         TwPre pre;
         tw_issue(pre, tw, c, t);
         LdPre<LD, CEPT> lpre;
-        load_pre<LD, CEPT>(J, c * CTILE + t, 128, lpre);
+        if (valid) load_pre<LD, CEPT>(J, c * CTILE + t, 128, lpre);
         pdl_wait();
-        load_post<LD, CEPT>(C, J, P, c * CTILE + t, 128, lpre, x);
+        if (valid) load_post<LD, CEPT>(C, J, P, c * CTILE + t, 128, lpre, x);
+        else
+            HC_UNROLL
+            for (int v = 0; v < CEPT; v++) x[v] = 0;
         tw_commit(twsl, pre, t);
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
@@ -582,7 +609,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT)
         HC_UNROLL
         for (int r = 0; r < CEPT; r++) x[r] = recv[r * 128 + t];
         c_phaseA_inv(x, tw, P);
-        store_n<EP, CEPT>(C, J, P, 128 * c + t, CTILE, x);
+        if (valid) store_n<EP, CEPT>(C, J, P, 128 * c + t, CTILE, x);
         TRACE(5);
     }
 }
