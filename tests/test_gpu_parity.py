@@ -204,6 +204,25 @@ def test_comp_p786433_N2_17_vs_oracle(pkg, oracle):
     assert (w, e) == O.expected_slots(dense, s, p)
 
 
+def test_comp_config4_N2_20_vs_oracle(pkg, oracle):
+    """Config 4 at N = 2^20, s = 16 (p = 1097729, 128 input ciphertexts, 256
+    blocks: the wide throughput schedule, CB = 64 chunks): bit-exact against
+    the oracle run end to end on the same seed, and decrypts to the power sums."""
+    P, O = pkg, oracle
+    N, s, p, seed = 1 << 20, 16, 1097729, 0
+    be, params, keys, dense, cts, hint = make_case(P, O, N8K, p, N, s, seed, guard=False)
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    obe = O.OracleBgv(N8K, p, 3, seed=seed, check_noise=False)
+    okeys = obe.keygen(*O.plan_rotation_amounts(s, N8K))
+    ocv = O.encrypt_vector(dense, N, obe, okeys)
+    ohint = O.encrypt_vector([1 if x else 0 for x in dense], N, obe, okeys)
+    oout = O.comp(ocv, N, s, obe, okeys, ohint)
+    assert np.array_equal(ans.cts[0].payload.res, oout.c)
+    assert O.sha256(ans.serialize(be)) == O.sha256(O.serialize_answer(obe, oout, s))
+    w, e = ans.payload_slots(be, keys)
+    assert (w, e) == O.expected_slots(dense, s, p)
+
+
 def test_comp_noise_guard_raises_like_reference(pkg, oracle):
     """(2^14, 32) overflows the reference's heuristic guard."""
     P, O = pkg, oracle

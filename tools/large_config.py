@@ -5,7 +5,11 @@ the package API (`comp`), the decrypted (w, e) slots checked against the
 power sums of the planted pairs (what the reference's decomp inverts,
 compress.py:1-16), then warm device-resident timing (`DeviceComp`).
 
-  python tools/large_config.py --N 1048576 --s 16 [--iters 5] [--json out.json]
+With --oracle the CPU oracle (oracle/, C + OpenMP restatement of the
+reference Comp) runs the same seed end to end and the answer must be
+bit-exact (ciphertext residues and serialized bytes).
+
+  python tools/large_config.py --N 1048576 --s 16 [--iters 5] [--oracle] [--json out.json]
 """
 import argparse
 import json
@@ -52,6 +56,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--json", default="")
+    ap.add_argument("--oracle", action="store_true",
+                    help="also run the CPU oracle (oracle/, C + OpenMP) on the same seed and require a bit-exact answer")
     a = ap.parse_args()
     p = 65537 if a.N < 65537 else next(c for c in (786433, 1097729, 4423681) if c > a.N)
     t0 = time.perf_counter()
@@ -86,12 +92,31 @@ def main():
         ms.append(ev[0].elapsed_time(ev[1]))
     ms.sort()
     med = ms[len(ms) // 2]
+    oracle_ok = None
+    if a.oracle:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+        from oracle import bgv_oracle as O
+
+        t4 = time.perf_counter()
+        obe = O.OracleBgv(8192, p, 3, seed=a.seed, check_noise=False)
+        okeys = obe.keygen(*O.plan_rotation_amounts(a.s, 8192))
+        ocd = O.encrypt_vector(dense, a.N, obe, okeys)
+        ocv = O.encrypt_vector([1 if x else 0 for x in dense], a.N, obe, okeys)
+        oout = O.comp(ocd, a.N, a.s, obe, okeys, ocv)
+        oracle_s = time.perf_counter() - t4
+        oracle_ok = bool(np.array_equal(ans.cts[0].payload.res, oout.c))
+        oracle_ser = O.sha256(O.serialize_answer(obe, oout, a.s))
+        gpu_ser = O.sha256(ans.serialize(be))
     r = {
         "N": a.N, "s": a.s, "p": p, "blocks": params.num_blocks, "ciphertexts": params.num_ciphertexts,
         "decomp_slots_match": ok, "device_rerun_identical": bool(same),
         "comp_ms_median": med, "comp_ms_min": ms[0], "entries_per_s": a.N / (med * 1e-3),
         "first_call_s": t3 - t2, "keygen_s": t1 - t0, "encrypt_s": t2 - t1,
     }
+    if a.oracle:
+        r.update({"oracle_bit_exact": oracle_ok, "answer_sha256_gpu": gpu_ser, "answer_sha256_oracle": oracle_ser,
+                  "oracle_keygen_encrypt_comp_s": oracle_s, "oracle_threads": O.lib().orc_num_threads()})
+        ok = ok and oracle_ok and gpu_ser == oracle_ser
     print(json.dumps(r))
     if a.json:
         with open(a.json, "a") as f:

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--N", type=int, default=1 << 16)
     ap.add_argument("--s", type=int, default=64)
     ap.add_argument("--rounds", type=int, default=20)
+    ap.add_argument("--oracle", type=int, default=0,
+                    help="check the first K queries bit-exact against the CPU oracle (own keygen/encrypt/Comp per seed)")
     a = ap.parse_args()
     p = 65537 if a.N < 65537 else next(c for c in (786433, 1097729, 4423681) if c > a.N)
     he = P.HeParams(8192, p, 3)
@@ -61,6 +63,20 @@ def main():
         want = [sum(pow(i + 1, j + 1, p) for i, v in enumerate(d["dense"]) if v) % p for j in range(a.s)]
         ok &= w == want
     res = {"N": a.N, "s": a.s, "p": p, "queries": a.Q, "decrypt_ok": ok, "setup_s": round(setup_s, 1), "concurrency": {}}
+    if a.oracle:
+        from oracle import bgv_oracle as O
+
+        exact = []
+        for q, d in enumerate(qs[: a.oracle]):
+            obe = O.OracleBgv(8192, p, 3, seed=q, check_noise=False)
+            okeys = obe.keygen(*O.plan_rotation_amounts(a.s, 8192))
+            ocd = O.encrypt_vector(d["dense"], a.N, obe, okeys)
+            ocv = O.encrypt_vector([1 if x else 0 for x in d["dense"]], a.N, obe, okeys)
+            oout = O.comp(ocd, a.N, a.s, obe, okeys, ocv)
+            exact.append(bool(np.array_equal(d["dc"].output(), oout.c)))
+            print(f"query {q}: GPU Comp == oracle Comp: {exact[-1]}", flush=True)
+        res["oracle_bit_exact"] = exact
+        ok &= all(exact)
     for conc in (1, 2, 4, 8):
         if conc > a.Q:
             break
