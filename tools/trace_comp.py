@@ -15,6 +15,7 @@ be = P.B200BgvBackend(he, seed=0, noise_guard=False)
 keys = be.keygen(*P.plan_rotation_amounts(s, 8192))
 rng = np.random.default_rng(1); C = params.num_ciphertexts
 cd = np.stack([np.stack([rng.integers(0, q, 8192, dtype=np.uint64) for q in be.q]) for _ in range(2 * C)]).reshape(C, 2, 4, 8192)
+if os.environ.get("TRACE_LANES"): _lib.lib().hc_set_lane_blocks(int(os.environ["TRACE_LANES"]))
 dc = P.DeviceComp(be, params, keys); dc.set_inputs(cd, cd.copy())
 L = _lib.lib()
 L.hc_trace_reset()
