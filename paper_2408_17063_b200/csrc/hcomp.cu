@@ -79,6 +79,7 @@ static bool pdl_on() {
 // PDL only on the main chain: inside parallel branches (lanes) an early-launched
 // kernel would hold SMs idle that the other branches need
 static thread_local bool g_step_pdl = true;
+static thread_local bool g_pdl_suspended = false;  // hc_comp_profile: launches timed one by one
 static thread_local int g_step_prio = 0;
 static int g_prio_on = -1;  // HC_PRIO=0 disables launch priorities (A/B)
 template <typename... KArgs, typename... Args>
@@ -94,7 +95,7 @@ static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     }
     cudaLaunchAttribute at[2];
     int na = 0;
-    if (pdl_on() && g_step_pdl) {
+    if (pdl_on() && g_step_pdl && !g_pdl_suspended) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
         na++;
@@ -1723,14 +1724,19 @@ extern "C" int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* st
     std::vector<cudaEvent_t> ev(ns + 1);
     for (auto& e : ev) CU(cudaEventCreate(&e));
     CU(cudaEventRecord(ev[0], s));
+    g_pdl_suspended = true;  // each launch timed on its own, no early start
     for (int i = 0; i < ns; i++) {
         Schedule one;
         one.steps.push_back(S.steps[i]);
         rc = enqueue(h, one, s);
         one.steps.clear();
-        if (rc) return rc;
+        if (rc) {
+            g_pdl_suspended = false;
+            return rc;
+        }
         CU(cudaEventRecord(ev[i + 1], s));
     }
+    g_pdl_suspended = false;
     CU(cudaStreamSynchronize(s));
     int k = 0;
     for (int i = 0; i < ns && k < max_steps; i++, k++) {
