@@ -396,6 +396,56 @@ __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// DSMEM all-to-all of the cluster transforms.  Default: every value goes out
+// as st.async to the peer CTA, whose mbarrier counts the incoming bytes
+// (complete_tx); a CTA proceeds once its own receive buffer is full -- no
+// cluster-wide release/acquire barrier (the latter costs a GPU-scope MEMBAR
+// and an L1 invalidate per exchange).  HC_CLUSTER_BAR builds the barrier form
+// (A/B).  Protocol: thread 0 initialises the CTA's mbarrier (one arrival) and
+// posts the expected byte count before the kernel's start-of-cluster barrier;
+// senders wait on that barrier before their first st.async.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void xch_init(u64* bar, uint32_t bytes) {
+#ifndef HC_CLUSTER_BAR
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+#endif
+}
+// value v into the peer CTA `rank` at the address `dst` has in this CTA
+__device__ __forceinline__ void xch_put(cooperative_groups::cluster_group& cl, u64* dst, int rank, u64 v, u64* bar) {
+#ifndef HC_CLUSTER_BAR
+    uint32_t ra, rb;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(smem_u32(dst)), "r"(rank));
+    asm("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u64 [%0], %1, [%2];\n" ::"r"(ra), "l"(v), "r"(rb)
+                 : "memory");
+#else
+    cl.map_shared_rank(dst, rank)[0] = v;
+#endif
+}
+// all values destined to this CTA have landed (and are visible to this thread)
+__device__ __forceinline__ void xch_wait(u64* bar) {
+#ifndef HC_CLUSTER_BAR
+    // bounded: a lost transfer traps (kernel error) instead of hanging the GPU
+    for (unsigned it = 0;; it++) {
+        uint32_t done;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar))
+            : "memory");
+        if (done) break;
+        if (it > (1u << 26)) __trap();
+    }
+#else
+    cluster_arrive_release();
+    cluster_wait();
+#endif
+}
+
 constexpr int CL_MAX = 60;  // jobs per cluster launch (passed by value): 15 clusters x 4
 constexpr int CL_JPC_MAX = 4;  // transforms per cluster (one per 128-thread group of each CTA)
 // dynamic smem of a cluster-transform CTA: JPC groups of [tile | recv (inverse) |
@@ -454,9 +504,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
     u64* tile = csm + grp * GW;
     u64* recv = tile + CTILE;  // inverse only
     Tw* twsl = reinterpret_cast<Tw*>(tile + (DIR ? 2 : 1) * CTILE);
+    u64* xbar = csm + JPC * GW;  // exchange mbarrier (one per CTA)
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     const int c = (int)cl.block_rank();
     const int t = threadIdx.x & (CNT - 1);
+    xch_init(xbar, JPC * CTILE * 8);  // every group receives 1024 values
     cluster_arrive_relaxed();  // "this CTA has started" (waited on before DSMEM stores)
     const int jid = (blockIdx.x / CL) * JPC + grp;
     const bool valid = jid < jobs.n;  // spare group of the last cluster: barriers only
@@ -534,12 +586,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
         cluster_wait();
         TRACE(2);
         HC_UNROLL
-        for (int r = 0; r < CEPT; r++) {
-            u64* peer = cl.map_shared_rank(tile, r);
-            peer[cswz(b)] = x[r];
-        }
-        cluster_arrive_release();
-        cluster_wait();  // also orders this CTA's twiddle-slice stores
+        for (int r = 0; r < CEPT; r++) xch_put(cl, tile + cswz(b), r, x[r], xbar);
+        xch_wait(xbar);
+        __syncthreads();  // this CTA's twiddle-slice stores
         TRACE(3);
         HC_UNROLL
         for (int p = 0; p < 3; p++) {
@@ -599,12 +648,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
         cluster_wait();
         TRACE(2);
         HC_UNROLL
-        for (int v = 0; v < CEPT; v++) {
-            u64* peer = cl.map_shared_rank(recv, v);
-            peer[c * 128 + t] = x[v];
-        }
-        cluster_arrive_release();
-        cluster_wait();
+        for (int v = 0; v < CEPT; v++) xch_put(cl, recv + c * 128 + t, v, x[v], xbar);
+        xch_wait(xbar);
         TRACE(3);
         HC_UNROLL
         for (int r = 0; r < CEPT; r++) x[r] = recv[r * 128 + t];
@@ -647,8 +692,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     u64* tile = dsm + pr * CTILE;
     u64* recvb = dsm + (2 + pr) * CTILE;
     Tw* twsl = reinterpret_cast<Tw*>(dsm + 4 * CTILE) + pr * 1024;
+    u64* xbar = dsm + 8 * CTILE;  // after the two twiddle slices
     cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
     const int c = (int)cl.block_rank();
+    xch_init(xbar, 2 * CTILE * 8);
     cluster_arrive_relaxed();
     const Intt2Job& JJ = jobs.j[blockIdx.x / CL];
     const XJob& J = JJ.j[pr];
@@ -684,9 +731,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     pdl_trigger();
     cluster_wait();
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) cl.map_shared_rank(recvb, v)[c * 128 + t] = x[v];
-    cluster_arrive_release();
-    cluster_wait();
+    for (int v = 0; v < CEPT; v++) xch_put(cl, recvb + c * 128 + t, v, x[v], xbar);
+    xch_wait(xbar);
     TRACE(3);
     HC_UNROLL
     for (int r = 0; r < CEPT; r++) x[r] = recvb[r * 128 + t];
