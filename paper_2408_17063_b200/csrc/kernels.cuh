@@ -883,7 +883,7 @@ struct MJob {
 // memory latency, not bandwidth, at the latency-path launch sizes); the
 // Galois permutation of the c0 term is constant and read before pdl_wait().
 template <int CPT, int KSB>
-__global__ void __launch_bounds__(256, KSB == 1 ? 5 : 2) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_constant__ DevCtx C, const MJob* __restrict__ jobs) {
     const MJob& J = jobs[blockIdx.z];
     TRACE(0);
     const int k = blockIdx.y;
@@ -914,6 +914,7 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 2) k_ksmac(const __grid_co
         const u64* vp = T.dntt + kn;
         const u64* bp = T.key + kn;
         u64 c0v[CPT];
+        HC_NOUNROLL
         for (int d0 = 0; d0 < D; d0 += KSB) {
             u64 v[KSB][CPT], kb[KSB][CPT], ka[KSB][CPT];
             HC_UNROLL
