@@ -497,8 +497,8 @@ static bool step_one_wave(const Step& st) {
             if (st.cl && st.njobs <= CL_MAX) return true;
             return st.njobs < g_vt2_jobs && st.njobs <= std::min(sms, g_pdl_maxcta);
         case ST_MA: return (NPOLY / 256) * st.gy * st.njobs <= g_pdl_maxcta;
-        case ST_DX:
-        case ST_CO: return (NPOLY / 256) * st.njobs <= g_pdl_maxcta;
+        case ST_DX: return (NPOLY / 256) * st.njobs <= g_pdl_maxcta;
+        case ST_CO: return (NPOLY / 256) * st.njobs <= std::max(g_pdl_maxcta, 148);  // small composes (latency path)
         default: return true;
     }
 }

@@ -805,13 +805,12 @@ struct CJob {
 };
 
 template <int L>
-__device__ __forceinline__ void compose_one(const DevCtx& C, const CJob& J, int pos) {
+__device__ __forceinline__ void compose_one(const DevCtx& C, const CJob& J, int pos, unsigned e) {
     const LevelC& LV = C.lv[L];
     constexpr int P = L + 1;
     const int D = LV.D;
     int src = pos, neg = 0;
     if (J.mode == 0 && J.gal) {
-        const unsigned e = J.gal[pos];
         src = e & 0x7FFF;
         neg = e >> 15;
     }
@@ -844,11 +843,12 @@ __device__ __forceinline__ void compose_one(const DevCtx& C, const CJob& J, int 
 __global__ void __launch_bounds__(256) k_compose(const __grid_constant__ DevCtx C, const CJob* __restrict__ jobs) {
     const CJob J = jobs[blockIdx.y];
     const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned e = (J.mode == 0 && J.gal) ? J.gal[pos] : 0u;  // constant gather table: before the wait
     pdl_wait();
     switch (J.level) {
-        case 1: compose_one<1>(C, J, pos); break;
-        case 2: compose_one<2>(C, J, pos); break;
-        case 3: compose_one<3>(C, J, pos); break;
+        case 1: compose_one<1>(C, J, pos, e); break;
+        case 2: compose_one<2>(C, J, pos, e); break;
+        case 3: compose_one<3>(C, J, pos, e); break;
         default: break;
     }
 }
@@ -914,7 +914,7 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_co
         const u64* vp = T.dntt + kn;
         const u64* bp = T.key + kn;
         u64 c0v[CPT];
-        HC_NOUNROLL
+#pragma unroll(KSB == 1 ? 4 : 1)  // batched digits: one batch body (registers); single digits: unrolled
         for (int d0 = 0; d0 < D; d0 += KSB) {
             u64 v[KSB][CPT], kb[KSB][CPT], ka[KSB][CPT];
             HC_UNROLL
