@@ -376,6 +376,7 @@ def main():
         assert np.array_equal(out_h.numpy().view(np.uint64), out), "e2e output differs from the device-resident run"
     e2e_serial_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
     e2e_ms = e2e_serial_ms
+    e2e_stream_ms = None
     if not shard:
         # ---- streamed end to end: step i+1's inputs go up over PCIe (H2D
         # stream) while step i computes, step i's result comes back (D2H
@@ -423,14 +424,18 @@ def main():
             stream.wait_event(d2h_done[-1])
             t1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = t0.elapsed_time(t1)
+        e2e_stream_ms = t0.elapsed_time(t1)
         assert np.array_equal(outs[(args.steps - 1) % 2].numpy().view(np.uint64), out), "streamed e2e output differs"
+        # both are end to end (every step copies its inputs in and its answer
+        # out inside the timed region); the line reports the faster schedule
+        e2e_ms = min(e2e_serial_ms, e2e_stream_ms)
     info = be.plan_info()  # kernel launches per Comp (graph built by now)
 
     if dist:
-        tt = torch.tensor([t_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_ms, e2e_ms, e2e_serial_ms, e2e_stream_ms or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms, e2e_ms = tt.tolist()
+        t_ms, e2e_ms, e2e_serial_ms, e2e_stream_ms = tt.tolist()
+        e2e_stream_ms = e2e_stream_ms or None
 
     # ---- live roofline of the dominant kernel (k_xform) ----
     max_steps = 4096
@@ -488,9 +493,15 @@ def main():
             "unit": "entries/s",
             "ms_per_step": e2e_ms / args.steps,
             "mode": ("sharded: per-step H2D of the rank's ciphertexts, partial, reduce, finish, D2H"
-                     if shard else "streamed: step i+1's H2D and step i's D2H overlap computation on copy "
-                     "streams; L2 flush inside the timed loop (counted)"),
+                     if shard else
+                     ("serial: each step's event pair holds the H2D of its input ciphertexts from pinned host "
+                      "memory, the Comp (hc_comp_async: one graph launch) and the D2H of the answer; L2 "
+                      "flushed before every step, untimed as for value")
+                     if e2e_stream_ms is None or e2e_serial_ms <= e2e_stream_ms else
+                     "streamed: step i+1's H2D and step i's D2H overlap computation on copy streams; L2 "
+                     "flush inside the timed loop (counted)"),
             "serial_ms_per_step": e2e_serial_ms / args.steps,
+            "streamed_ms_per_step": (e2e_stream_ms / args.steps) if e2e_stream_ms else None,
             "h2d_bytes_per_step": h2d_bytes,
             "d2h_bytes_per_step": 2 * RING * 8,
         },
