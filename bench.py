@@ -41,6 +41,11 @@ sys.path.insert(0, ROOT)
 N_DEFAULT, S_DEFAULT, P_DEFAULT, RING = 1 << 14, 16, 65537, 8192
 
 
+# hcomp.cu StepKind -> the kernels behind it (hc_comp_profile's step kinds)
+STEP_KINDS = {0: "transforms (k_xf, k_xf_cl)", 1: "crt_digits (k_compose)", 2: "key_mac (k_ksmac)",
+              3: "diag_mac (k_diagx)", 5: "memset", 6: "two_prime_intt (k_cl_intt2)"}
+
+
 def metric_name(N: int, s: int) -> str:
     n = f"2^{N.bit_length() - 1}" if N & (N - 1) == 0 else str(N)
     return f"Comp encrypted entries/sec (N={n}, s={s})"
@@ -437,7 +442,7 @@ def main():
         t_ms, e2e_ms, e2e_serial_ms, e2e_stream_ms = tt.tolist()
         e2e_stream_ms = e2e_stream_ms or None
 
-    # ---- live roofline of the dominant kernel (k_xform) ----
+    # ---- live roofline of the dominant kernel family (the transforms) ----
     max_steps = 4096
     sm_ = np.zeros(max_steps, dtype=np.float32)
     sk = np.zeros(max_steps, dtype=np.int32)
@@ -523,7 +528,7 @@ def main():
             "xform_jobs_per_comp": xf_jobs,
             "xform_launches_per_comp": xf_launch,
             "profiled_step_ms_ungraphed": prof_total,
-            "per_kind_ms": {str(k): round(v[0], 4) for k, v in sorted(kinds.items())},
+            "per_kind_ms": {STEP_KINDS.get(k, str(k)): round(v[0], 4) for k, v in sorted(kinds.items())},
             "saturated_592_jobs_gbfly_s": sat,
             "saturated_frac": {k: v / peak_g for k, v in sat.items()} if peak_g else None,
         },

@@ -110,17 +110,14 @@ static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_SUMC, ST_MEMSET, ST_I2 };
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6 };  // values: bench.py per_kind_ms keys
 struct Step {
     int kind = 0;
     int njobs = 0;
     int gy = 1;
     void* djobs = nullptr;
-    // ST_SUMC / ST_MEMSET
-    const u64* in = nullptr;
+    // ST_MEMSET
     u64* out = nullptr;
-    long long rows = 0, cstride = 0;
-    int period = 0, copies = 0;
     size_t bytes = 0;
     std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
     std::vector<Intt2Job> i2jobs;  // ST_I2
@@ -562,9 +559,6 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 break;
             case ST_DX:
                 CU(launch(k_diagx, dim3(NPOLY / 256, 1, st.njobs), 256, 0, s, h->hctx, (const DXJob*)st.djobs));
-                break;
-            case ST_SUMC:
-                CU(launch(k_sum_copies, 592, 256, 0, s, h->hctx, st.in, st.out, st.rows, st.period, st.copies, st.cstride));
                 break;
             case ST_MEMSET:
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
@@ -1753,7 +1747,7 @@ extern "C" int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* st
 // Butterfly-throughput ceiling: the CT butterfly of the NTT kernels
 // (Harvey lazy Shoup, bf_ct) in registers at full occupancy, no memory
 // traffic.  Returns butterflies per second; the integer-ALU roofline
-// denominator for k_xform.
+// denominator for the transform kernels (k_xf, k_xf_cl, k_cl_intt2).
 __global__ void __launch_bounds__(256) k_bf_peak(const __grid_constant__ DevCtx C, int iters, u64* sink) {
     const PrimeC P = C.pc[0];
     u64 x[16];

@@ -3,10 +3,15 @@
 // transform / CRT / MAC of a schedule step (hcomp.cu builds the lists once
 // per plan and replays them in a CUDA graph).
 //
-//   k_xform    one 8192-point NTT or INTT per CTA (256 threads, 64 KiB smem),
-//              with a fused loader (pointwise Montgomery product, digit
-//              gather through a Galois table, ...) and a fused epilogue
-//              (plaintext-multiply combine, modulus-switch correction, ...).
+//   k_xf       one 8192-point NTT or INTT per CTA (1024 threads, or 256
+//              threads running the 1024-thread schedule 4x, three CTAs per
+//              SM), 64 KiB smem tile, with a fused loader (pointwise
+//              Montgomery product, digit gather through a Galois table,
+//              key-switch finish, ...) and a fused epilogue (plaintext-
+//              multiply combine, modulus-switch correction, key MAC, ...).
+//   k_xf_cl    the same jobs on 8-CTA clusters, 1-4 transforms per cluster
+//              (latency path); k_cl_intt2 the two-prime INTT + CRT digits of
+//              a level-1 key switch on one cluster.
 //   k_compose  exact CRT + base-2^16 digit split (optionally through the
 //              coefficient-domain Galois gather), one thread per coefficient.
 //   k_ksmac    key-switch inner product sum_j NTT(digit_j) * ksk_j with
@@ -24,7 +29,7 @@
 namespace hc {
 
 // ---------------------------------------------------------------------------
-// k_xform
+// transform jobs: loaders and epilogues
 // ---------------------------------------------------------------------------
 enum : int {
     LD_U64 = 0,    // a[j]
@@ -1127,21 +1132,6 @@ __global__ void k_to_mont(const __grid_constant__ DevCtx C, u64* data, long long
         const int k = (int)((i / NPOLY) % period);
         const PrimeC P = C.pc[k];
         data[i] = mul_shoup(data[i], P.rmod, P.rmod_s, P.q);
-    }
-}
-
-// out[r][j] = sum_c red(in[c][r][j]) mod q_{r % period}
-__global__ void k_sum_copies(const __grid_constant__ DevCtx C, const u64* in, u64* out, long long rows,
-                             int period, int copies, long long cstride) {
-    pdl_wait();
-    const long long total = rows * NPOLY;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int k = (int)((i / NPOLY) % period);
-        const PrimeC P = C.pc[k];
-        u64 s = 0;
-        for (int c = 0; c < copies; c++) s = add_mod(s, red64(in[c * cstride + i], P.q, P.one_s), P.q);
-        out[i] = s;
     }
 }
 
