@@ -80,8 +80,6 @@ static bool pdl_on() {
 // kernel would hold SMs idle that the other branches need
 static thread_local bool g_step_pdl = true;
 static thread_local bool g_pdl_suspended = false;  // hc_comp_profile: launches timed one by one
-static thread_local int g_step_prio = 0;
-static int g_prio_on = -1;  // HC_PRIO=0 disables launch priorities (A/B)
 template <typename... KArgs, typename... Args>
 static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -89,20 +87,11 @@ static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    if (g_prio_on < 0) {
-        const char* e = getenv("HC_PRIO");
-        g_prio_on = (e && e[0] == '0') ? 0 : 1;
-    }
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[1];
     int na = 0;
     if (pdl_on() && g_step_pdl && !g_pdl_suspended) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
-        na++;
-    }
-    if (g_prio_on && g_step_prio) {
-        at[na].id = cudaLaunchAttributePriority;
-        at[na].val.priority = g_step_prio;
         na++;
     }
     cfg.attrs = at;
@@ -126,7 +115,6 @@ struct Step {
     int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
     int jpc = 1;              // ST_XF cluster launch: transforms per cluster
     int lane = -1;            // in a group: steps of one lane run in order on one branch
-    int prio = 0;             // launch priority (0 = default; lower = more urgent)
 };
 
 struct Schedule {
@@ -134,7 +122,7 @@ struct Schedule {
     std::vector<void*> allocs;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
-    int cur_group = 0, next_group = 1, cur_lane = -1, cur_prio = 0;
+    int cur_group = 0, next_group = 1, cur_lane = -1;
     bool cl_in_lane = false;  // allow cluster launches inside a lane
     // steps added between par_begin() and par_end() are independent: they are
     // captured on forked streams (parallel graph branches)
@@ -398,7 +386,6 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
             st.hjobs = part;
             st.group = S.cur_group;
             st.lane = S.cur_lane;
-            st.prio = S.cur_prio;
             int rc = upload_jobs(S, st, part.data(), part.size() * sizeof(XJob));
             if (rc) return rc;
             S.steps.push_back(st);
@@ -414,7 +401,6 @@ static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
     st.kind = ST_CO;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
-    st.prio = S.cur_prio;
     st.njobs = (int)jobs.size();
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(CJob));
     if (rc) return rc;
@@ -429,7 +415,6 @@ static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
     st.kind = ST_MA;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
-    st.prio = S.cur_prio;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(MJob));
@@ -445,7 +430,6 @@ static int add_dx(Schedule& S, std::vector<DXJob> jobs, int nprime) {
     st.kind = ST_DX;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
-    st.prio = S.cur_prio;
     st.njobs = (int)jobs.size();
     st.gy = nprime;
     int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(DXJob));
@@ -460,7 +444,6 @@ static int add_i2(Schedule& S, std::vector<Intt2Job> jobs) {
         st.kind = ST_I2;
         st.group = S.cur_group;
         st.lane = S.cur_lane;
-        st.prio = S.cur_prio;
         st.i2jobs.assign(jobs.begin() + c0, jobs.begin() + std::min(jobs.size(), c0 + (size_t)I2_MAX));
         for (Intt2Job& j : st.i2jobs) j.j[0].trace = j.j[1].trace = g_trace_seq;
         g_trace_seq++;
@@ -502,7 +485,6 @@ static bool step_one_wave(const Step& st) {
 
 static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
     g_step_pdl = st.group == 0 && step_one_wave(st);
-    g_step_prio = st.prio;
     {
         switch (st.kind) {
             case ST_XF: {
@@ -1120,17 +1102,10 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         if (nl > 1) S.par_begin();
         for (int lane = 0; lane < nl; lane++) {
             S.cur_lane = nl > 1 ? lane : -1;
-            // later pipeline stages first: when an SM frees up, a lane's MAC or
-            // diagonal INTTs take it before the other lanes' queued digit NTTs,
-            // so finished lanes drain instead of all meeting in one tail
             for (int tl = lane; tl < cb; tl += nl) {
-                S.cur_prio = 0;
                 rc = add_xf(S, s7[tl]); if (rc) return rc;
-                S.cur_prio = -1;
                 rc = add_ma(S, s8[tl], 3); if (rc) return rc;
-                S.cur_prio = -2;
                 rc = add_xf(S, s9[tl]); if (rc) return rc;
-                S.cur_prio = 0;
             }
         }
         S.cur_lane = -1;
