@@ -43,7 +43,8 @@ N_DEFAULT, S_DEFAULT, P_DEFAULT, RING = 1 << 14, 16, 65537, 8192
 
 # hcomp.cu StepKind -> the kernels behind it (hc_comp_profile's step kinds)
 STEP_KINDS = {0: "transforms (k_xf, k_xf_cl)", 1: "crt_digits (k_compose)", 2: "key_mac (k_ksmac)",
-              3: "diag_mac (k_diagx)", 5: "memset", 6: "two_prime_intt (k_cl_intt2)"}
+              3: "diag_mac (k_diagx)", 5: "memset", 6: "two_prime_intt (k_cl_intt2)",
+              7: "key_mac_grouped (k_ksmac_mb)"}
 
 
 def metric_name(N: int, s: int) -> str:

@@ -99,7 +99,7 @@ static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6 };  // values: bench.py per_kind_ms keys
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7 };  // values: bench.py per_kind_ms keys
 struct Step {
     int kind = 0;
     int njobs = 0;
@@ -409,6 +409,52 @@ static int add_co(Schedule& S, const std::vector<CJob>& jobs) {
 }
 static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
     if (jobs.empty()) return HC_OK;
+    // throughput regime: single-term jobs that share a key (one rotation or
+    // the column swap over several blocks) go out in groups of MB_MAX, each
+    // key digit loaded once per group (k_ksmac_mb; HC_KSMAC_MB=0: off)
+    static int mb_on = -1;
+    if (mb_on < 0) {
+        const char* e = getenv("HC_KSMAC_MB");
+        mb_on = (e && e[0] == '0') ? 0 : 1;
+    }
+    bool single = true;
+    for (const MJob& m : jobs) single = single && m.nterm == 1;
+    if (mb_on && single && jobs.size() > 16) {
+        std::vector<MBJob> mb;
+        std::vector<int> used(jobs.size(), 0);
+        for (size_t i = 0; i < jobs.size(); i++) {
+            if (used[i]) continue;
+            MBJob g{};
+            g.level = jobs[i].level;
+            g.key = jobs[i].t[0].key;
+            g.perm = jobs[i].t[0].perm;
+            for (size_t k2 = i; k2 < jobs.size() && g.nb < MB_MAX; k2++) {
+                const MJob& m = jobs[k2];
+                if (used[k2] || m.t[0].key != g.key || m.t[0].perm != g.perm || m.level != g.level) continue;
+                used[k2] = 1;
+                g.dntt[g.nb] = m.t[0].dntt;
+                g.c0src[g.nb] = m.t[0].c0src;
+                g.add0[g.nb] = m.add0;
+                g.add1[g.nb] = m.add1;
+                g.out0[g.nb] = m.out0;
+                g.out1[g.nb] = m.out1;
+                g.nb++;
+            }
+            g.trace = g_trace_seq;
+            mb.push_back(g);
+        }
+        g_trace_seq++;
+        Step st;
+        st.kind = ST_MB;
+        st.group = S.cur_group;
+        st.lane = S.cur_lane;
+        st.njobs = (int)mb.size();
+        st.gy = nprime;
+        int rc = upload_jobs(S, st, mb.data(), mb.size() * sizeof(MBJob));
+        if (rc) return rc;
+        S.steps.push_back(st);
+        return HC_OK;
+    }
     for (MJob& j : jobs) j.trace = g_trace_seq;
     g_trace_seq++;
     Step st;
@@ -476,7 +522,8 @@ static bool step_one_wave(const Step& st) {
             if (st.hjobs[0].noxf) return st.njobs * (NPOLY / 256) <= g_pdl_maxcta;
             if (st.cl && st.njobs <= CL_MAX) return true;
             return st.njobs < g_vt2_jobs && st.njobs <= std::min(sms, g_pdl_maxcta);
-        case ST_MA: return (NPOLY / 256) * st.gy * st.njobs <= g_pdl_maxcta;
+        case ST_MA:
+        case ST_MB: return (NPOLY / 256) * st.gy * st.njobs <= g_pdl_maxcta;
         case ST_DX: return (NPOLY / 256) * st.njobs <= g_pdl_maxcta;
         case ST_CO: return (NPOLY / 256) * st.njobs <= std::max(g_pdl_maxcta, 148);  // small composes (latency path)
         default: return true;
@@ -538,6 +585,9 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                     CU(launch(k_ksmac<1, 1>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
                 else  // small (latency path): 4 digits' loads in flight per thread
                     CU(launch(k_ksmac<1, 4>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
+                break;
+            case ST_MB:
+                CU(launch(k_ksmac_mb, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MBJob*)st.djobs));
                 break;
             case ST_DX:
                 CU(launch(k_diagx, dim3(NPOLY / 256, 1, st.njobs), 256, 0, s, h->hctx, (const DXJob*)st.djobs));

@@ -975,6 +975,72 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_co
 }
 
 // ---------------------------------------------------------------------------
+// k_ksmac_mb: the throughput-regime key-switch MAC over up to MB_MAX blocks
+// that share one key (the same rotation or the column swap of different
+// blocks): each thread loads a key digit pair once and applies it to every
+// block's digit NTT, so the key stream is read once per group instead of once
+// per block.  Same sums and output as k_ksmac with nterm = 1.
+// grid (n/256, P, ngroups).
+// ---------------------------------------------------------------------------
+constexpr int MB_MAX = 4;
+struct MBJob {
+    int level, nb;
+    int trace, pad;             // HC_TRACE builds: launch sequence number
+    const u64* key;             // [D_L][2][L+1][n] Montgomery, shared by the group
+    const uint16_t* perm;       // c0 permutation (shared), with c0src
+    const u64* dntt[MB_MAX];    // [D][P][n] per block
+    const u64* c0src[MB_MAX];   // [P][n] (nullable)
+    const u64* add0[MB_MAX];
+    const u64* add1[MB_MAX];
+    u64* out0[MB_MAX];
+    u64* out1[MB_MAX];
+};
+
+__global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx C, const MBJob* __restrict__ jobs) {
+    const MBJob& J = jobs[blockIdx.z];
+    TRACE(0);
+    const int k = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const LevelC& LV = C.lv[J.level];
+    const int P = LV.P, D = LV.D, L1 = C.L + 1;
+    const PrimeC pc = C.pc[k];
+    const size_t kn = (size_t)k * NPOLY + j;
+    const unsigned pe = J.perm ? J.perm[j] : 0u;
+    const int nb = J.nb;
+    pdl_wait();
+    u64 h0[MB_MAX], l0[MB_MAX], h1[MB_MAX], l1[MB_MAX];
+    HC_UNROLL
+    for (int b = 0; b < MB_MAX; b++) h0[b] = l0[b] = h1[b] = l1[b] = 0;
+    const u64* bp = J.key + kn;
+    const size_t vstep = (size_t)P * NPOLY, kstep = (size_t)2 * L1 * NPOLY, astep = (size_t)L1 * NPOLY;
+#pragma unroll 2
+    for (int d = 0; d < D; d++) {
+        const u64 kb = __ldg(bp + d * kstep);
+        const u64 ka = __ldg(bp + d * kstep + astep);
+        u64 v[MB_MAX];
+        HC_UNROLL
+        for (int b = 0; b < MB_MAX; b++) v[b] = b < nb ? __ldcs(J.dntt[b] + kn + d * vstep) : 0;
+        HC_UNROLL
+        for (int b = 0; b < MB_MAX; b++) {
+            mac128(h0[b], l0[b], v[b], kb);
+            mac128(h1[b], l1[b], v[b], ka);
+        }
+    }
+    TRACE(4);
+    HC_UNROLL
+    for (int b = 0; b < MB_MAX; b++) {
+        if (b >= nb) break;
+        u64 o0 = redc(h0[b], l0[b], pc.q, pc.qneg), o1 = redc(h1[b], l1[b], pc.q, pc.qneg);
+        if (J.add0[b]) o0 = add_mod(o0, J.add0[b][kn], pc.q);
+        if (J.add1[b]) o1 = add_mod(o1, J.add1[b][kn], pc.q);
+        if (J.c0src[b]) o0 = add_mod(o0, J.c0src[b][(size_t)k * NPOLY + pe], pc.q);
+        J.out0[b][kn] = o0;
+        J.out1[b][kn] = o1;
+    }
+    TRACE(5);
+}
+
+// ---------------------------------------------------------------------------
 // k_diagx: grid (n/256, 1, njobs), the two kept primes per thread.  X[k][j] += sum_t src_t[k][j] * dg_t[k][j]
 // (dg Montgomery with q^-1 folded in) -- the kept-prime half of each
 // plaintext product -- and E[k][j] += sum_t d_t - (sum_t r_t) q_l^-1 from the
