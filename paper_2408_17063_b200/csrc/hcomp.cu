@@ -419,6 +419,13 @@ static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
     }
     bool single = true;
     for (const MJob& m : jobs) single = single && m.nterm == 1;
+    // blocks per group: 2 (48 registers, 5 CTAs/SM) measured best -- N=2^20:
+    // 5.68 ms vs 5.77 with 4 and 7.08 with 8 (HC_KSMAC_MB_N=4 for A/B)
+    static int mb_n = -1;
+    if (mb_n < 0) {
+        const char* e = getenv("HC_KSMAC_MB_N");
+        mb_n = (e && atoi(e) >= 4) ? 4 : 2;
+    }
     if (mb_on && single && jobs.size() > 16) {
         std::vector<MBJob> mb;
         std::vector<int> used(jobs.size(), 0);
@@ -428,7 +435,7 @@ static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
             g.level = jobs[i].level;
             g.key = jobs[i].t[0].key;
             g.perm = jobs[i].t[0].perm;
-            for (size_t k2 = i; k2 < jobs.size() && g.nb < MB_MAX; k2++) {
+            for (size_t k2 = i; k2 < jobs.size() && g.nb < mb_n; k2++) {
                 const MJob& m = jobs[k2];
                 if (used[k2] || m.t[0].key != g.key || m.t[0].perm != g.perm || m.level != g.level) continue;
                 used[k2] = 1;
@@ -450,6 +457,7 @@ static int add_ma(Schedule& S, std::vector<MJob> jobs, int nprime) {
         st.lane = S.cur_lane;
         st.njobs = (int)mb.size();
         st.gy = nprime;
+        st.jpc = mb_n;  // group width -> instantiation
         int rc = upload_jobs(S, st, mb.data(), mb.size() * sizeof(MBJob));
         if (rc) return rc;
         S.steps.push_back(st);
@@ -587,7 +595,10 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                     CU(launch(k_ksmac<1, 4>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
                 break;
             case ST_MB:
-                CU(launch(k_ksmac_mb, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MBJob*)st.djobs));
+                if (st.jpc == 4)
+                    CU(launch(k_ksmac_mb<4>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MBJob*)st.djobs));
+                else
+                    CU(launch(k_ksmac_mb<2>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MBJob*)st.djobs));
                 break;
             case ST_DX:
                 CU(launch(k_diagx, dim3(NPOLY / 256, 1, st.njobs), 256, 0, s, h->hctx, (const DXJob*)st.djobs));

@@ -975,7 +975,7 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_co
 }
 
 // ---------------------------------------------------------------------------
-// k_ksmac_mb: the throughput-regime key-switch MAC over up to MB_MAX blocks
+// k_ksmac_mb<NB>: the throughput-regime key-switch MAC over up to NB blocks
 // that share one key (the same rotation or the column swap of different
 // blocks): each thread loads a key digit pair once and applies it to every
 // block's digit NTT, so the key stream is read once per group instead of once
@@ -996,6 +996,7 @@ struct MBJob {
     u64* out1[MB_MAX];
 };
 
+template <int NB>
 __global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx C, const MBJob* __restrict__ jobs) {
     const MBJob& J = jobs[blockIdx.z];
     TRACE(0);
@@ -1008,27 +1009,27 @@ __global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx
     const unsigned pe = J.perm ? J.perm[j] : 0u;
     const int nb = J.nb;
     pdl_wait();
-    u64 h0[MB_MAX], l0[MB_MAX], h1[MB_MAX], l1[MB_MAX];
+    u64 h0[NB], l0[NB], h1[NB], l1[NB];
     HC_UNROLL
-    for (int b = 0; b < MB_MAX; b++) h0[b] = l0[b] = h1[b] = l1[b] = 0;
+    for (int b = 0; b < NB; b++) h0[b] = l0[b] = h1[b] = l1[b] = 0;
     const u64* bp = J.key + kn;
     const size_t vstep = (size_t)P * NPOLY, kstep = (size_t)2 * L1 * NPOLY, astep = (size_t)L1 * NPOLY;
 #pragma unroll 2
     for (int d = 0; d < D; d++) {
         const u64 kb = __ldg(bp + d * kstep);
         const u64 ka = __ldg(bp + d * kstep + astep);
-        u64 v[MB_MAX];
+        u64 v[NB];
         HC_UNROLL
-        for (int b = 0; b < MB_MAX; b++) v[b] = b < nb ? __ldcs(J.dntt[b] + kn + d * vstep) : 0;
+        for (int b = 0; b < NB; b++) v[b] = b < nb ? __ldcs(J.dntt[b] + kn + d * vstep) : 0;
         HC_UNROLL
-        for (int b = 0; b < MB_MAX; b++) {
+        for (int b = 0; b < NB; b++) {
             mac128(h0[b], l0[b], v[b], kb);
             mac128(h1[b], l1[b], v[b], ka);
         }
     }
     TRACE(4);
     HC_UNROLL
-    for (int b = 0; b < MB_MAX; b++) {
+    for (int b = 0; b < NB; b++) {
         if (b >= nb) break;
         u64 o0 = redc(h0[b], l0[b], pc.q, pc.qneg), o1 = redc(h1[b], l1[b], pc.q, pc.qneg);
         if (J.add0[b]) o0 = add_mod(o0, J.add0[b][kn], pc.q);
