@@ -523,6 +523,10 @@ def main():
             "peak_source": "measured live: hc_bf_peak, register-only microbenchmark of the kernels' own lazy CT butterfly at full occupancy (MEASURED_PEAKS.json has no integer peak)",
             "work_unit": "one radix-2 butterfly = one 54-bit modmul + 2 modadds; 4096*13 per 8192-point transform",
             "traffic": None,
+            "traffic_note": ("DRAM bytes per launch from ncu --set full captures are in "
+                             "profiles/r01_ncu_full_summary.txt (the family mixes launches of 1-396 jobs, "
+                             "so no single per-launch figure applies); e.g. 592 forward transforms read "
+                             "39.4 MB = their inputs, no re-reads"),
             "comp_level_gbfly_s": comp_level,
             "comp_level_frac": comp_level / peak_g if peak_g else None,
             "xform_share_of_step": xf_ms / prof_total if prof_total else None,
