@@ -81,6 +81,9 @@ static bool pdl_on() {
 static thread_local bool g_step_pdl = true;
 static thread_local bool g_pdl_suspended = false;  // hc_comp_profile: launches timed one by one
 template <typename... KArgs, typename... Args>
+static cudaError_t launch_cl(void (*k)(KArgs...), int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args);
+template <typename... KArgs, typename... Args>
 static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -89,6 +92,31 @@ static cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     int na = 0;
+    if (pdl_on() && g_step_pdl && !g_pdl_suspended) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        na++;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+// runtime cluster dimension (non-portable sizes), PDL as launch()
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_cl(void (*k)(KArgs...), int cluster, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    na++;
     if (pdl_on() && g_step_pdl && !g_pdl_suspended) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
@@ -176,6 +204,7 @@ static void release_key(DevKey& k) {
     X(1, LD_KSFIN, EP_RESCALE)
 
 static int kernels_configured = 0;
+static int g_i2_16 = 0;  // co-resident 16-CTA clusters (0: two-prime INTTs on 8-CTA clusters)
 // co-resident 8-CTA transform clusters (one CTA per SM) on the current device
 static int max_active_clusters(int* clusters) {
     cudaLaunchConfig_t cfg{};
@@ -211,6 +240,28 @@ static int configure_kernels() {
     CU(cudaFuncSetAttribute(k_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * NPOLY * 8));
     CU(cudaFuncSetAttribute(k_cl_intt2<LD_KSFIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
     CU(cudaFuncSetAttribute(k_cl_intt2<LD_RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaFuncSetAttribute(k_cl16_intt2<LD_KSFIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaFuncSetAttribute(k_cl16_intt2<LD_RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaFuncSetAttribute(k_cl16_intt2<LD_KSFIN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CU(cudaFuncSetAttribute(k_cl16_intt2<LD_RED>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    {  // 16-CTA clusters for the two-prime INTT when the part can co-schedule them
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(CNT);
+        cfg.dynamicSmemBytes = CL_SPREAD_SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n16 = 0;
+        if (cudaOccupancyMaxActiveClusters(&n16, k_cl16_intt2<LD_KSFIN>, &cfg) != cudaSuccess) n16 = 0;
+        cudaGetLastError();
+        const char* e = getenv("HC_I2_16");
+        g_i2_16 = (e && e[0] == '0') ? 0 : n16;
+    }
     {
         int n = 0;
         if (max_active_clusters(&n) == HC_OK && n > 0) g_cl_chunk = std::min(n, CL_MAX / CL_JPC_MAX);
@@ -611,10 +662,15 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 memset(&jj, 0, sizeof jj);
                 memcpy(jj.j, st.i2jobs.data(), st.i2jobs.size() * sizeof(Intt2Job));
                 const int n = (int)st.i2jobs.size();
-                if (st.i2jobs[0].j[0].ld == LD_KSFIN)
+                const bool ksfin = st.i2jobs[0].j[0].ld == LD_KSFIN;
+                if (n <= g_i2_16) {  // one 16-CTA cluster per job (a prime per 8 CTAs)
+                    if (ksfin) CU(launch_cl(k_cl16_intt2<LD_KSFIN>, 16, n * 16, CNT, CL_SPREAD_SMEM, s, h->hctx, jj));
+                    else CU(launch_cl(k_cl16_intt2<LD_RED>, 16, n * 16, CNT, CL_SPREAD_SMEM, s, h->hctx, jj));
+                } else if (ksfin) {
                     CU(launch(k_cl_intt2<LD_KSFIN>, n * CL, 2 * CNT, CL_SPREAD_SMEM, s, h->hctx, jj));
-                else
+                } else {
                     CU(launch(k_cl_intt2<LD_RED>, n * CL, 2 * CNT, CL_SPREAD_SMEM, s, h->hctx, jj));
+                }
                 break;
             }
         }

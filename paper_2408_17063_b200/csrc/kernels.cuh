@@ -797,6 +797,129 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
 }
 
 // ---------------------------------------------------------------------------
+// k_cl16_intt2: the same job on a 16-CTA cluster (non-portable size, launched
+// with a runtime cluster dimension): CTAs 0-7 invert prime 0, CTAs 8-15 prime
+// 1, one INTT per CTA group as in k_xf_cl (128 threads x 8 coefficients), so
+// each SM carries half the butterflies of k_cl_intt2 (whose passes ran at
+// ~0.77 of the butterfly peak of one SM -- throughput-, not latency-bound).
+// Then CTA (0, c) and CTA (1, c), which hold the same coefficients mod the
+// two primes, swap halves over DSMEM and each composes 512 of them.
+// ---------------------------------------------------------------------------
+template <int LD>
+__global__ void __launch_bounds__(CNT) k_cl16_intt2(const __grid_constant__ DevCtx C, const __grid_constant__ Intt2Jobs jobs) {
+    extern __shared__ u64 dsm[];  // tile | recv | twiddle slice | half-exchange buffer | 2 mbarriers
+    u64* tile = dsm;
+    u64* recvb = dsm + CTILE;
+    Tw* twsl = reinterpret_cast<Tw*>(dsm + 2 * CTILE);
+    u64* half = dsm + 4 * CTILE;        // 4 x 128 values from the partner CTA
+    u64* xbar = dsm + 4 * CTILE + 512;  // INTT all-to-all
+    u64* hbar = xbar + 1;               // half exchange
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int pr = rank >> 3, c = rank & 7;
+    const int t = threadIdx.x;
+    xch_init(xbar, CTILE * 8);
+    xch_init(hbar, 4 * CNT * 8);
+    cluster_arrive_relaxed();
+    const Intt2Job& JJ = jobs.j[blockIdx.x / 16];
+    const XJob& J = JJ.j[pr];
+    TRACE(0);
+    const PrimeC& P = C.pc[pr];
+    const Tw* tw = C.twi + (size_t)pr * NPOLY;
+    u64 x[CEPT];
+    TwPre pre;
+    tw_issue(pre, tw, c, t);
+    Tw wa[8];
+    HC_UNROLL
+    for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);
+    const int jl = c * CTILE + t;
+    LdPre<LD, CEPT> lpre;
+    load_pre<LD, CEPT>(J, jl, 128, lpre);
+    pdl_wait();
+    load_post<LD, CEPT>(C, J, P, jl, 128, lpre, x);
+    tw_commit(twsl, pre, t);
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+    __syncthreads();
+    TRACE(1);
+    const TwL twl{twsl, c};
+    HC_UNROLL
+    for (int p = 0; p < 3; p++) {
+        const CPass I = cpass(2 - p, c, t);
+        c_load(x, tile, I);
+        if (p == 0) c_st0(c, t, x, twl, P.q, P.q2);
+        r8_gs(x, twl, 1 + 3 * p, I.G, P.q, 2 * P.q2);
+        if (p < 2) {
+            c_store(x, tile, I);
+            __syncthreads();
+        }
+    }
+    TRACE(4);
+    pdl_trigger();
+    cluster_wait();
+    HC_UNROLL
+    for (int v = 0; v < CEPT; v++) xch_put(cl, recvb + c * 128 + t, pr * 8 + v, x[v], xbar);
+    xch_wait(xbar);
+    HC_UNROLL
+    for (int r = 0; r < CEPT; r++) x[r] = recvb[r * 128 + t];
+    c_phaseA_inv_w(x, wa, P);
+    // x[r] = coefficient r*1024 + 128c + t mod q_pr.  Prime-0 CTAs compose
+    // r = 0..3, prime-1 CTAs r = 4..7: send the other half to the partner.
+    const int partner = (1 - pr) * 8 + c;
+    const int mine0 = pr ? 4 : 0, theirs0 = pr ? 0 : 4;
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) xch_put(cl, half + i * CNT + t, partner, x[theirs0 + i], hbar);
+    xch_wait(hbar);
+    TRACE(3);
+    const LevelC& LV = C.lv[1];
+    const int D = LV.D;
+    const u64* E = JJ.E;
+    uint16_t* dig = JJ.dig;
+    u64* out0 = JJ.j[0].out;
+    u64* out1 = JJ.j[1].out;
+    u64 a[4], b[4];
+    int jj[4];
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) {
+        const u64 mine = x[mine0 + i], other = half[i * CNT + t];
+        a[i] = pr ? other : mine;  // residue mod q0
+        b[i] = pr ? mine : other;  // residue mod q1
+        jj[i] = (mine0 + i) * CTILE + 128 * c + t;
+    }
+    if (E) {
+        HC_UNROLL
+        for (int i = 0; i < 4; i++) {
+            a[i] = add_mod(a[i], red64(E[jj[i]], C.pc[0].q, C.pc[0].one_s), C.pc[0].q);
+            b[i] = add_mod(b[i], red64(E[NPOLY + jj[i]], C.pc[1].q, C.pc[1].one_s), C.pc[1].q);
+        }
+    }
+    if (out0) {  // optional coefficient side store
+        HC_UNROLL
+        for (int i = 0; i < 4; i++) {
+            out0[jj[i]] = a[i];
+            out1[jj[i]] = b[i];
+        }
+    }
+    u64 X[4][NLIMB];
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) compose2(LV, C.pc, a[i], b[i], X[i]);
+    HC_UNROLL
+    for (int d = 0; d < 8; d++)
+        if (d < D)
+            HC_UNROLL
+            for (int i = 0; i < 4; i++) dig[(size_t)d * NPOLY + jj[i]] = digit16(X[i], d);
+    HC_UNROLL
+    for (int i = 0; i < 4; i++) neg_mod_Q<1>(LV, X[i]);
+    HC_UNROLL
+    for (int d = 0; d < 8; d++)
+        if (d < D)
+            HC_UNROLL
+            for (int i = 0; i < 4; i++) dig[(size_t)(D + d) * NPOLY + jj[i]] = digit16(X[i], d);
+    TRACE(5);
+}
+constexpr int CL16_SMEM = (4 * CTILE + 512 + 2) * 8;
+
+// ---------------------------------------------------------------------------
 // k_compose: grid (n/256, njobs)
 // ---------------------------------------------------------------------------
 struct CJob {

@@ -242,12 +242,11 @@ inline void host_st0(int c, int n, u64 (*regs)[CEPT], const TW& tw, u64 q, u64 q
 // forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
 HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q4) { r8_ct(x, TwG{tw}, 0, 0, q, q4); }
 
-// inverse phase A': GS stages 10, 11 on the column, then bit 12 folded with n^-1
-HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
+// inverse phase A': GS stages 10, 11 on the column, then bit 12 folded with n^-1;
+// wa = inv_tbl[1..7] (stages 10, 11 use indices 2..7), preloadable by the
+// caller (constant)
+HD void c_phaseA_inv_w(u64 (&x)[CEPT], const Tw (&wa)[8], const PrimeC& P) {
     const u64 q = P.q, q4 = 2 * P.q2;
-    Tw wa[8];  // inv_tbl[1..7] (stages 10, 11 use indices 2..7)
-    HC_UNROLL
-    for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);
     HC_UNROLL
     for (int u = 0; u < 2; u++) {
         const int half = 1 << u;
@@ -267,6 +266,12 @@ HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
         x[v] = reduce_once(mul_shoup_lazy(a + b, P.ninv, P.ninv_s, q), q);
         x[v + 4] = reduce_once(mul_shoup_lazy(a - b + q4, P.ninvw, P.ninvw_s, q), q);
     }
+}
+HD void c_phaseA_inv(u64 (&x)[CEPT], const Tw* tw, const PrimeC& P) {
+    Tw wa[8];
+    HC_UNROLL
+    for (int i = 1; i < 8; i++) wa[i] = ldtw(tw, i);
+    c_phaseA_inv_w(x, wa, P);
 }
 
 // ---- host emulation of the cluster schedule (CPU self-test only) ----------
