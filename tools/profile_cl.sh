@@ -7,7 +7,7 @@ $NCU --set full --import-source on --clock-control none --nvtx --nvtx-include "t
   -k "regex:k_xf_cl<.int.0, .int.5, .int.6, .int.1>" --launch-skip 3 -c 1 -o $O/ncu_full_xf_cl_fold -f \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_full_cl.log 2>&1
 $NCU --set full --import-source on --clock-control none --nvtx --nvtx-include "timed/" --kernel-name-base demangled \
-  -k "regex:k_cl_intt2<.int.8>" --launch-skip 3 -c 1 -o $O/ncu_full_intt2_fold -f \
+  -k "regex:k_cl16_intt2<.int.8>" --launch-skip 3 -c 1 -o $O/ncu_full_intt2_fold -f \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_full_i2.log 2>&1
 $NCU --set full --import-source on --clock-control none --nvtx --nvtx-include "timed/" --kernel-name-base demangled \
   -k "regex:k_xf<.int.1, .int.1, .int.5, .int.1>" --launch-skip 1 -c 1 -o $O/ncu_full_xf_diag_intt -f \
