@@ -1177,6 +1177,63 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         }
                     }
         }
+        // S10 job lists for the blocks [tl0, tl1) of the chunk; `atomic`: the
+        // lanes' per-block launches run concurrently and add their sums into
+        // PX with atomics (PX words stay < 4q: every consumer reduces them)
+        auto build_dx = [&](int tl0, int tl1, bool atomic) -> int {
+            std::vector<DXJob> dx;
+            std::vector<const u64*> srcs, dgs, ess;
+            struct Rng { size_t off, cnt; int g, poly; };
+            std::vector<Rng> rngs;
+            for (int g = 0; g < G; g++)
+                for (int poly = 0; poly < 2; poly++) {
+                    size_t off = srcs.size();
+                    for (int tl = tl0; tl < tl1; tl++) {
+                        const long long t = c0 + tl;
+                        for (int b = 0; b < baby; b++) {
+                            const int i = g * baby + b;
+                            if (!P.live[(size_t)t * sp + i]) continue;
+                            srcs.push_back(rot_src(P, tl, b, poly));
+                            dgs.push_back(P.diag + ((size_t)t * sp + i) * 3 * NB);
+                            ess.push_back(eslot(P, tl, b, g, poly));
+                        }
+                    }
+                    rngs.push_back({off, srcs.size() - off, g, poly});
+                }
+            if (srcs.empty()) return HC_OK;
+            const u64** dsrc = nullptr;
+            const u64** ddg = nullptr;
+            const u64** des = nullptr;
+            CU(cudaMalloc(&dsrc, srcs.size() * sizeof(u64*)));
+            S.allocs.push_back(dsrc);
+            CU(cudaMalloc(&ddg, dgs.size() * sizeof(u64*)));
+            S.allocs.push_back(ddg);
+            CU(cudaMalloc(&des, ess.size() * sizeof(u64*)));
+            S.allocs.push_back(des);
+            CU(cudaMemcpy(dsrc, srcs.data(), srcs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+            CU(cudaMemcpy(ddg, dgs.data(), dgs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+            CU(cudaMemcpy(des, ess.data(), ess.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+            for (const Rng& r : rngs) {
+                if (!r.cnt) continue;
+                DXJob d{};
+                d.nterm = (int)r.cnt;
+                d.level = 2;
+                d.atomic = atomic ? 1 : 0;
+                d.src = dsrc + r.off;
+                d.dg = ddg + r.off;
+                d.es = des + r.off;
+                d.X = P.PX + (size_t)1 * G * 2 * 2 * NB + (((size_t)r.g * 2 + r.poly) * 2) * NB;
+                d.E = P.PX + (((size_t)r.g * 2 + r.poly) * 2) * NB;
+                dx.push_back(d);
+            }
+            return add_dx(S, dx, 2);
+        };
+        static int lane_dx = -1;  // HC_LANE_DX=0: one S10 launch after all lanes (A/B)
+        if (lane_dx < 0) {
+            const char* e = getenv("HC_LANE_DX");
+            lane_dx = (e && e[0] == '0') ? 0 : 1;
+        }
+        bool lanes_dx = false;
         rc = add_xf(S, s1); if (rc) return rc;
         // S2 (P and R.c0 at level 2) is independent of S2c -> S3 (R.c1's
         // digits and their NTTs): at small chunks (latency regime) they run as
@@ -1219,10 +1276,15 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         if (nl > 1) S.par_begin();
         for (int lane = 0; lane < nl; lane++) {
             S.cur_lane = nl > 1 ? lane : -1;
+            lanes_dx = lane_dx && nl > 1;
             for (int tl = lane; tl < cb; tl += nl) {
                 rc = add_xf(S, s7[tl]); if (rc) return rc;
                 rc = add_ma(S, s8[tl], 3); if (rc) return rc;
                 rc = add_xf(S, s9[tl]); if (rc) return rc;
+                if (lanes_dx) {  // this block's diagonal MAC inside its lane
+                    rc = build_dx(tl, tl + 1, true);
+                    if (rc) return rc;
+                }
             }
         }
         S.cur_lane = -1;
@@ -1230,54 +1292,9 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         }
         // S10: per (g, poly): X += sum src * diag * q^-1 (kept primes) and
         //      E += sum of the chunk's correction slots
-        {
-            std::vector<DXJob> dx;
-            std::vector<const u64*> srcs, dgs, ess;
-            struct Rng { size_t off, cnt; int g, poly; };
-            std::vector<Rng> rngs;
-            for (int g = 0; g < G; g++)
-                for (int poly = 0; poly < 2; poly++) {
-                    size_t off = srcs.size();
-                    for (int tl = 0; tl < cb; tl++) {
-                        const long long t = c0 + tl;
-                        for (int b = 0; b < baby; b++) {
-                            const int i = g * baby + b;
-                            if (!P.live[(size_t)t * sp + i]) continue;
-                            srcs.push_back(rot_src(P, tl, b, poly));
-                            dgs.push_back(P.diag + ((size_t)t * sp + i) * 3 * NB);
-                            ess.push_back(eslot(P, tl, b, g, poly));
-                        }
-                    }
-                    rngs.push_back({off, srcs.size() - off, g, poly});
-                }
-            if (!srcs.empty()) {
-                const u64** dsrc = nullptr;
-                const u64** ddg = nullptr;
-                const u64** des = nullptr;
-                CU(cudaMalloc(&dsrc, srcs.size() * sizeof(u64*)));
-                S.allocs.push_back(dsrc);
-                CU(cudaMalloc(&ddg, dgs.size() * sizeof(u64*)));
-                S.allocs.push_back(ddg);
-                CU(cudaMalloc(&des, ess.size() * sizeof(u64*)));
-                S.allocs.push_back(des);
-                CU(cudaMemcpy(dsrc, srcs.data(), srcs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
-                CU(cudaMemcpy(ddg, dgs.data(), dgs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
-                CU(cudaMemcpy(des, ess.data(), ess.size() * sizeof(u64*), cudaMemcpyHostToDevice));
-                for (const Rng& r : rngs) {
-                    if (!r.cnt) continue;
-                    DXJob d{};
-                    d.nterm = (int)r.cnt;
-                    d.level = 2;
-                    d.src = dsrc + r.off;
-                    d.dg = ddg + r.off;
-                    d.es = des + r.off;
-                    d.X = P.PX + (size_t)1 * G * 2 * 2 * NB + (((size_t)r.g * 2 + r.poly) * 2) * NB;
-                    d.E = P.PX + (((size_t)r.g * 2 + r.poly) * 2) * NB;
-                    dx.push_back(d);
-                }
-                rc = add_dx(S, dx, 2);
-                if (rc) return rc;
-            }
+        if (!lanes_dx) {
+            rc = build_dx(0, cb, false);
+            if (rc) return rc;
         }
     }
     return HC_OK;

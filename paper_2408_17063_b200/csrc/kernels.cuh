@@ -1172,7 +1172,8 @@ __global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx
 // ---------------------------------------------------------------------------
 struct DXJob {
     int nterm, level;       // level: of the dropped prime behind the (r, d) slots
-    int trace, pad;         // HC_TRACE builds: launch sequence number
+    int trace;              // HC_TRACE builds: launch sequence number
+    int atomic;             // 1: add into X / E with atomics (concurrent launches; words < 4q)
     const u64* const* src;  // nterm pointers, each [>=nprime][n]
     const u64* const* dg;   // nterm pointers, each [>=nprime][n]
     const u64* const* es;   // nterm (r, d) slots [2][n] int64 (EP_RESCALE_RD), or null
@@ -1223,12 +1224,27 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
             }
     }
     TRACE(1);
-    J.X[j] = add_mod(J.X[j], redc(h0, l0, q0, C.pc[0].qneg), q0);
-    J.X[NPOLY + j] = add_mod(J.X[NPOLY + j], redc(h1, l1, q1, C.pc[1].qneg), q1);
+    const u64 x0 = redc(h0, l0, q0, C.pc[0].qneg), x1 = redc(h1, l1, q1, C.pc[1].qneg);
+    u64 e0 = 0, e1 = 0;
     if (es) {
         const LevelC& LV = C.lv[J.level];
-        J.E[j] = add_mod(J.E[j], corr_from_sums(sr, sd, q0, LV.qinv[0], LV.qinv_s[0], C.pc[0].one_s), q0);
-        J.E[NPOLY + j] = add_mod(J.E[NPOLY + j], corr_from_sums(sr, sd, q1, LV.qinv[1], LV.qinv_s[1], C.pc[1].one_s), q1);
+        e0 = corr_from_sums(sr, sd, q0, LV.qinv[0], LV.qinv_s[0], C.pc[0].one_s);
+        e1 = corr_from_sums(sr, sd, q1, LV.qinv[1], LV.qinv_s[1], C.pc[1].one_s);
+    }
+    if (J.atomic) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(J.X + j), (unsigned long long)x0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(J.X + NPOLY + j), (unsigned long long)x1);
+        if (es) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(J.E + j), (unsigned long long)e0);
+            atomicAdd(reinterpret_cast<unsigned long long*>(J.E + NPOLY + j), (unsigned long long)e1);
+        }
+    } else {
+        J.X[j] = add_mod(J.X[j], x0, q0);
+        J.X[NPOLY + j] = add_mod(J.X[NPOLY + j], x1, q1);
+        if (es) {
+            J.E[j] = add_mod(J.E[j], e0, q0);
+            J.E[NPOLY + j] = add_mod(J.E[NPOLY + j], e1, q1);
+        }
     }
     TRACE(4);
     TRACE(5);

@@ -4,9 +4,10 @@ The BSGS matvec is a sum over width-4096 blocks (compress.py:286-297): every
 block's pack, baby rotations and diagonal products are independent until
 they are added into the giant-step accumulators acc[g] at level 1.  Each
 rank runs those for a contiguous block range (libhcomp hc_comp_partial) and
-leaves partial accumulators whose words are all < 2^54; one uint64 SUM
-reduce to the root (NCCL over NVLink on GPUs; < 2^57 for <= 8 ranks, no
-overflow) combines them, and the root alone runs the giant-step and fold
+leaves partial accumulators whose words are all < 2^54 (< 2^56 when its
+last chunk ran as concurrent baby-step lanes, which add with atomics); one
+uint64 SUM reduce to the root (NCCL over NVLink on GPUs; < 2^59 for <= 8
+ranks, no overflow) combines them, and the root alone runs the giant-step and fold
 key switches and the output mask (hc_comp_finish), which do not shard:
 key switching is not additive bit-for-bit.
 
@@ -37,7 +38,7 @@ def shard_blocks(B: int, world: int, rank: int) -> tuple[int, int]:
 
 def reduce_partials(t, dist, group=None, root: int = 0):
     """Sum the ranks' partial accumulators on `root` (int64 view of uint64 words,
-    each < 2^54: the sum over <= 1023 ranks stays exact).  NCCL reduces device
+    each < 2^56: the sum over <= 255 ranks stays exact).  NCCL reduces device
     tensors in place; a CPU backend (gloo) goes through a host copy."""
     if t.is_cuda and dist.get_backend(group) != "nccl":
         h = t.cpu()
