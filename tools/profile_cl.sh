@@ -1,6 +1,7 @@
 #!/bin/bash
 # Full ncu capture of the latency-path transforms inside bench.py's timed region:
-# the fold digit NTT (k_xf_cl<0,5,6,1>) and the fold two-prime INTT (k_cl_intt2<8>).
+# the fold digit NTT (k_xf_cl<0,5,6,1>), the fold two-prime INTT (k_cl16_intt2<8>)
+# and the lane diagonal INTT (k_xf<1,1,5,1>).
 O=gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 $NCU --set full --import-source on --clock-control none --nvtx --nvtx-include "timed/" --kernel-name-base demangled \
