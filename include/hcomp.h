@@ -15,7 +15,10 @@
  * residue modulo level_prime(k) (bgv.py:104-106: row 0 = smallest prime,
  * the last row is the prime a modulus switch divides out), values in [0, q_k).
  * A ciphertext at level l is uint64[2][l+1][n] (c0 then c1), NTT domain.
- * Only n = 8192 and max_level <= 3 are supported.
+ * Only n = 8192 and max_level <= 4 are supported.  Key switching, CRT
+ * compose and the fused Comp run at levels <= 3 (the 4 smallest primes);
+ * level 4 is for the Mask / pack products of answer() (pdq.py:238-256),
+ * which enter Comp through hc_comp_packed.
  */
 #ifndef HCOMP_H
 #define HCOMP_H
@@ -38,6 +41,9 @@ typedef struct hc_ctx hc_ctx;
 
 /* last error message of the calling thread (static storage) */
 const char* hc_last_error(void);
+/* RNS table row of the plaintext prime p in hc_ntt / hc_pointwise prime
+ * indices (chain primes occupy rows 0..max_level) */
+int hc_plain_row(void);
 
 /* Replaces BgvBackend.__init__ tables (bgv.py:328-363) and NttContext.__init__
  * (bgv.py:150-174).  primes: the L+1 chain primes in LEVEL order
@@ -52,7 +58,9 @@ int hc_ctx_digits(const hc_ctx* h, int* digits);
 /* Replaces KeySet.rotation_keys / col_swap_key material (bgv.py:482-509,
  * _KskPair bgv.py:294-312).  Uploads one gadget key-switch key for the
  * Galois element t (3^r mod 2n for rot_row(r), 2n-1 for rot_col):
- * ksk = uint64[D_L][2][L+1][n] = (b_j, a_j) pairs, NTT domain residues. */
+ * ksk = uint64[D_L][2][L+1][n] = (b_j, a_j) pairs, NTT domain residues.
+ * At max_level 4 the device keeps the first D_3 digits on the 4 smallest
+ * primes (what _KskPair.at_level yields at levels <= 3). */
 int hc_load_ksk(hc_ctx* h, uint32_t galois_t, const uint64_t* ksk);
 int hc_clear_keys(hc_ctx* h);
 
@@ -75,6 +83,16 @@ int hc_plan_info(const hc_ctx* h, int64_t* info8);
  * host buffers: cd, cv = uint64[C][2][4][n] at level 3; out = uint64[2][1][n]
  * (the level-0 ciphertext of the CompressedAnswer).  Synchronous. */
 int hc_comp(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* out);
+
+/* Replaces compress.comp(cd, ..., index_hint=cv) when cd and cv sit at
+ * different levels -- answer()'s cd = mask(cv) (pdq.py:238-256) one level
+ * below cv, reconciled by add's _at_level (bgv.py:656-658) inside pack_pair
+ * (compress.py:338-367).  The caller runs pack_pair with the single-op entry
+ * points below and passes its outputs: u = uint64[B][2][3][n], the B packed
+ * two-row ciphertexts at level 2 (NTT domain, canonical residues); the
+ * baby steps, diagonal products, giant steps, folds and the output mask run
+ * as in hc_comp (one graph launch).  out = uint64[2][1][n].  Synchronous. */
+int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t* out);
 
 /* Device-resident variant for timing: inputs already uploaded with
  * hc_comp_set_inputs; hc_comp_launch enqueues the whole Comp (one graph

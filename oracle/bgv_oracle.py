@@ -748,6 +748,12 @@ def comp(cd, N: int, s: int, be: OracleBgv, keys: OKeys, index_hint=None, masked
     return bsgs_matvec(plan, u, be, keys)
 
 
+def mask(cv, db, N: int, be: OracleBgv) -> list[OCt]:
+    """pdq.mask (pdq.py:238-245): d_i = v_i * value_i, plaintext multiply by
+    the cleartext database block matrices (_db_block_matrices, pdq.py:207-208)."""
+    return [be.mul_plain(c, m) for c, m in zip(cv, encode_vector(db, N, be.n, be.p))]
+
+
 def serialize_answer(be: OracleBgv, ct: OCt, s: int) -> bytes:
     """CompressedAnswer.serialize (compress.py:403-416), packed, one ct."""
     head = struct.pack("<HIBBBIIB", 1, s, 1, 0, 1, 0, 0, 1)

@@ -51,7 +51,16 @@ CASES = {
     "masked_small_n64_N200_s5": (64, 257, 200, 5, 13, True),
     "masked_c1_N8192_s8": (8192, 65537, 8192, 8, 4, False),
     "masked_c2_N16384_s16": (8192, 65537, 16384, 16, 5, False),
+    # Mask + Comp (pdq.answer after Match, pdq.py:238-256) on a 5-prime chain
+    # (max_level 4): cv = encrypted 0/1 index vector at level 4, cd =
+    # pdq.mask(cv, db) at level 3, then comp(cd, index_hint=cv) -- mixed input
+    # levels, reconciled by add's _at_level (bgv.py:656-658)
+    "answer_small_n64_N200_s5": (64, 257, 200, 5, 14, True),
+    "answer_c1_N8192_s8": (8192, 65537, 8192, 8, 6, False),
 }
+
+# max_level per case (default 3, the BASELINE chain)
+MAX_LEVEL = {"answer_small_n64_N200_s5": 4, "answer_c1_N8192_s8": 4}
 
 
 def masked_payload(N, s, p, seed):
@@ -114,14 +123,32 @@ def run_case(name):
     )
     from hcpdq.heiface import HeParams
 
-    he = HeParams(n, p, 3)
+    he = HeParams(n, p, MAX_LEVEL.get(name, 3))
     params = CompressionParams(N, s, he)
     be = BgvBackend(he, seed=seed)
     amounts, col = plan_rotation_amounts(s, n)
     t0 = time.time()
     keys = be.keygen(amounts, col_swap=col)
     masked = name.startswith("masked_")
-    if masked:
+    answer = name.startswith("answer_")
+    mask_counters = None
+    if answer:
+        import types
+
+        from hcpdq import pdq
+
+        support, db = masked_payload(N, s, p, seed)
+        dense = [0] * N
+        for i in support:
+            dense[i - 1] = db[i - 1]
+        hint = encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+        m0 = be.counters.snapshot()
+        cts = pdq.mask(hint, types.SimpleNamespace(values=db), params, be, keys)
+        mask_counters = be.counters.delta(m0).as_dict()
+
+        def run():
+            return comp(cts, params, be, keys, index_hint=hint)
+    elif masked:
         support, db = masked_payload(N, s, p, seed)
         dense = [0] * N
         for i in support:
@@ -169,6 +196,10 @@ def run_case(name):
         "seed": seed,
         "noise_guard_disabled": guard_off,
         "masked": masked,
+        "answer": answer,
+        "mask_counters": mask_counters,
+        "cts_levels": [c.level for c in cts],
+        "hint_levels": [c.level for c in hint],
         "chain_primes_desc": list(be.chain.primes),
         "key_id": keys.key_id.hex(),
         "support": support,

@@ -19,10 +19,12 @@ from .compress import (
     CompressedAnswer,
     DeviceComp,
     MaskedMatrix,
+    answer_from_match,
     comp,
     comp_masked,
     encode_vector,
     encrypt_vector,
+    mask,
     precompute_masked_matrix,
 )
 from .params import (

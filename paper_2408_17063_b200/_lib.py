@@ -50,6 +50,8 @@ _SIGS = [
     ("hc_plan_masked", _I, [_P, ctypes.c_int64, _I, _I, _P]),
     ("hc_plan_info", _I, [_P, _P]),
     ("hc_comp", _I, [_P, _P, _P, _I, _P]),
+    ("hc_comp_packed", _I, [_P, _P, _I64, _P]),
+    ("hc_plain_row", _I, []),
     ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),
     ("hc_comp_set_inputs", _I, [_P, _P, _P, _I]),
     ("hc_comp_set_inputs_range", _I, [_P, _P, _P, _I, _I, _P]),

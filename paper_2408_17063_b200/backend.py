@@ -40,7 +40,6 @@ CBD_HALF_WIDTH = 21  # bgv.py:48
 _OBJ_KIND_CIPHERTEXT = 0x01
 MAGIC = b"HCV1"
 FORMAT_VERSION = 1
-PIDX = 4  # RNS table index of the plaintext prime inside libhcomp
 
 
 # ---------------------------------------------------------------------------
@@ -299,8 +298,8 @@ class B200BgvBackend:
     ):
         if params.n != 8192:
             raise ValueError("the B200 backend supports n = 8192 only")
-        if not (1 <= params.max_level <= 3):
-            raise ValueError("the B200 backend supports max_level 1..3")
+        if not (1 <= params.max_level <= 4):
+            raise ValueError("the B200 backend supports max_level 1..4")
         if ksw_base_bits != 16:
             raise ValueError("ksw_base_bits must be 16")
         self.params = params
@@ -361,7 +360,7 @@ class B200BgvBackend:
 
     def ntt_p(self, a: np.ndarray, inverse: bool) -> np.ndarray:
         a = np.ascontiguousarray(a, dtype=np.uint64).copy().reshape(1, -1)
-        pidx = np.array([PIDX], dtype=np.int32)
+        pidx = np.array([_lib.lib().hc_plain_row()], dtype=np.int32)
         _lib.check(_lib.lib().hc_ntt(self._ctx(), _lib.ptr(a), 1, _lib.ptr(pidx), 1 if inverse else 0))
         return a[0]
 

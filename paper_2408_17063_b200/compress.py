@@ -120,11 +120,14 @@ class _NoiseSim:
         return r
 
 
+FUSED_LEVEL = 3  # input level of the fused pack_pair (the BASELINE chain's max level)
+
+
 def comp_noise(be: B200BgvBackend, params: CompressionParams, cv_bits, cd_bits, live) -> tuple[float, _NoiseSim]:
-    """noise_bits of comp's output and the counter deltas, in reference order."""
+    """noise_bits of comp's output and the counter deltas, in reference order
+    (inputs at level 3: the fused path)."""
     sim = _NoiseSim(be)
-    L = be.params.max_level
-    m = params.block_width
+    L = FUSED_LEVEL
     u = []
     for j in range(params.num_blocks):
         src = j // 2
@@ -136,9 +139,15 @@ def comp_noise(be: B200BgvBackend, params: CompressionParams, cv_bits, cd_bits, 
             r = sim.rot(sim.mul_plain(cv_bits[src], L), L - 1)
             b = sim.mul_plain(cd_bits[src], L)
             u.append(sim.add(r, b, L - 1))
+    return bsgs_noise(sim, params, u, live, L - 1)
+
+
+def bsgs_noise(sim: _NoiseSim, params: CompressionParams, u, live, lv: int) -> tuple[float, _NoiseSim]:
+    """bsgs_matvec's part of the sequence (compress.py:273-310) from the
+    packed ciphertexts' noise bits u at level lv."""
+    m = params.block_width
     baby, giant = bsgs_shape(params.s)
     acc = [None] * giant
-    lv = L - 1
     for t, ub in enumerate(u):
         rotated = [ub] + [sim.rot(ub, lv) for _ in range(1, baby)]
         for g in range(giant):
@@ -184,15 +193,45 @@ def _stack_level3(cts: Sequence[Ciphertext], L: int) -> np.ndarray:
     return np.ascontiguousarray(np.stack([c.payload.res for c in cts]), dtype=np.uint64)
 
 
-def _check_inputs(cd, cv, params: CompressionParams, backend: B200BgvBackend, keys: KeySet):
+def _check_inputs(cd, cv, params: CompressionParams, backend: B200BgvBackend, keys: KeySet) -> bool:
+    """Argument checks of the reference; returns True when pack_pair must run
+    as single operations (inputs not all at level 3, e.g. answer()'s
+    cd = mask(cv) one level below cv)."""
     if len(cv) != params.num_ciphertexts or len(cd) != params.num_ciphertexts:
         raise ValueError("expected standard-layout ciphertext lists")  # compress.py:348-349
     for c in list(cv) + list(cd):
         backend._check_keys(c, keys)
-        if c.level != backend.params.max_level:
-            raise ValueError("the fused B200 Comp takes fresh max-level ciphertexts (mixed levels: SURVEY 8(f)#2)")
     if keys.col_swap_key is None:
         raise MissingRotationKey("column-swap key was not declared at keygen")
+    pair_levels = {min(a.level, b.level) for a, b in zip(cv, cd)}
+    if pair_levels != {FUSED_LEVEL}:
+        if min(pair_levels) < FUSED_LEVEL:
+            # pack_pair lands below level 2, so the output mask's mul_plain
+            # would run at level 0 (bgv.py:721-722): the reference raises there
+            raise LevelExhausted("plaintext multiply at level 0 (Comp inputs below level 3)")
+        raise NotImplementedError(
+            "the B200 Comp runs pack_pair's outputs at level 2 (inputs at levels 3/4); inputs above level 3 "
+            "on both sides are not built"
+        )
+    return any(c.level != FUSED_LEVEL for c in list(cv) + list(cd))
+
+
+def _pack_pair_ops(cv, cd, params: CompressionParams, backend: B200BgvBackend, keys: KeySet) -> list[Ciphertext]:
+    """pack_pair (compress.py:338-367) through the backend's single GPU
+    operations: mul_plain at each input's own level, rot_col, and add, whose
+    _at_level modulus switch (bgv.py:656-658) reconciles mixed levels."""
+    p, m = params.he.p, params.block_width
+    top = SlotMatrix.from_rows([1] * m, [0] * m, p)
+    bot = SlotMatrix.from_rows([0] * m, [1] * m, p)
+    out = []
+    for j in range(params.num_blocks):
+        src = j // 2
+        if j % 2 == 0:
+            u = backend.add(backend.mul_plain(cv[src], top), backend.rot_col(backend.mul_plain(cd[src], top), keys))
+        else:
+            u = backend.add(backend.rot_col(backend.mul_plain(cv[src], bot), keys), backend.mul_plain(cd[src], bot))
+        out.append(u)
+    return out
 
 
 def comp(
@@ -221,26 +260,55 @@ def comp(
         raise BackendMismatch("compression parameters do not match the backend")
     cd = list(cd)
     cv = list(cd) if masked is not None else list(index_hint)
-    _check_inputs(cd, cv, params, backend, keys)
-    live = live_diagonals(params)
-    bits, sim = comp_noise(
-        backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live
-    )
+    glue = _check_inputs(cd, cv, params, backend, keys)
     if masked is not None and masked.params != params:
         raise ValueError("masked matrix was built for different compression parameters")
-    backend.plan(params.N, params.s, keys, db=None if masked is None else masked.db_mod_p)
-    L = backend.params.max_level
-    cd_arr = _stack_level3(cd, L)
-    cv_arr = cd_arr if masked is not None else _stack_level3(cv, L)
+    live = live_diagonals(params)
     out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
-    _lib.check(
-        _lib.lib().hc_comp(backend._ctx(), _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd), _lib.ptr(out))
-    )
+    if glue:
+        # mixed input levels (answer(): SURVEY 8(f)#2): pack_pair as single
+        # GPU operations (they move the counters themselves), then the fused
+        # BSGS graph from the packed ciphertexts
+        backend.plan(params.N, params.s, keys, db=None if masked is None else masked.db_mod_p)
+        u = _pack_pair_ops(cv, cd, params, backend, keys)
+        bits, sim = bsgs_noise(_NoiseSim(backend), params, [c.payload.noise_bits for c in u], live, FUSED_LEVEL - 1)
+        u_arr = np.ascontiguousarray(np.stack([c.payload.res for c in u]), dtype=np.uint64)
+        _lib.check(_lib.lib().hc_comp_packed(backend._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
+    else:
+        bits, sim = comp_noise(
+            backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live
+        )
+        backend.plan(params.N, params.s, keys, db=None if masked is None else masked.db_mod_p)
+        cd_arr = _stack_level3(cd, FUSED_LEVEL)
+        cv_arr = cd_arr if masked is not None else _stack_level3(cv, FUSED_LEVEL)
+        _lib.check(
+            _lib.lib().hc_comp(backend._ctx(), _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd), _lib.ptr(out))
+        )
     backend.counters.keyswitches += sim.ks
     backend.counters.pt_mults += sim.pt
     backend.counters.adds += sim.adds
     ct = Ciphertext(backend.backend_id, keys.key_id, 0, RnsPayload(out, bits, (backend.q[0],)))
     return CompressedAnswer((ct,), params.s, True)
+
+
+def mask(cv: Sequence[Ciphertext], db, params: CompressionParams, backend, keys: KeySet) -> list[Ciphertext]:
+    """pdq.mask (pdq.py:238-245): d_i = v_i * value_i, one GPU mul_plain per
+    input ciphertext.  `db`: a reference Database (its .values) or the values."""
+    values = db.values if hasattr(db, "values") else db
+    return [backend.mul_plain(c, m) for c, m in zip(cv, encode_vector(list(values), params))]
+
+
+def answer_from_match(
+    cv: Sequence[Ciphertext], db, params: CompressionParams, backend, keys: KeySet
+) -> CompressedAnswer:
+    """pdq.answer (pdq.py:248-256) after Match: cd = mask(cv, db), then
+    comp(cd, index_hint=cv) with cd one level below cv.  Match (the Fermat
+    power, depth log2 p) is outside the B200 hot path."""
+    values = db.values if hasattr(db, "values") else db
+    if len(values) != params.N:
+        raise ValueError(f"database has {len(values)} records, params expect {params.N}")
+    cd = mask(cv, values, params, backend, keys)
+    return comp(cd, params, backend, keys, index_hint=cv)
 
 
 def comp_masked(

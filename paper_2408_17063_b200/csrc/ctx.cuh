@@ -6,10 +6,15 @@
 
 namespace hc {
 
-constexpr int MAXL = 3;        // max level supported (4 chain primes)
-constexpr int NPR = MAXL + 2;  // chain primes + plaintext prime p (index 4)
-constexpr int PIDX = 4;        // RNS index of p in the tables
-constexpr int NLIMB = 4;       // limbs for composed integers (216 bits max)
+// Chains of up to 5 primes (max_level 4).  Comp's fused schedule runs at
+// levels <= 3 (the 4 smallest primes); level 4 only carries the Mask /
+// pack-pair products of answer() (pdq.py:238-256) down to level 3, so CRT
+// compose, digit decomposition and key switching stop at level 3 (KEYL).
+constexpr int MAXL = 4;        // max level supported (5 chain primes)
+constexpr int KEYL = 3;        // highest level with device key switching / CRT compose
+constexpr int NPR = MAXL + 2;  // chain primes + plaintext prime p (index 5)
+constexpr int PIDX = MAXL + 1; // RNS index of p in the tables
+constexpr int NLIMB = 4;       // limbs for composed integers (216 bits: levels <= KEYL)
 constexpr int MAXD = 14;       // digits at level 3 (216-bit modulus, base 2^16)
 
 // Constants for level l (P = l+1 primes at RNS indices 0..l).
@@ -36,8 +41,8 @@ struct DevCtx {
     u64 p, half_p;
     double pinv;
     u64 pbar;  // floor(2^64 / p): integer Barrett for r mod p
-    int L;  // max level
-    int pad;
+    int L;    // max level
+    int KL1;  // RNS rows per key digit on the device: min(L, KEYL) + 1
     LevelC lv[MAXL + 1];
     const Tw* twf;       // [NPR][n]
     const Tw* twi;       // [NPR][n]

@@ -43,6 +43,7 @@ static int fail(int code, const std::string& msg) {
 
 extern "C" const char* hc_last_error(void) { return g_err.c_str(); }
 
+extern "C" int hc_plain_row(void) { return PIDX; }
 extern "C" uint64_t hc_prim_root_2n(uint64_t q, int n) { return prim_root_2n_host(q, n); }
 
 extern "C" int hc_galois_tables(int n, uint32_t t, uint16_t* coef, uint16_t* perm) {
@@ -273,7 +274,7 @@ static int configure_kernels() {
 extern "C" int hc_ctx_create(int n, int max_level, const uint64_t* primes, uint64_t p, int ksw_base_bits,
                              int device, hc_ctx** out) {
     if (n != NPOLY) return fail(HC_ERR_ARG, "only n = 8192 is supported");
-    if (max_level < 1 || max_level > MAXL) return fail(HC_ERR_ARG, "max_level must be 1..3");
+    if (max_level < 1 || max_level > MAXL) return fail(HC_ERR_ARG, "max_level must be 1..4");
     if (ksw_base_bits != 16) return fail(HC_ERR_ARG, "only ksw_base_bits = 16 is supported");
     if (p >= (1ull << 31) || p % (2 * (u64)n) != 1) return fail(HC_ERR_ARG, "bad plaintext modulus");
     for (int k = 0; k <= max_level; k++) {
@@ -342,11 +343,24 @@ extern "C" int hc_load_ksk(hc_ctx* h, uint32_t t, const uint64_t* ksk) {
         h->keys.erase(it);
     }
     DevKey k;
+    // ksk: [D_L][2][L+1][n] (the key at max level).  The device keeps the
+    // digits and primes key switching uses (levels <= KEYL): at max_level 4
+    // the first 14 digits on the 4 smallest primes (_KskPair.at_level,
+    // bgv.py:304-312, reduces exactly that way).
     const int L1 = h->L + 1, D = h->digits[h->L];
-    const size_t rows = (size_t)D * 2 * L1;
+    const int KL1 = h->hctx.KL1, DK = h->digits[KL1 - 1];
+    const size_t rows = (size_t)DK * 2 * KL1;
     CU(cudaMalloc(&k.key, rows * NPOLY * 8));
-    CU(cudaMemcpyAsync(k.key, ksk, rows * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
-    k_to_mont<<<592, 256, 0, h->stream>>>(h->hctx, k.key, (long long)rows, L1);
+    if (KL1 == L1) {
+        CU(cudaMemcpyAsync(k.key, ksk, rows * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
+    } else {
+        (void)D;
+        for (int d = 0; d < DK; d++)
+            for (int ab = 0; ab < 2; ab++)
+                CU(cudaMemcpyAsync(k.key + ((size_t)d * 2 + ab) * KL1 * NPOLY, ksk + ((size_t)d * 2 + ab) * L1 * NPOLY,
+                                   (size_t)KL1 * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
+    }
+    k_to_mont<<<592, 256, 0, h->stream>>>(h->hctx, k.key, (long long)rows, KL1);
     CU(cudaGetLastError());
     std::vector<uint16_t> gal(NPOLY), perm(NPOLY);
     int rc = hc_galois_tables(NPOLY, t, gal.data(), perm.data());
@@ -768,11 +782,13 @@ struct Plan {
     u64 *A0 = nullptr, *A1 = nullptr, *A1coef = nullptr, *dnttG = nullptr, *RES = nullptr;
     u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr, *ACC = nullptr;
     uint16_t *digG = nullptr, *digF = nullptr;
-    std::unique_ptr<Schedule> full, fin;
+    u64* uin = nullptr;  // hc_comp_packed: caller's pack_pair outputs u_t, [B][2][3][n] at level 2
+    std::unique_ptr<Schedule> full, fin, full_u;
     std::map<std::pair<long long, long long>, std::unique_ptr<Schedule>> partials;
     ~Plan() {
         full.reset();
         fin.reset();
+        full_u.reset();
         partials.clear();
         for (void* p : allocs) cudaFree(p);
     }
@@ -820,7 +836,7 @@ static const DevKey* need_key(hc_ctx* h, uint32_t t) {
 
 static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db) {
     if (!h) return fail(HC_ERR_ARG, "null context");
-    if (h->L != 3) return fail(HC_ERR_ARG, "Comp needs max_level = 3 (SURVEY F3)");
+    if (h->L < 3) return fail(HC_ERR_ARG, "Comp needs max_level >= 3 (SURVEY F3)");
     const int n = NPOLY, m = n / 2;
     if (N < 1 || s < 1) return fail(HC_ERR_ARG, "N and s must be positive");
     if ((u64)N >= h->p) return fail(HC_ERR_ARG, "p must exceed N (compress.py:52-53)");
@@ -1007,9 +1023,9 @@ extern "C" int64_t hc_partial_words(const hc_ctx* h) {
 
 // the level-2 ciphertext multiplied by diagonal (t, g, b): u_t for b = 0,
 // the baby rotation ROT[t][b] otherwise
-static const u64* rot_src(const Plan& P, int tl, int b, int poly) {
+static const u64* rot_src(const Plan& P, const u64* U, int tl, int b, int poly) {
     const size_t NB = NPOLY;
-    return b == 0 ? P.U + ((size_t)tl * 2 + poly) * 3 * NB
+    return b == 0 ? U + ((size_t)tl * 2 + poly) * 3 * NB
                   : P.ROT + (((size_t)tl * (P.baby - 1) + (b - 1)) * 2 + poly) * 3 * NB;
 }
 // correction slot of product (tl, b) for accumulator (g, poly): [2 primes][n]
@@ -1022,8 +1038,10 @@ static u64* eslot(const Plan& P, int tl, int b, int g, int poly) {
 // rotations and the diagonal products (compress.py:286-297), accumulated
 // into the partial PX = [E | X].  Blocks are independent until the
 // accumulation, so each chunk runs as up to 4 parallel lanes (graph
-// branches) of per-block pipelines S1..S9, joined by S10.
-static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedule& S) {
+// branches) of per-block pipelines S1..S9, joined by S10.  `from_u`: the
+// pack_pair outputs u_t are the caller's (P.uin, level 2; the mixed-level
+// answer() inputs), so S1..S4 are skipped.
+static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedule& S, bool from_u = false) {
     const size_t NB = NPOLY;
     const int D2 = P.D2, baby = P.baby, G = P.giant, sp = P.s_pad;
     const DevKey* kcol = need_key(h, P.t_col);
@@ -1031,6 +1049,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
     add_memset(S, P.PX, P.px_words() * 8);
     for (long long c0 = b0; c0 < b1; c0 += P.CB) {
         const int cb = (int)std::min<long long>(P.CB, b1 - c0);
+        const u64* Ub = from_u ? P.uin + (size_t)c0 * 2 * 3 * NB : P.U;  // u_t of chunk block tl at Ub[tl]
         // S1..S6 (pack, u = P + rot_col(R), hoisted baby INTT + digits) run as
         // one stream over the chunk (narrow levels may use cluster transforms);
         // the wide baby segment S7 (digit NTTs) -> S8 (MAC) -> S9 (diagonal
@@ -1052,6 +1071,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                 const u64* ctP = par == 0 ? cv : cd;
                 const u64* ctR = par == 0 ? cd : cv;
                 u64* ecor = P.ecor + (size_t)tl * 4 * 3 * NB;  // [P0,P1,R0,R1][3][n]
+                if (!from_u) {
                 // S1: the pack mul_plains' dropped-prime INTTs (+ modulus-switch
                 //     correction) and R.c1's kept-prime INTTs
                 for (int mm = 0; mm < 2; mm++)
@@ -1119,12 +1139,13 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     mj.out1 = P.U + ((size_t)tl * 2 + 1) * 3 * NB;
                     s4.push_back(mj);
                 }
+                }  // !from_u
                 // S5..S8: baby-step rotations of u (hoisted INTT + CRT digits)
                 if (baby > 1) {
                     for (int k = 0; k < 3; k++) {
                         XJob j{};
                         j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
-                        j.a = P.U + (((size_t)tl * 2 + 1) * 3 + k) * NB;
+                        j.a = Ub + (((size_t)tl * 2 + 1) * 3 + k) * NB;
                         j.out = P.Ucoef + ((size_t)tl * 3 + k) * NB;
                         s5.push_back(j);
                     }
@@ -1151,7 +1172,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         mj.level = 2; mj.nterm = 1;
                         mj.t[0].dntt = P.dnttB + rb * D2 * 3 * NB;
                         mj.t[0].key = kb->key;
-                        mj.t[0].c0src = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
+                        mj.t[0].c0src = Ub + ((size_t)tl * 2 + 0) * 3 * NB;
                         mj.t[0].perm = kb->perm;
                         mj.out0 = P.ROT + (rb * 2 + 0) * 3 * NB;
                         mj.out1 = P.ROT + (rb * 2 + 1) * 3 * NB;
@@ -1169,7 +1190,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         for (int poly = 0; poly < 2; poly++) {
                             XJob j{};
                             j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE_RD; j.level = 2;
-                            j.a = rot_src(P, tl, b, poly) + 2 * NB;
+                            j.a = rot_src(P, Ub, tl, b, poly) + 2 * NB;
                             j.b = dg + 2 * NB;
                             j.out = eslot(P, tl, b, g, poly);
                             j.ostride = NB;
@@ -1193,7 +1214,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         for (int b = 0; b < baby; b++) {
                             const int i = g * baby + b;
                             if (!P.live[(size_t)t * sp + i]) continue;
-                            srcs.push_back(rot_src(P, tl, b, poly));
+                            srcs.push_back(rot_src(P, Ub, tl, b, poly));
                             dgs.push_back(P.diag + ((size_t)t * sp + i) * 3 * NB);
                             ess.push_back(eslot(P, tl, b, g, poly));
                         }
@@ -1234,6 +1255,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
             lane_dx = (e && e[0] == '0') ? 0 : 1;
         }
         bool lanes_dx = false;
+        if (!from_u) {
         rc = add_xf(S, s1); if (rc) return rc;
         // S2 (P and R.c0 at level 2) is independent of S2c -> S3 (R.c1's
         // digits and their NTTs): at small chunks (latency regime) they run as
@@ -1256,6 +1278,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
             S.par_end();
         }
         rc = add_ma(S, s4, 3); if (rc) return rc;
+        }  // !from_u
         rc = add_xf(S, s5); if (rc) return rc;
         rc = add_co(S, s6); if (rc) return rc;
         if (cb > g_lane_max_blocks || cb < 3) {  // lanes pay off from 3 blocks (measured)
@@ -1604,6 +1627,35 @@ extern "C" int hc_comp_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, 
     return HC_OK;
 }
 
+// Comp from the caller's pack_pair outputs (answer()'s mixed-level inputs:
+// pack_pair runs through hc_mul_plain / hc_rotate / the add's modulus
+// switch): u: [B][2][3][n] at level 2, NTT domain,
+// canonical residues.  Same BSGS graph as hc_comp from the baby steps on.
+extern "C" int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t* out) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (B != P.B) return fail(HC_ERR_ARG, "expected one packed ciphertext per block");
+    CU(cudaSetDevice(h->dev));
+    const size_t words = (size_t)P.B * 2 * 3 * NPOLY;
+    if (!P.uin) {
+        int rc = palloc(P, &P.uin, words);
+        if (rc) return rc;
+    }
+    if (!P.full_u) {
+        std::unique_ptr<Schedule> S(new Schedule());
+        int rc = build_partial(h, P, 0, P.B, *S, true);
+        if (!rc) rc = build_finish(h, P, *S);
+        if (!rc) rc = capture(h, *S);
+        if (rc) return rc;
+        P.full_u = std::move(S);
+    }
+    CU(cudaMemcpyAsync(P.uin, u, words * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaGraphLaunch(P.full_u->exec, h->stream));
+    CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
 extern "C" int hc_comp_partial(hc_ctx* h, int64_t b0, int64_t b1, uint64_t* partial_dev, void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
@@ -1758,6 +1810,7 @@ extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint
 extern "C" int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t t, uint64_t* out) {
     if (!h) return fail(HC_ERR_ARG, "null context");
     if (level < 1 || level > h->L) return fail(HC_ERR_ARG, "rotation level must be 1..max_level");
+    if (level > KEYL) return fail(HC_ERR_ARG, "device key switching runs at levels <= 3");
     const DevKey* key = need_key(h, t);
     if (!key) return fail(HC_ERR_KEY, "rotation key was not declared at keygen");
     CU(cudaSetDevice(h->dev));

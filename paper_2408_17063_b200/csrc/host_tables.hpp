@@ -3,6 +3,7 @@
 // per-level rescale / CRT constants, slot map (bgv.py:367-377), Galois
 // index tables (bgv.py:258-261, 273-284).
 #pragma once
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -118,14 +119,14 @@ static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<T
         u64 q = (k == PIDX) ? p : (k <= max_level ? primes[k] : primes[0]);
         fill_prime(D.pc[k], &twf[(size_t)k * n], &twi[(size_t)k * n], q, n);
     }
+    D.KL1 = std::min(max_level, KEYL) + 1;
     for (int l = 0; l <= max_level; l++) {
         LevelC& C = D.lv[l];
         C.P = l + 1;
         C.nlimb = l + 1;
-        u64 Q[NLIMB] = {1, 0, 0, 0};
-        for (int k = 0; k <= l; k++) limbs_mul(Q, NLIMB, primes[k]);
-        memcpy(C.Q, Q, sizeof Q);
-        C.D = (bitlen_limbs(Q, NLIMB) + 15) / 16;
+        u64 Qw[MAXL + 1] = {1};  // Q_l over l+1 limbs (digit count at every level)
+        for (int k = 0; k <= l; k++) limbs_mul(Qw, MAXL + 1, primes[k]);
+        C.D = (bitlen_limbs(Qw, MAXL + 1) + 15) / 16;
         digits_out[l] = C.D;
         C.half_qd = primes[l] >> 1;
         for (int k = 0; k < l; k++) {
@@ -135,6 +136,8 @@ static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<T
             C.qinv_r[k] = mulmod_slow(qi, D.pc[k].rmod, primes[k]);
             C.qinv_rs[k] = shoup_const(C.qinv_r[k], primes[k]);
         }
+        if (l > KEYL) continue;  // level 4: modulus switch only (no compose on the device)
+        memcpy(C.Q, Qw, sizeof C.Q);
         for (int k = 0; k <= l; k++) {
             u64 M[NLIMB] = {1, 0, 0, 0};
             for (int i = 0; i <= l; i++)

@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_co
     const int k = blockIdx.y;
     const int j = CPT * (blockIdx.x * blockDim.x + threadIdx.x);
     const LevelC& LV = C.lv[J.level];
-    const int P = LV.P, D = LV.D, L1 = C.L + 1;
+    const int P = LV.P, D = LV.D, L1 = C.KL1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
     const int nt = J.nterm;
@@ -1126,7 +1126,7 @@ __global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx
     const int k = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const LevelC& LV = C.lv[J.level];
-    const int P = LV.P, D = LV.D, L1 = C.L + 1;
+    const int P = LV.P, D = LV.D, L1 = C.KL1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
     const unsigned pe = J.perm ? J.perm[j] : 0u;

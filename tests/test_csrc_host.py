@@ -6,6 +6,8 @@ bit-for-bit with the oracle."""
 
 import ctypes
 
+PIDX = 5  # csrc/ctx.cuh: RNS table row of the plaintext prime p (chains of up to 5 primes)
+
 import numpy as np
 import pytest
 
@@ -59,18 +61,19 @@ def test_ntt_schedule_matches_reference_transform(setup):
         a = rand_res(rng, q)
         want_f = (be.ntt if k < 4 else be.ntt_p).fwd(a[None, :], [k if k < 4 else 0])[0]
         want_i = (be.ntt if k < 4 else be.ntt_p).inv(a[None, :], [k if k < 4 else 0])[0]
+        t = k if k < 4 else PIDX  # table row of the plaintext prime
         got = a.copy()
-        ht.ht_ntt(k, p_(got), 0)
+        ht.ht_ntt(t, p_(got), 0)
         assert np.array_equal(got, want_f), f"forward NTT mismatch for prime {k}"
         got = a.copy()
-        ht.ht_ntt(k, p_(got), 1)
+        ht.ht_ntt(t, p_(got), 1)
         assert np.array_equal(got, want_i), f"inverse NTT mismatch for prime {k}"
         # cluster schedule (8 CTAs, DSMEM exchange) on the same data
         got = a.copy()
-        ht.ht_ntt_cl(k, p_(got), 0)
+        ht.ht_ntt_cl(t, p_(got), 0)
         assert np.array_equal(got, want_f), f"cluster forward NTT mismatch for prime {k}"
         got = a.copy()
-        ht.ht_ntt_cl(k, p_(got), 1)
+        ht.ht_ntt_cl(t, p_(got), 1)
         assert np.array_equal(got, want_i), f"cluster inverse NTT mismatch for prime {k}"
     # lazy-range inputs up to 4q (forward) are accepted
     q = be.q[0]

@@ -130,7 +130,8 @@ def test_decrypt_roundtrip(c1):
     assert [int(x) for x in m.rows[1]] == dense[4096:8192]
 
 
-GOLDEN_8K = [g for g in golden_names() if not g.startswith(("small_", "masked_"))]
+GOLDEN_8K = [g for g in golden_names() if not g.startswith(("small_", "masked_", "answer_"))]
+ANSWER_8K = [g for g in golden_names("answer_") if not g.startswith("answer_small_")]
 MASKED_8K = [g for g in golden_names("masked_") if not g.startswith("masked_small_")]
 
 
@@ -185,6 +186,75 @@ def test_comp_masked_matches_reference_golden(pkg, oracle, name):
     cts = P.encrypt_vector(dense, params, be, keys)
     ans2 = P.comp(cts, params, be, keys, index_hint=hint)
     assert ans2.payload_slots(be, keys) == (w, e)
+
+
+@pytest.mark.parametrize("name", ANSWER_8K)
+def test_answer_mask_then_comp_matches_reference_golden(pkg, oracle, name):
+    """pdq.answer after Match (pdq.py:248-256) on a 5-prime chain: cv at
+    level 4, cd = mask(cv, db) at level 3, comp(cd, index_hint=cv) -- mixed
+    levels through add's _at_level; byte-identical to the reference."""
+    P, O = pkg, oracle
+    g = load_golden(name)
+    n, p, N, s, seed = g["n"], g["p"], g["N"], g["s"], g["seed"]
+    he = P.HeParams(n, p, g["max_level"])
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed, noise_guard=not g["noise_guard_disabled"])
+    assert list(be.chain_primes) == g["chain_primes_desc"]
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    assert keys.key_id.hex() == g["key_id"]
+    support, db, dense = O.masked_payload(N, s, p, seed)
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    m0 = be.counters.snapshot()
+    cd = P.mask(hint, db, params, be, keys)
+    assert be.counters.delta(m0).as_dict() == g["mask_counters"]
+    assert [c.level for c in cd] == g["cts_levels"] and [c.level for c in hint] == g["hint_levels"]
+    before = be.counters.snapshot()
+    ans = P.comp(cd, params, be, keys, index_hint=hint)
+    delta = be.counters.delta(before)
+    blob = ans.serialize(be)
+    assert O.sha256(blob) == g["answer_sha256"], "mask + comp output differs from the reference"
+    assert ans.cts[0].payload.noise_bits == g["noise_bits"]
+    assert delta.as_dict() == g["counters"]
+    w, e = ans.payload_slots(be, keys)
+    assert (w, e) == (g["w"], g["e"]) == O.expected_slots(dense, s, p)
+    # the one-call form and a repeat on the cached packed-input graph
+    assert O.sha256(P.answer_from_match(hint, db, params, be, keys).serialize(be)) == g["answer_sha256"]
+
+
+def test_fused_comp_on_a_five_prime_chain_vs_oracle(pkg, oracle):
+    """max_level 4 backend, both inputs switched down to level 3: the fused
+    graph runs on the 4 smallest primes with keys sliced from level 4."""
+    P, O = pkg, oracle
+    n, p, N, s, seed = N8K, 65537, 8192, 8, 21
+    he = P.HeParams(n, p, 4)
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed)
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    dense = O.plant_sparse(random.Random(seed), N, s, p)
+    cts = [be._at_level(c, 3) for c in P.encrypt_vector(dense, params, be, keys)]
+    hint = [be._at_level(c, 3) for c in P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)]
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    obe = O.OracleBgv(n, p, 4, seed=seed)
+    okeys = obe.keygen(*O.plan_rotation_amounts(s, n))
+    octs = [obe.at_level(c, 3) for c in O.encrypt_vector(dense, N, obe, okeys)]
+    ohint = [obe.at_level(c, 3) for c in O.encrypt_vector([1 if x else 0 for x in dense], N, obe, okeys)]
+    for a, b in zip(cts + hint, octs + ohint):
+        assert np.array_equal(a.payload.res, b.c)
+    out = O.comp(octs, N, s, obe, okeys, ohint)
+    assert np.array_equal(ans.cts[0].payload.res, out.c)
+    assert ans.cts[0].payload.noise_bits == out.noise_bits
+    assert ans.payload_slots(be, keys) == O.expected_slots(dense, s, p)
+
+
+def test_comp_below_level_3_raises_like_reference(c1, pkg):
+    """mask + comp on the 4-prime chain: pack_pair lands at level 1 and the
+    reference raises LevelExhausted at the output mask (bgv.py:721-722)."""
+    P = pkg
+    be, params, keys, hint = c1["be"], c1["params"], c1["keys"], c1["hint"]
+    cd = P.mask(hint, [3] * params.N, params, be, keys)
+    assert cd[0].level == 2
+    with pytest.raises(P.LevelExhausted):
+        P.comp(cd, params, be, keys, index_hint=hint)
 
 
 def test_comp_p786433_N2_17_vs_oracle(pkg, oracle):

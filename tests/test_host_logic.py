@@ -80,6 +80,8 @@ def test_noise_and_counters_replay_reference(name):
     g = load_golden(name)
     if g["n"] != 8192:
         pytest.skip("the B200 backend is n = 8192 only")
+    if g.get("answer"):
+        pytest.skip("mixed-level pack_pair runs as backend ops (noise checked by the GPU and oracle tests)")
     he = P.HeParams(g["n"], g["p"], 3)
     params = P.CompressionParams(g["N"], g["s"], he)
     be = P.B200BgvBackend(he, seed=0, noise_guard=not g["noise_guard_disabled"])
