@@ -16,7 +16,8 @@ import numpy as np
 from .params import BackendMismatch, LevelExhausted, MissingRotationKey
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("HCOMP_LIB") or os.path.join(_HERE, "libhcomp.so")
+LIB_PATH = os.environ.get("HCOMP_LIB") or os.path.join(_HERE, "libhcomp.so")  # max_level <= 3
+LIB5_PATH = os.environ.get("HCOMP_LIB5") or os.path.join(_HERE, "libhcomp_l4.so")  # max_level 4
 
 HC_OK = 0
 HC_ERR_ARG = 1
@@ -31,7 +32,8 @@ class HcompError(RuntimeError):
     """CUDA / state failure inside libhcomp (no reference analogue)."""
 
 
-_lib = None
+_libs: dict = {}  # path -> CDLL
+_last = None  # the library of the most recent lib() call (its hc_last_error)
 
 # (name, restype, argtypes)
 _P = ctypes.c_void_p
@@ -87,22 +89,26 @@ _SIGS = [
 EXPORTS = [s[0] for s in _SIGS]
 
 
-def lib():
-    """Load the CUDA library (raises if it has not been built)."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
+def lib(max_level: int = 3):
+    """Load the CUDA library for chains up to max_level + 1 primes (raises if
+    it has not been built).  Both builds export the same C ABI."""
+    global _last
+    path = LIB_PATH if max_level <= 3 else LIB5_PATH
+    L = _libs.get(path)
+    if L is None:
+        if not os.path.exists(path):
             raise HcompError(
-                f"{LIB_PATH} is missing: build it with `python -m paper_2408_17063_b200.build` "
+                f"{path} is missing: build it with `python -m paper_2408_17063_b200.build` "
                 "(there is no CPU fallback for Comp)"
             )
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         for name, res, args in _SIGS:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        _lib = L
-    return _lib
+        _libs[path] = L
+    _last = L
+    return L
 
 
 def ptr(a: np.ndarray):
@@ -115,7 +121,7 @@ def check(rc: int) -> None:
     """Map libhcomp status codes onto the reference's exceptions."""
     if rc == HC_OK:
         return
-    msg = lib().hc_last_error().decode(errors="replace")
+    msg = (_last or lib()).hc_last_error().decode(errors="replace")
     if rc == HC_ERR_ARG:
         raise ValueError(msg)
     if rc == HC_ERR_LEVEL:

@@ -324,7 +324,7 @@ class B200BgvBackend:
 
     def _ctx(self):
         if self._h is None:
-            L = _lib.lib()
+            L = _lib.lib(self.params.max_level)
             h = ctypes.c_void_p()
             primes = np.asarray(self.q, dtype=np.uint64)
             _lib.check(
@@ -338,7 +338,7 @@ class B200BgvBackend:
 
     def close(self) -> None:
         if self._h is not None:
-            _lib.lib().hc_ctx_destroy(self._h)
+            _lib.lib(self.params.max_level).hc_ctx_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -355,13 +355,13 @@ class B200BgvBackend:
         a = np.ascontiguousarray(a, dtype=np.uint64).copy()
         rows = a.size // self.params.n
         pidx = self._pidx(rows, level)
-        _lib.check(_lib.lib().hc_ntt(self._ctx(), _lib.ptr(a), rows, _lib.ptr(pidx), 1 if inverse else 0))
+        _lib.check(_lib.lib(self.params.max_level).hc_ntt(self._ctx(), _lib.ptr(a), rows, _lib.ptr(pidx), 1 if inverse else 0))
         return a
 
     def ntt_p(self, a: np.ndarray, inverse: bool) -> np.ndarray:
         a = np.ascontiguousarray(a, dtype=np.uint64).copy().reshape(1, -1)
-        pidx = np.array([_lib.lib().hc_plain_row()], dtype=np.int32)
-        _lib.check(_lib.lib().hc_ntt(self._ctx(), _lib.ptr(a), 1, _lib.ptr(pidx), 1 if inverse else 0))
+        pidx = np.array([_lib.lib(self.params.max_level).hc_plain_row()], dtype=np.int32)
+        _lib.check(_lib.lib(self.params.max_level).hc_ntt(self._ctx(), _lib.ptr(a), 1, _lib.ptr(pidx), 1 if inverse else 0))
         return a[0]
 
     def pointwise(self, x: np.ndarray, y: np.ndarray, level: int, op: str) -> np.ndarray:
@@ -372,7 +372,7 @@ class B200BgvBackend:
         pidx = self._pidx(rows, level)
         code = {"mul": 0, "add": 1, "sub": 2}[op]
         _lib.check(
-            _lib.lib().hc_pointwise(self._ctx(), _lib.ptr(x), _lib.ptr(y), _lib.ptr(out), rows, _lib.ptr(pidx), code)
+            _lib.lib(self.params.max_level).hc_pointwise(self._ctx(), _lib.ptr(x), _lib.ptr(y), _lib.ptr(out), rows, _lib.ptr(pidx), code)
         )
         return out
 
@@ -597,7 +597,7 @@ class B200BgvBackend:
         ct = np.ascontiguousarray(res, dtype=np.uint64)
         pt = np.ascontiguousarray(pt, dtype=np.uint64)
         out = np.empty((2, level, n), dtype=np.uint64)
-        _lib.check(_lib.lib().hc_mul_plain(self._ctx(), _lib.ptr(ct), level, _lib.ptr(pt), _lib.ptr(out)))
+        _lib.check(_lib.lib(self.params.max_level).hc_mul_plain(self._ctx(), _lib.ptr(ct), level, _lib.ptr(pt), _lib.ptr(out)))
         return out
 
     def mul_plain(self, c: Ciphertext, m: SlotMatrix) -> Ciphertext:
@@ -616,7 +616,7 @@ class B200BgvBackend:
     def _load_keys(self, keys: KeySet) -> None:
         if self._loaded_keys is keys:
             return
-        L = _lib.lib()
+        L = _lib.lib(self.params.max_level)
         h = self._ctx()
         _lib.check(L.hc_clear_keys(h))
         entries = list(keys.rotation_keys.values())
@@ -635,7 +635,7 @@ class B200BgvBackend:
         self._load_keys(keys)
         ct = np.ascontiguousarray(c.payload.res, dtype=np.uint64)
         out = np.empty_like(ct)
-        _lib.check(_lib.lib().hc_rotate(self._ctx(), _lib.ptr(ct), lvl, int(t), _lib.ptr(out)))
+        _lib.check(_lib.lib(self.params.max_level).hc_rotate(self._ctx(), _lib.ptr(ct), lvl, int(t), _lib.ptr(out)))
         bits = self._check_noise(max(c.payload.noise_bits, self._ks_noise(lvl)) + 1, lvl)
         self.counters.keyswitches += 1
         return Ciphertext(self.backend_id, c.key_id, lvl, self._payload(out, bits, lvl))
@@ -685,14 +685,14 @@ class B200BgvBackend:
         tag = (N, s, chunk_blocks, None if db is None else hashlib.sha256(db.tobytes()).digest())
         if self._planned != tag:
             if db is None:
-                _lib.check(_lib.lib().hc_plan(self._ctx(), N, s, chunk_blocks))
+                _lib.check(_lib.lib(self.params.max_level).hc_plan(self._ctx(), N, s, chunk_blocks))
             else:
                 db = np.ascontiguousarray(db, dtype=np.uint64)
-                _lib.check(_lib.lib().hc_plan_masked(self._ctx(), N, s, chunk_blocks, _lib.ptr(db)))
+                _lib.check(_lib.lib(self.params.max_level).hc_plan_masked(self._ctx(), N, s, chunk_blocks, _lib.ptr(db)))
             self._planned = tag
 
     def plan_info(self) -> dict:
         info = np.zeros(8, dtype=np.int64)
-        _lib.check(_lib.lib().hc_plan_info(self._ctx(), _lib.ptr(info)))
+        _lib.check(_lib.lib(self.params.max_level).hc_plan_info(self._ctx(), _lib.ptr(info)))
         keys = ["B", "C", "baby", "giant", "F", "s_pad", "live_diagonals", "kernel_launches"]
         return dict(zip(keys, (int(x) for x in info)))

@@ -273,7 +273,7 @@ def comp(
         u = _pack_pair_ops(cv, cd, params, backend, keys)
         bits, sim = bsgs_noise(_NoiseSim(backend), params, [c.payload.noise_bits for c in u], live, FUSED_LEVEL - 1)
         u_arr = np.ascontiguousarray(np.stack([c.payload.res for c in u]), dtype=np.uint64)
-        _lib.check(_lib.lib().hc_comp_packed(backend._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
+        _lib.check(_lib.lib(backend.params.max_level).hc_comp_packed(backend._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
     else:
         bits, sim = comp_noise(
             backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live
@@ -282,7 +282,7 @@ def comp(
         cd_arr = _stack_level3(cd, FUSED_LEVEL)
         cv_arr = cd_arr if masked is not None else _stack_level3(cv, FUSED_LEVEL)
         _lib.check(
-            _lib.lib().hc_comp(backend._ctx(), _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd), _lib.ptr(out))
+            _lib.lib(backend.params.max_level).hc_comp(backend._ctx(), _lib.ptr(cd_arr), _lib.ptr(cv_arr), len(cd), _lib.ptr(out))
         )
     backend.counters.keyswitches += sim.ks
     backend.counters.pt_mults += sim.pt
@@ -332,14 +332,14 @@ class DeviceComp:
     def set_inputs(self, cd: np.ndarray, cv: np.ndarray) -> None:
         cd = np.ascontiguousarray(cd, dtype=np.uint64)
         cv = np.ascontiguousarray(cv, dtype=np.uint64)
-        _lib.check(_lib.lib().hc_comp_set_inputs(self.be._ctx(), _lib.ptr(cd), _lib.ptr(cv), cd.shape[0]))
+        _lib.check(_lib.lib(self.be.params.max_level).hc_comp_set_inputs(self.be._ctx(), _lib.ptr(cd), _lib.ptr(cv), cd.shape[0]))
 
     def launch(self, stream_handle: int = 0) -> None:
-        _lib.check(_lib.lib().hc_comp_launch(self.be._ctx(), stream_handle or None))
+        _lib.check(_lib.lib(self.be.params.max_level).hc_comp_launch(self.be._ctx(), stream_handle or None))
 
     def output(self) -> np.ndarray:
         out = np.empty((2, 1, self.be.params.n), dtype=np.uint64)
-        _lib.check(_lib.lib().hc_comp_get_output(self.be._ctx(), _lib.ptr(out)))
+        _lib.check(_lib.lib(self.be.params.max_level).hc_comp_get_output(self.be._ctx(), _lib.ptr(out)))
         return out
 
     def run_host(self, cd: np.ndarray, cv: np.ndarray) -> np.ndarray:
@@ -347,5 +347,5 @@ class DeviceComp:
         cd = np.ascontiguousarray(cd, dtype=np.uint64)
         cv = np.ascontiguousarray(cv, dtype=np.uint64)
         out = np.empty((2, 1, self.be.params.n), dtype=np.uint64)
-        _lib.check(_lib.lib().hc_comp(self.be._ctx(), _lib.ptr(cd), _lib.ptr(cv), cd.shape[0], _lib.ptr(out)))
+        _lib.check(_lib.lib(self.be.params.max_level).hc_comp(self.be._ctx(), _lib.ptr(cd), _lib.ptr(cv), cd.shape[0], _lib.ptr(out)))
         return out

@@ -10,8 +10,11 @@ namespace hc {
 // levels <= 3 (the 4 smallest primes); level 4 only carries the Mask /
 // pack-pair products of answer() (pdq.py:238-256) down to level 3, so CRT
 // compose, digit decomposition and key switching stop at level 3 (KEYL).
-constexpr int MAXL = 4;        // max level supported (5 chain primes)
-constexpr int KEYL = 3;        // highest level with device key switching / CRT compose
+#ifndef HC_MAXL
+#define HC_MAXL 4  // build.py compiles -DHC_MAXL=3 (libhcomp.so) and 4 (libhcomp_l4.so)
+#endif
+constexpr int MAXL = HC_MAXL;  // max level supported (MAXL + 1 chain primes)
+constexpr int KEYL = MAXL < 3 ? MAXL : 3;        // highest level with device key switching / CRT compose
 constexpr int NPR = MAXL + 2;  // chain primes + plaintext prime p (index 5)
 constexpr int PIDX = MAXL + 1; // RNS index of p in the tables
 constexpr int NLIMB = 4;       // limbs for composed integers (216 bits: levels <= KEYL)
@@ -24,29 +27,30 @@ struct LevelC {
     int pad;
     // modulus switch l -> l-1 (drops prime l), bgv.py:579-608
     u64 half_qd;          // q_l >> 1
-    u64 qinv[MAXL + 1];   // q_l^-1 mod q_k (k < l)
-    u64 qinv_s[MAXL + 1];
-    u64 qinv_r[MAXL + 1]; // q_l^-1 * R mod q_k (Montgomery, folded into plaintexts)
-    u64 qinv_rs[MAXL + 1];
-    // CRT compose at level l
-    u64 Minv[MAXL + 1], Minv_s[MAXL + 1];  // (Q_l/q_k)^-1 mod q_k
-    u64 M[MAXL + 1][NLIMB];                // Q_l/q_k
+    u64 qinv[KEYL + 1];   // q_l^-1 mod q_k (k < l <= MAXL)
+    u64 qinv_s[KEYL + 1];
+    u64 qinv_r[KEYL + 1]; // q_l^-1 * R mod q_k (Montgomery, folded into plaintexts)
+    u64 qinv_rs[KEYL + 1];
+    // CRT compose at level l <= KEYL
+    u64 Minv[KEYL + 1], Minv_s[KEYL + 1];  // (Q_l/q_k)^-1 mod q_k
+    u64 M[KEYL + 1][NLIMB];                // Q_l/q_k
     u64 Q[NLIMB];                          // Q_l
-    double qrecip[MAXL + 1];               // 1/q_k
+    double qrecip[KEYL + 1];               // 1/q_k
     u64 g01, g01_s;                        // Garner: q_0^-1 mod q_1 (compose2)
 };
 
 struct DevCtx {
-    PrimeC pc[NPR];
+    const Tw* twf;       // [NPR][n]
+    const Tw* twi;       // [NPR][n]
+    const uint16_t* slot_of;  // [n]: NTT index -> (row << 12 | col)
     u64 p, half_p;
     double pinv;
     u64 pbar;  // floor(2^64 / p): integer Barrett for r mod p
     int L;    // max level
     int KL1;  // RNS rows per key digit on the device: min(L, KEYL) + 1
-    LevelC lv[MAXL + 1];
-    const Tw* twf;       // [NPR][n]
-    const Tw* twi;       // [NPR][n]
-    const uint16_t* slot_of;  // [n]: NTT index -> (row << 12 | col)
+    PrimeC pc[NPR];
+    LevelC lvs[MAXL];  // levels 1..MAXL (kernel parameter space: no level-0 entry)
+    HD const LevelC& lv(int l) const { return lvs[l - 1]; }
 };
 
 }  // namespace hc

@@ -128,31 +128,37 @@ HD uint16_t digit16(const u64 (&X)[NLIMB], int j) {
 // Modulus-switch correction (see file header).  The constants of the
 // switch from level l are gathered once (RescaleK) so the per-coefficient
 // path touches registers only.
-struct RescaleK {
+// NQ: kept primes the switch can produce (KEYL for the Comp's levels <= 3;
+// MAXL only for the level-4 products of answer(), EP_RESCALE4).
+template <int NQ = KEYL>
+struct RescaleKT {
     int l;
     u64 ql, half_qd, p, half_p, pbar;
-    u64 q[MAXL], qinv[MAXL], qinv_s[MAXL];
+    u64 q[NQ], qinv[NQ], qinv_s[NQ];
 };
-HD RescaleK rescale_consts(const DevCtx& D, int l) {
-    RescaleK R;
+using RescaleK = RescaleKT<KEYL>;
+template <int NQ = KEYL>
+HD RescaleKT<NQ> rescale_consts(const DevCtx& D, int l) {
+    RescaleKT<NQ> R;
     R.l = l;
     R.ql = D.pc[l].q;
-    R.half_qd = D.lv[l].half_qd;
+    R.half_qd = D.lv(l).half_qd;
     R.p = D.p;
     R.half_p = D.half_p;
     R.pbar = D.pbar;
     HC_UNROLL
-    for (int k = 0; k < MAXL; k++) {
+    for (int k = 0; k < NQ; k++) {
         R.q[k] = D.pc[k].q;
-        R.qinv[k] = D.lv[l].qinv[k];
-        R.qinv_s[k] = D.lv[l].qinv_s[k];
+        R.qinv[k] = D.lv(l).qinv[k];
+        R.qinv_s[k] = D.lv(l).qinv_s[k];
     }
     return R;
 }
 
 // x = canonical residue of the coefficient modulo the dropped prime q_l;
 // writes e_k for k < l.
-HD void rescale_corr(const RescaleK& R, u64 x, u64* e) {
+template <int NQ>
+HD void rescale_corr(const RescaleKT<NQ>& R, u64 x, u64* e) {
     const int neg = x > R.half_qd;
     const u64 mag = neg ? R.ql - x : x;  // |r|
     u64 rm = mag - mulhi(mag, R.pbar) * R.p;  // Barrett: [0, 2p)
@@ -161,7 +167,7 @@ HD void rescale_corr(const RescaleK& R, u64 x, u64* e) {
     const int dneg = rm > R.half_p;
     const u64 dmag = dneg ? R.p - rm : rm;  // |d|
     HC_UNROLL
-    for (int k = 0; k < MAXL; k++) {
+    for (int k = 0; k < NQ; k++) {
         if (k >= R.l) break;
         const u64 q = R.q[k];
         const u64 rk = neg ? (mag ? q - mag : 0) : mag;  // r mod q_k (|r| < q_k)

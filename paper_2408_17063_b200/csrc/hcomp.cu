@@ -196,6 +196,7 @@ static void release_key(DevKey& k) {
     X(1, LD_RED, EP_STORE)            \
     X(1, LD_MONT, EP_RESCALE)         \
     X(1, LD_MONT, EP_RESCALE_RD)      \
+    X(1, LD_MONT, EP_RESCALE4)        \
     X(1, LD_MONT, EP_STORE)           \
     X(0, LD_U64, EP_ADDMONT)          \
     X(0, LD_DIG, EP_STORE_LAZY)       \
@@ -1762,7 +1763,7 @@ extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint
     const size_t NB = NPOLY;
     // plaintext in Montgomery form with the modulus-switch factor folded in
     std::vector<u64> ptm((size_t)P1 * NB);
-    const LevelC& LV = h->hctx.lv[l];
+    const LevelC& LV = h->hctx.lv(l);
     for (int k = 0; k <= l; k++) {
         const PrimeC& pc = h->hctx.pc[k];
         u64 w = k == l ? pc.rmod : LV.qinv_r[k];
@@ -1782,7 +1783,7 @@ extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint
     std::vector<XJob> a, b;
     for (int poly = 0; poly < 2; poly++) {
         XJob j{};
-        j.dir = 1; j.k = l; j.ld = LD_MONT; j.ep = EP_RESCALE; j.level = l;
+        j.dir = 1; j.k = l; j.ld = LD_MONT; j.ep = l > KEYL ? EP_RESCALE4 : EP_RESCALE; j.level = l;
         j.a = c + ((size_t)poly * P1 + l) * NB;
         j.b = p + (size_t)l * NB;
         j.out = corr + (size_t)poly * l * NB;

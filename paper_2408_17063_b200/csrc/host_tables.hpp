@@ -121,7 +121,8 @@ static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<T
     }
     D.KL1 = std::min(max_level, KEYL) + 1;
     for (int l = 0; l <= max_level; l++) {
-        LevelC& C = D.lv[l];
+        LevelC scratch;  // level 0: digit count only (nothing switches from or composes at level 0)
+        LevelC& C = l ? D.lvs[l - 1] : scratch;
         C.P = l + 1;
         C.nlimb = l + 1;
         u64 Qw[MAXL + 1] = {1};  // Q_l over l+1 limbs (digit count at every level)

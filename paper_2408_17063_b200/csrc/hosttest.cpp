@@ -41,7 +41,7 @@ extern "C" void ht_ntt_cl(int k, uint64_t* a, int inverse) {
 
 template <int L>
 static void compose_all(const uint64_t* x, const uint16_t* gal, int mode, uint16_t* dig) {
-    const LevelC& LV = g_ctx.lv[L];
+    const LevelC& LV = g_ctx.lv(L);
     const int D = LV.D;
     for (int pos = 0; pos < NPOLY; pos++) {
         int src = pos, neg = 0;
@@ -66,7 +66,7 @@ static void compose_all(const uint64_t* x, const uint16_t* gal, int mode, uint16
 
 // compose2 (Garner, level 1) against crt_compose<1>: number of mismatches
 extern "C" int ht_compose2_check(const uint64_t* x0, const uint64_t* x1, int count) {
-    const LevelC& LV = g_ctx.lv[1];
+    const LevelC& LV = g_ctx.lv(1);
     int bad = 0;
     for (int i = 0; i < count; i++) {
         u64 xr[2] = {x0[i], x1[i]};
@@ -112,14 +112,14 @@ extern "C" int ht_rescale_rd_check(int level, const uint64_t* x, int count) {
         sd += d;
         for (int k = 0; k < level; k++) {
             const PrimeC& P = g_ctx.pc[k];
-            const LevelC& LV = g_ctx.lv[level];
+            const LevelC& LV = g_ctx.lv(level);
             bad += corr_from_sums(r, d, P.q, LV.qinv[k], LV.qinv_s[k], P.one_s) != e[k];
             se[k] = add_mod(se[k], e[k], P.q);
         }
     }
     for (int k = 0; k < level; k++) {
         const PrimeC& P = g_ctx.pc[k];
-        const LevelC& LV = g_ctx.lv[level];
+        const LevelC& LV = g_ctx.lv(level);
         bad += corr_from_sums(sr, sd, P.q, LV.qinv[k], LV.qinv_s[k], P.one_s) != se[k];
     }
     return bad;

@@ -67,6 +67,7 @@ enum : int {
     EP_RESCALE_RD = 5,     // out[j] = r, out[ostride + j] = d (int64; summed by k_diagx)
     EP_KSACC = 6,          // key-switch digit product: out[j] += x*ea[j], out[ostride+j] += x*eb[j]
     EP_STORE_LAZY = 7,     // out[j] = x, x < 2^60 not canonicalised (forward NTT feeding k_ksmac)
+    EP_RESCALE4 = 8,       // EP_RESCALE from level 4 (answer()'s Mask / pack products; 4 kept primes)
 };
 
 struct XJob {
@@ -302,15 +303,16 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
             J.out[j0 + e * stride] = (u64)r;
             J.out[J.ostride + j0 + e * stride] = (u64)d;
         }
-    } else if constexpr (EP == EP_RESCALE) {
+    } else if constexpr (EP == EP_RESCALE || EP == EP_RESCALE4) {
+        constexpr int NQ = EP == EP_RESCALE4 ? MAXL : KEYL;
         const int l = J.level;
-        const RescaleK R = rescale_consts(D, l);
+        const RescaleKT<NQ> R = rescale_consts<NQ>(D, l);
         HC_UNROLL
         for (int e = 0; e < N; e++) {
-            u64 ek[MAXL];
+            u64 ek[NQ];
             rescale_corr(R, x[e], ek);
             HC_UNROLL
-            for (int k = 0; k < MAXL; k++) {
+            for (int k = 0; k < NQ; k++) {
                 if (k >= l) break;
                 J.out[(size_t)k * J.ostride + j0 + e * stride] = ek[k];
             }
@@ -746,7 +748,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     HC_UNROLL
     for (int r = 0; r < CEPT; r++) tile[r * 128 + t] = x[r];
     __syncthreads();
-    const LevelC& LV = C.lv[1];
+    const LevelC& LV = C.lv(1);
     const int D = LV.D;
     const u64* E = JJ.E;
     uint16_t* dig = JJ.dig;
@@ -871,7 +873,7 @@ __global__ void __launch_bounds__(CNT) k_cl16_intt2(const __grid_constant__ DevC
     for (int i = 0; i < 4; i++) xch_put(cl, half + i * CNT + t, partner, x[theirs0 + i], hbar);
     xch_wait(hbar);
     TRACE(3);
-    const LevelC& LV = C.lv[1];
+    const LevelC& LV = C.lv(1);
     const int D = LV.D;
     const u64* E = JJ.E;
     uint16_t* dig = JJ.dig;
@@ -934,7 +936,7 @@ struct CJob {
 
 template <int L>
 __device__ __forceinline__ void compose_one(const DevCtx& C, const CJob& J, int pos, unsigned e) {
-    const LevelC& LV = C.lv[L];
+    const LevelC& LV = C.lv(L);
     constexpr int P = L + 1;
     const int D = LV.D;
     int src = pos, neg = 0;
@@ -1016,7 +1018,7 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_co
     TRACE(0);
     const int k = blockIdx.y;
     const int j = CPT * (blockIdx.x * blockDim.x + threadIdx.x);
-    const LevelC& LV = C.lv[J.level];
+    const LevelC& LV = C.lv(J.level);
     const int P = LV.P, D = LV.D, L1 = C.KL1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
@@ -1125,7 +1127,7 @@ __global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx
     TRACE(0);
     const int k = blockIdx.y;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const LevelC& LV = C.lv[J.level];
+    const LevelC& LV = C.lv(J.level);
     const int P = LV.P, D = LV.D, L1 = C.KL1;
     const PrimeC pc = C.pc[k];
     const size_t kn = (size_t)k * NPOLY + j;
@@ -1227,7 +1229,7 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
     const u64 x0 = redc(h0, l0, q0, C.pc[0].qneg), x1 = redc(h1, l1, q1, C.pc[1].qneg);
     u64 e0 = 0, e1 = 0;
     if (es) {
-        const LevelC& LV = C.lv[J.level];
+        const LevelC& LV = C.lv(J.level);
         e0 = corr_from_sums(sr, sd, q0, LV.qinv[0], LV.qinv_s[0], C.pc[0].one_s);
         e1 = corr_from_sums(sr, sd, q1, LV.qinv[1], LV.qinv_s[1], C.pc[1].one_s);
     }
@@ -1311,7 +1313,7 @@ __global__ void __launch_bounds__(NT, 1) k_plain(const __grid_constant__ DevCtx 
     cta_ntt_inv(C.twi + (size_t)PIDX * NPOLY, C.pc[PIDX], sm);
     HC_NOUNROLL
     for (int j = tid; j < NPOLY; j += NT) coef[j] = sm[swz(j)];
-    const LevelC& LV = C.lv[J.level];
+    const LevelC& LV = C.lv(J.level);
     for (int k = 0; k <= J.level; k++) {
         const PrimeC P = C.pc[k];
         __syncthreads();

@@ -59,11 +59,12 @@ def comp_sharded(cd, params, backend, keys, index_hint, dist, group=None, root: 
     rank = dist.get_rank(group)
     cv = list(index_hint)
     cd = list(cd)
-    _check_inputs(cd, cv, params, backend, keys)
+    if _check_inputs(cd, cv, params, backend, keys):
+        raise NotImplementedError("sharded Comp takes level-3 inputs (mixed-level answer() inputs run unsharded)")
     live = live_diagonals(params)
     bits, sim = comp_noise(backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live)
     backend.plan(params.N, params.s, keys)
-    L = _lib.lib()
+    L = _lib.lib(backend.params.max_level)
     h = backend._ctx()
     b0, b1 = shard_blocks(params.num_blocks, world, rank)
     c0, c1 = b0 // 2, (b1 + 1) // 2  # the input ciphertexts this rank's blocks read

@@ -23,13 +23,16 @@ def header_symbols():
     return sorted(set(re.findall(r"\b(hc_[a-z0-9_]+)\s*\(", src)))
 
 
-def test_library_exports_every_declared_symbol():
-    L = _lib.lib()
+@pytest.mark.parametrize("max_level", [3, 4])
+def test_library_exports_every_declared_symbol(max_level):
+    """Both builds (4-prime libhcomp.so, 5-prime libhcomp_l4.so) export the ABI."""
+    L = _lib.lib(max_level)
     syms = header_symbols()
     assert len(syms) >= 20
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
     assert set(syms) <= set(_lib.EXPORTS) | {"hc_trace_reset", "hc_trace_read"}
+    assert L.hc_plain_row() == max_level + 1  # csrc/ctx.cuh PIDX: rows 0..MAXL are chain primes
 
 
 def test_host_helpers_without_gpu(oracle):
