@@ -93,6 +93,14 @@ int hc_comp(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* 
  * baby steps, diagonal products, giant steps, folds and the output mask run
  * as in hc_comp (one graph launch).  out = uint64[2][1][n].  Synchronous. */
 int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t* out);
+/* The same for answer()'s inputs as they arrive: cd = uint64[C][2][ld+1][n]
+ * at level ld, cv = uint64[C][2][lv+1][n] at level lv, min(ld, lv) = 3,
+ * max <= max_level (each list at one level).  pack_pair itself runs on the
+ * device -- mul_plain at each input's level, rot_col, the modulus switch of
+ * add's _at_level, the add -- in the same graph as the BSGS steps.
+ * HC_ERR_LEVEL when an input is below level 3 (the reference raises
+ * LevelExhausted at the output mask).  Synchronous. */
+int hc_comp_mixed(hc_ctx* h, const uint64_t* cd, int ld, const uint64_t* cv, int lv, int C, uint64_t* out);
 
 /* Device-resident variant for timing: inputs already uploaded with
  * hc_comp_set_inputs; hc_comp_launch enqueues the whole Comp (one graph

@@ -142,6 +142,38 @@ def comp_noise(be: B200BgvBackend, params: CompressionParams, cv_bits, cd_bits, 
     return bsgs_noise(sim, params, u, live, L - 1)
 
 
+def pack_noise_mixed(sim: _NoiseSim, params: CompressionParams, cv, cd) -> list[float]:
+    """pack_pair's noise sequence (compress.py:338-367) for inputs at their own
+    levels (cv, cd: lists of (noise_bits, level)); add's _at_level switches
+    the higher operand down first (bgv.py:610-614, 656-660)."""
+    be = sim.be
+
+    def mul(x):
+        return sim.mul_plain(x[0], x[1]), x[1] - 1
+
+    def rot(x):
+        return sim.rot(x[0], x[1]), x[1]
+
+    def add(x, y):
+        lvl = min(x[1], y[1])
+        bits = []
+        for b, l in (x, y):
+            while l > lvl:
+                b = be._ms_bits(b, l)
+                l -= 1
+            bits.append(b)
+        return sim.add(bits[0], bits[1], lvl)
+
+    u = []
+    for j in range(params.num_blocks):
+        src = j // 2
+        if j % 2 == 0:
+            u.append(add(mul(cv[src]), rot(mul(cd[src]))))
+        else:
+            u.append(add(rot(mul(cv[src])), mul(cd[src])))
+    return u
+
+
 def bsgs_noise(sim: _NoiseSim, params: CompressionParams, u, live, lv: int) -> tuple[float, _NoiseSim]:
     """bsgs_matvec's part of the sequence (compress.py:273-310) from the
     packed ciphertexts' noise bits u at level lv."""
@@ -266,14 +298,29 @@ def comp(
     live = live_diagonals(params)
     out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
     if glue:
-        # mixed input levels (answer(): SURVEY 8(f)#2): pack_pair as single
-        # GPU operations (they move the counters themselves), then the fused
-        # BSGS graph from the packed ciphertexts
+        # mixed input levels (answer(): SURVEY 8(f)#2)
         backend.plan(params.N, params.s, keys, db=None if masked is None else masked.db_mod_p)
-        u = _pack_pair_ops(cv, cd, params, backend, keys)
-        bits, sim = bsgs_noise(_NoiseSim(backend), params, [c.payload.noise_bits for c in u], live, FUSED_LEVEL - 1)
-        u_arr = np.ascontiguousarray(np.stack([c.payload.res for c in u]), dtype=np.uint64)
-        _lib.check(_lib.lib(backend.params.max_level).hc_comp_packed(backend._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
+        L = _lib.lib(backend.params.max_level)
+        ld, lv = {c.level for c in cd}, {c.level for c in cv}
+        if len(ld) == 1 and len(lv) == 1:
+            # pack_pair on the device: one graph launch for the whole Comp
+            sim = _NoiseSim(backend)
+            u_bits = pack_noise_mixed(
+                sim, params, [(c.payload.noise_bits, c.level) for c in cv], [(c.payload.noise_bits, c.level) for c in cd]
+            )
+            bits, sim = bsgs_noise(sim, params, u_bits, live, FUSED_LEVEL - 1)
+            cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd]), dtype=np.uint64)
+            cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv]), dtype=np.uint64)
+            _lib.check(
+                L.hc_comp_mixed(backend._ctx(), _lib.ptr(cd_arr), ld.pop(), _lib.ptr(cv_arr), lv.pop(), len(cd), _lib.ptr(out))
+            )
+        else:
+            # per-ciphertext levels: pack_pair as single GPU operations (they
+            # move the counters themselves), then the BSGS graph from u
+            u = _pack_pair_ops(cv, cd, params, backend, keys)
+            bits, sim = bsgs_noise(_NoiseSim(backend), params, [c.payload.noise_bits for c in u], live, FUSED_LEVEL - 1)
+            u_arr = np.ascontiguousarray(np.stack([c.payload.res for c in u]), dtype=np.uint64)
+            _lib.check(L.hc_comp_packed(backend._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
     else:
         bits, sim = comp_noise(
             backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live

@@ -128,14 +128,16 @@ static cudaError_t launch_cl(void (*k)(KArgs...), int cluster, dim3 grid, dim3 b
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7 };  // values: bench.py per_kind_ms keys
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7, ST_ADD = 8 };  // values: bench.py per_kind_ms keys
 struct Step {
     int kind = 0;
     int njobs = 0;
     int gy = 1;
     void* djobs = nullptr;
-    // ST_MEMSET
+    // ST_MEMSET, ST_ADD (out = pa + pb: njobs rows, gy primes)
     u64* out = nullptr;
+    const u64* pa = nullptr;
+    const u64* pb = nullptr;
     size_t bytes = 0;
     std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
     std::vector<Intt2Job> i2jobs;  // ST_I2
@@ -573,6 +575,92 @@ static int add_i2(Schedule& S, std::vector<Intt2Job> jobs) {
     return HC_OK;
 }
 
+static void add_add(Schedule& S, const u64* a, const u64* b, u64* out, int rows, int nprime) {
+    Step st;
+    st.kind = ST_ADD;
+    st.group = S.cur_group;
+    st.lane = S.cur_lane;
+    st.pa = a;
+    st.pb = b;
+    st.out = out;
+    st.njobs = rows;
+    st.gy = nprime;
+    S.steps.push_back(st);
+}
+
+// Job lists of single ring operations on device buffers (used by the
+// single-op entry points and by the mixed-level pack_pair schedule).
+// mul_plain + modulus switch at level l (bgv.py:717-733, 579-608):
+//   c [2][l+1][n] x ptm [l+1][n] (plaintext in Montgomery form with q_l^-1
+//   folded into rows k < l) -> o [2][l][n]; corr: scratch [2][l][n].
+static void jobs_mul_plain(std::vector<XJob>& inv, std::vector<XJob>& fwd, int l, const u64* c, const u64* ptm,
+                           u64* corr, u64* o) {
+    const size_t NB = NPOLY;
+    const int P1 = l + 1;
+    for (int poly = 0; poly < 2; poly++) {
+        XJob j{};
+        j.dir = 1; j.k = l; j.ld = LD_MONT; j.ep = l > KEYL ? EP_RESCALE4 : EP_RESCALE; j.level = l;
+        j.a = c + ((size_t)poly * P1 + l) * NB;
+        j.b = ptm + (size_t)l * NB;
+        j.out = corr + (size_t)poly * l * NB;
+        j.ostride = NB;
+        inv.push_back(j);
+        for (int k = 0; k < l; k++) {
+            XJob f{};
+            f.dir = 0; f.k = k; f.ld = LD_U64; f.ep = EP_ADDMONT;
+            f.a = corr + ((size_t)poly * l + k) * NB;
+            f.ea = c + ((size_t)poly * P1 + k) * NB;
+            f.eb = ptm + (size_t)k * NB;
+            f.out = o + ((size_t)poly * l + k) * NB;
+            fwd.push_back(f);
+        }
+    }
+}
+// rotation by Galois element `key` at level l <= KEYL (bgv.py:735-770,
+// 616-647): c [2][l+1][n] -> o [2][l+1][n] (+ add [2][l+1][n] when given);
+// scratch coef [l+1][n], dig [D_l][n], dntt [D_l][l+1][n].
+static void jobs_rotate(std::vector<XJob>& inv, std::vector<CJob>& co, std::vector<XJob>& fwd, std::vector<MJob>& ma,
+                        int l, int D, const DevKey* key, const u64* c, u64* coef, uint16_t* dig, u64* dntt, u64* o,
+                        const u64* add = nullptr) {
+    const size_t NB = NPOLY;
+    const int P1 = l + 1;
+    for (int k = 0; k < P1; k++) {
+        XJob j{};
+        j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+        j.a = c + ((size_t)1 * P1 + k) * NB;
+        j.out = coef + (size_t)k * NB;
+        inv.push_back(j);
+    }
+    CJob cj{};
+    cj.level = l; cj.mode = 0;
+    cj.x = coef;
+    cj.xstride = NB;
+    cj.gal = key->gal;
+    cj.dig = dig;
+    co.push_back(cj);
+    for (int jj = 0; jj < D; jj++)
+        for (int k = 0; k < P1; k++) {
+            XJob j{};
+            j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE_LAZY;  // feeds k_ksmac (<= 14 lazy terms < q 2^64)
+            j.a = (const u64*)(dig + (size_t)jj * NB);
+            j.out = dntt + ((size_t)jj * P1 + k) * NB;
+            fwd.push_back(j);
+        }
+    MJob mj{};
+    mj.level = l; mj.nterm = 1;
+    mj.t[0].dntt = dntt;
+    mj.t[0].key = key->key;
+    mj.t[0].c0src = c;
+    mj.t[0].perm = key->perm;
+    if (add) {
+        mj.add0 = add;
+        mj.add1 = add + (size_t)P1 * NB;
+    }
+    mj.out0 = o;
+    mj.out1 = o + (size_t)P1 * NB;
+    ma.push_back(mj);
+}
+
 static void add_memset(Schedule& S, void* p, size_t bytes) {
     Step st;
     st.kind = ST_MEMSET;
@@ -671,6 +759,9 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 break;
             case ST_MEMSET:
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
+                break;
+            case ST_ADD:
+                CU(launch(k_addmod, dim3(NPOLY / 256, st.njobs), 256, 0, s, h->hctx, st.pa, st.pb, st.out, st.gy));
                 break;
             case ST_I2: {
                 Intt2Jobs jj;
@@ -784,12 +875,17 @@ struct Plan {
     u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr, *ACC = nullptr;
     uint16_t *digG = nullptr, *digF = nullptr;
     u64* uin = nullptr;  // hc_comp_packed: caller's pack_pair outputs u_t, [B][2][3][n] at level 2
-    std::unique_ptr<Schedule> full, fin, full_u;
+    // hc_comp_mixed: inputs at levels (ld, lv), pack_pair on the device
+    int mix_ld = -1, mix_lv = -1;
+    u64 *mix_cd = nullptr, *mix_cv = nullptr, *mix_pt = nullptr, *mix_buf = nullptr;
+    uint16_t* mix_dig = nullptr;
+    std::unique_ptr<Schedule> full, fin, full_u, full_mix;
     std::map<std::pair<long long, long long>, std::unique_ptr<Schedule>> partials;
     ~Plan() {
         full.reset();
         fin.reset();
         full_u.reset();
+        full_mix.reset();
         partials.clear();
         for (void* p : allocs) cudaFree(p);
     }
@@ -1657,6 +1753,139 @@ extern "C" int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t*
     return HC_OK;
 }
 
+// pack_pair (compress.py:338-367) for inputs at levels ld (cd) and lv (cv),
+// min = 3, into P.uin at level 2: per block a P term mul_plain(ctP, mask) and
+// an R term rot_col(mul_plain(ctR, mask)), each switched down to level 2
+// when it lands at level 3 (add's _at_level, bgv.py:610-614, 656-658:
+// mul_plain by the constant 1), then u = P + R.  Batched over blocks: one
+// launch per stage.
+static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
+    const size_t NB = NPOLY;
+    const int ld = P.mix_ld, lv = P.mix_lv, D3 = h->digits[3], D2 = P.D2;
+    const DevKey* kcol = need_key(h, P.t_col);
+    // plaintexts: mask rows at level 4 ([2][5][n]) and 3 ([2][4][n]), one at level 3 ([4][n])
+    const u64* mk4 = P.mix_pt;
+    const u64* mk3 = P.mask;
+    const u64* one3 = P.mix_pt + (size_t)2 * 5 * NB;
+    const size_t SLOT = (size_t)2 * 4 * NB;  // one [2][<=4][n] ciphertext
+    // per block: Pm, Rm, Rr, P2, R2, cP, cR, cP2, cR2, coef(half), dntt(D3*4/2 slots)
+    const size_t per = (size_t)9 * SLOT + (size_t)4 * NB + (size_t)D3 * 4 * NB;
+    std::vector<XJob> i1, f1, i2, f2, i3, f3;
+    std::vector<CJob> co;
+    std::vector<MJob> ma3, ma2;
+    struct AddJ { const u64 *a, *b; u64* o; };
+    std::vector<AddJ> adds;
+    for (long long t = 0; t < P.B; t++) {
+        const long long src = t / 2;
+        const int par = (int)(t % 2);
+        const u64* cvp = P.mix_cv + (size_t)src * 2 * (lv + 1) * NB;
+        const u64* cdp = P.mix_cd + (size_t)src * 2 * (ld + 1) * NB;
+        // even: P = mp(cv, top), R = mp(cd, top); odd: P = mp(cd, bot), R = mp(cv, bot)
+        const u64* ctP = par == 0 ? cvp : cdp;
+        const u64* ctR = par == 0 ? cdp : cvp;
+        const int lP = par == 0 ? lv : ld, lR = par == 0 ? ld : lv;
+        auto mask = [&](int l) { return l == 4 ? mk4 + (size_t)par * 5 * NB : mk3 + (size_t)par * 4 * NB; };
+        u64* b = P.mix_buf + (size_t)t * per;
+        u64 *Pm = b, *Rm = b + SLOT, *Rr = b + 2 * SLOT, *P2 = b + 3 * SLOT, *R2 = b + 4 * SLOT;
+        u64 *cP = b + 5 * SLOT, *cR = b + 6 * SLOT, *cP2 = b + 7 * SLOT, *cR2 = b + 8 * SLOT;
+        u64* coef = b + 9 * SLOT;
+        u64* dntt = coef + (size_t)4 * NB;
+        uint16_t* dig = P.mix_dig + (size_t)t * D3 * NB;
+        jobs_mul_plain(i1, f1, lP, ctP, mask(lP), cP, Pm);  // level lP - 1
+        jobs_mul_plain(i1, f1, lR, ctR, mask(lR), cR, Rm);  // level lR - 1
+        const int lr = lR - 1;  // rotation level
+        jobs_rotate(i2, co, f2, lr == 3 ? ma3 : ma2, lr, lr == 3 ? D3 : D2, kcol, Rm, coef, dig, dntt, Rr);
+        const u64* pf = Pm;
+        const u64* rf = Rr;
+        if (lP - 1 == 3) {
+            jobs_mul_plain(i3, f3, 3, Pm, one3, cP2, P2);
+            pf = P2;
+        }
+        if (lr == 3) {
+            jobs_mul_plain(i3, f3, 3, Rr, one3, cR2, R2);
+            rf = R2;
+        }
+        adds.push_back({pf, rf, P.uin + (size_t)t * 2 * 3 * NB});
+    }
+    int rc = add_xf(S, i1); if (rc) return rc;
+    rc = add_xf(S, f1); if (rc) return rc;
+    rc = add_xf(S, i2); if (rc) return rc;
+    rc = add_co(S, co); if (rc) return rc;
+    rc = add_xf(S, f2); if (rc) return rc;
+    rc = add_ma(S, ma3, 4); if (rc) return rc;
+    rc = add_ma(S, ma2, 3); if (rc) return rc;
+    rc = add_xf(S, i3); if (rc) return rc;
+    rc = add_xf(S, f3); if (rc) return rc;
+    for (const AddJ& a : adds) add_add(S, a.a, a.b, a.o, 6, 3);
+    return HC_OK;
+}
+
+// Comp with inputs at different levels (answer(): cd = mask(cv) one level
+// below cv): cd = uint64[C][2][ld+1][n], cv =
+// uint64[C][2][lv+1][n], min(ld, lv) = 3, max <= max_level.  pack_pair runs
+// on the device (build_mixed_pack), then the BSGS graph of hc_comp_packed;
+// one graph launch.  out = uint64[2][1][n].  Synchronous.
+extern "C" int hc_comp_mixed(hc_ctx* h, const uint64_t* cd, int ld, const uint64_t* cv, int lv, int C, uint64_t* out) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    if (std::min(ld, lv) < 3) return fail(HC_ERR_LEVEL, "plaintext multiply at level 0 (Comp inputs below level 3)");
+    if (std::min(ld, lv) != 3 || std::max(ld, lv) > h->L)
+        return fail(HC_ERR_ARG, "mixed-level Comp takes inputs at levels 3 and <= max_level with min 3");
+    CU(cudaSetDevice(h->dev));
+    const size_t NB = NPOLY;
+    if (P.mix_ld != ld || P.mix_lv != lv) {
+        P.full_mix.reset();
+        P.mix_ld = ld;
+        P.mix_lv = lv;
+    }
+    if (!P.full_mix) {
+        int rc = HC_OK;
+        const int D3 = h->digits[3];
+        const size_t per = (size_t)9 * 2 * 4 * NB + (size_t)4 * NB + (size_t)D3 * 4 * NB;
+        if (!P.uin) rc = palloc(P, &P.uin, (size_t)P.B * 2 * 3 * NB);
+        if (!rc && !P.mix_cd) rc = palloc(P, &P.mix_cd, (size_t)P.C * 2 * 5 * NB);
+        if (!rc && !P.mix_cv) rc = palloc(P, &P.mix_cv, (size_t)P.C * 2 * 5 * NB);
+        if (!rc && !P.mix_buf) rc = palloc(P, &P.mix_buf, (size_t)P.B * per);
+        if (!rc && !P.mix_dig) rc = palloc(P, &P.mix_dig, (size_t)P.B * D3 * NB);
+        if (!rc && !P.mix_pt) {
+            rc = palloc(P, &P.mix_pt, (size_t)(2 * 5 + 4) * NB);
+            if (!rc) {
+                std::vector<PJob> pj;
+                PJob j{};
+                if (h->L >= 4) {
+                    j.kind = PT_TOP; j.level = 4; j.out = P.mix_pt; pj.push_back(j);
+                    j.kind = PT_BOT; j.level = 4; j.out = P.mix_pt + 5 * NB; pj.push_back(j);
+                }
+                j.kind = PT_ONE; j.level = 3; j.out = P.mix_pt + 10 * NB; pj.push_back(j);
+                PJob* dj = nullptr;
+                CU(cudaMalloc(&dj, pj.size() * sizeof(PJob)));
+                CU(cudaMemcpy(dj, pj.data(), pj.size() * sizeof(PJob), cudaMemcpyHostToDevice));
+                PlanShape sh{P.N, P.s, P.s_pad, P.baby, P.m, nullptr};
+                k_plain<<<(int)pj.size(), NT, 2 * NPOLY * 8, h->stream>>>(h->hctx, dj, sh);
+                cudaError_t e = cudaGetLastError();
+                if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+                cudaFree(dj);
+                if (e != cudaSuccess) return fail(HC_ERR_CUDA, std::string("plaintext generation: ") + cudaGetErrorString(e));
+            }
+        }
+        if (rc) return rc;
+        std::unique_ptr<Schedule> S(new Schedule());
+        rc = build_mixed_pack(h, P, *S);
+        if (!rc) rc = build_partial(h, P, 0, P.B, *S, true);
+        if (!rc) rc = build_finish(h, P, *S);
+        if (!rc) rc = capture(h, *S);
+        if (rc) return rc;
+        P.full_mix = std::move(S);
+    }
+    CU(cudaMemcpyAsync(P.mix_cd, cd, (size_t)C * 2 * (ld + 1) * NB * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(P.mix_cv, cv, (size_t)C * 2 * (lv + 1) * NB * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaGraphLaunch(P.full_mix->exec, h->stream));
+    CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
 extern "C" int hc_comp_partial(hc_ctx* h, int64_t b0, int64_t b1, uint64_t* partial_dev, void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
@@ -1781,24 +2010,7 @@ extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint
     u64* corr = (u64*)dcorr.p;
     u64* o = (u64*)dout.p;
     std::vector<XJob> a, b;
-    for (int poly = 0; poly < 2; poly++) {
-        XJob j{};
-        j.dir = 1; j.k = l; j.ld = LD_MONT; j.ep = l > KEYL ? EP_RESCALE4 : EP_RESCALE; j.level = l;
-        j.a = c + ((size_t)poly * P1 + l) * NB;
-        j.b = p + (size_t)l * NB;
-        j.out = corr + (size_t)poly * l * NB;
-        j.ostride = NB;
-        a.push_back(j);
-        for (int k = 0; k < l; k++) {
-            XJob f{};
-            f.dir = 0; f.k = k; f.ld = LD_U64; f.ep = EP_ADDMONT;
-            f.a = corr + ((size_t)poly * l + k) * NB;
-            f.ea = c + ((size_t)poly * P1 + k) * NB;
-            f.eb = p + (size_t)k * NB;
-            f.out = o + ((size_t)poly * l + k) * NB;
-            b.push_back(f);
-        }
-    }
+    jobs_mul_plain(a, b, l, c, p, corr, o);
     Schedule S;
     int rc = add_xf(S, a);
     if (!rc) rc = add_xf(S, b);
@@ -1826,40 +2038,14 @@ extern "C" int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t t, u
     CU(cudaMemcpy(dct.p, ct, (size_t)2 * P1 * NB * 8, cudaMemcpyHostToDevice));
     const u64* c = (const u64*)dct.p;
     std::vector<XJob> inv, fwd;
-    for (int k = 0; k < P1; k++) {
-        XJob j{};
-        j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
-        j.a = c + ((size_t)1 * P1 + k) * NB;
-        j.out = (u64*)dcoef.p + (size_t)k * NB;
-        inv.push_back(j);
-    }
-    CJob cj{};
-    cj.level = l; cj.mode = 0;
-    cj.x = (u64*)dcoef.p;
-    cj.xstride = NB;
-    cj.gal = key->gal;
-    cj.dig = (uint16_t*)ddig.p;
-    for (int jj = 0; jj < D; jj++)
-        for (int k = 0; k < P1; k++) {
-            XJob j{};
-            j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE_LAZY;  // feeds k_ksmac (<= 14 lazy terms < q 2^64)
-            j.a = (const u64*)((uint16_t*)ddig.p + (size_t)jj * NB);
-            j.out = (u64*)dntt.p + ((size_t)jj * P1 + k) * NB;
-            fwd.push_back(j);
-        }
-    MJob mj{};
-    mj.level = l; mj.nterm = 1;
-    mj.t[0].dntt = (u64*)dntt.p;
-    mj.t[0].key = key->key;
-    mj.t[0].c0src = c;
-    mj.t[0].perm = key->perm;
-    mj.out0 = (u64*)dout.p;
-    mj.out1 = (u64*)dout.p + (size_t)P1 * NB;
+    std::vector<CJob> co;
+    std::vector<MJob> ma;
+    jobs_rotate(inv, co, fwd, ma, l, D, key, c, (u64*)dcoef.p, (uint16_t*)ddig.p, (u64*)dntt.p, (u64*)dout.p);
     Schedule S;
     int rc = add_xf(S, inv);
-    if (!rc) rc = add_co(S, std::vector<CJob>{cj});
+    if (!rc) rc = add_co(S, co);
     if (!rc) rc = add_xf(S, fwd);
-    if (!rc) rc = add_ma(S, std::vector<MJob>{mj}, P1);
+    if (!rc) rc = add_ma(S, ma, P1);
     if (!rc) rc = run_now(h, S);
     if (rc) return rc;
     CU(cudaMemcpy(out, dout.p, (size_t)2 * P1 * NB * 8, cudaMemcpyDeviceToHost));

@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
 // -> Montgomery form with the modulus-switch factor folded in:
 //   k == level (dropped prime): pt * R;  k < level: pt * q_level^-1 * R.
 // ---------------------------------------------------------------------------
-enum : int { PT_DIAG = 0, PT_TOP = 1, PT_BOT = 2, PT_OUTMASK = 3 };
+enum : int { PT_DIAG = 0, PT_TOP = 1, PT_BOT = 2, PT_OUTMASK = 3, PT_ONE = 4 };  // PT_ONE: the modulus switch of add's _at_level
 struct PJob {
     int kind, t, g, b, level, pad;
     u64* out;  // [level+1][n]
@@ -1295,6 +1295,7 @@ HD u64 plain_slot_value(const PJob& J, const PlanShape& S, int r, int c, u64 p, 
         }
         case PT_TOP: return r == 0 ? 1 : 0;
         case PT_BOT: return r == 1 ? 1 : 0;
+        case PT_ONE: return 1;
         default: return c < S.s ? 1 : 0;  // PT_OUTMASK
     }
 }
@@ -1344,6 +1345,16 @@ __global__ void k_to_mont(const __grid_constant__ DevCtx C, u64* data, long long
 }
 
 // pointwise op over rows; prime of row r = pidx[r]
+// out = a + b mod q_k over rows of n, row r modulo prime r % P: the add of
+// pack_pair's two terms (bgv.py:651-670) in the mixed-level schedule
+__global__ void __launch_bounds__(256) k_addmod(const __grid_constant__ DevCtx C, const u64* __restrict__ a,
+                                                const u64* __restrict__ b, u64* __restrict__ out, int P) {
+    const size_t i = (size_t)blockIdx.y * NPOLY + blockIdx.x * 256 + threadIdx.x;
+    const u64 q = C.pc[blockIdx.y % P].q;
+    pdl_wait();
+    out[i] = add_mod(a[i], b[i], q);
+}
+
 __global__ void k_pointwise(const __grid_constant__ DevCtx C, const u64* a, const u64* b, u64* out, int rows,
                             const int* pidx, int op) {
     const long long total = (long long)rows * NPOLY;

@@ -217,8 +217,18 @@ def test_answer_mask_then_comp_matches_reference_golden(pkg, oracle, name):
     assert delta.as_dict() == g["counters"]
     w, e = ans.payload_slots(be, keys)
     assert (w, e) == (g["w"], g["e"]) == O.expected_slots(dense, s, p)
-    # the one-call form and a repeat on the cached packed-input graph
+    # the one-call form (a repeat on the cached mixed-level graph)
     assert O.sha256(P.answer_from_match(hint, db, params, be, keys).serialize(be)) == g["answer_sha256"]
+    # pack_pair as single GPU operations + the BSGS graph from u (the route
+    # for per-ciphertext levels): the same residues
+    from paper_2408_17063_b200 import _lib
+    from paper_2408_17063_b200.compress import _pack_pair_ops
+
+    u = _pack_pair_ops(hint, cd, params, be, keys)
+    u_arr = np.ascontiguousarray(np.stack([c.payload.res for c in u]), dtype=np.uint64)
+    out = np.empty((2, 1, n), dtype=np.uint64)
+    _lib.check(_lib.lib(4).hc_comp_packed(be._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
+    assert np.array_equal(out, ans.cts[0].payload.res)
 
 
 def test_fused_comp_on_a_five_prime_chain_vs_oracle(pkg, oracle):
