@@ -102,6 +102,15 @@ int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t* out);
  * LevelExhausted at the output mask).  Synchronous. */
 int hc_comp_mixed(hc_ctx* h, const uint64_t* cd, int ld, const uint64_t* cv, int lv, int C, uint64_t* out);
 
+/* Replaces pdq.answer after Match (pdq.py:248-256): cd = mask(cv, db)
+ * (pdq.py:238-245) then comp(cd, index_hint=cv), in one graph launch.
+ * hc_answer_db first turns the cleartext database (uint64[N], reduced mod p)
+ * into the mask plaintexts at `level` for the current plan (repeat after
+ * hc_plan); hc_answer then takes cv = uint64[C][2][lv+1][n] at level
+ * lv = 4 (max_level 4) and writes out = uint64[2][1][n].  Synchronous. */
+int hc_answer_db(hc_ctx* h, int level, const uint64_t* db_mod_p);
+int hc_answer(hc_ctx* h, const uint64_t* cv, int lv, int C, uint64_t* out);
+
 /* Device-resident variant for timing: inputs already uploaded with
  * hc_comp_set_inputs; hc_comp_launch enqueues the whole Comp (one graph
  * launch) on `stream` (a cudaStream_t, NULL = legacy default stream). */

@@ -691,6 +691,14 @@ class B200BgvBackend:
                 _lib.check(_lib.lib(self.params.max_level).hc_plan_masked(self._ctx(), N, s, chunk_blocks, _lib.ptr(db)))
             self._planned = tag
 
+    def answer_db(self, db_mod_p: np.ndarray, level: int) -> None:
+        """Mask plaintexts of the cleartext database for the current plan (hc_answer_db)."""
+        db = np.ascontiguousarray(db_mod_p, dtype=np.uint64)
+        tag = (self._planned, level, hashlib.sha256(db.tobytes()).digest())
+        if getattr(self, "_answer_db_tag", None) != tag:
+            _lib.check(_lib.lib(self.params.max_level).hc_answer_db(self._ctx(), level, _lib.ptr(db)))
+            self._answer_db_tag = tag
+
     def plan_info(self) -> dict:
         info = np.zeros(8, dtype=np.int64)
         _lib.check(_lib.lib(self.params.max_level).hc_plan_info(self._ctx(), _lib.ptr(info)))

@@ -354,6 +354,41 @@ def answer_from_match(
     values = db.values if hasattr(db, "values") else db
     if len(values) != params.N:
         raise ValueError(f"database has {len(values)} records, params expect {params.N}")
+    cv = list(cv)
+    if (
+        isinstance(backend, B200BgvBackend)
+        and backend.params == params.he
+        and len(cv) == params.num_ciphertexts
+        and {c.level for c in cv} == {FUSED_LEVEL + 1}
+    ):
+        # Mask and Comp in one graph launch (hc_answer)
+        for c in cv:
+            backend._check_keys(c, keys)
+        if keys.col_swap_key is None:
+            raise MissingRotationKey("column-swap key was not declared at keygen")
+        lv = FUSED_LEVEL + 1
+        sim = _NoiseSim(backend)
+        cv_bits = [(c.payload.noise_bits, lv) for c in cv]
+        cd_bits = [(sim.mul_plain(b, lv), lv - 1) for b, _ in cv_bits]  # mask's mul_plains
+        u_bits = pack_noise_mixed(sim, params, cv_bits, cd_bits)
+        bits, sim = bsgs_noise(sim, params, u_bits, live_diagonals(params), FUSED_LEVEL - 1)
+        backend.plan(params.N, params.s, keys)
+        p = params.he.p
+        try:
+            db_mod_p = (np.asarray(values, dtype=np.int64) % p).astype(np.uint64)
+        except OverflowError:  # entries beyond int64: reduce as Python ints
+            db_mod_p = np.fromiter((int(v) % p for v in values), dtype=np.uint64, count=params.N)
+        backend.answer_db(db_mod_p, lv)
+        cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv]), dtype=np.uint64)
+        out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
+        _lib.check(
+            _lib.lib(backend.params.max_level).hc_answer(backend._ctx(), _lib.ptr(cv_arr), lv, len(cv), _lib.ptr(out))
+        )
+        backend.counters.keyswitches += sim.ks
+        backend.counters.pt_mults += sim.pt
+        backend.counters.adds += sim.adds
+        ct = Ciphertext(backend.backend_id, keys.key_id, 0, RnsPayload(out, bits, (backend.q[0],)))
+        return CompressedAnswer((ct,), params.s, True)
     cd = mask(cv, values, params, backend, keys)
     return comp(cd, params, backend, keys, index_hint=cv)
 

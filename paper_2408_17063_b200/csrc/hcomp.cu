@@ -876,7 +876,9 @@ struct Plan {
     uint16_t *digG = nullptr, *digF = nullptr;
     u64* uin = nullptr;  // hc_comp_packed: caller's pack_pair outputs u_t, [B][2][3][n] at level 2
     // hc_comp_mixed: inputs at levels (ld, lv), pack_pair on the device
-    int mix_ld = -1, mix_lv = -1;
+    int mix_ld = -1, mix_lv = -1, mix_mask = -1;
+    u64* ans_pt = nullptr;  // hc_answer_db: mask plaintexts [C][ans_level+1][n]
+    int ans_level = -1;
     u64 *mix_cd = nullptr, *mix_cv = nullptr, *mix_pt = nullptr, *mix_buf = nullptr;
     uint16_t* mix_dig = nullptr;
     std::unique_ptr<Schedule> full, fin, full_u, full_mix;
@@ -1753,6 +1755,21 @@ extern "C" int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t*
     return HC_OK;
 }
 
+static int gen_plain(hc_ctx* h, const std::vector<PJob>& pj, const PlanShape& sh) {
+    PJob* dj = nullptr;
+    CU(cudaMalloc(&dj, pj.size() * sizeof(PJob)));
+    CU(cudaMemcpy(dj, pj.data(), pj.size() * sizeof(PJob), cudaMemcpyHostToDevice));
+    for (size_t off = 0; off < pj.size(); off += 65535) {
+        const int cnt = (int)std::min<size_t>(65535, pj.size() - off);
+        k_plain<<<cnt, NT, 2 * NPOLY * 8, h->stream>>>(h->hctx, dj + off, sh);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(dj);
+    if (e != cudaSuccess) return fail(HC_ERR_CUDA, std::string("plaintext generation: ") + cudaGetErrorString(e));
+    return HC_OK;
+}
+
 // pack_pair (compress.py:338-367) for inputs at levels ld (cd) and lv (cv),
 // min = 3, into P.uin at level 2: per block a P term mul_plain(ctP, mask) and
 // an R term rot_col(mul_plain(ctR, mask)), each switched down to level 2
@@ -1825,6 +1842,65 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
 // uint64[C][2][lv+1][n], min(ld, lv) = 3, max <= max_level.  pack_pair runs
 // on the device (build_mixed_pack), then the BSGS graph of hc_comp_packed;
 // one graph launch.  out = uint64[2][1][n].  Synchronous.
+static int ensure_mixed(hc_ctx* h, Plan& P, int ld, int lv, int with_mask) {
+    const size_t NB = NPOLY;
+    if (P.mix_ld != ld || P.mix_lv != lv || P.mix_mask != with_mask) {
+        P.full_mix.reset();
+        P.mix_ld = ld;
+        P.mix_lv = lv;
+        P.mix_mask = with_mask;
+    }
+    if (P.full_mix) return HC_OK;
+    int rc = HC_OK;
+    const int D3 = h->digits[3];
+    const size_t per = (size_t)9 * 2 * 4 * NB + (size_t)4 * NB + (size_t)D3 * 4 * NB;
+    if (!P.uin) rc = palloc(P, &P.uin, (size_t)P.B * 2 * 3 * NB);
+    if (!rc && !P.mix_cd) rc = palloc(P, &P.mix_cd, (size_t)P.C * 2 * 5 * NB);
+    if (!rc && !P.mix_cv) rc = palloc(P, &P.mix_cv, (size_t)P.C * 2 * 5 * NB);
+    if (!rc && !P.mix_buf) rc = palloc(P, &P.mix_buf, (size_t)P.B * per);
+    if (!rc && !P.mix_dig) rc = palloc(P, &P.mix_dig, (size_t)P.B * D3 * NB);
+    if (!rc && !P.mix_pt) {
+        rc = palloc(P, &P.mix_pt, (size_t)(2 * 5 + 4) * NB);
+        if (!rc) {
+            std::vector<PJob> pj;
+            PJob j{};
+            if (h->L >= 4) {
+                j.kind = PT_TOP; j.level = 4; j.out = P.mix_pt; pj.push_back(j);
+                j.kind = PT_BOT; j.level = 4; j.out = P.mix_pt + 5 * NB; pj.push_back(j);
+            }
+            j.kind = PT_ONE; j.level = 3; j.out = P.mix_pt + 10 * NB; pj.push_back(j);
+            PlanShape sh{P.N, P.s, P.s_pad, P.baby, P.m, nullptr};
+            rc = gen_plain(h, pj, sh);
+        }
+    }
+    if (rc) return rc;
+    std::unique_ptr<Schedule> S(new Schedule());
+    if (with_mask) {
+        // pdq.mask (pdq.py:238-245): cd_c = mul_plain(cv_c, DB block c) at level lv
+        std::vector<XJob> inv, fwd;
+        u64* corr = P.mix_buf;  // scratch before the pack uses it
+        if ((size_t)P.C * 2 * lv * NB > (size_t)P.B * per) return fail(HC_ERR_STATE, "mask scratch too small");
+        for (long long c = 0; c < P.C; c++)
+            jobs_mul_plain(inv, fwd, lv, P.mix_cv + (size_t)c * 2 * (lv + 1) * NB, P.ans_pt + (size_t)c * (lv + 1) * NB,
+                           corr + (size_t)c * 2 * lv * NB, P.mix_cd + (size_t)c * 2 * lv * NB);
+        rc = add_xf(*S, inv);
+        if (!rc) rc = add_xf(*S, fwd);
+        if (rc) return rc;
+    }
+    rc = build_mixed_pack(h, P, *S);
+    if (!rc) rc = build_partial(h, P, 0, P.B, *S, true);
+    if (!rc) rc = build_finish(h, P, *S);
+    if (!rc) rc = capture(h, *S);
+    if (rc) return rc;
+    P.full_mix = std::move(S);
+    return HC_OK;
+}
+
+// Comp with inputs at different levels (answer(): cd = mask(cv) one level
+// below cv): cd = uint64[C][2][ld+1][n], cv =
+// uint64[C][2][lv+1][n], min(ld, lv) = 3, max <= max_level.  pack_pair runs
+// on the device (build_mixed_pack), then the BSGS graph of hc_comp_packed;
+// one graph launch.  out = uint64[2][1][n].  Synchronous.
 extern "C" int hc_comp_mixed(hc_ctx* h, const uint64_t* cd, int ld, const uint64_t* cv, int lv, int C, uint64_t* out) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
@@ -1834,52 +1910,62 @@ extern "C" int hc_comp_mixed(hc_ctx* h, const uint64_t* cd, int ld, const uint64
         return fail(HC_ERR_ARG, "mixed-level Comp takes inputs at levels 3 and <= max_level with min 3");
     CU(cudaSetDevice(h->dev));
     const size_t NB = NPOLY;
-    if (P.mix_ld != ld || P.mix_lv != lv) {
-        P.full_mix.reset();
-        P.mix_ld = ld;
-        P.mix_lv = lv;
-    }
-    if (!P.full_mix) {
-        int rc = HC_OK;
-        const int D3 = h->digits[3];
-        const size_t per = (size_t)9 * 2 * 4 * NB + (size_t)4 * NB + (size_t)D3 * 4 * NB;
-        if (!P.uin) rc = palloc(P, &P.uin, (size_t)P.B * 2 * 3 * NB);
-        if (!rc && !P.mix_cd) rc = palloc(P, &P.mix_cd, (size_t)P.C * 2 * 5 * NB);
-        if (!rc && !P.mix_cv) rc = palloc(P, &P.mix_cv, (size_t)P.C * 2 * 5 * NB);
-        if (!rc && !P.mix_buf) rc = palloc(P, &P.mix_buf, (size_t)P.B * per);
-        if (!rc && !P.mix_dig) rc = palloc(P, &P.mix_dig, (size_t)P.B * D3 * NB);
-        if (!rc && !P.mix_pt) {
-            rc = palloc(P, &P.mix_pt, (size_t)(2 * 5 + 4) * NB);
-            if (!rc) {
-                std::vector<PJob> pj;
-                PJob j{};
-                if (h->L >= 4) {
-                    j.kind = PT_TOP; j.level = 4; j.out = P.mix_pt; pj.push_back(j);
-                    j.kind = PT_BOT; j.level = 4; j.out = P.mix_pt + 5 * NB; pj.push_back(j);
-                }
-                j.kind = PT_ONE; j.level = 3; j.out = P.mix_pt + 10 * NB; pj.push_back(j);
-                PJob* dj = nullptr;
-                CU(cudaMalloc(&dj, pj.size() * sizeof(PJob)));
-                CU(cudaMemcpy(dj, pj.data(), pj.size() * sizeof(PJob), cudaMemcpyHostToDevice));
-                PlanShape sh{P.N, P.s, P.s_pad, P.baby, P.m, nullptr};
-                k_plain<<<(int)pj.size(), NT, 2 * NPOLY * 8, h->stream>>>(h->hctx, dj, sh);
-                cudaError_t e = cudaGetLastError();
-                if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-                cudaFree(dj);
-                if (e != cudaSuccess) return fail(HC_ERR_CUDA, std::string("plaintext generation: ") + cudaGetErrorString(e));
-            }
-        }
-        if (rc) return rc;
-        std::unique_ptr<Schedule> S(new Schedule());
-        rc = build_mixed_pack(h, P, *S);
-        if (!rc) rc = build_partial(h, P, 0, P.B, *S, true);
-        if (!rc) rc = build_finish(h, P, *S);
-        if (!rc) rc = capture(h, *S);
-        if (rc) return rc;
-        P.full_mix = std::move(S);
-    }
+    int rc = ensure_mixed(h, P, ld, lv, 0);
+    if (rc) return rc;
     CU(cudaMemcpyAsync(P.mix_cd, cd, (size_t)C * 2 * (ld + 1) * NB * 8, cudaMemcpyHostToDevice, h->stream));
     CU(cudaMemcpyAsync(P.mix_cv, cv, (size_t)C * 2 * (lv + 1) * NB * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaGraphLaunch(P.full_mix->exec, h->stream));
+    CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
+// pdq.mask's plaintexts for the current plan: the cleartext database
+// (uint64[N], reduced mod p) as C block plaintexts at `level`
+// (_db_block_matrices, pdq.py:207-208), generated on the device.
+extern "C" int hc_answer_db(hc_ctx* h, int level, const uint64_t* db_mod_p) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    if (!db_mod_p) return fail(HC_ERR_ARG, "null database");
+    if (level < 4 || level > h->L) return fail(HC_ERR_ARG, "answer() on the device takes the index vector at level 4");
+    Plan& P = *h->plan;
+    CU(cudaSetDevice(h->dev));
+    const size_t NB = NPOLY;
+    std::vector<uint32_t> dbv((size_t)P.N);
+    for (long long i = 0; i < P.N; i++) {
+        if (db_mod_p[i] >= h->p) return fail(HC_ERR_ARG, "database values must be reduced mod p");
+        dbv[i] = (uint32_t)db_mod_p[i];
+    }
+    uint32_t* ddb = nullptr;
+    int rc = palloc(P, &ddb, (size_t)P.N);
+    if (rc) return rc;
+    CU(cudaMemcpy(ddb, dbv.data(), (size_t)P.N * 4, cudaMemcpyHostToDevice));
+    if (!P.ans_pt || P.ans_level != level) {
+        rc = palloc(P, &P.ans_pt, (size_t)P.C * (level + 1) * NB);
+        if (rc) return rc;
+        P.ans_level = level;
+    }
+    std::vector<PJob> pj;
+    for (long long c = 0; c < P.C; c++) {
+        PJob j{};
+        j.kind = PT_DBVEC; j.t = (int)c; j.level = level; j.out = P.ans_pt + (size_t)c * (level + 1) * NB;
+        pj.push_back(j);
+    }
+    PlanShape sh{P.N, P.s, P.s_pad, P.baby, P.m, ddb};
+    return gen_plain(h, pj, sh);
+}
+
+// pdq.answer after Match (pdq.py:248-256): mask (cv x the hc_answer_db
+// plaintexts) then comp(cd, index_hint=cv), cv = uint64[C][2][lv+1][n] at
+// level lv = 4; one graph launch.  out = uint64[2][1][n].  Synchronous.
+extern "C" int hc_answer(hc_ctx* h, const uint64_t* cv, int lv, int C, uint64_t* out) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    if (!P.ans_pt || P.ans_level != lv) return fail(HC_ERR_STATE, "hc_answer_db must run first at this level");
+    CU(cudaSetDevice(h->dev));
+    int rc = ensure_mixed(h, P, lv - 1, lv, 1);
+    if (rc) return rc;
+    CU(cudaMemcpyAsync(P.mix_cv, cv, (size_t)C * 2 * (lv + 1) * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
     CU(cudaGraphLaunch(P.full_mix->exec, h->stream));
     CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));

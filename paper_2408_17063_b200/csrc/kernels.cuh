@@ -1259,7 +1259,9 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
 // -> Montgomery form with the modulus-switch factor folded in:
 //   k == level (dropped prime): pt * R;  k < level: pt * q_level^-1 * R.
 // ---------------------------------------------------------------------------
-enum : int { PT_DIAG = 0, PT_TOP = 1, PT_BOT = 2, PT_OUTMASK = 3, PT_ONE = 4 };  // PT_ONE: the modulus switch of add's _at_level
+// PT_ONE: the modulus switch of add's _at_level; PT_DBVEC: block t of the
+// cleartext database vector (pdq.mask's _db_block_matrices, pdq.py:207-208)
+enum : int { PT_DIAG = 0, PT_TOP = 1, PT_BOT = 2, PT_OUTMASK = 3, PT_ONE = 4, PT_DBVEC = 5 };
 struct PJob {
     int kind, t, g, b, level, pad;
     u64* out;  // [level+1][n]
@@ -1296,6 +1298,10 @@ HD u64 plain_slot_value(const PJob& J, const PlanShape& S, int r, int c, u64 p, 
         case PT_TOP: return r == 0 ? 1 : 0;
         case PT_BOT: return r == 1 ? 1 : 0;
         case PT_ONE: return 1;
+        case PT_DBVEC: {  // SlotMatrix.from_vector: first m entries in row 0, the next m in row 1
+            const long long pos = (long long)J.t * 2 * S.m + (long long)r * S.m + c;
+            return pos < S.N ? S.db[pos] : 0;
+        }
         default: return c < S.s ? 1 : 0;  // PT_OUTMASK
     }
 }

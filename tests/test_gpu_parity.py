@@ -217,8 +217,15 @@ def test_answer_mask_then_comp_matches_reference_golden(pkg, oracle, name):
     assert delta.as_dict() == g["counters"]
     w, e = ans.payload_slots(be, keys)
     assert (w, e) == (g["w"], g["e"]) == O.expected_slots(dense, s, p)
-    # the one-call form (a repeat on the cached mixed-level graph)
-    assert O.sha256(P.answer_from_match(hint, db, params, be, keys).serialize(be)) == g["answer_sha256"]
+    # the one-call form: Mask and Comp in one graph launch (hc_answer), twice;
+    # counters move as mask + comp
+    for _ in range(2):
+        before = be.counters.snapshot()
+        a2 = P.answer_from_match(hint, db, params, be, keys)
+        d2 = be.counters.delta(before).as_dict()
+        assert O.sha256(a2.serialize(be)) == g["answer_sha256"]
+        assert a2.cts[0].payload.noise_bits == g["noise_bits"]
+        assert d2 == {k: g["counters"][k] + g["mask_counters"][k] for k in d2}
     # pack_pair as single GPU operations + the BSGS graph from u (the route
     # for per-ciphertext levels): the same residues
     from paper_2408_17063_b200 import _lib
