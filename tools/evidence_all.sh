@@ -10,6 +10,7 @@ python tools/sweep.py 16384:16 65536:64 1048576:16 --flush > $O/sweep_flush.txt 
 python tools/trace_comp.py > $O/trace.txt 2>&1
 python bench.py --N 1048576 --s 16 --steps 5 --warmup 3 > $O/bench_2e20.json 2>/dev/null
 python tools/multi_query.py --Q 8 > $O/mq.txt 2>&1
+(python tools/answer_bench.py --N 8192 --s 8; python tools/answer_bench.py --N 16384 --s 16; python tools/answer_bench.py --N 65536 --s 64) > $O/answer_bench.jsonl 2>&1
 python tools/ncu_summary.py $O/ncu_full_xf_vt4.ncu-rep $O/ncu_full_xf_cl_fold.ncu-rep $O/ncu_full_intt2_fold.ncu-rep \
   $O/ncu_full_xf_diag_intt.ncu-rep $O/ncu_full_ksmac_2e20.ncu-rep $O/ncu_full_diagx_2e20.ncu-rep > $O/ncu_summary.txt 2>&1
 for r in xf_vt4 xf_cl_fold intt2_fold xf_diag_intt ksmac_2e20 diagx_2e20; do
