@@ -83,8 +83,23 @@ def test_noise_and_counters_replay_reference(name):
     g = load_golden(name)
     if g["n"] != 8192:
         pytest.skip("the B200 backend is n = 8192 only")
-    if g.get("answer"):
-        pytest.skip("mixed-level pack_pair runs as backend ops (noise checked by the GPU and oracle tests)")
+    if g.get("answer"):  # mask (level 4 -> 3), then comp with mixed input levels
+        from paper_2408_17063_b200.compress import FUSED_LEVEL, _NoiseSim, bsgs_noise, pack_noise_mixed
+
+        he = P.HeParams(g["n"], g["p"], g["max_level"])
+        params = P.CompressionParams(g["N"], g["s"], he)
+        be = P.B200BgvBackend(he, seed=0, noise_guard=not g["noise_guard_disabled"])
+        fresh = be._fresh_noise_bits()
+        C = params.num_ciphertexts
+        msim = _NoiseSim(be)
+        cd = [(msim.mul_plain(fresh, 4), 3) for _ in range(C)]
+        assert {"keyswitches": msim.ks, "pt_mults": msim.pt, "adds": msim.adds, "ct_mults": 0} == g["mask_counters"]
+        sim = _NoiseSim(be)
+        u = pack_noise_mixed(sim, params, [(fresh, 4)] * C, cd)
+        bits, sim = bsgs_noise(sim, params, u, live_diagonals(params), FUSED_LEVEL - 1)
+        assert bits == g["noise_bits"]
+        assert {"keyswitches": sim.ks, "pt_mults": sim.pt, "adds": sim.adds, "ct_mults": 0} == g["counters"]
+        return
     he = P.HeParams(g["n"], g["p"], 3)
     params = P.CompressionParams(g["N"], g["s"], he)
     be = P.B200BgvBackend(he, seed=0, noise_guard=not g["noise_guard_disabled"])
