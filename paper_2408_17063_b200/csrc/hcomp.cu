@@ -878,6 +878,7 @@ struct Plan {
     // hc_comp_mixed: inputs at levels (ld, lv), pack_pair on the device
     int mix_ld = -1, mix_lv = -1, mix_mask = -1;
     u64* ans_pt = nullptr;  // hc_answer_db: mask plaintexts [C][ans_level+1][n]
+    uint32_t* ans_db = nullptr;  // hc_answer_db: the database mod p
     int ans_level = -1;
     u64 *mix_cd = nullptr, *mix_cv = nullptr, *mix_pt = nullptr, *mix_buf = nullptr;
     uint16_t* mix_dig = nullptr;
@@ -1935,15 +1936,17 @@ extern "C" int hc_answer_db(hc_ctx* h, int level, const uint64_t* db_mod_p) {
         if (db_mod_p[i] >= h->p) return fail(HC_ERR_ARG, "database values must be reduced mod p");
         dbv[i] = (uint32_t)db_mod_p[i];
     }
-    uint32_t* ddb = nullptr;
-    int rc = palloc(P, &ddb, (size_t)P.N);
+    int rc = HC_OK;
+    if (!P.ans_db) rc = palloc(P, &P.ans_db, (size_t)P.N);  // reused by later databases
     if (rc) return rc;
+    uint32_t* ddb = P.ans_db;
     CU(cudaMemcpy(ddb, dbv.data(), (size_t)P.N * 4, cudaMemcpyHostToDevice));
-    if (!P.ans_pt || P.ans_level != level) {
+    if (!P.ans_pt || P.ans_level < level) {  // sized for the highest level asked so far
         rc = palloc(P, &P.ans_pt, (size_t)P.C * (level + 1) * NB);
         if (rc) return rc;
-        P.ans_level = level;
+        P.full_mix.reset();  // a captured Mask graph read the old buffer
     }
+    P.ans_level = level;
     std::vector<PJob> pj;
     for (long long c = 0; c < P.C; c++) {
         PJob j{};
