@@ -110,6 +110,10 @@ int hc_comp_mixed(hc_ctx* h, const uint64_t* cd, int ld, const uint64_t* cv, int
  * lv = 4 (max_level 4) and writes out = uint64[2][1][n].  Synchronous. */
 int hc_answer_db(hc_ctx* h, int level, const uint64_t* db_mod_p);
 int hc_answer(hc_ctx* h, const uint64_t* cv, int lv, int C, uint64_t* out);
+/* Replay the last hc_comp_mixed / hc_answer graph on `stream` with the inputs
+ * already on the device (one graph launch; read the output with
+ * hc_comp_get_output). */
+int hc_mixed_launch(hc_ctx* h, void* stream);
 
 /* Device-resident variant for timing: inputs already uploaded with
  * hc_comp_set_inputs; hc_comp_launch enqueues the whole Comp (one graph

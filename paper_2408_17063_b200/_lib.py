@@ -56,6 +56,7 @@ _SIGS = [
     ("hc_comp_mixed", _I, [_P, _P, _I, _P, _I, _I, _P]),
     ("hc_answer_db", _I, [_P, _I, _P]),
     ("hc_answer", _I, [_P, _P, _I, _I, _P]),
+    ("hc_mixed_launch", _I, [_P, _P]),
     ("hc_plain_row", _I, []),
     ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),
     ("hc_comp_set_inputs", _I, [_P, _P, _P, _I]),

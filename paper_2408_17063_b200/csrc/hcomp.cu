@@ -1975,6 +1975,15 @@ extern "C" int hc_answer(hc_ctx* h, const uint64_t* cv, int lv, int C, uint64_t*
     return HC_OK;
 }
 
+// Device-resident replay of the last hc_comp_mixed / hc_answer graph on
+// `stream` (inputs stay in the plan's buffers; timing and serving loops).
+extern "C" int hc_mixed_launch(hc_ctx* h, void* stream) {
+    if (!h || !h->plan || !h->plan->full_mix) return fail(HC_ERR_STATE, "hc_comp_mixed or hc_answer must run first");
+    CU(cudaSetDevice(h->dev));
+    CU(cudaGraphLaunch(h->plan->full_mix->exec, stream ? (cudaStream_t)stream : h->stream));
+    return HC_OK;
+}
+
 extern "C" int hc_comp_partial(hc_ctx* h, int64_t b0, int64_t b1, uint64_t* partial_dev, void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
