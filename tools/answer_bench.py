@@ -37,7 +37,9 @@ def main():
     N, s, p, seed = a.N, a.s, 65537, 6
     he = P.HeParams(8192, p, 4)
     params = P.CompressionParams(N, s, he)
-    be = P.B200BgvBackend(he, seed=seed)
+    # noise guard off (as the oracle's guard-disabled goldens): the reference's
+    # heuristic bound trips from s = 32 at these levels; values never depend on it
+    be = P.B200BgvBackend(he, seed=seed, noise_guard=False)
     keys = be.keygen(*P.plan_rotation_amounts(s, 8192))
     support, db, dense = O.masked_payload(N, s, p, seed)
     hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
@@ -58,7 +60,7 @@ def main():
     t_bsgs, _ = med(lambda: _lib.check(L.hc_comp_packed(be._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out))), a.iters)
     # the fused level-3 Comp at the same point (4-prime chain)
     he3 = P.HeParams(8192, p, 3)
-    be3 = P.B200BgvBackend(he3, seed=seed)
+    be3 = P.B200BgvBackend(he3, seed=seed, noise_guard=False)
     k3 = be3.keygen(*P.plan_rotation_amounts(s, 8192))
     d3 = O.plant_sparse(random.Random(seed), N, s, p)
     c3 = P.encrypt_vector(d3, P.CompressionParams(N, s, he3), be3, k3)

@@ -1,5 +1,5 @@
 """Per-launch phase timeline of one Comp graph run (needs libhcomp_trace.so:
-nvcc ... -DHC_TRACE -o paper_2408_17063_b200/libhcomp_trace.so)."""
+nvcc ... -DHC_TRACE -DHC_MAXL=3 -o paper_2408_17063_b200/libhcomp_trace.so)."""
 import os, sys
 HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 os.environ.setdefault("HCOMP_LIB", os.path.join(HERE, "paper_2408_17063_b200", "libhcomp_trace.so"))
