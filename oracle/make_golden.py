@@ -57,10 +57,11 @@ CASES = {
     # levels, reconciled by add's _at_level (bgv.py:656-658)
     "answer_small_n64_N200_s5": (64, 257, 200, 5, 14, True),
     "answer_c1_N8192_s8": (8192, 65537, 8192, 8, 6, False),
+    "answer_c2_N16384_s16": (8192, 65537, 16384, 16, 7, False),
 }
 
 # max_level per case (default 3, the BASELINE chain)
-MAX_LEVEL = {"answer_small_n64_N200_s5": 4, "answer_c1_N8192_s8": 4}
+MAX_LEVEL = {"answer_small_n64_N200_s5": 4, "answer_c1_N8192_s8": 4, "answer_c2_N16384_s16": 4}
 
 
 def masked_payload(N, s, p, seed):
