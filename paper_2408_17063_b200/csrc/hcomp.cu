@@ -134,10 +134,9 @@ struct Step {
     int njobs = 0;
     int gy = 1;
     void* djobs = nullptr;
-    // ST_MEMSET, ST_ADD (out = pa + pb: njobs rows, gy primes)
+    // ST_MEMSET
     u64* out = nullptr;
-    const u64* pa = nullptr;
-    const u64* pb = nullptr;
+    int rows = 0;  // ST_ADD: rows per job (gy: primes)
     size_t bytes = 0;
     std::vector<XJob> hjobs;  // ST_XF: host copy (cluster launches pass jobs by value)
     std::vector<Intt2Job> i2jobs;  // ST_I2
@@ -575,17 +574,19 @@ static int add_i2(Schedule& S, std::vector<Intt2Job> jobs) {
     return HC_OK;
 }
 
-static void add_add(Schedule& S, const u64* a, const u64* b, u64* out, int rows, int nprime) {
+static int add_add(Schedule& S, const std::vector<AddJob>& jobs, int rows, int nprime) {
+    if (jobs.empty()) return HC_OK;
     Step st;
     st.kind = ST_ADD;
     st.group = S.cur_group;
     st.lane = S.cur_lane;
-    st.pa = a;
-    st.pb = b;
-    st.out = out;
-    st.njobs = rows;
+    st.njobs = (int)jobs.size();
+    st.rows = rows;
     st.gy = nprime;
+    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(AddJob));
+    if (rc) return rc;
     S.steps.push_back(st);
+    return HC_OK;
 }
 
 // Job lists of single ring operations on device buffers (used by the
@@ -761,7 +762,7 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
                 break;
             case ST_ADD:
-                CU(launch(k_addmod, dim3(NPOLY / 256, st.njobs), 256, 0, s, h->hctx, st.pa, st.pb, st.out, st.gy));
+                CU(launch(k_addmod, dim3(NPOLY / 256, st.rows, st.njobs), 256, 0, s, h->hctx, (const AddJob*)st.djobs, st.gy));
                 break;
             case ST_I2: {
                 Intt2Jobs jj;
@@ -1791,8 +1792,7 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
     std::vector<XJob> i1, f1, i2, f2, i3, f3;
     std::vector<CJob> co;
     std::vector<MJob> ma3, ma2;
-    struct AddJ { const u64 *a, *b; u64* o; };
-    std::vector<AddJ> adds;
+    std::vector<AddJob> adds;
     for (long long t = 0; t < P.B; t++) {
         const long long src = t / 2;
         const int par = (int)(t % 2);
@@ -1834,8 +1834,7 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
     rc = add_ma(S, ma2, 3); if (rc) return rc;
     rc = add_xf(S, i3); if (rc) return rc;
     rc = add_xf(S, f3); if (rc) return rc;
-    for (const AddJ& a : adds) add_add(S, a.a, a.b, a.o, 6, 3);
-    return HC_OK;
+    return add_add(S, adds, 6, 3);  // u = P + R, all blocks in one launch
 }
 
 // Comp with inputs at different levels (answer(): cd = mask(cv) one level

@@ -1353,12 +1353,18 @@ __global__ void k_to_mont(const __grid_constant__ DevCtx C, u64* data, long long
 // pointwise op over rows; prime of row r = pidx[r]
 // out = a + b mod q_k over rows of n, row r modulo prime r % P: the add of
 // pack_pair's two terms (bgv.py:651-670) in the mixed-level schedule
-__global__ void __launch_bounds__(256) k_addmod(const __grid_constant__ DevCtx C, const u64* __restrict__ a,
-                                                const u64* __restrict__ b, u64* __restrict__ out, int P) {
+struct AddJob {
+    const u64* a;
+    const u64* b;
+    u64* out;
+};
+// grid (n/256, rows, jobs)
+__global__ void __launch_bounds__(256) k_addmod(const __grid_constant__ DevCtx C, const AddJob* __restrict__ jobs, int P) {
+    const AddJob J = jobs[blockIdx.z];
     const size_t i = (size_t)blockIdx.y * NPOLY + blockIdx.x * 256 + threadIdx.x;
     const u64 q = C.pc[blockIdx.y % P].q;
     pdl_wait();
-    out[i] = add_mod(a[i], b[i], q);
+    J.out[i] = add_mod(J.a[i], J.b[i], q);
 }
 
 __global__ void k_pointwise(const __grid_constant__ DevCtx C, const u64* a, const u64* b, u64* out, int rows,
