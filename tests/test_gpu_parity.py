@@ -263,6 +263,33 @@ def test_fused_comp_on_a_five_prime_chain_vs_oracle(pkg, oracle):
     assert ans.payload_slots(be, keys) == O.expected_slots(dense, s, p)
 
 
+def test_comp_mixed_levels_reversed_vs_oracle(pkg, oracle):
+    """cd at level 4 and cv at level 3 (the reverse of answer()'s skew): the
+    device pack_pair rotates at level 3 on the even blocks instead."""
+    P, O = pkg, oracle
+    n, p, N, s, seed = N8K, 65537, 16384, 16, 23
+    he = P.HeParams(n, p, 4)
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed)
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    dense = O.plant_sparse(random.Random(seed), N, s, p)
+    cts = P.encrypt_vector(dense, params, be, keys)
+    hint = [be._at_level(c, 3) for c in P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)]
+    before = be.counters.snapshot()
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    delta = be.counters.delta(before).as_dict()
+    obe = O.OracleBgv(n, p, 4, seed=seed)
+    okeys = obe.keygen(*O.plan_rotation_amounts(s, n))
+    octs = O.encrypt_vector(dense, N, obe, okeys)
+    ohint = [obe.at_level(c, 3) for c in O.encrypt_vector([1 if x else 0 for x in dense], N, obe, okeys)]
+    obe.counters = O.OCounters()
+    out = O.comp(octs, N, s, obe, okeys, ohint)
+    assert np.array_equal(ans.cts[0].payload.res, out.c)
+    assert ans.cts[0].payload.noise_bits == out.noise_bits
+    assert delta == vars(obe.counters)
+    assert ans.payload_slots(be, keys) == O.expected_slots(dense, s, p)
+
+
 def test_comp_below_level_3_raises_like_reference(c1, pkg):
     """mask + comp on the 4-prime chain: pack_pair lands at level 1 and the
     reference raises LevelExhausted at the output mask (bgv.py:721-722)."""
