@@ -881,7 +881,7 @@ struct Plan {
     u64* ans_pt = nullptr;  // hc_answer_db: mask plaintexts [C][ans_level+1][n]
     uint32_t* ans_db = nullptr;  // hc_answer_db: the database mod p
     int ans_level = -1;
-    u64 *mix_cd = nullptr, *mix_cv = nullptr, *mix_pt = nullptr, *mix_buf = nullptr;
+    u64 *mix_cd = nullptr, *mix_cv = nullptr, *mix_pt = nullptr, *mix_buf = nullptr, *mix_mcorr = nullptr;
     uint16_t* mix_dig = nullptr;
     std::unique_ptr<Schedule> full, fin, full_u, full_mix;
     std::map<std::pair<long long, long long>, std::unique_ptr<Schedule>> partials;
@@ -1778,7 +1778,7 @@ static int gen_plain(hc_ctx* h, const std::vector<PJob>& pj, const PlanShape& sh
 // when it lands at level 3 (add's _at_level, bgv.py:610-614, 656-658:
 // mul_plain by the constant 1), then u = P + R.  Batched over blocks: one
 // launch per stage.
-static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
+static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S, int with_mask) {
     const size_t NB = NPOLY;
     const int ld = P.mix_ld, lv = P.mix_lv, D3 = h->digits[3], D2 = P.D2;
     const DevKey* kcol = need_key(h, P.t_col);
@@ -1787,11 +1787,16 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
     const u64* mk3 = P.mask;
     const u64* one3 = P.mix_pt + (size_t)2 * 5 * NB;
     const size_t SLOT = (size_t)2 * 4 * NB;  // one [2][<=4][n] ciphertext
-    // per block: Pm, Rm, Rr, P2, R2, cP, cR, cP2, cR2, coef(half), dntt(D3*4/2 slots)
+    // per block: Pm, Rm, Rr, P2, R2, cP, cR, cP2, cR2, coef, dntt
     const size_t per = (size_t)9 * SLOT + (size_t)4 * NB + (size_t)D3 * 4 * NB;
-    std::vector<XJob> i1, f1, i2, f2, i3, f3;
-    std::vector<CJob> co;
-    std::vector<MJob> ma3, ma2;
+    // two independent chains (graph lanes): terms derived from cd (lane 0,
+    // after Mask when it is fused) and from cv (lane 1); each runs
+    // mul_plain -> rot_col (its R terms) -> modulus switch (terms at level 3)
+    struct Lane {
+        std::vector<XJob> i1, f1, i2, f2, i3, f3;
+        std::vector<CJob> co;
+        std::vector<MJob> ma3, ma2;
+    } ln[2];
     std::vector<AddJob> adds;
     for (long long t = 0; t < P.B; t++) {
         const long long src = t / 2;
@@ -1802,6 +1807,8 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
         const u64* ctP = par == 0 ? cvp : cdp;
         const u64* ctR = par == 0 ? cdp : cvp;
         const int lP = par == 0 ? lv : ld, lR = par == 0 ? ld : lv;
+        Lane& LP = ln[par == 0 ? 1 : 0];  // the lane of the P term's source
+        Lane& LR = ln[par == 0 ? 0 : 1];
         auto mask = [&](int l) { return l == 4 ? mk4 + (size_t)par * 5 * NB : mk3 + (size_t)par * 4 * NB; };
         u64* b = P.mix_buf + (size_t)t * per;
         u64 *Pm = b, *Rm = b + SLOT, *Rr = b + 2 * SLOT, *P2 = b + 3 * SLOT, *R2 = b + 4 * SLOT;
@@ -1809,39 +1816,70 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S) {
         u64* coef = b + 9 * SLOT;
         u64* dntt = coef + (size_t)4 * NB;
         uint16_t* dig = P.mix_dig + (size_t)t * D3 * NB;
-        jobs_mul_plain(i1, f1, lP, ctP, mask(lP), cP, Pm);  // level lP - 1
-        jobs_mul_plain(i1, f1, lR, ctR, mask(lR), cR, Rm);  // level lR - 1
+        jobs_mul_plain(LP.i1, LP.f1, lP, ctP, mask(lP), cP, Pm);  // level lP - 1
+        jobs_mul_plain(LR.i1, LR.f1, lR, ctR, mask(lR), cR, Rm);  // level lR - 1
         const int lr = lR - 1;  // rotation level
-        jobs_rotate(i2, co, f2, lr == 3 ? ma3 : ma2, lr, lr == 3 ? D3 : D2, kcol, Rm, coef, dig, dntt, Rr);
+        jobs_rotate(LR.i2, LR.co, LR.f2, lr == 3 ? LR.ma3 : LR.ma2, lr, lr == 3 ? D3 : D2, kcol, Rm, coef, dig, dntt, Rr);
         const u64* pf = Pm;
         const u64* rf = Rr;
         if (lP - 1 == 3) {
-            jobs_mul_plain(i3, f3, 3, Pm, one3, cP2, P2);
+            jobs_mul_plain(LP.i3, LP.f3, 3, Pm, one3, cP2, P2);
             pf = P2;
         }
         if (lr == 3) {
-            jobs_mul_plain(i3, f3, 3, Rr, one3, cR2, R2);
+            jobs_mul_plain(LR.i3, LR.f3, 3, Rr, one3, cR2, R2);
             rf = R2;
         }
         adds.push_back({pf, rf, P.uin + (size_t)t * 2 * 3 * NB});
     }
-    int rc = add_xf(S, i1); if (rc) return rc;
-    rc = add_xf(S, f1); if (rc) return rc;
-    rc = add_xf(S, i2); if (rc) return rc;
-    rc = add_co(S, co); if (rc) return rc;
-    rc = add_xf(S, f2); if (rc) return rc;
-    rc = add_ma(S, ma3, 4); if (rc) return rc;
-    rc = add_ma(S, ma2, 3); if (rc) return rc;
-    rc = add_xf(S, i3); if (rc) return rc;
-    rc = add_xf(S, f3); if (rc) return rc;
+    static int lanes_on = -1, cl_lanes = -1;  // HC_MIX_LANES=0: one chain; HC_MIX_CL=0: clusters in lane 0 only
+    if (lanes_on < 0) {
+        const char* e = getenv("HC_MIX_LANES");
+        lanes_on = (e && e[0] == '0') ? 0 : 1;
+        e = getenv("HC_MIX_CL");
+        cl_lanes = (e && e[0] == '0') ? 0 : 1;
+    }
+    int rc = HC_OK;
+    if (lanes_on) S.par_begin();
+    for (int l = 0; l < 2; l++) {
+        if (lanes_on) {
+            S.cur_lane = l;
+            S.cl_in_lane = l == 0 || cl_lanes;
+        }
+        Lane& L = ln[l];
+        if (l == 0 && with_mask) {
+            // pdq.mask (pdq.py:238-245): cd_c = mul_plain(cv_c, DB block c) at level lv
+            std::vector<XJob> inv, fwd;
+            for (long long c = 0; c < P.C; c++)
+                jobs_mul_plain(inv, fwd, lv, P.mix_cv + (size_t)c * 2 * (lv + 1) * NB, P.ans_pt + (size_t)c * (lv + 1) * NB,
+                               P.mix_mcorr + (size_t)c * 2 * lv * NB, P.mix_cd + (size_t)c * 2 * lv * NB);
+            rc = add_xf(S, inv); if (rc) return rc;
+            rc = add_xf(S, fwd); if (rc) return rc;
+        }
+        if (!lanes_on && l == 1) break;
+        auto both = [&](auto Lane::*m) {  // one chain: both lanes' jobs in one launch
+            auto v = L.*m;
+            if (!lanes_on) v.insert(v.end(), (ln[1].*m).begin(), (ln[1].*m).end());
+            return v;
+        };
+        rc = add_xf(S, both(&Lane::i1)); if (rc) return rc;
+        rc = add_xf(S, both(&Lane::f1)); if (rc) return rc;
+        rc = add_xf(S, both(&Lane::i2)); if (rc) return rc;
+        rc = add_co(S, both(&Lane::co)); if (rc) return rc;
+        rc = add_xf(S, both(&Lane::f2)); if (rc) return rc;
+        rc = add_ma(S, both(&Lane::ma3), 4); if (rc) return rc;
+        rc = add_ma(S, both(&Lane::ma2), 3); if (rc) return rc;
+        rc = add_xf(S, both(&Lane::i3)); if (rc) return rc;
+        rc = add_xf(S, both(&Lane::f3)); if (rc) return rc;
+    }
+    if (lanes_on) {
+        S.cur_lane = -1;
+        S.cl_in_lane = false;
+        S.par_end();
+    }
     return add_add(S, adds, 6, 3);  // u = P + R, all blocks in one launch
 }
 
-// Comp with inputs at different levels (answer(): cd = mask(cv) one level
-// below cv): cd = uint64[C][2][ld+1][n], cv =
-// uint64[C][2][lv+1][n], min(ld, lv) = 3, max <= max_level.  pack_pair runs
-// on the device (build_mixed_pack), then the BSGS graph of hc_comp_packed;
-// one graph launch.  out = uint64[2][1][n].  Synchronous.
 static int ensure_mixed(hc_ctx* h, Plan& P, int ld, int lv, int with_mask) {
     const size_t NB = NPOLY;
     if (P.mix_ld != ld || P.mix_lv != lv || P.mix_mask != with_mask) {
@@ -1859,6 +1897,7 @@ static int ensure_mixed(hc_ctx* h, Plan& P, int ld, int lv, int with_mask) {
     if (!rc && !P.mix_cv) rc = palloc(P, &P.mix_cv, (size_t)P.C * 2 * 5 * NB);
     if (!rc && !P.mix_buf) rc = palloc(P, &P.mix_buf, (size_t)P.B * per);
     if (!rc && !P.mix_dig) rc = palloc(P, &P.mix_dig, (size_t)P.B * D3 * NB);
+    if (!rc && !P.mix_mcorr) rc = palloc(P, &P.mix_mcorr, (size_t)P.C * 2 * 4 * NB);  // Mask's switch scratch
     if (!rc && !P.mix_pt) {
         rc = palloc(P, &P.mix_pt, (size_t)(2 * 5 + 4) * NB);
         if (!rc) {
@@ -1875,19 +1914,7 @@ static int ensure_mixed(hc_ctx* h, Plan& P, int ld, int lv, int with_mask) {
     }
     if (rc) return rc;
     std::unique_ptr<Schedule> S(new Schedule());
-    if (with_mask) {
-        // pdq.mask (pdq.py:238-245): cd_c = mul_plain(cv_c, DB block c) at level lv
-        std::vector<XJob> inv, fwd;
-        u64* corr = P.mix_buf;  // scratch before the pack uses it
-        if ((size_t)P.C * 2 * lv * NB > (size_t)P.B * per) return fail(HC_ERR_STATE, "mask scratch too small");
-        for (long long c = 0; c < P.C; c++)
-            jobs_mul_plain(inv, fwd, lv, P.mix_cv + (size_t)c * 2 * (lv + 1) * NB, P.ans_pt + (size_t)c * (lv + 1) * NB,
-                           corr + (size_t)c * 2 * lv * NB, P.mix_cd + (size_t)c * 2 * lv * NB);
-        rc = add_xf(*S, inv);
-        if (!rc) rc = add_xf(*S, fwd);
-        if (rc) return rc;
-    }
-    rc = build_mixed_pack(h, P, *S);
+    rc = build_mixed_pack(h, P, *S, with_mask);
     if (!rc) rc = build_partial(h, P, 0, P.B, *S, true);
     if (!rc) rc = build_finish(h, P, *S);
     if (!rc) rc = capture(h, *S);
