@@ -52,21 +52,27 @@ def metric_name(N: int, s: int) -> str:
     return f"Comp encrypted entries/sec (N={n}, s={s})"
 
 
-def parse():
+def make_parser() -> argparse.ArgumentParser:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--N", type=int, default=N_DEFAULT)
-    ap.add_argument("--s", type=int, default=S_DEFAULT)
+    # --sparsity: same option under a name torchrun's own parser cannot
+    # prefix-match (it reads "--s" as --standalone / --start-method / ...)
+    ap.add_argument("--s", "--sparsity", dest="s", type=int, default=S_DEFAULT)
     ap.add_argument("--p", type=int, default=0, help="plaintext prime (default: 65537, or per SURVEY F4 for N >= p)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-flush", type=int, default=1, help="flush L2 inside the streamed e2e loop (counted)")
     ap.add_argument("--shard", default="auto", choices=["auto", "on", "off"],
                     help="block-sharded Comp over the ranks (SURVEY 8(e)); auto = on for N >= 2^20 with >1 rank")
-    return ap.parse_args()
+    return ap
+
+
+def parse(argv=None):
+    return make_parser().parse_args(argv)
 
 
 def pick_p(N: int, p: int) -> int:
@@ -436,6 +442,8 @@ def main():
         # out inside the timed region); the line reports the faster schedule
         e2e_ms = min(e2e_serial_ms, e2e_stream_ms)
     info = be.plan_info()  # kernel launches per Comp (graph built by now)
+    if int(info["kernel_launches"]) <= 0:
+        raise RuntimeError(f"no captured Comp graph to count launches from: {info}")
 
     if dist:
         tt = torch.tensor([t_ms, e2e_ms, e2e_serial_ms, e2e_stream_ms or 0.0], dtype=torch.float64, device="cuda")

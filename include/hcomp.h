@@ -76,7 +76,9 @@ int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks);
  * db_mod_p = uint64[N], the cleartext database reduced mod p (int(v) % p).
  * Run it with hc_comp(h, cv, cv, ...): the index vector is both inputs. */
 int hc_plan_masked(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db_mod_p);
-/* schedule facts: [B, C, baby, giant, F, s_pad, live_diagonals, kernel_launches] */
+/* schedule facts: [B, C, baby, giant, F, s_pad, live_diagonals, kernel_launches];
+ * kernel_launches counts the one-graph Comp, or in sharded mode the captured
+ * hc_comp_partial graphs plus the hc_comp_finish graph; -1 before a capture */
 int hc_plan_info(const hc_ctx* h, int64_t* info8);
 
 /* Replaces compress.comp(cd, ..., index_hint=cv) (compress.py:488-514),

@@ -1113,7 +1113,17 @@ extern "C" int hc_plan_info(const hc_ctx* h, int64_t* info) {
     info[4] = P.F;
     info[5] = P.s_pad;
     info[6] = P.live_count;
-    info[7] = P.full ? P.full->launches : -1;
+    // kernel launches per Comp: the one-graph path, else (sharded mode,
+    // hc_comp_partial + hc_comp_finish) the partial graphs this rank has
+    // captured plus the root's finish graph; -1 before any capture
+    long long launches = -1;
+    if (P.full) {
+        launches = P.full->launches;
+    } else if (!P.partials.empty() || P.fin) {
+        launches = P.fin ? P.fin->launches : 0;
+        for (const auto& kv : P.partials) launches += kv.second->launches;
+    }
+    info[7] = launches;
     return HC_OK;
 }
 

@@ -230,3 +230,31 @@ def test_host_rng_reproduces_python_random(seed):
     vals = [py.randrange(Q) for _ in range(300)]
     assert np.array_equal(got, np.array([[v % q for v in vals] for q in primes], dtype=np.uint64))
     assert hr.getrandbits(128) == py.getrandbits(128)  # still in lockstep
+
+
+def test_bench_options_pass_through_torchrun():
+    """Every bench.py option has a spelling torchrun hands to the script.
+
+    argparse prefix-matches, so torchrun's parser takes an option such as
+    "--s" for its own (--standalone / --start-method / ...) and exits before
+    bench.py runs; the N>1 driver launch goes through that parser."""
+    import bench
+    from torch.distributed.run import get_args_parser
+
+    tr = get_args_parser()
+    for act in bench.make_parser()._actions:
+        longs = [o for o in act.option_strings if o.startswith("--") and o != "--help"]
+        if not longs:
+            continue
+        ok = []
+        for o in longs:
+            argv = [o] if act.nargs == 0 else [o, act.choices[0] if act.choices else "1"]
+            try:
+                got = tr.parse_args(["--nproc-per-node", "2", "bench.py", *argv]).training_script_args
+            except SystemExit:
+                continue
+            if got == argv:
+                ok.append(o)
+        assert ok, f"no spelling of {longs} survives torchrun's parser"
+    a = bench.parse(["--gpus", "2", "--steps", "3", "--warmup", "3", "--sparsity", "32", "--N", "1048576"])
+    assert (a.gpus, a.steps, a.warmup, a.s, a.N) == (2, 3, 3, 32, 1 << 20)
