@@ -165,13 +165,23 @@ def plant(N, s, p, seed):
     return dense
 
 
+def host_threads(O) -> int:
+    """Give the CPU oracle every core this process may run on.
+
+    torchrun exports OMP_NUM_THREADS=1 to each rank, which would leave the
+    rank-0 CPU leg single-threaded under the driver's N>1 launch."""
+    n = len(os.sched_getaffinity(0))
+    O.lib().orc_set_num_threads(n)
+    return O.lib().orc_num_threads()
+
+
 def run_reference(args, p, rank):
     """CPU arm: the oracle port of the reference Comp with every host thread."""
     if rank != 0:
         return None
     from oracle import bgv_oracle as O
 
-    O.lib()
+    host_threads(O)
     threads = O.lib().orc_num_threads()
     be = O.OracleBgv(RING, p, 3, seed=0, check_noise=False)
     keys = be.keygen(*O.plan_rotation_amounts(args.s, RING))
@@ -218,7 +228,7 @@ def cpu_baseline_sample(args, p, budget_s):
     """Oracle port timed on this host on full Comps until ~budget_s of work."""
     from oracle import bgv_oracle as O
 
-    O.lib()
+    host_threads(O)
     be = O.OracleBgv(RING, p, 3, seed=0, check_noise=False)
     keys = be.keygen(*O.plan_rotation_amounts(args.s, RING))
     dense = plant(args.N, args.s, p, 0)

@@ -58,6 +58,8 @@ def lib():
         L.orc_mac_digits.argtypes = [P, P, P, P, P, I, I, I, P]
         L.orc_compose.argtypes = [P, P, I, I, P, I]
         L.orc_num_threads.restype = I
+        L.orc_set_num_threads.argtypes = [I]
+        L.orc_set_num_threads.restype = None
         _LIB = L
     return _LIB
 

@@ -331,6 +331,17 @@ void orc_compose(const u64 *x, u64 *out, int P, int n, const u64 *q, int W) {
     }
 }
 
+/* thread count for the calling thread's later parallel regions (torchrun
+ * exports OMP_NUM_THREADS=1 to every rank; the CPU baseline wants them all) */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);
