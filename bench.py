@@ -66,6 +66,8 @@ def make_parser() -> argparse.ArgumentParser:
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-flush", type=int, default=1, help="flush L2 inside the streamed e2e loop (counted)")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the bit-exact check of the GPU answer against the CPU oracle (large N)")
     ap.add_argument("--shard", default="auto", choices=["auto", "on", "off"],
                     help="block-sharded Comp over the ranks (SURVEY 8(e)); auto = on for N >= 2^20 with >1 rank")
     return ap
@@ -237,18 +239,34 @@ def cpu_baseline_sample(args, p, budget_s):
     n, t_total = 0, 0.0
     while t_total < budget_s or n == 0:
         t0 = time.perf_counter()
-        O.comp(cts, args.N, args.s, be, keys, hint)
+        out = O.comp(cts, args.N, args.s, be, keys, hint)
         t_total += time.perf_counter() - t0
         n += 1
         if n >= 50:
             break
-    return {
+    return out.c, {
         "value": args.N * n / t_total,
         "unit": "entries/s",
         "cores": O.lib().orc_num_threads(),
         "kind": "port",
         "sample": f"{n} full Comps (N={args.N}, s={args.s}), {t_total:.1f} s, C/OpenMP oracle port of the reference Comp",
     }
+
+
+def oracle_answer(args, p, seed):
+    """The CPU oracle's Comp output (level-0 residues [2][1][n]) for the same
+    seeded keys, payload and encryption as the GPU arm: the bench line's
+    bit-exact parity reference (reference bench.py:96-103 asserts its own
+    round trip the same way)."""
+    from oracle import bgv_oracle as O
+
+    host_threads(O)
+    be = O.OracleBgv(RING, p, 3, seed=seed, check_noise=False)
+    keys = be.keygen(*O.plan_rotation_amounts(args.s, RING))
+    dense = plant(args.N, args.s, p, seed)
+    cts = O.encrypt_vector(dense, args.N, be, keys)
+    hint = O.encrypt_vector([1 if x else 0 for x in dense], args.N, be, keys)
+    return O.comp(cts, args.N, args.s, be, keys, hint).c
 
 
 def main():
@@ -339,7 +357,8 @@ def main():
 
     def output():
         torch.cuda.synchronize()
-        return dc.output() if rank == 0 else None
+        # sharded: only the root holds the answer; replicas: every rank has its own
+        return dc.output() if (rank == 0 or not shard) else None
 
     # correctness gate: the timed Comp must decrypt to the payload's power sums
     with torch.cuda.stream(stream):
@@ -349,8 +368,11 @@ def main():
         ct = P.Ciphertext(be.backend_id, keys.key_id, 0, P.RnsPayload(out, 0.0, (be.q[0],)))
         m = be.decrypt(ct, keys)
         w = [int(x) for x in m.rows[0][: args.s]]
+        e = [int(x) for x in m.rows[1][: args.s]]
         want_w = [sum(pow(i + 1, j + 1, p) for i, v in enumerate(dense) if v) % p for j in range(args.s)]
-        assert w == want_w, "Comp output does not decrypt to the expected power sums"
+        want_e = [sum(v * pow(i + 1, j + 1, p) for i, v in enumerate(dense) if v) % p for j in range(args.s)]
+        assert w == want_w, "Comp output does not decrypt to the expected power sums w"
+        assert e == want_e, "Comp output does not decrypt to the expected weighted sums e"
 
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
@@ -404,9 +426,25 @@ def main():
         # stream) while step i computes, step i's result comes back (D2H
         # stream) while step i+1 computes; every step still copies its own
         # inputs in and its result out inside the timed region, and the L2
-        # flush stays in the loop (its time is counted) ----
+        # flush stays in the loop (its time is counted).  Steps alternate
+        # between two DIFFERENT input sets (a second encryption of the same
+        # payload), and each result is copied on the compute stream into one
+        # of two device staging slots before its D2H, so step i+1's Comp
+        # never overwrites an answer still being read back: both final
+        # answers are checked against their own device-resident results ----
+        cts2 = P.encrypt_vector(dense, params, be, keys)
+        hint2 = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+        cd2 = np.ascontiguousarray(np.stack([c.payload.res for c in cts2]))
+        cv2 = np.ascontiguousarray(np.stack([c.payload.res for c in hint2]))
+        dc.set_inputs(cd2, cv2)
+        dc.launch(sh)
+        out2 = output()
+        dc.set_inputs(cd, cv)
+        src_h = [(cd_h, cv_h), (torch.from_numpy(cd2).pin_memory(), torch.from_numpy(cv2).pin_memory())]
+        want = [out, out2]
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
         stage = [torch.empty((2,) + cd.shape, dtype=cd_h.dtype, device="cuda") for _ in range(2)]
+        outs_dev = [torch.empty((2, 1, RING), dtype=torch.int64, device="cuda") for _ in range(2)]
         outs = [torch.empty((2, 1, RING), dtype=torch.int64).pin_memory() for _ in range(2)]
         ev = lambda: torch.cuda.Event()
         h2d_done = [ev() for _ in range(args.steps)]
@@ -420,8 +458,8 @@ def main():
             with torch.cuda.stream(h2d_s):
                 if i >= 2:
                     h2d_s.wait_event(set_done[i - 2])  # staging buffer free again
-                stage[i % 2][0].copy_(cd_h, non_blocking=True)
-                stage[i % 2][1].copy_(cv_h, non_blocking=True)
+                stage[i % 2][0].copy_(src_h[i % 2][0], non_blocking=True)
+                stage[i % 2][1].copy_(src_h[i % 2][1], non_blocking=True)
                 h2d_done[i].record(h2d_s)
 
         with torch.cuda.stream(stream):
@@ -438,16 +476,20 @@ def main():
                 _lib.check(L.hc_comp_set_inputs_device(h, st_i[0].data_ptr(), st_i[1].data_ptr(), cd.shape[0], sh))
                 set_done[i].record(stream)
                 dc.launch(sh)
+                if i >= 2:
+                    stream.wait_event(d2h_done[i - 2])  # staging slot read back
+                _lib.check(L.hc_comp_get_output_async(h, outs_dev[i % 2].data_ptr(), sh))  # device to device
                 comp_done[i].record(stream)
                 d2h_s.wait_event(comp_done[i])
                 with torch.cuda.stream(d2h_s):
-                    _lib.check(L.hc_comp_get_output_async(h, outs[i % 2].data_ptr(), d2h_s.cuda_stream))
+                    outs[i % 2].copy_(outs_dev[i % 2], non_blocking=True)
                     d2h_done[i].record(d2h_s)
             stream.wait_event(d2h_done[-1])
             t1.record(stream)
         torch.cuda.synchronize()
         e2e_stream_ms = t0.elapsed_time(t1)
-        assert np.array_equal(outs[(args.steps - 1) % 2].numpy().view(np.uint64), out), "streamed e2e output differs"
+        for i in range(max(0, args.steps - 2), args.steps):
+            assert np.array_equal(outs[i % 2].numpy().view(np.uint64), want[i % 2]), "streamed e2e output differs"
         # both are end to end (every step copies its inputs in and its answer
         # out inside the timed region); the line reports the faster schedule
         e2e_ms = min(e2e_serial_ms, e2e_stream_ms)
@@ -558,8 +600,26 @@ def main():
         "clocks": clk,
         "plan": info,
     }
+    cpu_out = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_sample(args, p, args.cpu_seconds)
+        cpu_out, line["cpu_baseline"] = cpu_baseline_sample(args, p, args.cpu_seconds)
+    if rank == 0 and not args.no_parity:
+        # bit-exact gate: the answer every timed step produced (device-resident,
+        # e2e and streamed runs were checked equal to it above) against the CPU
+        # oracle's Comp on the same seeded keys, payload and encryption
+        t_or = time.perf_counter()
+        ref = cpu_out if cpu_out is not None else oracle_answer(args, p, seed)
+        ok = bool(np.array_equal(np.asarray(ref, dtype=np.uint64), out))
+        line["parity"] = {
+            "status": "bit-exact" if ok else "MISMATCH",
+            "against": "CPU oracle port of the reference Comp (oracle/, pinned to reference goldens), same seed",
+            "compared": "all 2 x 8192 residues of the level-0 answer ciphertext (+ decrypted w and e vs the planted payload)",
+            "query_seed": seed,
+            "oracle_s": round(time.perf_counter() - t_or, 2),
+        }
+        assert ok, "GPU Comp answer differs from the CPU oracle"
+    elif rank == 0:
+        line["parity"] = {"status": "decrypt-checked only (--no-parity)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -46,6 +46,13 @@ CASES = {
     "c2_N16384_s16": (8192, 65537, 16384, 16, 0, False),
     "odd_N10000_s5": (8192, 65537, 10000, 5, 3, True),
     "c2_N16384_s32": (8192, 65537, 16384, 32, 0, True),
+    # round 2: the rest of config 2's sparsity sweep (baby = 4 / 8 / 16 in the
+    # latency schedule) and config 3's N = 2^15, 2^16 points
+    "c2_N16384_s8": (8192, 65537, 16384, 8, 0, False),
+    "c2_N16384_s64": (8192, 65537, 16384, 64, 0, True),
+    "c2_N16384_s128": (8192, 65537, 16384, 128, 0, True),
+    "c3_N32768_s16": (8192, 65537, 32768, 16, 0, True),
+    "c3_N65536_s16": (8192, 65537, 65536, 16, 0, True),
     # comp_masked (compress.py:521-530): cleartext DB on every position,
     # encrypted 0/1 index vector on the support (masked_payload below)
     "masked_small_n64_N200_s5": (64, 257, 200, 5, 13, True),

@@ -197,6 +197,16 @@ def write_envelope(backend_id: int, payload: bytes) -> bytes:
     return MAGIC + struct.pack("<BH", backend_id, FORMAT_VERSION) + payload
 
 
+def read_envelope(data: bytes) -> tuple[int, int, bytes]:
+    """heiface.py:273-279."""
+    if len(data) < 7 or data[:4] != MAGIC:
+        raise ValueError("not an HCV1 blob")
+    backend_id, version = struct.unpack("<BH", data[4:7])
+    if version != FORMAT_VERSION:
+        raise ValueError(f"unsupported format version {version}")
+    return backend_id, version, data[7:]
+
+
 # ---------------------------------------------------------------------------
 # tables shared with libhcomp (bgv.py:115-117, 170-174, 258-261, 367-377)
 # ---------------------------------------------------------------------------
@@ -296,6 +306,9 @@ class B200BgvBackend:
         device: int = 0,
         noise_guard: bool = True,
     ):
+        from .refcompat import he_params
+
+        params = he_params(params)  # an hcpdq HeParams passes through
         if params.n != 8192:
             raise ValueError("the B200 backend supports n = 8192 only")
         if not (1 <= params.max_level <= 4):
@@ -319,6 +332,8 @@ class B200BgvBackend:
         self._slot_index = slot_index(n)
         self._loaded_keys = None
         self._planned = None
+        self._plan_gen = 0  # bumped whenever the device plan is rebuilt (hc_plan*)
+        self._answer_db_tag = None
 
     # -- GPU context ------------------------------------------------------------
 
@@ -677,6 +692,31 @@ class B200BgvBackend:
                     parts.append(int(x).to_bytes(8 * W, "little"))
         return write_envelope(self.backend_id, b"".join(parts))
 
+    def deserialize_ciphertext(self, data: bytes) -> Ciphertext:
+        """bgv.py:792-814: coefficient-domain integers -> RNS residues -> NTT
+        on the GPU (the inverse of serialize_ciphertext)."""
+        backend_id, _, payload = read_envelope(data)
+        if backend_id != self.backend_id:
+            raise BackendMismatch("blob was produced by a different backend")
+        kind, level, n, p, max_level = struct.unpack("<BBIQB", payload[:15])
+        if kind != _OBJ_KIND_CIPHERTEXT:
+            raise ValueError("blob is not a ciphertext")
+        if (n, p, max_level) != (self.params.n, self.params.p, self.params.max_level):
+            raise BackendMismatch("ciphertext parameters do not match backend")
+        key_id = bytes(payload[15:31])
+        (noise_bits,) = struct.unpack("<d", payload[31:39])
+        W = self._words(level)
+        body = np.frombuffer(payload, dtype="<u8", count=2 * n * W, offset=39).reshape(2, n, W)
+        res = np.empty((2, level + 1, n), dtype=np.uint64)
+        for k, q in enumerate(self.q[: level + 1]):
+            # sum_i w_i 2^(64 i) mod q, limb by limb (every limb < 2^64)
+            acc = np.zeros((2, n), dtype=object)
+            for i in range(W):
+                acc = acc + body[:, :, i].astype(object) * (pow(2, 64 * i, q))
+            res[:, k] = (acc % q).astype(np.uint64)
+        res = self.ntt(res, level)
+        return Ciphertext(self.backend_id, key_id, level, self._payload(res, noise_bits, level))
+
     # -- the fused Comp (compress.py:488-514) ------------------------------------------
 
     def plan(self, N: int, s: int, keys: KeySet, chunk_blocks: int = 0, db: np.ndarray | None = None) -> None:
@@ -690,12 +730,16 @@ class B200BgvBackend:
                 db = np.ascontiguousarray(db, dtype=np.uint64)
                 _lib.check(_lib.lib(self.params.max_level).hc_plan_masked(self._ctx(), N, s, chunk_blocks, _lib.ptr(db)))
             self._planned = tag
+            # a new device Plan drops the previous plan's answer() mask
+            # plaintexts (hc_answer_db), so their cache tag is stale too
+            self._plan_gen += 1
+            self._answer_db_tag = None
 
     def answer_db(self, db_mod_p: np.ndarray, level: int) -> None:
         """Mask plaintexts of the cleartext database for the current plan (hc_answer_db)."""
         db = np.ascontiguousarray(db_mod_p, dtype=np.uint64)
-        tag = (self._planned, level, hashlib.sha256(db.tobytes()).digest())
-        if getattr(self, "_answer_db_tag", None) != tag:
+        tag = (self._plan_gen, level, hashlib.sha256(db.tobytes()).digest())
+        if self._answer_db_tag != tag:
             _lib.check(_lib.lib(self.params.max_level).hc_answer_db(self._ctx(), level, _lib.ptr(db)))
             self._answer_db_tag = tag
 

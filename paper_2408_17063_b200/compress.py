@@ -18,7 +18,7 @@ from typing import Sequence
 
 import numpy as np
 
-from . import _lib
+from . import _lib, refcompat
 from .backend import B200BgvBackend, Ciphertext, KeySet, RnsPayload, SlotMatrix
 from .params import (
     BackendMismatch,
@@ -55,9 +55,25 @@ class CompressedAnswer:
         blobs = [backend.serialize_ciphertext(c) for c in self.cts]
         return head + b"".join(struct.pack("<I", len(b)) + b for b in blobs)
 
+    @staticmethod
+    def deserialize(data: bytes, backend) -> "CompressedAnswer":
+        """compress.py:419-430 (the client side of the wire format)."""
+        version, s, packed, _, _, _, _, count = struct.unpack("<HIBBBIIB", data[:18])
+        if version != LAYOUT_VERSION:
+            raise ValueError(f"unsupported payload layout version {version}")
+        off = 18
+        cts = []
+        for _ in range(count):
+            (ln,) = struct.unpack("<I", data[off : off + 4])
+            off += 4
+            cts.append(backend.deserialize_ciphertext(data[off : off + ln]))
+            off += ln
+        return CompressedAnswer(tuple(cts), s, bool(packed))
+
 
 def encode_vector(values: Sequence[int], params: CompressionParams) -> list[SlotMatrix]:
     """compress.py:318-329."""
+    params = refcompat.compression_params(params)
     he = params.he
     vals = list(values)
     if len(vals) != params.N:
@@ -209,11 +225,16 @@ class MaskedMatrix:
     database reduced mod p; the device generates the scaled diagonals."""
 
     def __init__(self, params: CompressionParams, db_values: Sequence[int]):
+        params = refcompat.compression_params(params)
         if len(db_values) != params.N:
             raise ValueError("database length must equal N")
         p = params.he.p
         self.params = params
         self.db_mod_p = np.ascontiguousarray([int(v) % p for v in db_values], dtype=np.uint64)
+
+    @classmethod
+    def from_db_mod_p(cls, params: CompressionParams, db_mod_p: np.ndarray) -> "MaskedMatrix":
+        return cls(params, [int(v) for v in db_mod_p])
 
 
 def precompute_masked_matrix(db_values: Sequence[int], params: CompressionParams) -> MaskedMatrix:
@@ -286,8 +307,12 @@ def comp(
             "the B200 path implements comp with an index hint or a masked matrix in the packed "
             "layout; power_fermat / pack=False are not built"
         )
+    params = refcompat.compression_params(params)  # hcpdq CompressionParams pass through
     if masked is not None and not isinstance(masked, MaskedMatrix):
-        raise TypeError("masked must come from precompute_masked_matrix")
+        if not hasattr(masked, "block"):
+            raise TypeError("masked must come from precompute_masked_matrix")
+        # the reference's VandermondeTable(params, db_values) (compress.py:154-157)
+        masked = MaskedMatrix.from_db_mod_p(params, refcompat.db_mod_p_from_table(masked, params))
     if backend.params != params.he:
         raise BackendMismatch("compression parameters do not match the backend")
     cd = list(cd)
@@ -351,6 +376,7 @@ def answer_from_match(
     """pdq.answer (pdq.py:248-256) after Match: cd = mask(cv, db), then
     comp(cd, index_hint=cv) with cd one level below cv.  Match (the Fermat
     power, depth log2 p) is outside the B200 hot path."""
+    params = refcompat.compression_params(params)
     values = db.values if hasattr(db, "values") else db
     if len(values) != params.N:
         raise ValueError(f"database has {len(values)} records, params expect {params.N}")

@@ -330,6 +330,8 @@ extern "C" int hc_ctx_digits(const hc_ctx* h, int* digits) {
 extern "C" int hc_clear_keys(hc_ctx* h) {
     if (!h) return fail(HC_ERR_ARG, "null context");
     cudaSetDevice(h->dev);
+    cudaDeviceSynchronize();
+    h->plan.reset();  // captured graphs hold key pointers: re-plan after a key change
     for (auto& kv : h->keys) release_key(kv.second);
     h->keys.clear();
     return HC_OK;
@@ -341,6 +343,8 @@ extern "C" int hc_load_ksk(hc_ctx* h, uint32_t t, const uint64_t* ksk) {
     CU(cudaSetDevice(h->dev));
     auto it = h->keys.find(t);
     if (it != h->keys.end()) {
+        CU(cudaDeviceSynchronize());
+        h->plan.reset();  // the plan's graphs point at the key being replaced
         release_key(it->second);
         h->keys.erase(it);
     }
@@ -1410,7 +1414,11 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         if (nl > 1) S.par_begin();
         for (int lane = 0; lane < nl; lane++) {
             S.cur_lane = nl > 1 ? lane : -1;
-            lanes_dx = lane_dx && nl > 1;
+            // per-lane diagonal MACs add into PX with atomics and no reduction
+            // in between: only when this chunk is the range's only one, so PX
+            // words stay below cb * q < 4q (< 2^56: the sharded uint64 reduce
+            // of up to 255 partials is exact)
+            lanes_dx = lane_dx && nl > 1 && b1 - b0 <= P.CB;
             for (int tl = lane; tl < cb; tl += nl) {
                 rc = add_xf(S, s7[tl]); if (rc) return rc;
                 rc = add_ma(S, s8[tl], 3); if (rc) return rc;
@@ -1701,7 +1709,9 @@ extern "C" int hc_comp_get_output_async(hc_ctx* h, uint64_t* out, void* stream) 
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     CU(cudaSetDevice(h->dev));
     cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
-    CU(cudaMemcpyAsync(out, h->plan->OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, s));
+    // cudaMemcpyDefault: `out` may be pinned host memory or a device buffer
+    // (a staging slot of a double-buffered serving loop)
+    CU(cudaMemcpyAsync(out, h->plan->OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDefault, s));
     return HC_OK;
 }
 

@@ -52,7 +52,12 @@ def reduce_partials(t, dist, group=None, root: int = 0):
 def comp_sharded(cd, params, backend, keys, index_hint, dist, group=None, root: int = 0):
     """compress.comp (hint path, packed) with the blocks sharded over the ranks
     of `group`.  Every rank holds the full standard-layout inputs; the
-    CompressedAnswer is returned on `root` (None elsewhere)."""
+    CompressedAnswer is returned on `root` (None elsewhere).
+
+    A rank whose block range is empty (world > num_blocks) uploads nothing and
+    contributes a zero partial, so every rank still joins the reduce.  All
+    device work runs on torch's current stream of the backend's device, the
+    stream the reduce is ordered on."""
     import torch
 
     world = dist.get_world_size(group)
@@ -66,20 +71,27 @@ def comp_sharded(cd, params, backend, keys, index_hint, dist, group=None, root: 
     backend.plan(params.N, params.s, keys)
     L = _lib.lib(backend.params.max_level)
     h = backend._ctx()
+    dev = torch.device("cuda", backend.device)
+    stream = torch.cuda.current_stream(dev)
+    sh = ctypes.c_void_p(stream.cuda_stream)
     b0, b1 = shard_blocks(params.num_blocks, world, rank)
     c0, c1 = b0 // 2, (b1 + 1) // 2  # the input ciphertexts this rank's blocks read
-    cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd[c0:c1]]), dtype=np.uint64)
-    cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv[c0:c1]]), dtype=np.uint64)
-    _lib.check(L.hc_comp_set_inputs_range(h, _lib.ptr(cd_arr), _lib.ptr(cv_arr), c0, c1, None))
+    if c1 > c0:
+        cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd[c0:c1]]), dtype=np.uint64)
+        cv_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cv[c0:c1]]), dtype=np.uint64)
+        _lib.check(L.hc_comp_set_inputs_range(h, _lib.ptr(cd_arr), _lib.ptr(cv_arr), c0, c1, sh))
+        stream.synchronize()  # pageable host buffers: the copies have landed
     words = L.hc_partial_words(h)
-    part = torch.zeros(words, dtype=torch.int64, device="cuda")
-    _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(part.data_ptr()), None))
-    torch.cuda.synchronize()
-    reduce_partials(part, dist, group, root)
+    part = torch.zeros(words, dtype=torch.int64, device=dev)
+    _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(part.data_ptr()), sh))
+    with torch.cuda.device(dev):
+        reduce_partials(part, dist, group, root)
     if rank != root:
+        stream.synchronize()
         return None
-    _lib.check(L.hc_comp_finish(h, ctypes.c_void_p(part.data_ptr()), None))
+    _lib.check(L.hc_comp_finish(h, ctypes.c_void_p(part.data_ptr()), sh))
     out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
+    stream.synchronize()
     _lib.check(L.hc_comp_get_output(h, _lib.ptr(out)))
     backend.counters.keyswitches += sim.ks
     backend.counters.pt_mults += sim.pt

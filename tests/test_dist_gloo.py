@@ -51,7 +51,7 @@ def _partial_accs(O, be, keys, u, plan, blocks):
     return acc
 
 
-def _worker(rank, world, port, result_q):
+def _worker(rank, world, port, result_q, N=200):
     import torch
     import torch.distributed as dist
 
@@ -62,7 +62,7 @@ def _worker(rank, world, port, result_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        n, p, N, s = 64, 257, 200, 5  # 7 blocks of 32 slots, odd count
+        n, p, s = 64, 257, 5  # N=200: 7 blocks of 32 slots, odd count; N=64: 2 blocks
         be = O.OracleBgv(n, p, 3, seed=21, check_noise=False)
         keys = be.keygen(*O.plan_rotation_amounts(s, n))
         dense = O.plant_sparse(__import__("random").Random(21), N, s, p)
@@ -81,20 +81,25 @@ def _worker(rank, world, port, result_q):
             folded = total % qv
             full = _partial_accs(O, be, keys, u, plan, range(B))
             result_q.put(bool(np.array_equal(folded, full)) and b1 - b0 >= 1)
+        elif b1 == b0:  # world > blocks: an empty range contributes a zero partial
+            result_q.put(bool(not part.any()))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_partials_reduce_to_full_accumulators():
+@pytest.mark.parametrize("N,world", [(200, 2), (64, 3)])
+def test_sharded_partials_reduce_to_full_accumulators(N, world):
+    """world 2 over 7 blocks, and world 3 over 2 blocks (one rank empty)."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, N)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
         pr.join(timeout=300)
         assert pr.exitcode == 0
-    assert q.get(timeout=5) is True
+    n_results = 1 + sum(1 for r in range(1, world) if shard_blocks(-(-N // 32), world, r)[0] == shard_blocks(-(-N // 32), world, r)[1])
+    assert all(q.get(timeout=5) is True for _ in range(n_results))

@@ -1,0 +1,168 @@
+"""GPU parity at the BASELINE config points the reference goldens do not
+reach (configs 4 and 5), plus serving-path edge cases.  Every Comp here is
+compared residue for residue with the CPU oracle run end to end on the same
+seed (keys, payload and encryption regenerated independently on both sides),
+and decrypted against the planted payload.  Configs 1-3 (every point of the
+sparsity and size sweeps) are pinned to the reference itself through
+tests/golden/ in test_gpu_parity.py.  Run on a B200 with `pytest -m gpu`."""
+
+import random
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+RING = 8192
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA GPU required for -m gpu tests")
+    import paper_2408_17063_b200 as P
+    from paper_2408_17063_b200 import build
+
+    build.build_lib()
+    return P
+
+
+def _gpu_case(P, O, N, s, p, seed):
+    he = P.HeParams(RING, p, 3)
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed, noise_guard=False)
+    keys = be.keygen(*P.plan_rotation_amounts(s, RING))
+    dense = O.plant_sparse(random.Random(seed), N, s, p)
+    cts = P.encrypt_vector(dense, params, be, keys)
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    return be, params, keys, dense, cts, hint
+
+
+def _oracle_answer(O, N, s, p, seed):
+    obe = O.OracleBgv(RING, p, 3, seed=seed, check_noise=False)
+    okeys = obe.keygen(*O.plan_rotation_amounts(s, RING))
+    dense = O.plant_sparse(random.Random(seed), N, s, p)
+    ocd = O.encrypt_vector(dense, N, obe, okeys)
+    ocv = O.encrypt_vector([1 if x else 0 for x in dense], N, obe, okeys)
+    obe.counters = O.OCounters()
+    out = O.comp(ocd, N, s, obe, okeys, ocv)
+    return obe, out
+
+
+def _check_vs_oracle(P, O, N, s, p, seed):
+    be, params, keys, dense, cts, hint = _gpu_case(P, O, N, s, p, seed)
+    before = be.counters.snapshot()
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    delta = be.counters.delta(before).as_dict()
+    obe, out = _oracle_answer(O, N, s, p, seed)
+    assert np.array_equal(ans.cts[0].payload.res, out.c), f"(N={N}, s={s}, seed={seed}) differs from the oracle"
+    assert ans.cts[0].payload.noise_bits == out.noise_bits
+    assert delta == vars(obe.counters)
+    assert O.sha256(ans.serialize(be)) == O.sha256(O.serialize_answer(obe, out, s))
+    assert ans.payload_slots(be, keys) == O.expected_slots(dense, s, p)
+    return be, ans
+
+
+def test_config5_independent_queries_vs_oracle(pkg, oracle):
+    """Config 5 shape: (N=2^16, s=64) queries, each with its own seeded key
+    pair and rotation keys (baby 8 x giant 8, 16 blocks: the wide schedule
+    with k_ksmac_mb grouping), over one GPU; two seeds, both bit-exact."""
+    P, O = pkg, oracle
+    answers = [_check_vs_oracle(P, O, 1 << 16, 64, 65537, seed)[1] for seed in (100, 101)]
+    assert not np.array_equal(answers[0].cts[0].payload.res, answers[1].cts[0].payload.res)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("N,s,p", [(1 << 20, 128, 1097729), (1 << 22, 16, 4423681)])
+def test_config4_large_vs_oracle(pkg, oracle, N, s, p):
+    """Config 4: (2^20, 128) -- 256 blocks, baby 16 in the throughput
+    schedule, 4 chunks of 64 -- and (2^22, 16) -- 1024 blocks, 16 chunks;
+    real keygen and encryption on both sides, bit-exact against the oracle."""
+    _check_vs_oracle(pkg, oracle, N, s, p, 0)
+
+
+def test_answer_db_after_key_change(pkg, oracle):
+    """Serving two clients against one database: answer_from_match with key
+    set A, then key set B (a re-plan with an identical plan tag), then A
+    again -- the device mask plaintexts are regenerated each time the plan is
+    (a stale answer_db tag used to skip hc_answer_db)."""
+    P, O = pkg, oracle
+    g = load_golden("answer_c1_N8192_s8")
+    n, p, N, s, seed = g["n"], g["p"], g["N"], g["s"], g["seed"]
+    he = P.HeParams(n, p, g["max_level"])
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed, noise_guard=not g["noise_guard_disabled"])
+    keys_a = be.keygen(*P.plan_rotation_amounts(s, n))
+    support, db, dense = O.masked_payload(N, s, p, seed)
+    hint_a = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys_a)
+    keys_b = be.keygen(*P.plan_rotation_amounts(s, n))
+    hint_b = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys_b)
+    want = O.expected_slots(dense, s, p)
+    a1 = P.answer_from_match(hint_a, db, params, be, keys_a)
+    assert O.sha256(a1.serialize(be)) == g["answer_sha256"]
+    b1 = P.answer_from_match(hint_b, db, params, be, keys_b)
+    assert b1.payload_slots(be, keys_b) == want
+    a2 = P.answer_from_match(hint_a, db, params, be, keys_a)
+    assert O.sha256(a2.serialize(be)) == g["answer_sha256"]
+    # a different plan in between (other chunking), same keys
+    P.DeviceComp(be, params, keys_a, chunk_blocks=1)
+    a3 = P.answer_from_match(hint_a, db, params, be, keys_a)
+    assert O.sha256(a3.serialize(be)) == g["answer_sha256"]
+
+
+def test_chunked_lane_plans_vs_single_chunk(pkg, oracle):
+    """chunk_blocks 3 and 4 with more blocks than a chunk (N=2^16: 16 blocks):
+    several latency-regime chunks in one range now accumulate through the
+    non-atomic diagonal MAC; the answer equals the default plan's."""
+    P, O = pkg, oracle
+    be, params, keys, dense, cts, hint = _gpu_case(P, O, 1 << 16, 16, 65537, 3)
+    cd = np.stack([c.payload.res for c in cts])
+    cv = np.stack([c.payload.res for c in hint])
+    ref = P.DeviceComp(be, params, keys).run_host(cd, cv)
+    for cb in (3, 4, 5):
+        out = P.DeviceComp(be, params, keys, chunk_blocks=cb).run_host(cd, cv)
+        assert np.array_equal(out, ref), f"chunk_blocks={cb}"
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    assert ans.payload_slots(be, keys) == O.expected_slots(dense, 16, 65537)
+
+
+def test_reference_shaped_objects_and_wire_round_trip(pkg, oracle):
+    """The INTEGRATION.md dispatch path with reference-shaped arguments:
+    parameter objects that only carry the reference's public attributes and a
+    comp_masked table that only offers VandermondeTable.block (compress.py:
+    103-157).  The answer is byte-identical to the reference golden, and
+    CompressedAnswer.deserialize / deserialize_ciphertext (compress.py:419-430,
+    bgv.py:792-814) read it back to the same residues and slots."""
+    import types
+
+    P, O = pkg, oracle
+    g = load_golden("masked_c1_N8192_s8")
+    n, p, N, s, seed = g["n"], g["p"], g["N"], g["s"], g["seed"]
+    he_ref = types.SimpleNamespace(n=n, p=p, max_level=3)
+    cp_ref = types.SimpleNamespace(N=N, s=s, he=he_ref)
+    be = P.make_backend("bgv-b200", he_ref, seed=seed)
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    support, db, dense = O.masked_payload(N, s, p, seed)
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], cp_ref, be, keys)
+
+    class Table:  # what hcpdq.compress.precompute_masked_matrix returns, public API only
+        def block(self, k):
+            return O.vandermonde_block(N, s, p, n // 2, k, db)
+
+    ans = P.comp(hint, cp_ref, be, keys, masked=Table())
+    blob = ans.serialize(be)
+    assert O.sha256(blob) == g["answer_sha256"]
+    back = P.CompressedAnswer.deserialize(blob, be)
+    assert back.s == s and back.packed
+    assert np.array_equal(back.cts[0].payload.res, ans.cts[0].payload.res)
+    assert back.cts[0].payload.noise_bits == ans.cts[0].payload.noise_bits
+    assert back.cts[0].key_id == keys.key_id
+    assert back.payload_slots(be, keys) == (g["w"], g["e"])
+    # a level-3 ciphertext (4-limb integers on the wire) round-trips too
+    c = hint[0]
+    c2 = be.deserialize_ciphertext(be.serialize_ciphertext(c))
+    assert c2.level == 3 and np.array_equal(c2.payload.res, c.payload.res)

@@ -390,7 +390,7 @@ def test_missing_rotation_key_raises(c1, pkg):
         be.rot_row(c1["cts"][0], 5, keys)
 
 
-def _sharded_worker(rank, world, port, q):
+def _sharded_worker(rank, world, port, q, name="c2_N16384_s16"):
     """One rank of a two-process sharded Comp on the same GPU (gloo for the
     uint64 reduce: NCCL needs one GPU per rank)."""
     import os
@@ -405,7 +405,7 @@ def _sharded_worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        g = load_golden("c2_N16384_s16")
+        g = load_golden(name)
         n, p, N, s, seed = g["n"], g["p"], g["N"], g["s"], g["seed"]
         be, params, keys, dense, cts, hint = make_case(P, O, n, p, N, s, seed, guard=not g["noise_guard_disabled"])
         ans = comp_sharded(cts, params, be, keys, hint, dist)
@@ -417,10 +417,13 @@ def _sharded_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_comp_two_processes_matches_reference_golden(pkg):
-    """SURVEY 8(e) end to end with real ranks: blocks [0,2) and [2,4) of the
-    headline Comp on two processes (hc_comp_partial + per-rank input upload),
-    uint64 SUM reduce, hc_comp_finish on rank 0 == the reference's answer."""
+@pytest.mark.parametrize("name,world", [("c2_N16384_s16", 2), ("c1_N8192_s8", 3)])
+def test_sharded_comp_multi_process_matches_reference_golden(pkg, name, world):
+    """SURVEY 8(e) end to end with real ranks: the headline Comp's blocks
+    [0,2) and [2,4) on two processes (hc_comp_partial + per-rank input upload),
+    uint64 SUM reduce, hc_comp_finish on rank 0 == the reference's answer.
+    World 3 over config 1's two blocks leaves one rank an empty range: it
+    uploads nothing, joins the reduce with a zero partial, nothing hangs."""
     import socket
 
     import torch.multiprocessing as mp
@@ -431,10 +434,10 @@ def test_sharded_comp_two_processes_matches_reference_golden(pkg):
     sock.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q, name)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
         pr.join(timeout=600)
         assert pr.exitcode == 0
-    assert q.get(timeout=5) is True and q.get(timeout=5) is True
+    assert all(q.get(timeout=5) is True for _ in range(world))
