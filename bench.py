@@ -44,7 +44,7 @@ N_DEFAULT, S_DEFAULT, P_DEFAULT, RING = 1 << 14, 16, 65537, 8192
 # hcomp.cu StepKind -> the kernels behind it (hc_comp_profile's step kinds)
 STEP_KINDS = {0: "transforms (k_xf, k_xf_cl)", 1: "crt_digits (k_compose)", 2: "key_mac (k_ksmac)",
               3: "diag_mac (k_diagx)", 5: "memset", 6: "two_prime_intt (k_cl_intt2)",
-              7: "key_mac_grouped (k_ksmac_mb)"}
+              7: "key_mac_grouped (k_ksmac_mb)", 8: "add (k_addmod)", 9: "fold_chain (k_tail, persistent)"}
 
 
 def metric_name(N: int, s: int) -> str:
@@ -66,6 +66,10 @@ def make_parser() -> argparse.ArgumentParser:
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-flush", type=int, default=1, help="flush L2 inside the streamed e2e loop (counted)")
+    ap.add_argument("--queries", type=int, default=0,
+                    help="config 5: Q independent queries (own seeded keys and payloads, one shared database "
+                         "shape) spread over the ranks; a step runs every query once; value = aggregate entries/s")
+    ap.add_argument("--query-streams", type=int, default=8, help="concurrent CUDA streams per rank in --queries mode")
     ap.add_argument("--no-parity", action="store_true",
                     help="skip the bit-exact check of the GPU answer against the CPU oracle (large N)")
     ap.add_argument("--shard", default="auto", choices=["auto", "on", "off"],
@@ -269,6 +273,228 @@ def oracle_answer(args, p, seed):
     return O.comp(cts, args.N, args.s, be, keys, hint).c
 
 
+def roofline(L, h, sh, comp_ms):
+    """Live roofline of the dominant kernel family (the transforms k_xf /
+    k_xf_cl): algorithmic butterflies per launch over the launches' event-timed
+    duration (un-graphed profile of one Comp), against the measured butterfly
+    peak; plus the Comp-level figure and the same kernel saturated."""
+    import ctypes
+
+    import numpy as np
+
+    from paper_2408_17063_b200 import _lib
+
+    max_steps = 4096
+    sm_ = np.zeros(max_steps, dtype=np.float32)
+    sk = np.zeros(max_steps, dtype=np.int32)
+    sj = np.zeros(max_steps, dtype=np.int32)
+    nsteps = L.hc_comp_profile(h, sh, max_steps, _lib.ptr(sm_), _lib.ptr(sk), _lib.ptr(sj))
+    if nsteps < 0:
+        _lib.check(nsteps)
+    kinds = {}
+    for i in range(nsteps):
+        d = kinds.setdefault(int(sk[i]), [0.0, 0, 0])
+        d[0] += float(sm_[i])
+        d[1] += int(sj[i])
+        d[2] += 1
+    xf_ms, xf_jobs, xf_launch = kinds.get(0, [0.0, 0, 0])
+    prof_total = float(sm_[:nsteps].sum())
+    peak = ctypes.c_double()
+    _lib.check(L.hc_bf_peak(h, ctypes.byref(peak)))
+    # the same transform kernel saturated (4 full waves of 148 single-CTA jobs):
+    # what it reaches when the GPU is full, vs the latency-bound launches above
+    sat = {}
+    for dname, dval in (("fwd", 0), ("inv", 1)):
+        us = ctypes.c_double()
+        _lib.check(L.hc_bench_xform(h, 592, dval, 20, ctypes.byref(us)))
+        sat[dname] = 592 * (RING // 2) * 13 / (us.value * 1e-6) / 1e9
+    bfly_per_ntt = (RING // 2) * 13
+    achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
+    peak_g = peak.value / 1e9
+    comp_level = xf_jobs * bfly_per_ntt / comp_ms / 1e6
+    return {
+        "kernel": "k_xf / k_xf_cl: 8192-point NTT/INTT launches (1 CTA or one 8-CTA cluster per transform, fused loaders/epilogues)",
+        "bound": "int-modmul (IMAD pipe; SURVEY 8(d))",
+        "achieved": achieved,
+        "peak": peak_g,
+        "unit": "Gbutterfly/s",
+        "frac": achieved / peak_g if peak_g else None,
+        "peak_source": "measured live: hc_bf_peak, register-only microbenchmark of the kernels' own lazy CT butterfly at full occupancy (MEASURED_PEAKS.json has no integer peak)",
+        "work_unit": "one radix-2 butterfly = one 54-bit modmul + 2 modadds; 4096*13 per 8192-point transform",
+        "traffic": None,
+        "traffic_note": ("DRAM bytes per launch from ncu --set full captures are in profiles/ (the family "
+                         "mixes launches of 1-396 jobs, so no single per-launch figure applies)"),
+        "comp_level_gbfly_s": comp_level,
+        "comp_level_frac": comp_level / peak_g if peak_g else None,
+        "xform_share_of_step": xf_ms / prof_total if prof_total else None,
+        "xform_jobs_per_comp": xf_jobs,
+        "xform_launches_per_comp": xf_launch,
+        "profiled_step_ms_ungraphed": prof_total,
+        "per_kind_ms": {STEP_KINDS.get(k, str(k)): round(v[0], 4) for k, v in sorted(kinds.items())},
+        "saturated_592_jobs_gbfly_s": sat,
+        "saturated_frac": {k: v / peak_g for k, v in sat.items()} if peak_g else None,
+    }
+
+
+def run_queries(args, p, world, rank, local, dist):
+    """Config 5: Q independent queries, each with its own seeded
+    key pair, rotation keys and s-sparse payload (query q: seed q), over one
+    (N, s) database shape.  Query q runs on rank q % world; every rank keeps
+    its queries device-resident (own keys, inputs and CUDA graph) and shares
+    ONE copy of the plan's diagonals among them (hc_plan_shared).  A step
+    launches every query once, round-robin over --query-streams streams;
+    value = Q * N / (max-over-ranks step time).  No collective: replicas."""
+    import numpy as np
+    import torch
+
+    import paper_2408_17063_b200 as P
+    from paper_2408_17063_b200 import _lib
+
+    he = P.HeParams(RING, p, 3)
+    params = P.CompressionParams(args.N, args.s, he)
+    mine = [q for q in range(args.queries) if q % world == rank]
+    L = _lib.lib()
+    t_setup = time.perf_counter()
+    qs, first = [], None
+    for q in mine:
+        be = P.B200BgvBackend(he, seed=q, device=local, noise_guard=False)
+        keys = be.keygen(*P.plan_rotation_amounts(args.s, RING))
+        dense = plant(args.N, args.s, p, q)
+        cd = np.ascontiguousarray(np.stack([c.payload.res for c in P.encrypt_vector(dense, params, be, keys)]))
+        cv = np.ascontiguousarray(np.stack([c.payload.res for c in P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)]))
+        dc = P.DeviceComp(be, params, keys, share_with=first)
+        first = first or dc
+        dc.set_inputs(cd, cv)
+        qs.append(dict(q=q, be=be, keys=keys, dense=dense, dc=dc, h=be._ctx(),
+                       cd_h=torch.from_numpy(cd).pin_memory(), cv_h=torch.from_numpy(cv).pin_memory(),
+                       out_h=torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()))
+    setup_s = time.perf_counter() - t_setup
+    ns = max(1, min(args.query_streams, len(qs)))
+    streams = [torch.cuda.Stream() for _ in range(ns)]
+    main_s = torch.cuda.Stream()
+    C = params.num_ciphertexts
+
+    def step(e2e: bool):
+        ev = torch.cuda.Event()
+        ev.record(main_s)
+        for st in streams:
+            st.wait_event(ev)
+        for i, d in enumerate(qs):
+            sh = streams[i % ns].cuda_stream
+            if e2e:
+                _lib.check(L.hc_comp_async(d["h"], d["cd_h"].data_ptr(), d["cv_h"].data_ptr(), C, d["out_h"].data_ptr(), sh))
+            else:
+                d["dc"].launch(sh)
+        for st in streams:
+            e = torch.cuda.Event()
+            e.record(st)
+            main_s.wait_event(e)
+
+    # correctness: every query decrypts to its own payload's power sums
+    step(False)
+    torch.cuda.synchronize()
+    outs = {}
+    for d in qs:
+        out = d["dc"].output()
+        outs[d["q"]] = out
+        be = d["be"]
+        m = be.decrypt(P.Ciphertext(be.backend_id, d["keys"].key_id, 0, P.RnsPayload(out, 0.0, (be.q[0],))), d["keys"])
+        w = [int(x) for x in m.rows[0][: args.s]]
+        assert w == [sum(pow(i + 1, j + 1, p) for i, v in enumerate(d["dense"]) if v) % p for j in range(args.s)], \
+            f"query {d['q']} does not decrypt to its power sums"
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(main_s):
+        for _ in range(args.warmup):
+            flush.zero_()
+            step(False)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(main_s):
+        for a, b in evs:
+            flush.zero_()
+            a.record(main_s)
+            step(False)
+            b.record(main_s)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    e2e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with torch.cuda.stream(main_s):
+        step(True)
+        torch.cuda.synchronize()
+        for a, b in e2e_evs:
+            flush.zero_()
+            a.record(main_s)
+            step(True)
+            b.record(main_s)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    for d in qs:
+        assert np.array_equal(d["out_h"].numpy().view(np.uint64), outs[d["q"]]), "e2e answer differs"
+    t_ms, e2e_ms = sum(step_ms), sum(a.elapsed_time(b) for a, b in e2e_evs)
+    if dist:
+        tt = torch.tensor([t_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms, e2e_ms = tt.tolist()
+    per_step = t_ms / args.steps
+    units = args.queries * args.N
+    info = qs[0]["be"].plan_info()
+    rf = roofline(L, qs[0]["h"], main_s.cuda_stream, per_step / max(1, len(qs)))
+    line = {
+        "metric": metric_name(args.N, args.s) + f", {args.queries} independent queries",
+        "value": units / (per_step * 1e-3),
+        "unit": "entries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": per_step,
+        "latency_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms),
+                       "per_query_amortised": per_step / max(1, len(qs))},
+        "higher_is_better": True,
+        "scaling": "strong",  # total work (Q queries) fixed as N grows
+        "vs_baseline": None,
+        "dtype": "u64 (RNS, 54-bit primes)",
+        "data": "synthetic (seeded per query; real keygen + encryption per query)",
+        "config": dict(workload(args, p), workload=f"config 5: {args.queries} independent queries, BGV Comp N={args.N} "
+                       f"s={args.s} n={RING} p={p}, own keys per query, diagonals shared per GPU",
+                       queries=args.queries, queries_per_rank=len(qs), streams_per_rank=ns,
+                       parallelism=f"queries round-robin over {world} GPU(s), {ns} streams each (no collective)"),
+        "e2e": {"value": units / (e2e_ms / args.steps * 1e-3), "unit": "entries/s", "ms_per_step": e2e_ms / args.steps,
+                "mode": "every query: H2D of its inputs from pinned memory, its Comp graph, D2H of its answer "
+                        "(hc_comp_async on its stream)",
+                "h2d_bytes_per_step": int(sum(d["cd_h"].numel() * 8 * 2 for d in qs)),
+                "d2h_bytes_per_step": int(len(qs) * 2 * RING * 8)},
+        "gpu_launches": int(info["kernel_launches"]) * len(qs) * args.steps * 2,
+        "kernel_launches_per_comp": int(info["kernel_launches"]),
+        "roofline": rf,
+        "clocks": clk,
+        "setup_s": round(setup_s, 1),
+        "plan": info,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_out, line["cpu_baseline"] = cpu_baseline_sample(args, p, args.cpu_seconds)
+        cpu_out = np.asarray(cpu_out, dtype=np.uint64)
+    else:
+        cpu_out = None
+    if rank == 0 and not args.no_parity:  # query 0 (seed 0) against the oracle
+        ref = cpu_out if cpu_out is not None else np.asarray(oracle_answer(args, p, 0), dtype=np.uint64)
+        ok = bool(np.array_equal(ref, outs[0]))
+        line["parity"] = {"status": "bit-exact" if ok else "MISMATCH",
+                          "against": "CPU oracle port of the reference Comp, query 0 (seed 0); every query decrypt-checked",
+                          "query_seed": 0}
+        assert ok, "query 0 differs from the CPU oracle"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     p = pick_p(args.N, args.p)
@@ -299,6 +525,8 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.queries:
+        return run_queries(args, p, world, rank, local, dist)
     shard = args.shard_on
     he = P.HeParams(RING, p, 3)
     params = P.CompressionParams(args.N, args.s, he)
@@ -308,7 +536,14 @@ def main():
     dense = plant(args.N, args.s, p, seed)
     cts = P.encrypt_vector(dense, params, be, keys)
     hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
-    dc = P.DeviceComp(be, params, keys)
+    if shard:  # this rank's plan covers its own blocks only (hc_plan_range)
+        from paper_2408_17063_b200.dist import shard_blocks
+
+        b0, b1 = shard_blocks(params.num_blocks, world, rank)
+        be.plan(args.N, args.s, keys, block_range=(b0, b1))
+        dc = None
+    else:
+        dc = P.DeviceComp(be, params, keys)
     cd = np.ascontiguousarray(np.stack([c.payload.res for c in cts]))
     cv = np.ascontiguousarray(np.stack([c.payload.res for c in hint]))
 
@@ -320,9 +555,6 @@ def main():
     out_h = torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()
 
     if shard:
-        from paper_2408_17063_b200.dist import shard_blocks
-
-        b0, b1 = shard_blocks(params.num_blocks, world, rank)
         c0, c1 = b0 // 2, (b1 + 1) // 2
         cd_h = torch.from_numpy(np.ascontiguousarray(cd[c0:c1])).pin_memory()
         cv_h = torch.from_numpy(np.ascontiguousarray(cv[c0:c1])).pin_memory()
@@ -358,7 +590,11 @@ def main():
     def output():
         torch.cuda.synchronize()
         # sharded: only the root holds the answer; replicas: every rank has its own
-        return dc.output() if (rank == 0 or not shard) else None
+        if rank != 0 and shard:
+            return None
+        o = np.empty((2, 1, RING), dtype=np.uint64)
+        _lib.check(L.hc_comp_get_output(h, _lib.ptr(o)))
+        return o
 
     # correctness gate: the timed Comp must decrypt to the payload's power sums
     with torch.cuda.stream(stream):
@@ -503,37 +739,7 @@ def main():
         t_ms, e2e_ms, e2e_serial_ms, e2e_stream_ms = tt.tolist()
         e2e_stream_ms = e2e_stream_ms or None
 
-    # ---- live roofline of the dominant kernel family (the transforms) ----
-    max_steps = 4096
-    sm_ = np.zeros(max_steps, dtype=np.float32)
-    sk = np.zeros(max_steps, dtype=np.int32)
-    sj = np.zeros(max_steps, dtype=np.int32)
-    nsteps = L.hc_comp_profile(h, sh, max_steps, _lib.ptr(sm_), _lib.ptr(sk), _lib.ptr(sj))
-    if nsteps < 0:
-        _lib.check(nsteps)
-    kinds = {}
-    for i in range(nsteps):
-        d = kinds.setdefault(int(sk[i]), [0.0, 0, 0])
-        d[0] += float(sm_[i])
-        d[1] += int(sj[i])
-        d[2] += 1
-    xf_ms, xf_jobs, xf_launch = kinds.get(0, [0.0, 0, 0])
-    prof_total = float(sm_[:nsteps].sum())
-    peak = ctypes.c_double()
-    _lib.check(L.hc_bf_peak(h, ctypes.byref(peak)))
-    # the same transform kernel saturated (4 full waves of 148 single-CTA jobs):
-    # what it reaches when the GPU is full, vs the latency-bound launches above
-    sat = {}
-    for dname, dval in (("fwd", 0), ("inv", 1)):
-        us = ctypes.c_double()
-        _lib.check(L.hc_bench_xform(h, 592, dval, 20, ctypes.byref(us)))
-        sat[dname] = 592 * (RING // 2) * 13 / (us.value * 1e-6) / 1e9
-    bfly_per_ntt = (RING // 2) * 13
-    # dominant kernel family = the transform launches (k_xf / k_xf_cl):
-    # algorithmic butterflies per launch / that launch's event-timed duration
-    achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
-    peak_g = peak.value / 1e9
-    comp_level = xf_jobs * bfly_per_ntt / (per_step_ms_pre := (t_ms / args.steps)) / 1e6
+    rf = roofline(L, h, sh, t_ms / args.steps)
 
     per_step_ms = t_ms / args.steps
     units = args.N if shard else args.N * world  # sharded: one Comp per step; replicas: one per rank
@@ -573,30 +779,7 @@ def main():
         },
         "gpu_launches": int(info["kernel_launches"]) * args.steps * 2,
         "kernel_launches_per_comp": int(info["kernel_launches"]),
-        "roofline": {
-            "kernel": "k_xf / k_xf_cl: 8192-point NTT/INTT launches (1 CTA or one 8-CTA cluster per transform, fused loaders/epilogues)",
-            "bound": "int-modmul (IMAD pipe; SURVEY 8(d))",
-            "achieved": achieved,
-            "peak": peak_g,
-            "unit": "Gbutterfly/s",
-            "frac": achieved / peak_g if peak_g else None,
-            "peak_source": "measured live: hc_bf_peak, register-only microbenchmark of the kernels' own lazy CT butterfly at full occupancy (MEASURED_PEAKS.json has no integer peak)",
-            "work_unit": "one radix-2 butterfly = one 54-bit modmul + 2 modadds; 4096*13 per 8192-point transform",
-            "traffic": None,
-            "traffic_note": ("DRAM bytes per launch from ncu --set full captures are in "
-                             "profiles/r01_ncu_full_summary.txt (the family mixes launches of 1-396 jobs, "
-                             "so no single per-launch figure applies); e.g. 592 forward transforms read "
-                             "39.4 MB = their inputs, no re-reads"),
-            "comp_level_gbfly_s": comp_level,
-            "comp_level_frac": comp_level / peak_g if peak_g else None,
-            "xform_share_of_step": xf_ms / prof_total if prof_total else None,
-            "xform_jobs_per_comp": xf_jobs,
-            "xform_launches_per_comp": xf_launch,
-            "profiled_step_ms_ungraphed": prof_total,
-            "per_kind_ms": {STEP_KINDS.get(k, str(k)): round(v[0], 4) for k, v in sorted(kinds.items())},
-            "saturated_592_jobs_gbfly_s": sat,
-            "saturated_frac": {k: v / peak_g for k, v in sat.items()} if peak_g else None,
-        },
+        "roofline": rf,
         "clocks": clk,
         "plan": info,
     }

@@ -70,6 +70,20 @@ int hc_clear_keys(hc_ctx* h);
  * chunk_blocks: blocks processed per pass (0 = automatic).
  * Fails with HC_ERR_KEY if a needed rotation key is not loaded. */
 int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks);
+/* hc_plan for one rank of a block-sharded Comp: only the
+ * diagonals of blocks [b0, b1) are generated and only input ciphertexts
+ * [b0/2, (b1+1)/2) are allocated, so a rank's plan memory and generation
+ * time are O(N / world); run it with hc_comp_set_inputs_range +
+ * hc_comp_partial(h, b', b'', ...) for sub-ranges of [b0, b1) and
+ * hc_comp_finish.  The whole-matrix entry points return HC_ERR_STATE. */
+int hc_plan_range(hc_ctx* h, int64_t N, int s, int chunk_blocks, int64_t b0, int64_t b1);
+/* hc_plan with the plaintexts (pack masks, diagonals, output mask) of
+ * another context's current plan on the same device and chain: config 5's
+ * independent queries over one database share one copy of the diagonals
+ * (the buffers are reference counted and live while any plan uses them).
+ * The source plan must be a whole-matrix hint-path plan (hc_plan). */
+int hc_plan_shared(hc_ctx* h, const hc_ctx* src, int chunk_blocks);
+
 /* Replaces _plan(params, "packed", masked) for comp_masked (compress.py:
  * 154-157, 521-530): as hc_plan, but the bottom lane evaluates
  * D = C diag(DB) (VandermondeTable with db_values, compress.py:107-135).

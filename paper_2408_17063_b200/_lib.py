@@ -50,6 +50,8 @@ _SIGS = [
     ("hc_clear_keys", _I, [_P]),
     ("hc_plan", _I, [_P, _I64, _I, _I]),
     ("hc_plan_masked", _I, [_P, ctypes.c_int64, _I, _I, _P]),
+    ("hc_plan_range", _I, [_P, _I64, _I, _I, _I64, _I64]),
+    ("hc_plan_shared", _I, [_P, _P, _I]),
     ("hc_plan_info", _I, [_P, _P]),
     ("hc_comp", _I, [_P, _P, _P, _I, _P]),
     ("hc_comp_packed", _I, [_P, _P, _I64, _P]),

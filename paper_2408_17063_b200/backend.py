@@ -719,13 +719,42 @@ class B200BgvBackend:
 
     # -- the fused Comp (compress.py:488-514) ------------------------------------------
 
-    def plan(self, N: int, s: int, keys: KeySet, chunk_blocks: int = 0, db: np.ndarray | None = None) -> None:
-        """Device plan for (N, s); `db` (uint64[N], mod p) selects comp_masked's D = C diag(DB)."""
+    def plan(
+        self,
+        N: int,
+        s: int,
+        keys: KeySet,
+        chunk_blocks: int = 0,
+        db: np.ndarray | None = None,
+        block_range: tuple[int, int] | None = None,
+        share_with: "B200BgvBackend | None" = None,
+    ) -> None:
+        """Device plan for (N, s); `db` (uint64[N], mod p) selects comp_masked's D = C diag(DB).
+
+        block_range=(b0, b1): a sharded rank's plan (hc_plan_range), only its
+        blocks' diagonals and input ciphertexts on the device.  share_with: a
+        backend whose current (N, s) plan's plaintexts this one reuses
+        (hc_plan_shared; independent queries over one database)."""
         self._load_keys(keys)
-        tag = (N, s, chunk_blocks, None if db is None else hashlib.sha256(db.tobytes()).digest())
+        rng = None if block_range is None else (int(block_range[0]), int(block_range[1]))
+        src = None
+        if share_with is not None:
+            if db is not None or rng is not None:
+                raise ValueError("a shared plan is a whole-matrix hint-path plan")
+            sp = share_with._planned
+            if sp is None or sp[:2] != (N, s) or sp[3] is not None or sp[4] is not None:
+                raise ValueError("share_with has no hint-path plan for this (N, s)")
+            src = share_with
+        tag = (N, s, chunk_blocks, None if db is None else hashlib.sha256(db.tobytes()).digest(), rng, id(src) if src else None)
         if self._planned != tag:
-            if db is None:
-                _lib.check(_lib.lib(self.params.max_level).hc_plan(self._ctx(), N, s, chunk_blocks))
+            L = _lib.lib(self.params.max_level)
+            if src is not None:
+                _lib.check(L.hc_plan_shared(self._ctx(), src._ctx(), chunk_blocks))
+                self._plan_src = src  # keep the source alive beside the shared buffers
+            elif rng is not None:
+                _lib.check(L.hc_plan_range(self._ctx(), N, s, chunk_blocks, rng[0], rng[1]))
+            elif db is None:
+                _lib.check(L.hc_plan(self._ctx(), N, s, chunk_blocks))
             else:
                 db = np.ascontiguousarray(db, dtype=np.uint64)
                 _lib.check(_lib.lib(self.params.max_level).hc_plan_masked(self._ctx(), N, s, chunk_blocks, _lib.ptr(db)))

@@ -431,11 +431,20 @@ class DeviceComp:
     (`set_inputs`), each `launch(stream)` enqueues one full Comp (one CUDA
     graph launch), `output()` reads the level-0 ciphertext residues."""
 
-    def __init__(self, backend: B200BgvBackend, params: CompressionParams, keys: KeySet, chunk_blocks: int = 0):
+    def __init__(
+        self,
+        backend: B200BgvBackend,
+        params: CompressionParams,
+        keys: KeySet,
+        chunk_blocks: int = 0,
+        share_with: "DeviceComp | None" = None,
+    ):
+        """share_with: another DeviceComp over the same database shape whose
+        plaintexts (diagonals, masks) this query reuses (hc_plan_shared)."""
         self.be = backend
         self.params = params
         self.keys = keys
-        backend.plan(params.N, params.s, keys, chunk_blocks)
+        backend.plan(params.N, params.s, keys, chunk_blocks, share_with=None if share_with is None else share_with.be)
 
     def set_inputs(self, cd: np.ndarray, cv: np.ndarray) -> None:
         cd = np.ascontiguousarray(cd, dtype=np.uint64)

@@ -856,12 +856,30 @@ static int capture(hc_ctx* h, Schedule& S) {
 // ---------------------------------------------------------------------------
 // Comp plan (compress.py:198-367 on the BGV semantics of bgv.py:579-770)
 // ---------------------------------------------------------------------------
+// The plan's plaintexts (pack masks, diagonals, output mask), reference
+// counted: a plan built with hc_plan_shared points at another context's
+// (config 5: one database, many queries with their own keys).
+struct PlainBufs {
+    u64* mask = nullptr;   // [2][4][n]
+    u64* diag = nullptr;   // [blocks of the plan's range][s_pad][3][n]
+    u64* omask = nullptr;  // [2][n]
+    ~PlainBufs() {
+        cudaFree(mask);
+        cudaFree(diag);
+        cudaFree(omask);
+    }
+};
 struct Plan {
     long long N = 0;
     int s = 0, s_pad = 0, baby = 0, giant = 0, m = 0, F = 0, CB = 0, ncopy = 1;
     long long B = 0, C = 0;
     int D1 = 0, D2 = 0;
     bool masked = false;  // comp_masked plan (row-1 diagonals scaled by the DB)
+    // block range the plan covers (hc_plan_range; the whole matrix otherwise):
+    // diagonals of blocks [rb0, rb1), input ciphertexts [rc0, rc1)
+    long long rb0 = 0, rb1 = 0, rc0 = 0, rc1 = 0;
+    bool full_range() const { return rb0 == 0 && rb1 == B; }
+    std::shared_ptr<PlainBufs> plain;
     std::vector<int> fold;
     std::vector<uint8_t> live;      // [B][s_pad]
     std::vector<uint8_t> acc_live;  // [giant]
@@ -939,7 +957,10 @@ static const DevKey* need_key(hc_ctx* h, uint32_t t) {
     return it == h->keys.end() ? nullptr : &it->second;
 }
 
-static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db) {
+// b0 < 0: the whole matrix; else blocks [b0, b1) only (a rank's shard).
+// share: take the plaintexts of another context's plan (same chain, N, s).
+static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db, int64_t b0 = -1,
+                     int64_t b1 = -1, const Plan* share = nullptr) {
     if (!h) return fail(HC_ERR_ARG, "null context");
     if (h->L < 3) return fail(HC_ERR_ARG, "Comp needs max_level >= 3 (SURVEY F3)");
     const int n = NPOLY, m = n / 2;
@@ -955,6 +976,15 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
     bsgs_shape(s, &P->baby, &P->giant, &P->s_pad);
     P->B = (N + m - 1) / m;
     P->C = (P->B + 1) / 2;
+    if (b0 < 0) {
+        b0 = 0;
+        b1 = P->B;
+    }
+    if (b0 > b1 || b1 > P->B) return fail(HC_ERR_ARG, "block range out of bounds");
+    P->rb0 = b0;
+    P->rb1 = b1;
+    P->rc0 = b0 / 2;
+    P->rc1 = (b1 + 1) / 2;
     for (int step = P->s_pad; step < m; step <<= 1) P->fold.push_back(step);
     P->F = (int)P->fold.size();
     P->D1 = h->digits[1];
@@ -1020,11 +1050,22 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
         rc = palloc(*P, &(ptr), (cnt)); \
         if (rc) return rc;              \
     } while (0)
-    PA(P->cv, (size_t)P->C * 2 * 4 * NB);
-    PA(P->cd, (size_t)P->C * 2 * 4 * NB);
-    PA(P->mask, (size_t)2 * 4 * NB);
-    PA(P->diag, (size_t)P->B * P->s_pad * 3 * NB);
-    PA(P->omask, (size_t)2 * NB);
+    // inputs and diagonals of the plan's block range only
+    const size_t ncts = (size_t)std::max<long long>(1, P->rc1 - P->rc0);
+    const size_t nblk = (size_t)std::max<long long>(1, P->rb1 - P->rb0);
+    PA(P->cv, ncts * 2 * 4 * NB);
+    PA(P->cd, ncts * 2 * 4 * NB);
+    if (share) {
+        P->plain = share->plain;
+    } else {
+        P->plain = std::make_shared<PlainBufs>();
+        CU(cudaMalloc(&P->plain->mask, (size_t)2 * 4 * NB * 8));
+        CU(cudaMalloc(&P->plain->diag, nblk * P->s_pad * 3 * NB * 8));
+        CU(cudaMalloc(&P->plain->omask, (size_t)2 * NB * 8));
+    }
+    P->mask = P->plain->mask;
+    P->diag = P->plain->diag;
+    P->omask = P->plain->omask;
     PA(P->ecor, (size_t)CB * 4 * 3 * NB);
     PA(P->rc1raw, (size_t)CB * 3 * NB);
     PA(P->pn, (size_t)CB * 2 * 3 * NB);
@@ -1053,20 +1094,20 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
 #undef PA
 
     // ---- plaintexts on device (K6) ----
-    {
+    if (!share) {
         std::vector<PJob> pj;
         PJob j{};
         j.kind = PT_TOP; j.level = 3; j.out = P->mask; pj.push_back(j);
         j.kind = PT_BOT; j.level = 3; j.out = P->mask + 4 * NB; pj.push_back(j);
         j.kind = PT_OUTMASK; j.level = 1; j.out = P->omask; pj.push_back(j);
-        for (long long t = 0; t < P->B; t++)
+        for (long long t = P->rb0; t < P->rb1; t++)
             for (int g = 0; g < P->giant; g++)
                 for (int b = 0; b < P->baby; b++) {
                     int i = g * P->baby + b;
                     if (!P->live[(size_t)t * P->s_pad + i]) continue;
                     PJob d{};
                     d.kind = PT_DIAG; d.t = (int)t; d.g = g; d.b = b; d.level = 2;
-                    d.out = P->diag + ((size_t)t * P->s_pad + i) * 3 * NB;
+                    d.out = P->diag + ((size_t)(t - P->rb0) * P->s_pad + i) * 3 * NB;
                     pj.push_back(d);
                 }
         PlanShape S{N, s, P->s_pad, P->baby, m, nullptr};
@@ -1101,6 +1142,22 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
 }
 
 extern "C" int hc_plan(hc_ctx* h, int64_t N, int s, int chunk_blocks) { return plan_impl(h, N, s, chunk_blocks, nullptr); }
+
+extern "C" int hc_plan_range(hc_ctx* h, int64_t N, int s, int chunk_blocks, int64_t b0, int64_t b1) {
+    if (b0 < 0) return fail(HC_ERR_ARG, "block range out of bounds");
+    return plan_impl(h, N, s, chunk_blocks, nullptr, b0, b1);
+}
+
+extern "C" int hc_plan_shared(hc_ctx* h, const hc_ctx* src, int chunk_blocks) {
+    if (!h || !src) return fail(HC_ERR_ARG, "null context");
+    if (!src->plan) return fail(HC_ERR_STATE, "the source context has no plan");
+    const Plan& S = *src->plan;
+    if (!S.full_range() || S.masked) return fail(HC_ERR_ARG, "only whole-matrix hint-path plans are shared");
+    if (src->dev != h->dev || src->L != h->L || src->p != h->p) return fail(HC_ERR_MISMATCH, "contexts differ");
+    for (int k = 0; k <= h->L; k++)
+        if (src->hctx.pc[k].q != h->hctx.pc[k].q) return fail(HC_ERR_MISMATCH, "contexts have different chains");
+    return plan_impl(h, S.N, S.s, chunk_blocks, nullptr, -1, -1, &S);
+}
 
 extern "C" int hc_plan_masked(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64_t* db_mod_p) {
     if (!db_mod_p) return fail(HC_ERR_ARG, "null database");
@@ -1180,8 +1237,8 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                 const long long src = t / 2;
                 const int par = (int)(t % 2);
                 const u64* mk = P.mask + (size_t)par * 4 * NB;
-                const u64* cv = P.cv + (size_t)src * 2 * 4 * NB;
-                const u64* cd = P.cd + (size_t)src * 2 * 4 * NB;
+                const u64* cv = P.cv + (size_t)(src - P.rc0) * 2 * 4 * NB;
+                const u64* cd = P.cd + (size_t)(src - P.rc0) * 2 * 4 * NB;
                 // even block: u = mp(cv, top) + rot_col(mp(cd, top)); odd: rot_col(mp(cv, bot)) + mp(cd, bot)
                 const u64* ctP = par == 0 ? cv : cd;
                 const u64* ctR = par == 0 ? cd : cv;
@@ -1301,7 +1358,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     for (int b = 0; b < baby; b++) {
                         const int i = g * baby + b;
                         if (!P.live[(size_t)t * sp + i]) continue;
-                        const u64* dg = P.diag + ((size_t)t * sp + i) * 3 * NB;
+                        const u64* dg = P.diag + ((size_t)(t - P.rb0) * sp + i) * 3 * NB;
                         for (int poly = 0; poly < 2; poly++) {
                             XJob j{};
                             j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE_RD; j.level = 2;
@@ -1330,7 +1387,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                             const int i = g * baby + b;
                             if (!P.live[(size_t)t * sp + i]) continue;
                             srcs.push_back(rot_src(P, Ub, tl, b, poly));
-                            dgs.push_back(P.diag + ((size_t)t * sp + i) * 3 * NB);
+                            dgs.push_back(P.diag + ((size_t)(t - P.rb0) * sp + i) * 3 * NB);
                             ess.push_back(eslot(P, tl, b, g, poly));
                         }
                     }
@@ -1634,9 +1691,16 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     return HC_OK;
 }
 
+static int need_full_range(const Plan& P) {
+    if (P.full_range()) return HC_OK;
+    return fail(HC_ERR_STATE, "the plan covers blocks [" + std::to_string(P.rb0) + ", " + std::to_string(P.rb1) +
+                                  ") only: use hc_comp_partial");
+}
+
 static int ensure_full(hc_ctx* h) {
     Plan& P = *h->plan;
     if (P.full) return HC_OK;
+    if (int rc = need_full_range(P)) return rc;
     std::unique_ptr<Schedule> S(new Schedule());
     int rc = build_partial(h, P, 0, P.B, *S);
     if (rc) return rc;
@@ -1652,6 +1716,7 @@ extern "C" int hc_comp_set_inputs(hc_ctx* h, const uint64_t* cd, const uint64_t*
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
     if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    if (int rc = need_full_range(P)) return rc;
     CU(cudaSetDevice(h->dev));
     const size_t bytes = (size_t)C * 2 * 4 * NPOLY * 8;
     CU(cudaMemcpyAsync(P.cd, cd, bytes, cudaMemcpyHostToDevice, h->stream));
@@ -1665,6 +1730,7 @@ extern "C" int hc_comp_set_inputs_device(hc_ctx* h, const uint64_t* cd_dev, cons
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
     if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    if (int rc = need_full_range(P)) return rc;
     CU(cudaSetDevice(h->dev));
     cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
     const size_t bytes = (size_t)C * 2 * 4 * NPOLY * 8;
@@ -1677,13 +1743,14 @@ extern "C" int hc_comp_set_inputs_range(hc_ctx* h, const uint64_t* cd, const uin
                                         void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
-    if (c0 < 0 || c1 > P.C || c0 > c1) return fail(HC_ERR_ARG, "ciphertext range out of bounds");
+    if (c0 < P.rc0 || c1 > P.rc1 || c0 > c1) return fail(HC_ERR_ARG, "ciphertext range out of bounds");
+    if (c0 == c1) return HC_OK;
     CU(cudaSetDevice(h->dev));
     cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
     const size_t ct = (size_t)2 * 4 * NPOLY;
     const size_t bytes = (size_t)(c1 - c0) * ct * 8;
-    CU(cudaMemcpyAsync(P.cd + (size_t)c0 * ct, cd, bytes, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(P.cv + (size_t)c0 * ct, cv, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(P.cd + (size_t)(c0 - P.rc0) * ct, cd, bytes, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(P.cv + (size_t)(c0 - P.rc0) * ct, cv, bytes, cudaMemcpyHostToDevice, s));
     return HC_OK;
 }
 
@@ -1756,6 +1823,7 @@ extern "C" int hc_comp_packed(hc_ctx* h, const uint64_t* u, int64_t B, uint64_t*
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
     if (B != P.B) return fail(HC_ERR_ARG, "expected one packed ciphertext per block");
+    if (int rc = need_full_range(P)) return rc;
     CU(cudaSetDevice(h->dev));
     const size_t words = (size_t)P.B * 2 * 3 * NPOLY;
     if (!P.uin) {
@@ -1902,6 +1970,7 @@ static int build_mixed_pack(hc_ctx* h, Plan& P, Schedule& S, int with_mask) {
 
 static int ensure_mixed(hc_ctx* h, Plan& P, int ld, int lv, int with_mask) {
     const size_t NB = NPOLY;
+    if (int rc = need_full_range(P)) return rc;
     if (P.mix_ld != ld || P.mix_lv != lv || P.mix_mask != with_mask) {
         P.full_mix.reset();
         P.mix_ld = ld;
@@ -2033,7 +2102,7 @@ extern "C" int hc_mixed_launch(hc_ctx* h, void* stream) {
 extern "C" int hc_comp_partial(hc_ctx* h, int64_t b0, int64_t b1, uint64_t* partial_dev, void* stream) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     Plan& P = *h->plan;
-    if (b0 < 0 || b1 > P.B || b0 > b1) return fail(HC_ERR_ARG, "block range out of bounds");
+    if (b0 < P.rb0 || b1 > P.rb1 || b0 > b1) return fail(HC_ERR_ARG, "block range outside the plan's");
     CU(cudaSetDevice(h->dev));
     auto key = std::make_pair((long long)b0, (long long)b1);
     auto it = P.partials.find(key);

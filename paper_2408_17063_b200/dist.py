@@ -68,13 +68,14 @@ def comp_sharded(cd, params, backend, keys, index_hint, dist, group=None, root: 
         raise NotImplementedError("sharded Comp takes level-3 inputs (mixed-level answer() inputs run unsharded)")
     live = live_diagonals(params)
     bits, sim = comp_noise(backend, params, [c.payload.noise_bits for c in cv], [c.payload.noise_bits for c in cd], live)
-    backend.plan(params.N, params.s, keys)
+    b0, b1 = shard_blocks(params.num_blocks, world, rank)
+    # this rank's plan: only its blocks' diagonals and input ciphertexts
+    backend.plan(params.N, params.s, keys, block_range=(b0, b1))
     L = _lib.lib(backend.params.max_level)
     h = backend._ctx()
     dev = torch.device("cuda", backend.device)
     stream = torch.cuda.current_stream(dev)
     sh = ctypes.c_void_p(stream.cuda_stream)
-    b0, b1 = shard_blocks(params.num_blocks, world, rank)
     c0, c1 = b0 // 2, (b1 + 1) // 2  # the input ciphertexts this rank's blocks read
     if c1 > c0:
         cd_arr = np.ascontiguousarray(np.stack([c.payload.res for c in cd[c0:c1]]), dtype=np.uint64)

@@ -166,3 +166,65 @@ def test_reference_shaped_objects_and_wire_round_trip(pkg, oracle):
     c = hint[0]
     c2 = be.deserialize_ciphertext(be.serialize_ciphertext(c))
     assert c2.level == 3 and np.array_equal(c2.payload.res, c.payload.res)
+
+
+def test_block_range_plans_sum_to_the_full_comp(pkg, oracle):
+    """Per-rank plans (hc_plan_range): each range plan holds only its blocks'
+    diagonals and input ciphertexts; the partials of [0, 7) and [7, 16) summed
+    as uint64 and finished equal the whole-matrix Comp (N = 2^16, 16 blocks).
+    Whole-matrix entry points refuse a range plan."""
+    import ctypes
+
+    import torch
+
+    from paper_2408_17063_b200 import _lib
+
+    P, O = pkg, oracle
+    be, params, keys, dense, cts, hint = _gpu_case(P, O, 1 << 16, 16, 65537, 5)
+    cd = np.stack([c.payload.res for c in cts])
+    cv = np.stack([c.payload.res for c in hint])
+    ref = P.DeviceComp(be, params, keys).run_host(cd, cv)
+    L = _lib.lib()
+    h = be._ctx()
+    total = None
+    for b0, b1 in ((0, 7), (7, 16)):
+        be.plan(params.N, params.s, keys, block_range=(b0, b1))
+        c0, c1 = b0 // 2, (b1 + 1) // 2
+        cdr = np.ascontiguousarray(cd[c0:c1])
+        cvr = np.ascontiguousarray(cv[c0:c1])
+        _lib.check(L.hc_comp_set_inputs_range(h, _lib.ptr(cdr), _lib.ptr(cvr), c0, c1, None))
+        part = torch.zeros(L.hc_partial_words(h), dtype=torch.int64, device="cuda")
+        _lib.check(L.hc_comp_partial(h, b0, b1, ctypes.c_void_p(part.data_ptr()), None))
+        torch.cuda.synchronize()
+        total = part if total is None else total + part
+        with pytest.raises(_lib.HcompError, match="covers blocks"):
+            out = np.empty((2, 1, 8192), dtype=np.uint64)
+            _lib.check(L.hc_comp(h, _lib.ptr(cd), _lib.ptr(cv), cd.shape[0], _lib.ptr(out)))
+    _lib.check(L.hc_comp_finish(h, ctypes.c_void_p(total.data_ptr()), None))
+    out = np.empty((2, 1, 8192), dtype=np.uint64)
+    _lib.check(L.hc_comp_get_output(h, _lib.ptr(out)))
+    assert np.array_equal(out, ref)
+
+
+def test_shared_plan_queries_vs_oracle(pkg, oracle):
+    """Config 5's memory layout: query B's plan reuses query A's diagonals
+    (hc_plan_shared) with its own keys and inputs; both answers equal the
+    oracle's for their seeds, and A re-planning does not disturb B."""
+    P, O = pkg, oracle
+    N, s, p = 1 << 14, 16, 65537
+    qa = _gpu_case(P, O, N, s, p, 200)
+    qb = _gpu_case(P, O, N, s, p, 201)
+    dca = P.DeviceComp(qa[0], qa[1], qa[2])
+    dcb = P.DeviceComp(qb[0], qb[1], qb[2], share_with=dca)
+    outs = []
+    for (be, params, keys, dense, cts, hint), dc in ((qa, dca), (qb, dcb)):
+        out = dc.run_host(np.stack([c.payload.res for c in cts]), np.stack([c.payload.res for c in hint]))
+        outs.append(out)
+    # the source re-plans (other chunking); the shared buffers stay alive
+    P.DeviceComp(qa[0], qa[1], qa[2], chunk_blocks=1)
+    be, params, keys, dense, cts, hint = qb
+    again = dcb.run_host(np.stack([c.payload.res for c in cts]), np.stack([c.payload.res for c in hint]))
+    assert np.array_equal(again, outs[1])
+    for seed, out in zip((200, 201), outs):
+        _, oout = _oracle_answer(O, N, s, p, seed)
+        assert np.array_equal(out, oout.c), f"seed {seed}"
