@@ -273,6 +273,40 @@ def oracle_answer(args, p, seed):
     return O.comp(cts, args.N, args.s, be, keys, hint).c
 
 
+def sass_mix(lib_path: str, mangled: str, bfly: float) -> dict | None:
+    """Static fma-pipe instruction mix of a shipped kernel (cuobjdump -sass),
+    per butterfly of its 1024-thread schedule (one schedule thread = 52
+    butterflies): IMAD-class (IMAD, IMAD.MOV/IADD/X/SHL, HFMA2 moves),
+    IMAD.WIDE.U32, IMAD.HI.U32."""
+    import re
+
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", lib_path], capture_output=True, text=True, timeout=60).stdout
+    except Exception:
+        return None
+    body = None
+    for f in re.split(r"\n\s*Function : ", out)[1:]:
+        if f.split("\n", 1)[0].strip() == mangled:
+            body = f
+            break
+    if body is None:
+        return None
+    ops = {"imad": 0, "wide": 0, "hi": 0, "total": 0}
+    for ln in body.split("\n"):
+        m = re.match(r"\s*/\*[0-9a-f]{4,}\*/\s+(?:@!?U?P\w+\s+)?([A-Z0-9_.]+)", ln)
+        if not m:
+            continue
+        op = m.group(1)
+        ops["total"] += 1
+        if op.startswith("IMAD.WIDE"):
+            ops["wide"] += 1
+        elif op.startswith("IMAD.HI"):
+            ops["hi"] += 1
+        elif op.startswith(("IMAD", "IMUL", "HFMA2")):
+            ops["imad"] += 1
+    return {k: v / bfly for k, v in ops.items()}
+
+
 def roofline(L, h, sh, comp_ms):
     """Live roofline of the dominant kernel family (the transforms k_xf /
     k_xf_cl): algorithmic butterflies per launch over the launches' event-timed
@@ -312,6 +346,14 @@ def roofline(L, h, sh, comp_ms):
     achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
     peak_g = peak.value / 1e9
     comp_level = xf_jobs * bfly_per_ntt / comp_ms / 1e6
+    # independent ceiling: measured INT32 multiply-pipe rates x the shipped
+    # transform kernel's fma-pipe instruction mix per butterfly (SASS)
+    rates = (ctypes.c_double * 3)()
+    _lib.check(L.hc_imad_peak(h, rates))
+    mix = sass_mix(_lib.LIB_PATH, "_ZN2hc4k_xfILi0ELi0ELi0ELi4EEEvNS_6DevCtxEPKNS_4XJobE", 52.0)
+    pipe_bound = None
+    if mix and all(r > 0 for r in rates):
+        pipe_bound = 1.0 / (mix["imad"] / rates[0] + mix["wide"] / rates[1] + mix["hi"] / rates[2]) / 1e9
     return {
         "kernel": "k_xf / k_xf_cl: 8192-point NTT/INTT launches (1 CTA or one 8-CTA cluster per transform, fused loaders/epilogues)",
         "bound": "int-modmul (IMAD pipe; SURVEY 8(d))",
@@ -333,6 +375,16 @@ def roofline(L, h, sh, comp_ms):
         "per_kind_ms": {STEP_KINDS.get(k, str(k)): round(v[0], 4) for k, v in sorted(kinds.items())},
         "saturated_592_jobs_gbfly_s": sat,
         "saturated_frac": {k: v / peak_g for k, v in sat.items()} if peak_g else None,
+        "int32_pipe": {
+            "measured_gops_s": {"IMAD": rates[0] / 1e9, "IMAD.WIDE.U32": rates[1] / 1e9, "IMAD.HI.U32": rates[2] / 1e9},
+            "source": "hc_imad_peak: register-only mad.lo / mad.wide / mad.hi u32 streams, 8 chains x 2048 threads per SM",
+            "k_per_butterfly": mix,
+            "k_source": "cuobjdump -sass of the shipped k_xf<0,0,0,4> (throughput forward transform), per butterfly",
+            "modeled_bound_gbfly_s": pipe_bound,
+            "frac_of_modeled_bound": (achieved / pipe_bound) if pipe_bound else None,
+            "comp_level_frac_of_modeled_bound": (comp_level / pipe_bound) if pipe_bound else None,
+            "saturated_frac_of_modeled_bound": {k: v / pipe_bound for k, v in sat.items()} if pipe_bound else None,
+        },
     }
 
 

@@ -15,7 +15,9 @@
  * residue modulo level_prime(k) (bgv.py:104-106: row 0 = smallest prime,
  * the last row is the prime a modulus switch divides out), values in [0, q_k).
  * A ciphertext at level l is uint64[2][l+1][n] (c0 then c1), NTT domain.
- * Only n = 8192 and max_level <= 4 are supported.  Key switching, CRT
+ * Only n = 8192 is supported; max_level <= 3 (libhcomp.so), 4 (libhcomp_l4.so)
+ * or up to 22 (libhcomp_deep.so: pdq's protocol chain, whose levels above 4
+ * carry ring transforms and mul_plain's modulus switch only).  Key switching, CRT
  * compose and the fused Comp run at levels <= 3 (the 4 smallest primes);
  * level 4 is for the Mask / pack products of answer() (pdq.py:238-256),
  * which enter Comp through hc_comp_packed.
@@ -63,6 +65,12 @@ int hc_ctx_digits(const hc_ctx* h, int* digits);
  * primes (what _KskPair.at_level yields at levels <= 3). */
 int hc_load_ksk(hc_ctx* h, uint32_t galois_t, const uint64_t* ksk);
 int hc_clear_keys(hc_ctx* h);
+/* The same from a slice of a deep chain's key: ksk = uint64[digits][2][rows][n]
+ * holding the first `digits` pairs on the `rows` smallest primes (level
+ * order).  A protocol chain (pdq.protocol_max_level = 21: 75 digits x 22
+ * primes) only ever key-switches at levels <= 3, where _KskPair.at_level
+ * (bgv.py:304-312) reads the first 14 digits on the 4 smallest primes. */
+int hc_load_ksk_slice(hc_ctx* h, uint32_t galois_t, const uint64_t* ksk, int digits, int rows);
 
 /* Replaces compress._plan / build_plan (compress.py:198-270, packed mode,
  * no cleartext database): generates every diagonal, the pack masks and the
@@ -174,6 +182,13 @@ int hc_ntt(hc_ctx* h, uint64_t* data, int rows, const int* prime_idx, int invers
 int hc_pointwise(hc_ctx* h, const uint64_t* a, const uint64_t* b, uint64_t* out, int rows,
                  const int* prime_idx, int op);
 
+/* Replaces BgvBackend.decrypt (bgv.py:559-575) for levels 0..3, in one
+ * device call: phase = c0 + c1 s (ct = uint64[2][level+1][n], NTT domain;
+ * secret = the ternary key, int64[n]), INTT, exact integer in [0, Q_level)
+ * by CRT, centred, reduced mod p, slot_decode (bgv.py:387-394).
+ * slots = int64[2][n/2] (SlotMatrix rows). */
+int hc_decrypt(hc_ctx* h, const uint64_t* ct, int level, const int64_t* secret, int64_t* slots);
+
 /* Single backend operations (BgvBackend.mul_plain bgv.py:717-733 and
  * _apply_galois bgv.py:735-747) on host buffers.
  * hc_mul_plain: ct uint64[2][l+1][n] at level l >= 1, pt = NttContext
@@ -189,6 +204,10 @@ int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int*
 /* Measured butterfly-throughput ceiling of this GPU for the NTT butterfly
  * used by the transform kernel (register-only microbenchmark). */
 int hc_bf_peak(hc_ctx* h, double* bfly_per_s);
+/* INT32 multiply-pipe ceilings of this GPU, independent of the Comp code:
+ * ops_per_s[0..2] = IMAD (mad.lo.u32), IMAD.WIDE.U32 (mad.wide.u32) and
+ * IMAD.HI.U32 (mad.hi.u32) per second, register-only instruction streams. */
+int hc_imad_peak(hc_ctx* h, double* ops_per_s);
 /* Transform microbenchmark: njobs plain NTTs (dir 0) or INTTs (dir 1) per
  * launch, iters back-to-back launches; writes microseconds per launch. */
 int hc_bench_xform(hc_ctx* h, int njobs, int dir, int iters, double* us_per_launch);

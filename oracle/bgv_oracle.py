@@ -388,24 +388,33 @@ class OracleBgv:
         pk_b = self.pointwise(pe_ntt, self.pointwise(pk_a, s_ntt, L, "mul"), L, "sub")
 
         D = self.digits[L]
+        # deep protocol chains (L > 4): keep the slice levels <= 3 read (first
+        # D_3 pairs on the 4 smallest primes, _KskPair.at_level bgv.py:304-312)
+        # while drawing every pair's samples in the reference's order
+        kl = 3 if L > 4 else L
+        dk = self.digits[3] if L > 4 else D
+        s_k = np.ascontiguousarray(s_ntt[: kl + 1])
 
         def make_ksk(target_res: np.ndarray) -> np.ndarray:
-            target_ntt = self.fwd(target_res, L)
-            ksk = np.empty((D, 2, L + 1, n), dtype=np.uint64)
+            target_ntt = self.fwd(np.ascontiguousarray(target_res[: kl + 1]), kl)
+            ksk = np.empty((dk, 2, kl + 1, n), dtype=np.uint64)
             for j in range(D):
-                a_j = self.sample_uniform_ntt(L)
+                vals = [self.rng.randrange(self.moduli[L]) for _ in range(n)]  # a_j (bgv.py:412-414)
                 e_j = self.sample_cbd()
-                pej = self.fwd(self.small_residues(np.asarray(e_j) * p, L), L)
-                shift = np.array([pow(2, 16 * j, int(q)) for q in self.q], dtype=np.uint64)
-                sh_t = self.pointwise(target_ntt, np.repeat(shift[:, None], n, axis=1), L, "mul")
+                if j >= dk:
+                    continue
+                a_j = self.residues(vals, kl)
+                pej = self.fwd(self.small_residues(np.asarray(e_j) * p, kl), kl)
+                shift = np.array([pow(2, 16 * j, int(q)) for q in self.q[: kl + 1]], dtype=np.uint64)
+                sh_t = self.pointwise(target_ntt, np.repeat(shift[:, None], n, axis=1), kl, "mul")
                 b_j = self.pointwise(
-                    self.pointwise(pej, self.pointwise(a_j, s_ntt, L, "mul"), L, "sub"), sh_t, L, "add"
+                    self.pointwise(pej, self.pointwise(a_j, s_k, kl, "mul"), kl, "sub"), sh_t, kl, "add"
                 )
                 ksk[j, 0] = b_j
                 ksk[j, 1] = a_j
             return ksk
 
-        s_sq = self.inv(self.pointwise(s_ntt, s_ntt, L, "mul"), L)  # residues of [0,Q) ints
+        s_sq = self.inv(self.pointwise(s_k, s_k, kl, "mul"), kl)  # residues of [0,Q) ints
         relin = make_ksk(s_sq)
         two_n = 2 * n
         rot = {}
@@ -413,11 +422,11 @@ class OracleBgv:
             if r == 0:
                 continue
             t = pow(3, r, two_n)
-            rot[r] = (t, make_ksk(self.small_residues(self.coeff_automorphism(s, t), L)))
+            rot[r] = (t, make_ksk(self.small_residues(self.coeff_automorphism(s, t), kl)))
         col = None
         if col_swap:
             t = two_n - 1
-            col = (t, make_ksk(self.small_residues(self.coeff_automorphism(s, t), L)))
+            col = (t, make_ksk(self.small_residues(self.coeff_automorphism(s, t), kl)))
         key_id = self.rng.getrandbits(128).to_bytes(16, "little")
         return OKeys(key_id, s, pk_b, pk_a, relin, rot, col)
 
@@ -462,6 +471,37 @@ class OracleBgv:
 
     # -- level plumbing (bgv.py:579-647) ------------------------------------------
 
+    def _rescale_deep(self, res: np.ndarray, level: int) -> np.ndarray:
+        """bgv.py:592-603 literally on Python integers for levels past the C
+        oracle's 4-limb compose: x = CRT(res), r = centred(x mod q),
+        y = (x - r) / q, d = centred_p((x - y) mod p), out = (y + d) mod Q_{l-1}."""
+        primes = [int(q) for q in self.q[: level + 1]]
+        Q = self.moduli[level]
+        q = primes[level]
+        p = self.p
+        coef = []
+        for k, qk in enumerate(primes):
+            Mk = Q // qk
+            coef.append(Mk * pow(Mk, -1, qk))
+        rows = [res[k].tolist() for k in range(level + 1)]
+        out = np.empty((level, self.n), dtype=np.uint64)
+        Qn = self.moduli[level - 1]
+        ys = []
+        for j in range(self.n):
+            x = sum(int(rows[k][j]) * coef[k] for k in range(level + 1)) % Q
+            r = x % q
+            if r > q // 2:
+                r -= q
+            y = (x - r) // q
+            d = (x - y) % p
+            if d > p // 2:
+                d -= p
+            ys.append((y + d) % Qn)
+        for k in range(level):
+            qk = primes[k]
+            out[k] = np.array([v % qk for v in ys], dtype=np.uint64)
+        return out
+
     def mod_switch(self, c: np.ndarray, noise: float, level: int):
         """_mod_switch_once: INTT mod Q_l, rescale (orc_rescale), NTT mod Q_{l-1}."""
         coeffs = self.inv(c, level)  # [2][l+1][n]
@@ -469,6 +509,9 @@ class OracleBgv:
         qv = np.asarray(self.q[: level + 1], dtype=np.uint64)
         for i in range(2):
             src = np.ascontiguousarray(coeffs[i])
+            if level > 4:
+                out[i] = self._rescale_deep(src, level)
+                continue
             dst = np.empty((level, self.n), dtype=np.uint64)
             lib().orc_rescale(_p(src), _p(dst), level + 1, self.n, _p(qv), self.p)
             out[i] = dst

@@ -65,10 +65,19 @@ CASES = {
     "answer_small_n64_N200_s5": (64, 257, 200, 5, 14, True),
     "answer_c1_N8192_s8": (8192, 65537, 8192, 8, 6, False),
     "answer_c2_N16384_s16": (8192, 65537, 16384, 16, 7, False),
+    # answer() on the protocol's own chain: max_level = pdq.protocol_max_level(p)
+    # = 21 (pdq.py:181-184; Match's depth 17 + mask + 3), 22 primes.  The index
+    # vector is encrypted at level 21 and brought to level 4 -- where Match
+    # leaves it -- by the backend's own _at_level (bgv.py:610-614), then
+    # pdq.mask and comp run exactly as in pdq.answer (pdq.py:248-256)
+    "answer_deep_c1_N8192_s8": (8192, 65537, 8192, 8, 8, False),
 }
 
 # max_level per case (default 3, the BASELINE chain)
-MAX_LEVEL = {"answer_small_n64_N200_s5": 4, "answer_c1_N8192_s8": 4, "answer_c2_N16384_s16": 4}
+MAX_LEVEL = {"answer_small_n64_N200_s5": 4, "answer_c1_N8192_s8": 4, "answer_c2_N16384_s16": 4,
+             "answer_deep_c1_N8192_s8": 21}
+# level the index vector enters Mask at (Match's output level on the protocol chain)
+ANSWER_LEVEL = {"answer_deep_c1_N8192_s8": 4}
 
 
 def masked_payload(N, s, p, seed):
@@ -104,6 +113,22 @@ def keys_residues(be, keys):
             out.append(residues_of(a, primes))
 
     ksk(keys.relin_key)
+    for r in sorted(keys.rotation_keys):
+        ksk(keys.rotation_keys[r][1])
+    if keys.col_swap_key is not None:
+        ksk(keys.col_swap_key[1])
+    return out
+
+
+def keys_residues_low(be, keys, levels=4, digits=14):
+    primes = [be.chain.level_prime(k) for k in range(levels)]
+    out = []
+
+    def ksk(k):
+        for b, a in k.pairs[:digits]:
+            out.append(residues_of(b, primes))
+            out.append(residues_of(a, primes))
+
     for r in sorted(keys.rotation_keys):
         ksk(keys.rotation_keys[r][1])
     if keys.col_swap_key is not None:
@@ -150,6 +175,8 @@ def run_case(name):
         for i in support:
             dense[i - 1] = db[i - 1]
         hint = encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+        if name in ANSWER_LEVEL:
+            hint = [be._at_level(c, ANSWER_LEVEL[name]) for c in hint]
         m0 = be.counters.snapshot()
         cts = pdq.mask(hint, types.SimpleNamespace(values=db), params, be, keys)
         mask_counters = be.counters.delta(m0).as_dict()
@@ -219,7 +246,10 @@ def run_case(name):
         "noise_bits": out.payload.noise_bits,
         "out_level": out.level,
         "counters": delta.as_dict(),
-        "keys_sha256": digest_arrays(keys_residues(be, keys)),
+        "keys_sha256": digest_arrays(keys_residues(be, keys)) if L <= 4 else None,
+        # deep chains: the key digits levels <= 3 use (_KskPair.at_level,
+        # bgv.py:304-312) -- first 14 pairs on the 4 smallest primes
+        "keys_low_sha256": digest_arrays(keys_residues_low(be, keys)) if L > 4 else None,
         "cts_sha256": digest_arrays([ct_residues(be, c) for c in cts]),
         "hint_sha256": digest_arrays([ct_residues(be, c) for c in hint]),
         "out_sha256": digest_arrays([ct_residues(be, out)]),

@@ -18,6 +18,7 @@ from .params import BackendMismatch, LevelExhausted, MissingRotationKey
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HCOMP_LIB") or os.path.join(_HERE, "libhcomp.so")  # max_level <= 3
 LIB5_PATH = os.environ.get("HCOMP_LIB5") or os.path.join(_HERE, "libhcomp_l4.so")  # max_level 4
+LIBDEEP_PATH = os.environ.get("HCOMP_LIBDEEP") or os.path.join(_HERE, "libhcomp_deep.so")  # max_level 5..22
 
 HC_OK = 0
 HC_ERR_ARG = 1
@@ -48,6 +49,7 @@ _SIGS = [
     ("hc_ctx_digits", _I, [_P, _P]),
     ("hc_load_ksk", _I, [_P, _U32, _P]),
     ("hc_clear_keys", _I, [_P]),
+    ("hc_load_ksk_slice", _I, [_P, _U32, _P, _I, _I]),
     ("hc_plan", _I, [_P, _I64, _I, _I]),
     ("hc_plan_masked", _I, [_P, ctypes.c_int64, _I, _I, _P]),
     ("hc_plan_range", _I, [_P, _I64, _I, _I, _I64, _I64]),
@@ -73,10 +75,12 @@ _SIGS = [
     ("hc_ntt", _I, [_P, _P, _I, _P, _I]),
     ("hc_pointwise", _I, [_P, _P, _P, _P, _I, _P, _I]),
     ("hc_mul_plain", _I, [_P, _P, _I, _P, _P]),
+    ("hc_decrypt", _I, [_P, _P, _I, _P, _P]),
     ("hc_rotate", _I, [_P, _P, _I, _U32, _P]),
     ("hc_comp_profile", _I, [_P, _P, _I, _P, _P, _P]),
     ("hc_bf_peak", _I, [_P, ctypes.POINTER(ctypes.c_double)]),
     ("hc_bench_xform", _I, [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_double)]),
+    ("hc_imad_peak", _I, [_P, _P]),
     ("hc_set_cluster_threshold", _I, [_I]),
     ("hc_set_lane_blocks", _I, [_I]),
     ("hc_set_vt2_jobs", _I, [_I]),
@@ -99,7 +103,7 @@ def lib(max_level: int = 3):
     """Load the CUDA library for chains up to max_level + 1 primes (raises if
     it has not been built).  Both builds export the same C ABI."""
     global _last
-    path = LIB_PATH if max_level <= 3 else LIB5_PATH
+    path = LIB_PATH if max_level <= 3 else LIB5_PATH if max_level == 4 else LIBDEEP_PATH
     L = _libs.get(path)
     if L is None:
         if not os.path.exists(path):

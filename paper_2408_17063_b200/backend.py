@@ -311,8 +311,8 @@ class B200BgvBackend:
         params = he_params(params)  # an hcpdq HeParams passes through
         if params.n != 8192:
             raise ValueError("the B200 backend supports n = 8192 only")
-        if not (1 <= params.max_level <= 4):
-            raise ValueError("the B200 backend supports max_level 1..4")
+        if not (1 <= params.max_level <= 22):
+            raise ValueError("the B200 backend supports max_level 1..22")
         if ksw_base_bits != 16:
             raise ValueError("ksw_base_bits must be 16")
         self.params = params
@@ -472,27 +472,40 @@ class B200BgvBackend:
         pe_ntt = self.ntt(self.small_residues(p * e, L), L)
         pk_b = self.pointwise(pe_ntt, self.pointwise(pk_a, s_ntt, L, "mul"), L, "sub")
         D = self.digits[L]
+        # Deep protocol chains (max_level > 4: 75 digits x 22 primes at level 21)
+        # keep only the key slice key switching ever reads -- the first D_3
+        # digits on the 4 smallest primes (_KskPair.at_level at levels <= 3,
+        # bgv.py:304-312) -- while every digit's samples are still drawn, so
+        # the random stream, key_id and all later encryptions stay the
+        # reference's.  Shallow chains keep the whole key.
+        deep = L > 4
+        kl = 3 if deep else L  # key rows 0..kl (level order)
+        dk = self.digits[3] if deep else D
+        s_k = s_ntt[: kl + 1]
 
         def make_ksk(target_res: np.ndarray) -> np.ndarray:
-            target_ntt = self.ntt(target_res, L)
-            ksk = np.empty((D, 2, L + 1, n), dtype=np.uint64)
-            pe = np.empty((D, L + 1, n), dtype=np.uint64)
+            target_ntt = self.ntt(target_res[: kl + 1], kl)
+            ksk = np.empty((dk, 2, kl + 1, n), dtype=np.uint64)
+            pe = np.empty((dk, kl + 1, n), dtype=np.uint64)
             for j in range(D):  # the reference's sampling order: a_j then e_j
-                ksk[j, 1] = self._sample_uniform_ntt(L)
-                pe[j] = self.small_residues(p * self._sample_cbd(), L)
-            ksk[:, 0] = self.ntt(pe, L)  # p*e_j in one batched transform, finished below
+                a_j = self._rng.uniform(n, self.moduli[L], self.q[: kl + 1])  # randrange(Q_L) residues
+                e_j = self._sample_cbd()
+                if j < dk:
+                    ksk[j, 1] = a_j
+                    pe[j] = self.small_residues(p * e_j, kl)
+            ksk[:, 0] = self.ntt(pe, kl)  # p*e_j in one batched transform, finished below
             # b_j = p e_j - a_j s + 2^(16 j) t  (bgv.py:488-493), batched on the GPU
             shifts = np.array(
-                [[pow(2, self.w * j, int(q)) for q in self.q] for j in range(D)], dtype=np.uint64
+                [[pow(2, self.w * j, int(q)) for q in self.q[: kl + 1]] for j in range(dk)], dtype=np.uint64
             )
             shift_t = self.pointwise(
-                np.broadcast_to(target_ntt, (D, L + 1, n)), np.repeat(shifts[:, :, None], n, axis=2), L, "mul"
+                np.broadcast_to(target_ntt, (dk, kl + 1, n)), np.repeat(shifts[:, :, None], n, axis=2), kl, "mul"
             )
-            a_s = self.pointwise(ksk[:, 1], np.broadcast_to(s_ntt, (D, L + 1, n)), L, "mul")
-            ksk[:, 0] = self.pointwise(self.pointwise(ksk[:, 0], a_s, L, "sub"), shift_t, L, "add")
+            a_s = self.pointwise(ksk[:, 1], np.broadcast_to(s_k, (dk, kl + 1, n)), kl, "mul")
+            ksk[:, 0] = self.pointwise(self.pointwise(ksk[:, 0], a_s, kl, "sub"), shift_t, kl, "add")
             return ksk
 
-        s_sq = self.ntt(self.pointwise(s_ntt, s_ntt, L, "mul"), L, inverse=True)
+        s_sq = self.ntt(self.pointwise(s_k, s_k, kl, "mul"), kl, inverse=True)
         relin = make_ksk(s_sq)
         two_n = 2 * n
         rot_keys = {}
@@ -500,11 +513,11 @@ class B200BgvBackend:
             if r == 0:
                 continue
             t = pow(3, r, two_n)
-            rot_keys[r] = (t, make_ksk(self.small_residues(self._coeff_automorphism(s, t), L)))
+            rot_keys[r] = (t, make_ksk(self.small_residues(self._coeff_automorphism(s, t), kl)))
         col_key = None
         if col_swap:
             t = two_n - 1
-            col_key = (t, make_ksk(self.small_residues(self._coeff_automorphism(s, t), L)))
+            col_key = (t, make_ksk(self.small_residues(self._coeff_automorphism(s, t), kl)))
         return KeySet(
             backend_id=self.backend_id,
             params=params,
@@ -544,6 +557,12 @@ class B200BgvBackend:
         if keys.secret is None:
             raise BackendMismatch("decryption requires the secret key")
         l = c.level
+        if l <= 3:  # one device call: phase, INTT, CRT lift, centring, slot decode (hc_decrypt)
+            ct = np.ascontiguousarray(c.payload.res, dtype=np.uint64)
+            sec = np.ascontiguousarray(keys.secret, dtype=np.int64)
+            rows = np.empty((2, self.params.slots), dtype=np.int64)
+            _lib.check(_lib.lib(self.params.max_level).hc_decrypt(self._ctx(), _lib.ptr(ct), l, _lib.ptr(sec), _lib.ptr(rows)))
+            return SlotMatrix(self.params.p, rows)
         s_ntt = self.ntt(self.small_residues(keys.secret, l), l)
         res = c.payload.res
         phase = self.ntt(self.pointwise(res[0], self.pointwise(res[1], s_ntt, l, "mul"), l, "add"), l, inverse=True)
@@ -638,8 +657,8 @@ class B200BgvBackend:
         if keys.col_swap_key is not None:
             entries.append(keys.col_swap_key)
         for t, ksk in entries:
-            arr = np.ascontiguousarray(ksk, dtype=np.uint64)
-            _lib.check(L.hc_load_ksk(h, int(t), _lib.ptr(arr)))
+            arr = np.ascontiguousarray(ksk, dtype=np.uint64)  # [digits][2][rows][n]
+            _lib.check(L.hc_load_ksk_slice(h, int(t), _lib.ptr(arr), arr.shape[0], arr.shape[2]))
         self._loaded_keys = keys
         self._planned = None
 

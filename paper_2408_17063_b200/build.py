@@ -14,9 +14,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhcomp.so")  # chains of up to 4 primes (max_level <= 3: every BASELINE config)
 LIB5 = os.path.join(HERE, "libhcomp_l4.so")  # the same sources for 5-prime chains (max_level 4: answer())
+# pdq's protocol chain (protocol_max_level = 21, CLI default 22): deep levels
+# carry ring transforms and mul_plain only; Comp runs at levels <= 4
+LIBDEEP = os.path.join(HERE, "libhcomp_deep.so")
 # The 5-prime build's larger device context costs ~1% at the headline (measured
 # A/B, tools/ab_old_new.sh), so each chain length gets its own build.
-LIBS = {LIB: 3, LIB5: 4}
+LIBS = {LIB: 3, LIB5: 4, LIBDEEP: 22}
 SELFTEST = os.path.join(HERE, "libhcomp_hosttest.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -11,10 +11,16 @@ namespace hc {
 // pack-pair products of answer() (pdq.py:238-256) down to level 3, so CRT
 // compose, digit decomposition and key switching stop at level 3 (KEYL).
 #ifndef HC_MAXL
-#define HC_MAXL 4  // build.py compiles -DHC_MAXL=3 (libhcomp.so) and 4 (libhcomp_l4.so)
+#define HC_MAXL 4  // build.py compiles -DHC_MAXL=3 (libhcomp.so), 4 (libhcomp_l4.so), 22 (libhcomp_deep.so)
 #endif
 constexpr int MAXL = HC_MAXL;  // max level supported (MAXL + 1 chain primes)
 constexpr int KEYL = MAXL < 3 ? MAXL : 3;        // highest level with device key switching / CRT compose
+// levels with a LevelC entry: the Comp's levels (<= 4).  Deeper levels of a
+// protocol chain (pdq.protocol_max_level = 21) only carry ring transforms and
+// the modulus switch of mul_plain, whose per-prime constants travel with the
+// call (hcomp.cu, mul_plain_deep) -- the context passed by value to every
+// kernel stays small.
+constexpr int LVC = MAXL < 4 ? MAXL : 4;
 constexpr int NPR = MAXL + 2;  // chain primes + plaintext prime p (index 5)
 constexpr int PIDX = MAXL + 1; // RNS index of p in the tables
 constexpr int NLIMB = 4;       // limbs for composed integers (216 bits: levels <= KEYL)
@@ -49,7 +55,7 @@ struct DevCtx {
     int L;    // max level
     int KL1;  // RNS rows per key digit on the device: min(L, KEYL) + 1
     PrimeC pc[NPR];
-    LevelC lvs[MAXL];  // levels 1..MAXL (kernel parameter space: no level-0 entry)
+    LevelC lvs[LVC];  // levels 1..LVC (kernel parameter space: no level-0 entry)
     HD const LevelC& lv(int l) const { return lvs[l - 1]; }
 };
 

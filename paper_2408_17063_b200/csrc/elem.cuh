@@ -155,6 +155,18 @@ HD RescaleKT<NQ> rescale_consts(const DevCtx& D, int l) {
     return R;
 }
 
+// the constants rescale_rd reads, at any level (deep protocol chains: no LevelC)
+HD RescaleK rescale_consts_rd(const DevCtx& D, int l) {
+    RescaleK R;
+    R.l = l;
+    R.ql = D.pc[l].q;
+    R.half_qd = D.pc[l].q >> 1;
+    R.p = D.p;
+    R.half_p = D.half_p;
+    R.pbar = D.pbar;
+    return R;
+}
+
 // x = canonical residue of the coefficient modulo the dropped prime q_l;
 // writes e_k for k < l.
 template <int NQ>

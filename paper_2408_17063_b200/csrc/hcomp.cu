@@ -179,7 +179,7 @@ struct hc_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
     std::map<uint32_t, DevKey> keys;
     std::unique_ptr<Plan> plan;
-    int digits[MAXL + 1] = {0, 0, 0, 0};
+    int digits[MAXL + 1] = {};
 };
 
 static void release_key(DevKey& k) {
@@ -276,7 +276,8 @@ static int configure_kernels() {
 extern "C" int hc_ctx_create(int n, int max_level, const uint64_t* primes, uint64_t p, int ksw_base_bits,
                              int device, hc_ctx** out) {
     if (n != NPOLY) return fail(HC_ERR_ARG, "only n = 8192 is supported");
-    if (max_level < 1 || max_level > MAXL) return fail(HC_ERR_ARG, "max_level must be 1..4");
+    if (max_level < 1 || max_level > MAXL)
+        return fail(HC_ERR_ARG, "max_level must be 1.." + std::to_string(MAXL) + " for this build");
     if (ksw_base_bits != 16) return fail(HC_ERR_ARG, "only ksw_base_bits = 16 is supported");
     if (p >= (1ull << 31) || p % (2 * (u64)n) != 1) return fail(HC_ERR_ARG, "bad plaintext modulus");
     for (int k = 0; k <= max_level; k++) {
@@ -337,8 +338,16 @@ extern "C" int hc_clear_keys(hc_ctx* h) {
     return HC_OK;
 }
 
+static int load_ksk_impl(hc_ctx* h, uint32_t t, const uint64_t* ksk, int dig_have, int rows_have);
 extern "C" int hc_load_ksk(hc_ctx* h, uint32_t t, const uint64_t* ksk) {
     if (!h || !ksk) return fail(HC_ERR_ARG, "null argument");
+    return load_ksk_impl(h, t, ksk, h->digits[h->L], h->L + 1);
+}
+extern "C" int hc_load_ksk_slice(hc_ctx* h, uint32_t t, const uint64_t* ksk, int digits, int rows) {
+    if (!h || !ksk) return fail(HC_ERR_ARG, "null argument");
+    return load_ksk_impl(h, t, ksk, digits, rows);
+}
+static int load_ksk_impl(hc_ctx* h, uint32_t t, const uint64_t* ksk, int dig_have, int rows_have) {
     if ((t & 1) == 0 || t >= 2u * NPOLY) return fail(HC_ERR_ARG, "galois element must be odd and < 2n");
     CU(cudaSetDevice(h->dev));
     auto it = h->keys.find(t);
@@ -353,14 +362,19 @@ extern "C" int hc_load_ksk(hc_ctx* h, uint32_t t, const uint64_t* ksk) {
     // digits and primes key switching uses (levels <= KEYL): at max_level 4
     // the first 14 digits on the 4 smallest primes (_KskPair.at_level,
     // bgv.py:304-312, reduces exactly that way).
-    const int L1 = h->L + 1, D = h->digits[h->L];
+    // ksk: [dig_have][2][rows_have][n] (rows in level order); the device keeps
+    // the first DK digits on the KL1 smallest primes
+    const int L1 = rows_have;
     const int KL1 = h->hctx.KL1, DK = h->digits[KL1 - 1];
+    if (dig_have < DK || rows_have < KL1) {
+        release_key(k);
+        return fail(HC_ERR_ARG, "key-switch key slice smaller than the device's levels need");
+    }
     const size_t rows = (size_t)DK * 2 * KL1;
     CU(cudaMalloc(&k.key, rows * NPOLY * 8));
     if (KL1 == L1) {
         CU(cudaMemcpyAsync(k.key, ksk, rows * NPOLY * 8, cudaMemcpyHostToDevice, h->stream));
     } else {
-        (void)D;
         for (int d = 0; d < DK; d++)
             for (int ab = 0; ab < 2; ab++)
                 CU(cudaMemcpyAsync(k.key + ((size_t)d * 2 + ab) * KL1 * NPOLY, ksk + ((size_t)d * 2 + ab) * L1 * NPOLY,
@@ -2196,6 +2210,178 @@ extern "C" int hc_pointwise(hc_ctx* h, const uint64_t* a, const uint64_t* b, uin
     return HC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// decrypt (bgv.py:559-575) on the device: phase = c0 + c1 s (NTT domain),
+// INTT, the exact integer in [0, Q_l) (CRT compose), centred, reduced mod p,
+// slot_decode (NTT mod p + slot gather, bgv.py:387-394)
+// ---------------------------------------------------------------------------
+// s (ternary, int64) -> residues [l+1][n]
+__global__ void k_ternary_res(const __grid_constant__ DevCtx C, const int64_t* s, int P1, u64* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (j >= NPOLY || k >= P1) return;
+    const int64_t v = s[j];
+    const u64 q = C.pc[k].q;
+    out[(size_t)k * NPOLY + j] = v >= 0 ? (u64)v : q - (u64)(-v);
+}
+// phase = c0 + c1 * s_ntt per prime (canonical residues)
+__global__ void k_phase(const __grid_constant__ DevCtx C, const u64* ct, const u64* sn, int P1, u64* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (j >= NPOLY || k >= P1) return;
+    const PrimeC& P = C.pc[k];
+    const size_t o = (size_t)k * NPOLY + j;
+    // c1 * s mod q: Montgomery product then * R (Shoup) back to the plain residue
+    u64 hi, lo;
+    mul128(hi, lo, ct[(size_t)P1 * NPOLY + o], sn[o]);
+    const u64 m = mul_shoup(redc(hi, lo, P.q, P.qneg), P.rmod, P.rmod_s, P.q);
+    out[o] = add_mod(ct[o], m, P.q);
+}
+// coefficient residues [l+1][n] -> centred integer mod p  (l <= KEYL)
+template <int L>
+__device__ __forceinline__ u64 lift_one(const DevCtx& C, const u64* x, int j) {
+    u64 X[NLIMB];
+    if constexpr (L == 0) {
+        X[0] = x[j];
+        X[1] = X[2] = X[3] = 0;
+    } else {
+        u64 xr[L + 1];
+        HC_UNROLL
+        for (int k = 0; k <= L; k++) xr[k] = x[(size_t)k * NPOLY + j];
+        crt_compose<L>(C.lv(L), C.pc, xr, X);
+    }
+    // Q_l and X as limbs; centred: X > Q/2 -> X - Q (negative)
+    u64 Q[NLIMB];
+    if constexpr (L == 0) {
+        Q[0] = C.pc[0].q;
+        Q[1] = Q[2] = Q[3] = 0;
+    } else {
+        HC_UNROLL
+        for (int i = 0; i < NLIMB; i++) Q[i] = C.lv(L).Q[i];
+    }
+    // X > floor(Q / 2)  <=>  2X > Q  (X < Q < 2^216, so 2X fits 4 limbs)
+    u64 X2[NLIMB];
+    u64 carry = 0;
+    HC_UNROLL
+    for (int i = 0; i < NLIMB; i++) {
+        X2[i] = (X[i] << 1) | carry;
+        carry = X[i] >> 63;
+    }
+    int gt = 0, decided = 0;
+    HC_UNROLL
+    for (int i = NLIMB - 1; i >= 0; i--) {
+        if (!decided && X2[i] != Q[i]) {
+            gt = X2[i] > Q[i];
+            decided = 1;
+        }
+    }
+    const u64 p = C.p;
+    auto modp = [&](const u64 (&V)[NLIMB]) {
+        unsigned __int128 acc = 0;
+        HC_UNROLL
+        for (int i = NLIMB - 1; i >= 0; i--) acc = ((acc << 64) | V[i]) % p;
+        return (u64)acc;
+    };
+    const u64 xm = modp(X);
+    if (!gt) return xm;
+    const u64 qm = modp(Q);
+    return xm >= qm ? xm - qm : xm + p - qm;  // (X - Q) mod p
+}
+__global__ void k_lift(const __grid_constant__ DevCtx C, const u64* x, int level, u64* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= NPOLY) return;
+    u64 v = 0;
+    switch (level) {
+        case 0: v = lift_one<0>(C, x, j); break;
+        case 1: v = lift_one<1>(C, x, j); break;
+        case 2: v = lift_one<2>(C, x, j); break;
+        default: v = lift_one<KEYL>(C, x, j); break;
+    }
+    out[j] = v;
+}
+// evaluations mod p (NTT index order) -> slot matrix [2][n/2]
+__global__ void k_slot_gather(const __grid_constant__ DevCtx C, const u64* ev, int64_t* rows) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= NPOLY) return;
+    const unsigned so = C.slot_of[j];
+    rows[(size_t)(so >> 12) * (NPOLY / 2) + (so & 4095)] = (int64_t)ev[j];
+}
+
+extern "C" int hc_decrypt(hc_ctx* h, const uint64_t* ct, int level, const int64_t* secret, int64_t* slots) {
+    if (!h || !ct || !secret || !slots) return fail(HC_ERR_ARG, "null argument");
+    if (level < 0 || level > KEYL || level > h->L) return fail(HC_ERR_ARG, "device decrypt takes levels 0..3");
+    CU(cudaSetDevice(h->dev));
+    const int P1 = level + 1;
+    const size_t NB = NPOLY;
+    DevBuf dct, ds, dsn, dph, dlift, drows;
+    CU(cudaMalloc(&dct.p, (size_t)2 * P1 * NB * 8));
+    CU(cudaMalloc(&ds.p, NB * 8));
+    CU(cudaMalloc(&dsn.p, (size_t)P1 * NB * 8));
+    CU(cudaMalloc(&dph.p, (size_t)P1 * NB * 8));
+    CU(cudaMalloc(&dlift.p, NB * 8));
+    CU(cudaMalloc(&drows.p, NB * 8));
+    CU(cudaMemcpyAsync(dct.p, ct, (size_t)2 * P1 * NB * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(ds.p, secret, NB * 8, cudaMemcpyHostToDevice, h->stream));
+    k_ternary_res<<<dim3(NB / 256, P1), 256, 0, h->stream>>>(h->hctx, (const int64_t*)ds.p, P1, (u64*)dsn.p);
+    CU(cudaGetLastError());
+    {  // NTT(s) per prime
+        std::vector<XJob> jobs;
+        for (int k = 0; k < P1; k++) {
+            XJob j{};
+            j.dir = 0; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+            j.a = (u64*)dsn.p + (size_t)k * NB;
+            j.out = (u64*)dsn.p + (size_t)k * NB;
+            jobs.push_back(j);
+        }
+        Schedule S;
+        int rc = add_xf(S, jobs);
+        if (!rc) rc = enqueue(h, S, h->stream);
+        if (rc) return rc;
+        k_phase<<<dim3(NB / 256, P1), 256, 0, h->stream>>>(h->hctx, (const u64*)dct.p, (const u64*)dsn.p, P1, (u64*)dph.p);
+        CU(cudaGetLastError());
+        std::vector<XJob> inv;
+        for (int k = 0; k < P1; k++) {
+            XJob j{};
+            j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
+            j.a = (u64*)dph.p + (size_t)k * NB;
+            j.out = (u64*)dph.p + (size_t)k * NB;
+            inv.push_back(j);
+        }
+        Schedule S2;
+        rc = add_xf(S2, inv);
+        if (!rc) rc = enqueue(h, S2, h->stream);
+        if (rc) return rc;
+        k_lift<<<NB / 256, 256, 0, h->stream>>>(h->hctx, (const u64*)dph.p, level, (u64*)dlift.p);
+        CU(cudaGetLastError());
+        std::vector<XJob> fp(1);
+        fp[0].dir = 0; fp[0].k = PIDX; fp[0].ld = LD_U64; fp[0].ep = EP_STORE;
+        fp[0].a = (u64*)dlift.p;
+        fp[0].out = (u64*)dlift.p;
+        Schedule S3;
+        rc = add_xf(S3, fp);
+        if (!rc) rc = enqueue(h, S3, h->stream);
+        if (rc) return rc;
+        k_slot_gather<<<NB / 256, 256, 0, h->stream>>>(h->hctx, (const u64*)dlift.p, (int64_t*)drows.p);
+        CU(cudaGetLastError());
+    }
+    CU(cudaMemcpyAsync(slots, drows.p, NB * 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    return HC_OK;
+}
+
+// modulus-switch correction of a deep level (l > LVC): per kept prime k,
+// e_k = (d - r q_l^-1) mod q_k from the dropped prime's (r, d) integers
+// (EP_RESCALE_RD); the constants of (l, k) come in `qk` = [qinv, qinv_s]
+// grid (n/256, l, 2 polys)
+__global__ void k_deep_corr(const __grid_constant__ DevCtx C, const u64* rd, const u64* qk, int l, u64* corr) {
+    const int j = blockIdx.x * 256 + threadIdx.x;
+    const int k = blockIdx.y, poly = blockIdx.z;
+    const u64* s = rd + (size_t)poly * 2 * NPOLY;
+    const PrimeC& P = C.pc[k];
+    corr[((size_t)poly * l + k) * NPOLY + j] =
+        corr_from_sums((long long)s[j], (long long)s[NPOLY + j], P.q, qk[2 * k], qk[2 * k + 1], P.one_s);
+}
+
 extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint64_t* pt, uint64_t* out) {
     if (!h) return fail(HC_ERR_ARG, "null context");
     if (level < 1) return fail(HC_ERR_LEVEL, "plaintext multiply at level 0");
@@ -2204,12 +2390,61 @@ extern "C" int hc_mul_plain(hc_ctx* h, const uint64_t* ct, int level, const uint
     const int l = level, P1 = l + 1;
     const size_t NB = NPOLY;
     // plaintext in Montgomery form with the modulus-switch factor folded in
-    std::vector<u64> ptm((size_t)P1 * NB);
-    const LevelC& LV = h->hctx.lv(l);
+    std::vector<u64> ptm((size_t)P1 * NB), qk((size_t)2 * l);
     for (int k = 0; k <= l; k++) {
         const PrimeC& pc = h->hctx.pc[k];
-        u64 w = k == l ? pc.rmod : LV.qinv_r[k];
+        u64 w = pc.rmod;
+        if (k < l) {
+            const u64 qi = inv_mod(h->hctx.pc[l].q % pc.q, pc.q);  // q_l^-1 mod q_k
+            qk[2 * k] = qi;
+            qk[2 * k + 1] = shoup_const(qi, pc.q);
+            w = mulmod_slow(qi, pc.rmod, pc.q);
+        }
         for (size_t j = 0; j < NB; j++) ptm[k * NB + j] = mulmod_slow(pt[k * NB + j] % pc.q, w, pc.q);
+    }
+    if (l > LVC) {  // deep level of a protocol chain: (r, d) -> per-prime corrections -> NTTs
+        DevBuf dct, dpt, drd, dqk, dcorr, dout;
+        CU(cudaMalloc(&dct.p, (size_t)2 * P1 * NB * 8));
+        CU(cudaMalloc(&dpt.p, (size_t)P1 * NB * 8));
+        CU(cudaMalloc(&drd.p, (size_t)2 * 2 * NB * 8));
+        CU(cudaMalloc(&dqk.p, qk.size() * 8));
+        CU(cudaMalloc(&dcorr.p, (size_t)2 * l * NB * 8));
+        CU(cudaMalloc(&dout.p, (size_t)2 * l * NB * 8));
+        CU(cudaMemcpy(dct.p, ct, (size_t)2 * P1 * NB * 8, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dpt.p, ptm.data(), (size_t)P1 * NB * 8, cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dqk.p, qk.data(), qk.size() * 8, cudaMemcpyHostToDevice));
+        const u64* c = (const u64*)dct.p;
+        const u64* p = (const u64*)dpt.p;
+        std::vector<XJob> inv, fwd;
+        for (int poly = 0; poly < 2; poly++) {
+            XJob j{};
+            j.dir = 1; j.k = l; j.ld = LD_MONT; j.ep = EP_RESCALE_RD; j.level = l;
+            j.a = c + ((size_t)poly * P1 + l) * NB;
+            j.b = p + (size_t)l * NB;
+            j.out = (u64*)drd.p + (size_t)poly * 2 * NB;
+            j.ostride = NB;
+            inv.push_back(j);
+            for (int k = 0; k < l; k++) {
+                XJob f{};
+                f.dir = 0; f.k = k; f.ld = LD_U64; f.ep = EP_ADDMONT;
+                f.a = (u64*)dcorr.p + ((size_t)poly * l + k) * NB;
+                f.ea = c + ((size_t)poly * P1 + k) * NB;
+                f.eb = p + (size_t)k * NB;
+                f.out = (u64*)dout.p + ((size_t)poly * l + k) * NB;
+                fwd.push_back(f);
+            }
+        }
+        Schedule S1, S2;
+        int rc = add_xf(S1, inv);
+        if (!rc) rc = run_now(h, S1);
+        if (rc) return rc;
+        k_deep_corr<<<dim3(NB / 256, l, 2), 256, 0, h->stream>>>(h->hctx, (const u64*)drd.p, (const u64*)dqk.p, l, (u64*)dcorr.p);
+        CU(cudaGetLastError());
+        rc = add_xf(S2, fwd);
+        if (!rc) rc = run_now(h, S2);
+        if (rc) return rc;
+        CU(cudaMemcpy(out, dout.p, (size_t)2 * l * NB * 8, cudaMemcpyDeviceToHost));
+        return HC_OK;
     }
     DevBuf dct, dpt, dcorr, dout;
     CU(cudaMalloc(&dct.p, (size_t)2 * P1 * NB * 8));
@@ -2347,6 +2582,66 @@ extern "C" int hc_bf_peak(hc_ctx* h, double* bfly_per_s) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     *bfly_per_s = (double)blocks * 256 * iters * 16 / (ms * 1e-3);
+    return HC_OK;
+}
+
+// INT32 multiply-pipe ceilings, independent of the kernels' code: streams of
+// one instruction kind (mad.lo.u32 -> IMAD, mad.wide.u32 -> IMAD.WIDE.U32,
+// mad.hi.u32 -> IMAD.HI.U32; 8 independent accumulator chains per thread,
+// 2048 threads per SM), no memory traffic.  Writes ops/s for the three kinds.
+__global__ void __launch_bounds__(256) k_imad_peak(int mode, int iters, uint32_t seed, u64* sink) {
+    uint32_t a[8], b = seed ^ (threadIdx.x * 2654435761u), c = blockIdx.x * 40503u + 7u;
+    u64 w[8];
+    HC_UNROLL
+    for (int i = 0; i < 8; i++) {
+        a[i] = b + 977u * i;
+        w[i] = a[i];
+    }
+    if (mode == 0) {
+        for (int it = 0; it < iters; it++) {
+            HC_UNROLL
+            for (int i = 0; i < 8; i++) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(b), "r"(c));
+        }
+    } else if (mode == 1) {
+        for (int it = 0; it < iters; it++) {
+            HC_UNROLL
+            for (int i = 0; i < 8; i++) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[i]) : "r"(a[i]), "r"(b));
+        }
+    } else {
+        for (int it = 0; it < iters; it++) {
+            HC_UNROLL
+            for (int i = 0; i < 8; i++) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[i]) : "r"(b), "r"(c));
+        }
+    }
+    u64 acc = 0;
+    HC_UNROLL
+    for (int i = 0; i < 8; i++) acc ^= a[i] ^ w[i];
+    if (acc == 0x1234567ull) sink[0] = acc;
+}
+
+extern "C" int hc_imad_peak(hc_ctx* h, double* ops_per_s) {
+    if (!h || !ops_per_s) return fail(HC_ERR_ARG, "bad arguments");
+    CU(cudaSetDevice(h->dev));
+    int nsm = 0;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->dev));
+    DevBuf sink;
+    CU(cudaMalloc(&sink.p, 8));
+    const int blocks = nsm * 8, iters = 8192;
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    for (int mode = 0; mode < 3; mode++) {
+        k_imad_peak<<<blocks, 256, 0, h->stream>>>(mode, 256, 1u, (u64*)sink.p);  // warm-up
+        CU(cudaEventRecord(a, h->stream));
+        k_imad_peak<<<blocks, 256, 0, h->stream>>>(mode, iters, 1u, (u64*)sink.p);
+        CU(cudaEventRecord(b, h->stream));
+        CU(cudaEventSynchronize(b));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, a, b));
+        ops_per_s[mode] = (double)blocks * 256 * iters * 8 / (ms * 1e-3);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
     return HC_OK;
 }
 
@@ -2498,15 +2793,26 @@ extern "C" int hc_rng_cbd(hc_rng* r, int n, int k, int64_t* out) {
 // [randrange(Q) for _ in range(n)] reduced mod each prime: out[np][n]
 extern "C" int hc_rng_uniform(hc_rng* r, int n, const uint32_t* q, int nw, int kbits, const uint64_t* primes, int np,
                               uint64_t* out) {
-    if (!r || n < 0 || !q || nw < 1 || nw > 16 || kbits < 1 || kbits > 32 * nw || !primes || np < 1 || !out)
+    if (!r || n < 0 || !q || nw < 1 || nw > 48 || kbits < 1 || kbits > 32 * nw || !primes || np < 1 || !out)
         return fail(HC_ERR_ARG, "bad arguments");
-    uint32_t w[16];
+    uint32_t w[48];
+    // 2^(32 j) mod q_k: a draw's residue is sum_j w_j (2^(32 j) mod q_k) with
+    // one reduction (48 terms < 2^86 each stay below 2^92)
+    std::vector<uint64_t> pw((size_t)np * nw);
+    for (int k = 0; k < np; k++) {
+        unsigned __int128 v = 1;
+        for (int j = 0; j < nw; j++) {
+            pw[(size_t)k * nw + j] = (uint64_t)v;
+            v = (v << 32) % primes[k];
+        }
+    }
     for (int i = 0; i < n; i++) {
         r->mt.randbelow_words(q, nw, kbits, w);
         for (int k = 0; k < np; k++) {
             unsigned __int128 acc = 0;
-            for (int j = nw - 1; j >= 0; j--) acc = ((acc << 32) | w[j]) % primes[k];
-            out[(size_t)k * n + i] = (uint64_t)acc;
+            const uint64_t* pk = &pw[(size_t)k * nw];
+            for (int j = 0; j < nw; j++) acc += (unsigned __int128)w[j] * pk[j];
+            out[(size_t)k * n + i] = (uint64_t)(acc % primes[k]);
         }
     }
     return HC_OK;

@@ -121,14 +121,15 @@ static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<T
     }
     D.KL1 = std::min(max_level, KEYL) + 1;
     for (int l = 0; l <= max_level; l++) {
-        LevelC scratch;  // level 0: digit count only (nothing switches from or composes at level 0)
-        LevelC& C = l ? D.lvs[l - 1] : scratch;
+        LevelC scratch;  // level 0 and levels > LVC: digit count only
+        LevelC& C = (l && l <= LVC) ? D.lvs[l - 1] : scratch;
         C.P = l + 1;
         C.nlimb = l + 1;
         u64 Qw[MAXL + 1] = {1};  // Q_l over l+1 limbs (digit count at every level)
         for (int k = 0; k <= l; k++) limbs_mul(Qw, MAXL + 1, primes[k]);
         C.D = (bitlen_limbs(Qw, MAXL + 1) + 15) / 16;
         digits_out[l] = C.D;
+        if (l > LVC) continue;  // deep protocol levels: digit count only (no LevelC)
         C.half_qd = primes[l] >> 1;
         for (int k = 0; k < l; k++) {
             u64 qi = inv_mod(primes[l], primes[k]);

@@ -295,7 +295,7 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
         for (int e = 0; e < N; e++)
             J.out[j0 + e * stride] = add_mod(x[e], EP == EP_ADD ? a[e] : red64(a[e], P.q, P.one_s), P.q);
     } else if constexpr (EP == EP_RESCALE_RD) {
-        const RescaleK R = rescale_consts(D, J.level);
+        const RescaleK R = rescale_consts_rd(D, J.level);
         HC_UNROLL
         for (int e = 0; e < N; e++) {
             long long r, d;
@@ -304,7 +304,7 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
             J.out[J.ostride + j0 + e * stride] = (u64)d;
         }
     } else if constexpr (EP == EP_RESCALE || EP == EP_RESCALE4) {
-        constexpr int NQ = EP == EP_RESCALE4 ? MAXL : KEYL;
+        constexpr int NQ = EP == EP_RESCALE4 ? LVC : KEYL;
         const int l = J.level;
         const RescaleKT<NQ> R = rescale_consts<NQ>(D, l);
         HC_UNROLL

@@ -228,3 +228,24 @@ def test_shared_plan_queries_vs_oracle(pkg, oracle):
     for seed, out in zip((200, 201), outs):
         _, oout = _oracle_answer(O, N, s, p, seed)
         assert np.array_equal(out, oout.c), f"seed {seed}"
+
+
+def test_device_decrypt_vs_oracle_every_level(pkg, oracle):
+    """hc_decrypt (phase, INTT, CRT lift, centring, slot decode in one device
+    call) against the oracle's decrypt (bgv.py:559-575) at levels 3, 2, 1, 0."""
+    P, O = pkg, oracle
+    be, params, keys, dense, cts, hint = _gpu_case(P, O, 8192, 8, 65537, 31)
+    obe = O.OracleBgv(8192, 65537, 3, seed=31, check_noise=False)
+    okeys = obe.keygen(*O.plan_rotation_amounts(8, 8192))
+    octs = O.encrypt_vector(dense, 8192, obe, okeys)
+    rows = np.random.default_rng(2).integers(0, 65537, (2, 4096)).astype(np.int64)
+    m = P.SlotMatrix(65537, rows)
+    cur, ocur = cts[0], octs[0]
+    for lvl in (3, 2, 1, 0):
+        assert cur.level == lvl
+        got = be.decrypt(cur, keys).rows
+        want = obe.decrypt(ocur, okeys)
+        assert np.array_equal(np.asarray(got, dtype=np.int64), np.asarray(want, dtype=np.int64)), f"level {lvl}"
+        if lvl:
+            cur = be.mul_plain(cur, m)
+            ocur = obe.mul_plain(ocur, rows)

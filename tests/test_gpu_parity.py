@@ -204,6 +204,9 @@ def test_answer_mask_then_comp_matches_reference_golden(pkg, oracle, name):
     assert keys.key_id.hex() == g["key_id"]
     support, db, dense = O.masked_payload(N, s, p, seed)
     hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    # deep protocol chain (answer_deep_*: max_level 21): the index vector is
+    # brought to Match's output level 4 by the backend's own _at_level
+    hint = [be._at_level(c, g["hint_levels"][0]) for c in hint]
     m0 = be.counters.snapshot()
     cd = P.mask(hint, db, params, be, keys)
     assert be.counters.delta(m0).as_dict() == g["mask_counters"]
@@ -234,7 +237,7 @@ def test_answer_mask_then_comp_matches_reference_golden(pkg, oracle, name):
     u = _pack_pair_ops(hint, cd, params, be, keys)
     u_arr = np.ascontiguousarray(np.stack([c.payload.res for c in u]), dtype=np.uint64)
     out = np.empty((2, 1, n), dtype=np.uint64)
-    _lib.check(_lib.lib(4).hc_comp_packed(be._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
+    _lib.check(_lib.lib(be.params.max_level).hc_comp_packed(be._ctx(), _lib.ptr(u_arr), len(u), _lib.ptr(out)))
     assert np.array_equal(out, ans.cts[0].payload.res)
 
 

@@ -23,16 +23,17 @@ def header_symbols():
     return sorted(set(re.findall(r"\b(hc_[a-z0-9_]+)\s*\(", src)))
 
 
-@pytest.mark.parametrize("max_level", [3, 4])
-def test_library_exports_every_declared_symbol(max_level):
-    """Both builds (4-prime libhcomp.so, 5-prime libhcomp_l4.so) export the ABI."""
+@pytest.mark.parametrize("max_level,plain_row", [(3, 4), (4, 5), (21, 23)])
+def test_library_exports_every_declared_symbol(max_level, plain_row):
+    """Every build (4-prime libhcomp.so, 5-prime libhcomp_l4.so, protocol-chain
+    libhcomp_deep.so) exports the ABI."""
     L = _lib.lib(max_level)
     syms = header_symbols()
     assert len(syms) >= 20
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
     assert set(syms) <= set(_lib.EXPORTS) | {"hc_trace_reset", "hc_trace_read"}
-    assert L.hc_plain_row() == max_level + 1  # csrc/ctx.cuh PIDX: rows 0..MAXL are chain primes
+    assert L.hc_plain_row() == plain_row  # csrc/ctx.cuh PIDX = MAXL + 1: rows 0..MAXL are chain primes
 
 
 def test_host_helpers_without_gpu(oracle):
