@@ -55,6 +55,20 @@ def build_lib(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+CHECK = os.path.join(HERE, "libhcomp_check.so")
+
+
+def build_check(force: bool = False) -> str:
+    """The 4-prime library with the device-side invariant assertions
+    (-DHC_CHECK, kernels.cuh HC_ASSERT): run the GPU tests against it with
+    HCOMP_LIB=paper_2408_17063_b200/libhcomp_check.so."""
+    if force or _stale(CHECK):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-DHC_MAXL=3", "-DHC_CHECK", "-o", CHECK, os.path.join(CSRC, "hcomp.cu")]
+        subprocess.check_call(cmd)
+    return CHECK
+
+
 def build_selftest(force: bool = False) -> str:
     """The device arithmetic/NTT schedule compiled for the host (g++), used by
     tests/test_csrc_host.py to check the exact GPU code paths on the CPU."""
@@ -71,4 +85,6 @@ if __name__ == "__main__":
     build_lib(force="--force" in sys.argv, verbose="-v" in sys.argv)
     if "--selftest" in sys.argv:
         build_selftest(force="--force" in sys.argv)
+    if "--check" in sys.argv:
+        build_check(force="--force" in sys.argv)
     print(LIB)

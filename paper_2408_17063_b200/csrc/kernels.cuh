@@ -28,6 +28,35 @@
 
 namespace hc {
 
+// Checked builds (-DHC_CHECK, libhcomp_check.so): device-side assertions of
+// the value-range invariants the exact arithmetic relies on -- lazy ranges of
+// transform inputs/outputs, Galois gather indices, REDC preconditions
+// (128-bit sums below q * 2^64) and the no-overflow bounds of every red.add
+// accumulator.  A violated invariant traps (kernel error) instead of
+// producing a silently wrong residue.  Release builds compile them away.
+#ifdef HC_CHECK
+#define HC_ASSERT(c)          \
+    do {                      \
+        if (!(c)) __trap();   \
+    } while (0)
+#else
+#define HC_ASSERT(c) \
+    do {             \
+    } while (0)
+#endif
+// red.add into an accumulator whose words must stay below `bound`
+__device__ __forceinline__ void acc_add(u64* p, u64 v, u64 bound) {
+#ifdef HC_CHECK
+    const u64 old = atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+    HC_ASSERT(old + v >= old && old + v < bound);
+#else
+    (void)bound;
+    atomicAdd(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+#endif
+}
+constexpr u64 KSACC_BOUND = 1ull << 62;  // <= 49 digit products < q < 2^54 per word (+ slack)
+constexpr u64 PX_BOUND = 1ull << 56;     // diagonal-MAC lanes: < cb * q < 4q per word
+
 // ---------------------------------------------------------------------------
 // transform jobs: loaders and epilogues
 // ---------------------------------------------------------------------------
@@ -252,14 +281,20 @@ __device__ __forceinline__ void load_post(const DevCtx& C, const XJob& J, const 
         const uint16_t* dp = reinterpret_cast<const uint16_t*>(J.a);
         const uint16_t* dn = reinterpret_cast<const uint16_t*>(J.b);
         HC_UNROLL
-        for (int e = 0; e < N; e++) x[e] = ((pre.g[e] >> 15) ? dn : dp)[pre.g[e] & 0x7FFF];
+        for (int e = 0; e < N; e++) {
+            HC_ASSERT((pre.g[e] & 0x7FFF) < NPOLY);
+            x[e] = ((pre.g[e] >> 15) ? dn : dp)[pre.g[e] & 0x7FFF];
+        }
     } else if constexpr (LD == LD_KSFIN) {
         KsLd<N> v;
         ksfin_load<N>(J, P, j0, stride, pre, v);
         ksfin_finish<N>(J, P, j0, stride, pre, v, x);
     } else {  // LD_U64
         HC_UNROLL
-        for (int e = 0; e < N; e++) x[e] = J.a[j0 + e * stride];
+        for (int e = 0; e < N; e++) {
+            x[e] = J.a[j0 + e * stride];
+            HC_ASSERT(x[e] < (J.dir ? 2 * P.q : 4 * P.q));  // lazy input ranges of the GS / CT transforms
+        }
     }
 }
 
@@ -283,8 +318,8 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
             if constexpr (EP == EP_ADDMONT) {
                 J.out[j] = add_mod(x[e], mul_mont(a[e], b[e], P.q, P.qneg), P.q);
             } else {
-                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + j), (unsigned long long)mul_mont(x[e], a[e], P.q, P.qneg));
-                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + J.ostride + j), (unsigned long long)mul_mont(x[e], b[e], P.q, P.qneg));
+                acc_add(J.out + j, mul_mont(x[e], a[e], P.q, P.qneg), KSACC_BOUND);
+                acc_add(J.out + J.ostride + j, mul_mont(x[e], b[e], P.q, P.qneg), KSACC_BOUND);
             }
         }
     } else if constexpr (EP == EP_ADD || EP == EP_ADDRED) {
@@ -319,7 +354,10 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
         }
     } else {  // EP_STORE, EP_STORE_LAZY
         HC_UNROLL
-        for (int e = 0; e < N; e++) J.out[j0 + e * stride] = x[e];
+        for (int e = 0; e < N; e++) {
+            HC_ASSERT(EP == EP_STORE ? x[e] < P.q : x[e] < (1ull << 60));
+            J.out[j0 + e * stride] = x[e];
+        }
     }
 }
 
@@ -615,8 +653,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
             HC_UNROLL
             for (int v = 0; v < CEPT; v++) {
                 const int j = c * CTILE + t + 128 * v;
-                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + j), (unsigned long long)mul_mont(x[v], ka[v], P.q, P.qneg));
-                atomicAdd(reinterpret_cast<unsigned long long*>(J.out + J.ostride + j), (unsigned long long)mul_mont(x[v], kb[v], P.q, P.qneg));
+                acc_add(J.out + j, mul_mont(x[v], ka[v], P.q, P.qneg), KSACC_BOUND);
+                acc_add(J.out + J.ostride + j, mul_mont(x[v], kb[v], P.q, P.qneg), KSACC_BOUND);
             }
         } else {
             store_n<EP, CEPT>(C, J, P, c * CTILE + t, 128, x);
@@ -1081,6 +1119,7 @@ __global__ void __launch_bounds__(256, KSB == 1 ? 5 : 3) k_ksmac(const __grid_co
         }
         HC_UNROLL
         for (int c = 0; c < CPT; c++) {
+            HC_ASSERT(h0[c] < pc.q && h1[c] < pc.q);  // REDC precondition of the digit MAC
             o0[c] = add_mod(o0[c], redc(h0[c], l0[c], pc.q, pc.qneg), pc.q);
             o1[c] = add_mod(o1[c], redc(h1[c], l1[c], pc.q, pc.qneg), pc.q);
         }
@@ -1156,6 +1195,7 @@ __global__ void __launch_bounds__(256) k_ksmac_mb(const __grid_constant__ DevCtx
     HC_UNROLL
     for (int b = 0; b < NB; b++) {
         if (b >= nb) break;
+        HC_ASSERT(h0[b] < pc.q && h1[b] < pc.q);
         u64 o0 = redc(h0[b], l0[b], pc.q, pc.qneg), o1 = redc(h1[b], l1[b], pc.q, pc.qneg);
         if (J.add0[b]) o0 = add_mod(o0, J.add0[b][kn], pc.q);
         if (J.add1[b]) o1 = add_mod(o1, J.add1[b][kn], pc.q);
@@ -1226,6 +1266,7 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
             }
     }
     TRACE(1);
+    HC_ASSERT(nt <= 1024 && h0 < q0 && h1 < q1);  // one REDC of the 128-bit sums (sum < q 2^64)
     const u64 x0 = redc(h0, l0, q0, C.pc[0].qneg), x1 = redc(h1, l1, q1, C.pc[1].qneg);
     u64 e0 = 0, e1 = 0;
     if (es) {
@@ -1234,11 +1275,11 @@ __global__ void __launch_bounds__(256) k_diagx(const __grid_constant__ DevCtx C,
         e1 = corr_from_sums(sr, sd, q1, LV.qinv[1], LV.qinv_s[1], C.pc[1].one_s);
     }
     if (J.atomic) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(J.X + j), (unsigned long long)x0);
-        atomicAdd(reinterpret_cast<unsigned long long*>(J.X + NPOLY + j), (unsigned long long)x1);
+        acc_add(J.X + j, x0, PX_BOUND);
+        acc_add(J.X + NPOLY + j, x1, PX_BOUND);
         if (es) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(J.E + j), (unsigned long long)e0);
-            atomicAdd(reinterpret_cast<unsigned long long*>(J.E + NPOLY + j), (unsigned long long)e1);
+            acc_add(J.E + j, e0, PX_BOUND);
+            acc_add(J.E + NPOLY + j, e1, PX_BOUND);
         }
     } else {
         J.X[j] = add_mod(J.X[j], x0, q0);
