@@ -781,6 +781,29 @@ def main():
         # both are end to end (every step copies its inputs in and its answer
         # out inside the timed region); the line reports the faster schedule
         e2e_ms = min(e2e_serial_ms, e2e_stream_ms)
+    # pinned H2D bandwidth of this box for the e2e input volume (the two
+    # input lists on two copy streams, as hc_comp_async issues them)
+    h2d_gbs = None
+    if not shard:
+        dst = [torch.empty_like(cd_h, device="cuda"), torch.empty_like(cv_h, device="cuda")]
+        cps = [torch.cuda.Stream(), torch.cuda.Stream()]
+        ts = []
+        for it in range(12):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for i, (src, st) in enumerate(zip((cd_h, cv_h), cps)):
+                st.wait_event(a)
+                with torch.cuda.stream(st):
+                    dst[i].copy_(src, non_blocking=True)
+            for st in cps:
+                e = torch.cuda.Event()
+                e.record(st)
+                stream.wait_event(e)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if it >= 2:
+                ts.append(a.elapsed_time(b))
+        h2d_gbs = h2d_bytes / (statistics.median(ts) * 1e-3) / 1e9
     info = be.plan_info()  # kernel launches per Comp (graph built by now)
     if int(info["kernel_launches"]) <= 0:
         raise RuntimeError(f"no captured Comp graph to count launches from: {info}")
@@ -828,6 +851,8 @@ def main():
             "streamed_ms_per_step": (e2e_stream_ms / args.steps) if e2e_stream_ms else None,
             "h2d_bytes_per_step": h2d_bytes,
             "d2h_bytes_per_step": 2 * RING * 8,
+            "h2d_gbs_measured": h2d_gbs,
+            "h2d_note": "pinned host memory; the two input lists go up on two copy engines (hc_comp_async)",
         },
         "gpu_launches": int(info["kernel_launches"]) * args.steps * 2,
         "kernel_launches_per_comp": int(info["kernel_launches"]),
