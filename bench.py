@@ -203,8 +203,11 @@ def run_reference(args, p, rank):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = args.N * args.steps / total
+    metric = metric_name(args.N, args.s)
+    if args.queries:  # config 5: the CPU processes the queries one after another at this rate
+        metric += f", {args.queries} independent queries"
     line = {
-        "metric": metric_name(args.N, args.s),
+        "metric": metric,
         "impl": "reference",
         "value": value,
         "unit": "entries/s",
@@ -307,6 +310,16 @@ def sass_mix(lib_path: str, mangled: str, bfly: float) -> dict | None:
     return {k: v / bfly for k, v in ops.items()}
 
 
+def kernel_name(tag: int) -> str:
+    """hc_comp_profile_ex tag -> the kernel instantiation (kernels.cuh names)."""
+    if not tag:
+        return "?"
+    clu, d, ld, ep, noxf, vt = tag >> 20 & 1, tag >> 16 & 15, tag >> 12 & 15, tag >> 8 & 15, tag >> 4 & 1, tag & 15
+    if noxf:
+        return f"k_elem<{ld}>"
+    return f"k_xf_cl<{d}, {ld}, {ep}, {vt}>" if clu else f"k_xf<{d}, {ld}, {ep}, {vt}>"
+
+
 def roofline(L, h, sh, comp_ms):
     """Live roofline of the dominant kernel family (the transforms k_xf /
     k_xf_cl): algorithmic butterflies per launch over the launches' event-timed
@@ -322,9 +335,21 @@ def roofline(L, h, sh, comp_ms):
     sm_ = np.zeros(max_steps, dtype=np.float32)
     sk = np.zeros(max_steps, dtype=np.int32)
     sj = np.zeros(max_steps, dtype=np.int32)
-    nsteps = L.hc_comp_profile(h, sh, max_steps, _lib.ptr(sm_), _lib.ptr(sk), _lib.ptr(sj))
+    st_tag = np.zeros(max_steps, dtype=np.int32)
+    nsteps = L.hc_comp_profile_ex(h, sh, max_steps, _lib.ptr(sm_), _lib.ptr(sk), _lib.ptr(sj), _lib.ptr(st_tag))
     if nsteps < 0:
         _lib.check(nsteps)
+    # the dominant transform kernel: the instantiation with the largest share of
+    # the (un-graphed, event-timed) Comp; achieved = its butterflies per launch /
+    # its average launch duration
+    by_kernel = {}
+    for i in range(nsteps):
+        if int(sk[i]) == 0 and int(st_tag[i]):
+            d = by_kernel.setdefault(int(st_tag[i]), [0.0, 0, 0])
+            d[0] += float(sm_[i])
+            d[1] += int(sj[i])
+            d[2] += 1
+    dom_tag, (dom_ms, dom_jobs, dom_launches) = max(by_kernel.items(), key=lambda kv: kv[1][0])
     kinds = {}
     for i in range(nsteps):
         d = kinds.setdefault(int(sk[i]), [0.0, 0, 0])
@@ -346,6 +371,14 @@ def roofline(L, h, sh, comp_ms):
     achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
     peak_g = peak.value / 1e9
     comp_level = xf_jobs * bfly_per_ntt / comp_ms / 1e6
+    dom_name = kernel_name(dom_tag)
+    dom_achieved = (dom_jobs / dom_launches) * bfly_per_ntt / (dom_ms / dom_launches * 1e-3) / 1e9
+    ncu_traffic = None
+    try:  # DRAM bytes per launch of that kernel from the committed ncu --set full capture
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_dominant_traffic.json")) as fh:
+            ncu_traffic = json.load(fh).get(dom_name)
+    except (OSError, ValueError):
+        pass
     # independent ceiling: measured INT32 multiply-pipe rates x the shipped
     # transform kernel's fma-pipe instruction mix per butterfly (SASS)
     rates = (ctypes.c_double * 3)()
@@ -355,17 +388,25 @@ def roofline(L, h, sh, comp_ms):
     if mix and all(r > 0 for r in rates):
         pipe_bound = 1.0 / (mix["imad"] / rates[0] + mix["wide"] / rates[1] + mix["hi"] / rates[2]) / 1e9
     return {
-        "kernel": "k_xf / k_xf_cl: 8192-point NTT/INTT launches (1 CTA or one 8-CTA cluster per transform, fused loaders/epilogues)",
+        "kernel": dom_name + " (the dominant transform launch of the Comp; family: k_xf / k_xf_cl, 1 CTA or one "
+                  "8-CTA cluster per 8192-point transform, fused loaders/epilogues)",
         "bound": "int-modmul (IMAD pipe; SURVEY 8(d))",
-        "achieved": achieved,
+        "achieved": dom_achieved,
         "peak": peak_g,
         "unit": "Gbutterfly/s",
-        "frac": achieved / peak_g if peak_g else None,
+        "frac": dom_achieved / peak_g if peak_g else None,
+        "dominant_kernel": {"name": dom_name, "launches_per_comp": dom_launches, "jobs_per_launch": dom_jobs / dom_launches,
+                            "avg_launch_ms": dom_ms / dom_launches,
+                            "share_of_profiled_step": dom_ms / prof_total if prof_total else None,
+                            "algorithmic_unit": "53,248 butterflies per 8192-point transform job"},
+        "family_achieved_gbfly_s": achieved,
+        "family_frac": achieved / peak_g if peak_g else None,
         "peak_source": "measured live: hc_bf_peak, register-only microbenchmark of the kernels' own lazy CT butterfly at full occupancy (MEASURED_PEAKS.json has no integer peak)",
         "work_unit": "one radix-2 butterfly = one 54-bit modmul + 2 modadds; 4096*13 per 8192-point transform",
-        "traffic": None,
-        "traffic_note": ("DRAM bytes per launch from ncu --set full captures are in profiles/ (the family "
-                         "mixes launches of 1-396 jobs, so no single per-launch figure applies)"),
+        "traffic": (ncu_traffic or {}).get("dram_bytes_per_launch"),
+        "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, "
+                         "ncu --set full capture in the timed region (profiles/r02_ncu_dominant_traffic.json); "
+                         "algorithmic bytes per launch: " + str((ncu_traffic or {}).get("algorithmic_bytes_per_launch"))),
         "comp_level_gbfly_s": comp_level,
         "comp_level_frac": comp_level / peak_g if peak_g else None,
         "xform_share_of_step": xf_ms / prof_total if prof_total else None,

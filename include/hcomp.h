@@ -201,6 +201,11 @@ int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t galois_t, uint6
  * every step (kind: 0 transform, 1 CRT/digits, 2 key-switch MAC, 3 diagonal
  * MAC, 4 copy fold, 5 memset).  Returns the number of steps written. */
 int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind, int* step_jobs);
+/* The same with step_tag[i] naming a transform launch's kernel instantiation:
+ * (cluster << 20) | (dir << 16) | (loader << 12) | (epilogue << 8) |
+ * (transform-less << 4) | (VT or transforms per cluster); 0 for other steps. */
+int hc_comp_profile_ex(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind, int* step_jobs,
+                       int* step_tag);
 /* Measured butterfly-throughput ceiling of this GPU for the NTT butterfly
  * used by the transform kernel (register-only microbenchmark). */
 int hc_bf_peak(hc_ctx* h, double* bfly_per_s);

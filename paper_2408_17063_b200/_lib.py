@@ -78,6 +78,7 @@ _SIGS = [
     ("hc_decrypt", _I, [_P, _P, _I, _P, _P]),
     ("hc_rotate", _I, [_P, _P, _I, _U32, _P]),
     ("hc_comp_profile", _I, [_P, _P, _I, _P, _P, _P]),
+    ("hc_comp_profile_ex", _I, [_P, _P, _I, _P, _P, _P, _P]),
     ("hc_bf_peak", _I, [_P, ctypes.POINTER(ctypes.c_double)]),
     ("hc_bench_xform", _I, [_P, _I, _I, _I, ctypes.POINTER(ctypes.c_double)]),
     ("hc_imad_peak", _I, [_P, _P]),

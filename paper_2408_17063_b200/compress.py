@@ -262,11 +262,87 @@ def _check_inputs(cd, cv, params: CompressionParams, backend: B200BgvBackend, ke
             # pack_pair lands below level 2, so the output mask's mul_plain
             # would run at level 0 (bgv.py:721-722): the reference raises there
             raise LevelExhausted("plaintext multiply at level 0 (Comp inputs below level 3)")
-        raise NotImplementedError(
-            "the B200 Comp runs pack_pair's outputs at level 2 (inputs at levels 3/4); inputs above level 3 "
-            "on both sides are not built"
-        )
+        if max(pair_levels) > FUSED_LEVEL + 1:
+            raise NotImplementedError(
+                "the B200 backend key-switches at levels <= 3: Comp needs each input pair's lower level <= 4"
+            )
+        return OPS_PATH
     return any(c.level != FUSED_LEVEL for c in list(cv) + list(cd))
+
+
+OPS_PATH = "ops"  # _check_inputs: pack_pair's outputs above level 2 -> _comp_ops
+
+
+def _vandermonde_block(params: CompressionParams, k: int, db_mod_p: np.ndarray | None) -> np.ndarray:
+    """VandermondeTable.block (compress.py:118-139): rows j = 0..s-1 hold
+    col^(j+1) mod p for the block's columns k*m+1 .. (k+1)*m, zero past N,
+    column-scaled by the cleartext database for comp_masked."""
+    p, m = params.he.p, params.block_width
+    cols = np.arange(k * m + 1, (k + 1) * m + 1, dtype=np.int64)
+    valid = cols <= params.N
+    base = np.where(valid, cols % p, 0)
+    table = np.zeros((params.s, m), dtype=np.int64)
+    row = base.copy()
+    for j in range(params.s):
+        table[j] = row
+        row = row * base % p
+    if db_mod_p is not None:
+        scale = np.zeros(m, dtype=np.int64)
+        nv = int(valid.sum())
+        scale[:nv] = db_mod_p[k * m : k * m + nv].astype(np.int64)
+        table = table * scale[None, :] % p
+    return table
+
+
+def _diag_rows(table: np.ndarray, g: int, b: int, baby: int, s_pad: int, m: int) -> np.ndarray:
+    """_diag_vector (compress.py:186-195): entry[pos] = M[(pos - g*baby) % s_pad][(pos + b) % m]."""
+    pos = np.arange(m)
+    rows = (pos - g * baby) % s_pad
+    cols = (pos + b) % m
+    live = rows < table.shape[0]
+    out = np.zeros(m, dtype=np.int64)
+    out[live] = table[rows[live], cols[live]]
+    return out
+
+
+def _comp_ops(cd, cv, params: CompressionParams, backend, keys: KeySet, masked) -> CompressedAnswer:
+    """Comp for inputs whose pack_pair outputs sit above level 2 (e.g. fresh
+    ciphertexts at level 4 on a 5-prime chain): the reference's pack_pair and
+    bsgs_matvec (compress.py:273-310, 338-367) step by step through the
+    backend's single GPU operations (mul_plain, rot_row / rot_col, add), which
+    move the counters and noise bits themselves.  The answer lands above
+    level 0, exactly where the reference's does."""
+    p, m = params.he.p, params.block_width
+    s_pad = params.s_pad
+    baby, giant = bsgs_shape(params.s)
+    u = _pack_pair_ops(cv, cd, params, backend, keys)
+    db = None if masked is None else masked.db_mod_p
+    acc = [None] * giant
+    for t, ub in enumerate(u):
+        top = _vandermonde_block(params, t, None)
+        bot = top if db is None else _vandermonde_block(params, t, db)
+        rotated = [ub] + [backend.rot_row(ub, b, keys) for b in range(1, baby)]
+        for g in range(giant):
+            for b in range(baby):
+                r0 = _diag_rows(top, g, b, baby, s_pad, m)
+                r1 = _diag_rows(bot, g, b, baby, s_pad, m)
+                if not r0.any() and not r1.any():
+                    continue
+                prod = backend.mul_plain(rotated[b], SlotMatrix(p, np.stack([r0, r1]) % p))
+                acc[g] = prod if acc[g] is None else backend.add(acc[g], prod)
+    res = acc[0]
+    for g in range(1, giant):
+        if acc[g] is None:
+            continue
+        part = backend.rot_row(acc[g], (g * baby) % m, keys)
+        res = part if res is None else backend.add(res, part)
+    if res is None:
+        raise ValueError("matrix plan had no nonzero diagonals")
+    for a in fold_amounts(s_pad, m):
+        res = backend.add(res, backend.rot_row(res, a, keys))
+    mask_row = np.array([1] * params.s + [0] * (m - params.s), dtype=np.int64)
+    out = backend.mul_plain(res, SlotMatrix(p, np.stack([mask_row, mask_row])))
+    return CompressedAnswer((out,), params.s, True)
 
 
 def _pack_pair_ops(cv, cd, params: CompressionParams, backend: B200BgvBackend, keys: KeySet) -> list[Ciphertext]:
@@ -320,6 +396,8 @@ def comp(
     glue = _check_inputs(cd, cv, params, backend, keys)
     if masked is not None and masked.params != params:
         raise ValueError("masked matrix was built for different compression parameters")
+    if glue == OPS_PATH:
+        return _comp_ops(cd, cv, params, backend, keys, masked)
     live = live_diagonals(params)
     out = np.empty((2, 1, backend.params.n), dtype=np.uint64)
     if glue:

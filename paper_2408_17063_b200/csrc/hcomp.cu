@@ -910,10 +910,15 @@ struct Plan {
     // device buffers
     std::vector<void*> allocs;
     u64 *cv = nullptr, *cd = nullptr, *mask = nullptr, *diag = nullptr, *omask = nullptr;
-    u64 *ecor = nullptr, *rc1raw = nullptr, *pn = nullptr, *rc0n = nullptr, *dnttR = nullptr;
-    u64 *U = nullptr, *Ucoef = nullptr, *dnttB = nullptr, *ROT = nullptr;
-    uint16_t *digR = nullptr, *digU = nullptr;
-    u64 *Eslot = nullptr, *PX = nullptr;
+    // per-chunk scratch of the block segment (S1..S10); two sets when wide
+    // chunks are pipelined (chunk c uses set c % 2, see build_partial)
+    struct Scratch {
+        u64 *ecor = nullptr, *rc1raw = nullptr, *pn = nullptr, *rc0n = nullptr, *dnttR = nullptr;
+        u64 *U = nullptr, *Ucoef = nullptr, *dnttB = nullptr, *ROT = nullptr, *Eslot = nullptr;
+        uint16_t *digR = nullptr, *digU = nullptr;
+    } scr[2];
+    int nsets = 1;
+    u64* PX = nullptr;
     u64 *A0 = nullptr, *A1 = nullptr, *A1coef = nullptr, *dnttG = nullptr, *RES = nullptr;
     u64 *rc1coef = nullptr, *dnttF = nullptr, *corr = nullptr, *OUT = nullptr, *ACC = nullptr;
     uint16_t *digG = nullptr, *digF = nullptr;
@@ -1086,18 +1091,33 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
     P->mask = P->plain->mask;
     P->diag = P->plain->diag;
     P->omask = P->plain->omask;
-    PA(P->ecor, (size_t)CB * 4 * 3 * NB);
-    PA(P->rc1raw, (size_t)CB * 3 * NB);
-    PA(P->pn, (size_t)CB * 2 * 3 * NB);
-    PA(P->rc0n, (size_t)CB * 3 * NB);
-    PA(P->digR, (size_t)CB * P->D2 * NB);
-    PA(P->dnttR, (size_t)CB * P->D2 * 3 * NB);
-    PA(P->U, (size_t)CB * 2 * 3 * NB);
-    PA(P->Ucoef, (size_t)CB * 3 * NB);
-    PA(P->digU, (size_t)CB * 2 * P->D2 * NB);
-    PA(P->dnttB, (size_t)std::max(1, CB * bm1) * P->D2 * 3 * NB);
-    PA(P->ROT, (size_t)std::max(1, CB * bm1) * 2 * 3 * NB);
-    PA(P->Eslot, (size_t)CB * P->baby * G * 2 * 2 * NB);
+    // wide chunks (throughput regime) pipeline over two scratch sets when the
+    // range has several: chunk c+1's transforms overlap chunk c's
+    // memory-bound MACs (HC_CHUNK_LANES=0: one set, chunks in sequence)
+    {
+        static int chunk_lanes = -1;
+        if (chunk_lanes < 0) {
+            const char* e = getenv("HC_CHUNK_LANES");
+            chunk_lanes = (e && e[0] == '0') ? 0 : 1;
+        }
+        const long long nchunks = (P->rb1 - P->rb0 + CB - 1) / CB;
+        P->nsets = (chunk_lanes && CB > g_lane_max_blocks && nchunks >= 2 && nchunks <= 64) ? 2 : 1;
+    }
+    for (int si = 0; si < P->nsets; si++) {
+        Plan::Scratch& X = P->scr[si];
+        PA(X.ecor, (size_t)CB * 4 * 3 * NB);
+        PA(X.rc1raw, (size_t)CB * 3 * NB);
+        PA(X.pn, (size_t)CB * 2 * 3 * NB);
+        PA(X.rc0n, (size_t)CB * 3 * NB);
+        PA(X.digR, (size_t)CB * P->D2 * NB);
+        PA(X.dnttR, (size_t)CB * P->D2 * 3 * NB);
+        PA(X.U, (size_t)CB * 2 * 3 * NB);
+        PA(X.Ucoef, (size_t)CB * 3 * NB);
+        PA(X.digU, (size_t)CB * 2 * P->D2 * NB);
+        PA(X.dnttB, (size_t)std::max(1, CB * bm1) * P->D2 * 3 * NB);
+        PA(X.ROT, (size_t)std::max(1, CB * bm1) * 2 * 3 * NB);
+        PA(X.Eslot, (size_t)CB * P->baby * G * 2 * 2 * NB);
+    }
     PA(P->PX, P->px_words());
     PA(P->A0, (size_t)G * 2 * NB);
     PA(P->A1, (size_t)2 * NB);
@@ -1215,15 +1235,15 @@ extern "C" int64_t hc_partial_words(const hc_ctx* h) {
 
 // the level-2 ciphertext multiplied by diagonal (t, g, b): u_t for b = 0,
 // the baby rotation ROT[t][b] otherwise
-static const u64* rot_src(const Plan& P, const u64* U, int tl, int b, int poly) {
+static const u64* rot_src(const Plan& P, const Plan::Scratch& X, const u64* U, int tl, int b, int poly) {
     const size_t NB = NPOLY;
     return b == 0 ? U + ((size_t)tl * 2 + poly) * 3 * NB
-                  : P.ROT + (((size_t)tl * (P.baby - 1) + (b - 1)) * 2 + poly) * 3 * NB;
+                  : X.ROT + (((size_t)tl * (P.baby - 1) + (b - 1)) * 2 + poly) * 3 * NB;
 }
 // correction slot of product (tl, b) for accumulator (g, poly): [2 primes][n]
-static u64* eslot(const Plan& P, int tl, int b, int g, int poly) {
+static u64* eslot(const Plan& P, const Plan::Scratch& X, int tl, int b, int g, int poly) {
     const size_t NB = NPOLY;
-    return P.Eslot + ((((size_t)tl * P.baby + b) * P.giant + g) * 2 + poly) * 2 * NB;
+    return X.Eslot + ((((size_t)tl * P.baby + b) * P.giant + g) * 2 + poly) * 2 * NB;
 }
 
 // Steps S1..S10 for blocks [b0, b1): pack_pair (compress.py:338-367), baby
@@ -1239,9 +1259,18 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
     const DevKey* kcol = need_key(h, P.t_col);
     int rc;
     add_memset(S, P.PX, P.px_words() * 8);
+    // pipelined wide chunks: chunk i on graph lane i % 2 with scratch set
+    // i % 2, the two lanes' diagonal MACs adding into PX with atomics (words
+    // stay < nchunks * q <= 64 q < 2^60; every consumer reduces them)
+    const long long nchunks = (b1 - b0 + P.CB - 1) / P.CB;
+    const bool pipe = P.nsets == 2 && nchunks >= 2;
+    if (pipe) S.par_begin();
     for (long long c0 = b0; c0 < b1; c0 += P.CB) {
         const int cb = (int)std::min<long long>(P.CB, b1 - c0);
-        const u64* Ub = from_u ? P.uin + (size_t)c0 * 2 * 3 * NB : P.U;  // u_t of chunk block tl at Ub[tl]
+        const int ci = (int)((c0 - b0) / P.CB);
+        const Plan::Scratch& X = P.scr[pipe ? ci % 2 : 0];
+        if (pipe) S.cur_lane = ci % 2;
+        const u64* Ub = from_u ? P.uin + (size_t)c0 * 2 * 3 * NB : X.U;  // u_t of chunk block tl at Ub[tl]
         // S1..S6 (pack, u = P + rot_col(R), hoisted baby INTT + digits) run as
         // one stream over the chunk (narrow levels may use cluster transforms);
         // the wide baby segment S7 (digit NTTs) -> S8 (MAC) -> S9 (diagonal
@@ -1262,7 +1291,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                 // even block: u = mp(cv, top) + rot_col(mp(cd, top)); odd: rot_col(mp(cv, bot)) + mp(cd, bot)
                 const u64* ctP = par == 0 ? cv : cd;
                 const u64* ctR = par == 0 ? cd : cv;
-                u64* ecor = P.ecor + (size_t)tl * 4 * 3 * NB;  // [P0,P1,R0,R1][3][n]
+                u64* ecor = X.ecor + (size_t)tl * 4 * 3 * NB;  // [P0,P1,R0,R1][3][n]
                 if (!from_u) {
                 // S1: the pack mul_plains' dropped-prime INTTs (+ modulus-switch
                 //     correction) and R.c1's kept-prime INTTs
@@ -1282,7 +1311,7 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     j.dir = 1; j.k = k; j.ld = LD_MONT; j.ep = EP_STORE;
                     j.a = ctR + ((size_t)1 * 4 + k) * NB;
                     j.b = mk + (size_t)k * NB;
-                    j.out = P.rc1raw + ((size_t)tl * 3 + k) * NB;
+                    j.out = X.rc1raw + ((size_t)tl * 3 + k) * NB;
                     s1.push_back(j);
                 }
                 // S2: NTT of corrections + plaintext-product combine
@@ -1295,18 +1324,18 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         j.a = ecor + ((size_t)(mm * 2 + poly) * 3 + k) * NB;
                         j.ea = ct + ((size_t)poly * 4 + k) * NB;
                         j.eb = mk + (size_t)k * NB;
-                        j.out = which < 2 ? P.pn + (((size_t)tl * 2 + poly) * 3 + k) * NB : P.rc0n + ((size_t)tl * 3 + k) * NB;
+                        j.out = which < 2 ? X.pn + (((size_t)tl * 2 + poly) * 3 + k) * NB : X.rc0n + ((size_t)tl * 3 + k) * NB;
                         s2.push_back(j);
                     }
                 }
                 {
                     CJob c{};
                     c.level = 2; c.mode = 0;
-                    c.x = P.rc1raw + (size_t)tl * 3 * NB;
+                    c.x = X.rc1raw + (size_t)tl * 3 * NB;
                     c.xadd = ecor + (size_t)3 * 3 * NB;
                     c.xstride = NB;
                     c.gal = kcol->gal;
-                    c.dig = P.digR + (size_t)tl * D2 * NB;
+                    c.dig = X.digR + (size_t)tl * D2 * NB;
                     s2c.push_back(c);
                 }
                 // S3/S4: column-swap key switch of R, u = P + rot_col(R)
@@ -1314,21 +1343,21 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     for (int k = 0; k < 3; k++) {
                         XJob j{};
                         j.dir = 0; j.k = k; j.ld = LD_DIG; j.ep = EP_STORE_LAZY;  // feeds k_ksmac only
-                        j.a = (const u64*)(P.digR + ((size_t)tl * D2 + jj) * NB);
-                        j.out = P.dnttR + (((size_t)tl * D2 + jj) * 3 + k) * NB;
+                        j.a = (const u64*)(X.digR + ((size_t)tl * D2 + jj) * NB);
+                        j.out = X.dnttR + (((size_t)tl * D2 + jj) * 3 + k) * NB;
                         s3.push_back(j);
                     }
                 {
                     MJob mj{};
                     mj.level = 2; mj.nterm = 1;
-                    mj.t[0].dntt = P.dnttR + (size_t)tl * D2 * 3 * NB;
+                    mj.t[0].dntt = X.dnttR + (size_t)tl * D2 * 3 * NB;
                     mj.t[0].key = kcol->key;
-                    mj.t[0].c0src = P.rc0n + (size_t)tl * 3 * NB;
+                    mj.t[0].c0src = X.rc0n + (size_t)tl * 3 * NB;
                     mj.t[0].perm = kcol->perm;
-                    mj.add0 = P.pn + ((size_t)tl * 2 + 0) * 3 * NB;
-                    mj.add1 = P.pn + ((size_t)tl * 2 + 1) * 3 * NB;
-                    mj.out0 = P.U + ((size_t)tl * 2 + 0) * 3 * NB;
-                    mj.out1 = P.U + ((size_t)tl * 2 + 1) * 3 * NB;
+                    mj.add0 = X.pn + ((size_t)tl * 2 + 0) * 3 * NB;
+                    mj.add1 = X.pn + ((size_t)tl * 2 + 1) * 3 * NB;
+                    mj.out0 = X.U + ((size_t)tl * 2 + 0) * 3 * NB;
+                    mj.out1 = X.U + ((size_t)tl * 2 + 1) * 3 * NB;
                     s4.push_back(mj);
                 }
                 }  // !from_u
@@ -1338,14 +1367,14 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         XJob j{};
                         j.dir = 1; j.k = k; j.ld = LD_U64; j.ep = EP_STORE;
                         j.a = Ub + (((size_t)tl * 2 + 1) * 3 + k) * NB;
-                        j.out = P.Ucoef + ((size_t)tl * 3 + k) * NB;
+                        j.out = X.Ucoef + ((size_t)tl * 3 + k) * NB;
                         s5.push_back(j);
                     }
                     CJob c{};
                     c.level = 2; c.mode = 1;
-                    c.x = P.Ucoef + (size_t)tl * 3 * NB;
+                    c.x = X.Ucoef + (size_t)tl * 3 * NB;
                     c.xstride = NB;
-                    c.dig = P.digU + (size_t)tl * 2 * D2 * NB;
+                    c.dig = X.digU + (size_t)tl * 2 * D2 * NB;
                     s6.push_back(c);
                     for (int b = 1; b < baby; b++) {
                         const DevKey* kb = need_key(h, P.t_baby[b]);
@@ -1354,20 +1383,20 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                             for (int k = 0; k < 3; k++) {
                                 XJob j{};
                                 j.dir = 0; j.k = k; j.ld = LD_DIGGAL; j.ep = EP_STORE_LAZY;  // feeds k_ksmac only
-                                j.a = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + jj) * NB);
-                                j.b = (const u64*)(P.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
+                                j.a = (const u64*)(X.digU + ((size_t)tl * 2 * D2 + jj) * NB);
+                                j.b = (const u64*)(X.digU + ((size_t)tl * 2 * D2 + D2 + jj) * NB);
                                 j.gal = kb->gal;
-                                j.out = P.dnttB + ((rb * D2 + jj) * 3 + k) * NB;
+                                j.out = X.dnttB + ((rb * D2 + jj) * 3 + k) * NB;
                                 s7[tl].push_back(j);
                             }
                         MJob mj{};
                         mj.level = 2; mj.nterm = 1;
-                        mj.t[0].dntt = P.dnttB + rb * D2 * 3 * NB;
+                        mj.t[0].dntt = X.dnttB + rb * D2 * 3 * NB;
                         mj.t[0].key = kb->key;
                         mj.t[0].c0src = Ub + ((size_t)tl * 2 + 0) * 3 * NB;
                         mj.t[0].perm = kb->perm;
-                        mj.out0 = P.ROT + (rb * 2 + 0) * 3 * NB;
-                        mj.out1 = P.ROT + (rb * 2 + 1) * 3 * NB;
+                        mj.out0 = X.ROT + (rb * 2 + 0) * 3 * NB;
+                        mj.out1 = X.ROT + (rb * 2 + 1) * 3 * NB;
                         s8[tl].push_back(mj);
                     }
                 }
@@ -1382,9 +1411,9 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         for (int poly = 0; poly < 2; poly++) {
                             XJob j{};
                             j.dir = 1; j.k = 2; j.ld = LD_MONT; j.ep = EP_RESCALE_RD; j.level = 2;
-                            j.a = rot_src(P, Ub, tl, b, poly) + 2 * NB;
+                            j.a = rot_src(P, X, Ub, tl, b, poly) + 2 * NB;
                             j.b = dg + 2 * NB;
-                            j.out = eslot(P, tl, b, g, poly);
+                            j.out = eslot(P, X, tl, b, g, poly);
                             j.ostride = NB;
                             s9[tl].push_back(j);
                         }
@@ -1406,9 +1435,9 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         for (int b = 0; b < baby; b++) {
                             const int i = g * baby + b;
                             if (!P.live[(size_t)t * sp + i]) continue;
-                            srcs.push_back(rot_src(P, Ub, tl, b, poly));
+                            srcs.push_back(rot_src(P, X, Ub, tl, b, poly));
                             dgs.push_back(P.diag + ((size_t)(t - P.rb0) * sp + i) * 3 * NB);
-                            ess.push_back(eslot(P, tl, b, g, poly));
+                            ess.push_back(eslot(P, X, tl, b, g, poly));
                         }
                     }
                     rngs.push_back({off, srcs.size() - off, g, poly});
@@ -1512,9 +1541,13 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         // S10: per (g, poly): X += sum src * diag * q^-1 (kept primes) and
         //      E += sum of the chunk's correction slots
         if (!lanes_dx) {
-            rc = build_dx(0, cb, false);
+            rc = build_dx(0, cb, pipe);
             if (rc) return rc;
         }
+    }
+    if (pipe) {
+        S.cur_lane = -1;
+        S.par_end();
     }
     return HC_OK;
 }
@@ -2523,8 +2556,18 @@ extern "C" int hc_rotate(hc_ctx* h, const uint64_t* ct, int level, uint32_t t, u
 // ---------------------------------------------------------------------------
 // measurement helpers
 // ---------------------------------------------------------------------------
+static int comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind, int* step_jobs,
+                        int* step_tag);
 extern "C" int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind,
                                int* step_jobs) {
+    return comp_profile(h, stream, max_steps, step_ms, step_kind, step_jobs, nullptr);
+}
+extern "C" int hc_comp_profile_ex(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind,
+                                  int* step_jobs, int* step_tag) {
+    return comp_profile(h, stream, max_steps, step_ms, step_kind, step_jobs, step_tag);
+}
+static int comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, int* step_kind, int* step_jobs,
+                        int* step_tag) {
     if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
     CU(cudaSetDevice(h->dev));
     int rc = ensure_full(h);
@@ -2556,6 +2599,17 @@ extern "C" int hc_comp_profile(hc_ctx* h, void* stream, int max_steps, float* st
         step_ms[k] = ms;
         step_kind[k] = S.steps[i].kind;
         step_jobs[k] = S.steps[i].njobs;
+        if (step_tag) {  // transform launches: which instantiation ran
+            const Step& st = S.steps[i];
+            int tag = 0;
+            if (st.kind == ST_XF && !st.hjobs.empty()) {
+                const XJob& j = st.hjobs[0];
+                const bool clu = st.cl && st.njobs <= CL_MAX;
+                const int vt = clu ? st.jpc : (st.njobs >= g_vt2_jobs ? 4 : 1);
+                tag = (clu ? 1 << 20 : 0) | (j.dir << 16) | (j.ld << 12) | (j.ep << 8) | (j.noxf << 4) | vt;
+            }
+            step_tag[k] = tag;
+        }
     }
     for (auto& e : ev) cudaEventDestroy(e);
     return k;

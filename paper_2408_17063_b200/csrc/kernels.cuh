@@ -55,7 +55,7 @@ __device__ __forceinline__ void acc_add(u64* p, u64 v, u64 bound) {
 #endif
 }
 constexpr u64 KSACC_BOUND = 1ull << 62;  // <= 49 digit products < q < 2^54 per word (+ slack)
-constexpr u64 PX_BOUND = 1ull << 56;     // diagonal-MAC lanes: < cb * q < 4q per word
+constexpr u64 PX_BOUND = 1ull << 61;     // diagonal-MAC atomics: < 4q (block lanes) or < 64q (pipelined chunks) per word
 
 // ---------------------------------------------------------------------------
 // transform jobs: loaders and epilogues

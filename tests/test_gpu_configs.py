@@ -249,3 +249,36 @@ def test_device_decrypt_vs_oracle_every_level(pkg, oracle):
         if lvl:
             cur = be.mul_plain(cur, m)
             ocur = obe.mul_plain(ocur, rows)
+
+
+def test_comp_inputs_above_level_3_on_both_sides_vs_oracle(pkg, oracle):
+    """Fresh ciphertexts at level 4 on a 5-prime chain (both inputs above the
+    fused schedule's level 3): pack_pair at level 4, BSGS at level 3, the
+    answer at level 1 -- as the reference computes it -- through the backend's
+    single GPU operations; bit-exact with the oracle (residues, noise bits,
+    counters, serialized bytes) and decrypting to the power sums."""
+    P, O = pkg, oracle
+    n, p, N, s, seed = 8192, 65537, 8192, 8, 41
+    he = P.HeParams(n, p, 4)
+    params = P.CompressionParams(N, s, he)
+    be = P.B200BgvBackend(he, seed=seed)
+    keys = be.keygen(*P.plan_rotation_amounts(s, n))
+    dense = O.plant_sparse(random.Random(seed), N, s, p)
+    cts = P.encrypt_vector(dense, params, be, keys)
+    hint = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
+    before = be.counters.snapshot()
+    ans = P.comp(cts, params, be, keys, index_hint=hint)
+    delta = be.counters.delta(before).as_dict()
+    assert ans.cts[0].level == 1
+    obe = O.OracleBgv(n, p, 4, seed=seed)
+    okeys = obe.keygen(*O.plan_rotation_amounts(s, n))
+    octs = O.encrypt_vector(dense, N, obe, okeys)
+    ohint = O.encrypt_vector([1 if x else 0 for x in dense], N, obe, okeys)
+    obe.counters = O.OCounters()
+    out = O.comp(octs, N, s, obe, okeys, ohint)
+    assert out.level == 1
+    assert np.array_equal(ans.cts[0].payload.res, out.c)
+    assert ans.cts[0].payload.noise_bits == out.noise_bits
+    assert delta == vars(obe.counters)
+    assert O.sha256(ans.serialize(be)) == O.sha256(O.serialize_answer(obe, out, s))
+    assert ans.payload_slots(be, keys) == O.expected_slots(dense, s, p)

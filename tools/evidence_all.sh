@@ -2,7 +2,7 @@
 # Full round evidence on one B200; keeps gpurun_out/ small (ncu reports are
 # summarised on the box and removed).
 O=gpurun_out
-bash tools/profile_round.sh > $O/pr.log 2>&1
+bash tools/profile_r02.sh > $O/pr.log 2>&1
 bash tools/profile_cl.sh > $O/pc.log 2>&1
 bash tools/profile_mac.sh > $O/pm.log 2>&1
 python tools/sweep.py 8192:8 16384:8 16384:16 16384:32 16384:64 16384:128 8192:16 32768:16 65536:16 131072:16 65536:64 1048576:16 1048576:128 4194304:16 4194304:128 > $O/sweep.txt 2>&1
