@@ -916,7 +916,7 @@ struct Plan {
         u64 *ecor = nullptr, *rc1raw = nullptr, *pn = nullptr, *rc0n = nullptr, *dnttR = nullptr;
         u64 *U = nullptr, *Ucoef = nullptr, *dnttB = nullptr, *ROT = nullptr, *Eslot = nullptr;
         uint16_t *digR = nullptr, *digU = nullptr;
-    } scr[2];
+    } scr[4];
     int nsets = 1;
     u64* PX = nullptr;
     u64 *A0 = nullptr, *A1 = nullptr, *A1coef = nullptr, *dnttG = nullptr, *RES = nullptr;
@@ -1091,17 +1091,20 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
     P->mask = P->plain->mask;
     P->diag = P->plain->diag;
     P->omask = P->plain->omask;
-    // wide chunks (throughput regime) pipeline over two scratch sets when the
-    // range has several: chunk c+1's transforms overlap chunk c's
-    // memory-bound MACs (HC_CHUNK_LANES=0: one set, chunks in sequence)
+    // wide chunks (throughput regime) pipeline over up to four scratch sets
+    // when the range has several: chunk c+1's transforms overlap chunk c's
+    // memory-bound MACs.  N=2^20, s=16: 5.67 ms (one set) -> 5.39 (two) ->
+    // 5.28 (four); N=2^22, s=16: 22.19 -> 20.92 -> 20.61 ms
+    // (profiles/r02_ab_chunk_pipelining*.txt).  HC_CHUNK_LANES=1: one set.
     {
-        static int chunk_lanes = -1;
+        static int chunk_lanes = -1;  // HC_CHUNK_LANES: graph lanes for wide chunks (0/1: none, <= 4)
         if (chunk_lanes < 0) {
             const char* e = getenv("HC_CHUNK_LANES");
-            chunk_lanes = (e && e[0] == '0') ? 0 : 1;
+            chunk_lanes = e ? std::max(1, std::min(4, atoi(e))) : 4;
         }
         const long long nchunks = (P->rb1 - P->rb0 + CB - 1) / CB;
-        P->nsets = (chunk_lanes && CB > g_lane_max_blocks && nchunks >= 2 && nchunks <= 64) ? 2 : 1;
+        P->nsets = (chunk_lanes > 1 && CB > g_lane_max_blocks && nchunks >= 2 && nchunks <= 64)
+                       ? (int)std::min<long long>(chunk_lanes, nchunks) : 1;
     }
     for (int si = 0; si < P->nsets; si++) {
         Plan::Scratch& X = P->scr[si];
@@ -1259,17 +1262,17 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
     const DevKey* kcol = need_key(h, P.t_col);
     int rc;
     add_memset(S, P.PX, P.px_words() * 8);
-    // pipelined wide chunks: chunk i on graph lane i % 2 with scratch set
-    // i % 2, the two lanes' diagonal MACs adding into PX with atomics (words
+    // pipelined wide chunks: chunk i on graph lane i % nsets with scratch set
+    // i % nsets, the lanes' diagonal MACs adding into PX with atomics (words
     // stay < nchunks * q <= 64 q < 2^60; every consumer reduces them)
     const long long nchunks = (b1 - b0 + P.CB - 1) / P.CB;
-    const bool pipe = P.nsets == 2 && nchunks >= 2;
+    const bool pipe = P.nsets >= 2 && nchunks >= 2;
     if (pipe) S.par_begin();
     for (long long c0 = b0; c0 < b1; c0 += P.CB) {
         const int cb = (int)std::min<long long>(P.CB, b1 - c0);
         const int ci = (int)((c0 - b0) / P.CB);
-        const Plan::Scratch& X = P.scr[pipe ? ci % 2 : 0];
-        if (pipe) S.cur_lane = ci % 2;
+        const Plan::Scratch& X = P.scr[pipe ? ci % P.nsets : 0];
+        if (pipe) S.cur_lane = ci % P.nsets;
         const u64* Ub = from_u ? P.uin + (size_t)c0 * 2 * 3 * NB : X.U;  // u_t of chunk block tl at Ub[tl]
         // S1..S6 (pack, u = P + rot_col(R), hoisted baby INTT + digits) run as
         // one stream over the chunk (narrow levels may use cluster transforms);

@@ -37,6 +37,7 @@ for r in diag_intt fold_ntt fold_intt2 ksmac_lat compose pack_intt ksmac_2e20 di
   $NCU -i $O/$r.ncu-rep --page raw --csv > $O/${r}_raw.csv 2>/dev/null
 done
 python tools/ncu_summary.py $O/*.ncu-rep > $O/summary.txt 2>&1
-[ -f $O/diag_intt_raw.csv ] && python tools/ncu_traffic.py $O/diag_intt_raw.csv 'k_xf<1, 1, 5, 1>' 32 262144 > $O/dominant_traffic.json
+[ -f $O/diag_intt_raw.csv ] && python tools/ncu_traffic.py $O/diag_intt_raw.csv 'k_xf<1, 1, 5, 1>' 32 262144 > $O/traffic_diag_intt.json
+[ -f $O/fold_ntt_raw.csv ] && python tools/ncu_traffic.py $O/fold_ntt_raw.csv 'k_xf_cl<0, 5, 6, 1>' 14 294912 > $O/traffic_fold_ntt.json
 rm -f $O/*.ncu-rep
 cat $O/summary.txt | head -80
