@@ -233,6 +233,8 @@ int hc_max_active_clusters(hc_ctx* h, int* clusters);
  * per-CTA %globaltimer stamps [128 launches][512 CTAs][8 points]. */
 int hc_trace_reset(void);
 int hc_trace_read(uint64_t* out);
+/* k_foldchain's per-fold phase stamps [12 folds][128 CTAs][12 points] */
+int hc_trace_read_tail(uint64_t* out);
 
 /* Pure host helpers (no GPU needed): Galois tables for element t.
  * coef: uint16[n] (source index | negate << 15) realising X -> X^t on

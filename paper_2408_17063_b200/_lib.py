@@ -88,6 +88,7 @@ _SIGS = [
     ("hc_max_active_clusters", _I, [_P, _P]),
     ("hc_trace_reset", _I, []),
     ("hc_trace_read", _I, [_P]),
+    ("hc_trace_read_tail", _I, [_P]),
     ("hc_rng_create", _I, [_P, _I, _P]),
     ("hc_rng_destroy", None, [_P]),
     ("hc_rng_getrandbits", _I, [_P, _I, _P]),

@@ -18,6 +18,7 @@
 
 #include "../../include/hcomp.h"
 #include "kernels.cuh"
+#include "foldchain.cuh"
 #include "pyrng.hpp"
 #include "host_tables.hpp"
 
@@ -58,6 +59,7 @@ struct DevKey {
     u64* key = nullptr;        // [D_L][2][L+1][n] Montgomery form
     uint16_t* gal = nullptr;   // coefficient gather
     uint16_t* perm = nullptr;  // NTT-domain permutation
+    uint16_t* igal = nullptr;  // inverse coefficient gather: source i -> (j | neg << 15) with gal[j] = i | neg << 15
 };
 
 // transform launches with at most this many jobs use the cluster kernel
@@ -128,7 +130,7 @@ static cudaError_t launch_cl(void (*k)(KArgs...), int cluster, dim3 grid, dim3 b
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7, ST_ADD = 8 };  // values: bench.py per_kind_ms keys
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7, ST_ADD = 8, ST_FOLD = 9 };  // values: bench.py per_kind_ms keys
 struct Step {
     int kind = 0;
     int njobs = 0;
@@ -145,6 +147,7 @@ struct Step {
     int cl = 0;               // ST_XF: launch as 8-CTA clusters (<= CL_MAX jobs)
     int jpc = 1;              // ST_XF cluster launch: transforms per cluster
     int lane = -1;            // in a group: steps of one lane run in order on one branch
+    FcArgs fc{};              // ST_FOLD: the persistent fold chain (k_foldchain)
 };
 
 struct Schedule {
@@ -189,6 +192,7 @@ static void release_key(DevKey& k) {
     cudaFree(k.key);
     cudaFree(k.gal);
     cudaFree(k.perm);
+    cudaFree(k.igal);
 }
 
 // (direction, loader, epilogue) combinations the schedules use; each gets a
@@ -210,6 +214,9 @@ static void release_key(DevKey& k) {
     X(1, LD_KSFIN, EP_RESCALE)
 
 static int kernels_configured = 0;
+// co-resident 16-CTA clusters for k_foldchain (it needs D_1 = 7; 0: the fold
+// chain runs as two launches per fold).  HC_FOLDCHAIN=0 disables it.
+static int g_fc_clusters = 0;
 static int g_i2_16 = 0;  // co-resident 16-CTA clusters (0: two-prime INTTs on 8-CTA clusters)
 // co-resident 8-CTA transform clusters (one CTA per SM) on the current device
 static int max_active_clusters(int* clusters) {
@@ -271,6 +278,26 @@ static int configure_kernels() {
     {
         int n = 0;
         if (max_active_clusters(&n) == HC_OK && n > 0) g_cl_chunk = std::min(n, CL_MAX / CL_JPC_MAX);
+    }
+    CU(cudaFuncSetAttribute(k_foldchain, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
+    CU(cudaFuncSetAttribute(k_foldchain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(FC_CL);
+        cfg.blockDim = dim3(CNT);
+        cfg.dynamicSmemBytes = CL_SPREAD_SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = FC_CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_foldchain, &cfg) != cudaSuccess) n = 0;
+        cudaGetLastError();
+        const char* e = getenv("HC_FOLDCHAIN");
+        g_fc_clusters = (e && e[0] == '0') ? 0 : n;
     }
     kernels_configured = 1;
     return HC_OK;
@@ -395,6 +422,12 @@ static int load_ksk_impl(hc_ctx* h, uint32_t t, const uint64_t* ksk, int dig_hav
     CU(cudaMalloc(&k.perm, NPOLY * 2));
     CU(cudaMemcpy(k.gal, gal.data(), NPOLY * 2, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(k.perm, perm.data(), NPOLY * 2, cudaMemcpyHostToDevice));
+    {  // the automorphism is a signed bijection of the coefficients: invert it
+        std::vector<uint16_t> igal(NPOLY);
+        for (int j = 0; j < NPOLY; j++) igal[gal[j] & 0x7FFF] = (uint16_t)(j | (gal[j] & 0x8000));
+        CU(cudaMalloc(&k.igal, NPOLY * 2));
+        CU(cudaMemcpy(k.igal, igal.data(), NPOLY * 2, cudaMemcpyHostToDevice));
+    }
     CU(cudaStreamSynchronize(h->stream));
     h->keys[t] = k;
     return HC_OK;
@@ -788,6 +821,12 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
             case ST_ADD:
                 CU(launch(k_addmod, dim3(NPOLY / 256, st.rows, st.njobs), 256, 0, s, h->hctx, (const AddJob*)st.djobs, st.gy));
                 break;
+            case ST_FOLD:
+                // k_foldchain never triggers its dependents early: the next
+                // launch starts when the chain (which spins on grid barriers,
+                // all clusters co-resident) is complete
+                CU(launch_cl(k_foldchain, FC_CL, st.fc.D * FC_CL, CNT, CL_SPREAD_SMEM, s, h->hctx, st.fc));
+                break;
             case ST_I2: {
                 Intt2Jobs jj;
                 memset(&jj, 0, sizeof jj);
@@ -1133,7 +1172,7 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
     PA(P->dnttF, (size_t)P->D1 * 2 * NB);
     PA(P->corr, (size_t)2 * NB);
     PA(P->OUT, (size_t)2 * NB);
-    PA(P->ACC, (size_t)2 * 2 * 2 * NB);  // two [poly][prime][n] buffers (folds alternate)
+    PA(P->ACC, (size_t)3 * 2 * 2 * NB + 8);  // three [poly][prime][n] buffers (folds rotate) + k_foldchain's barrier counter
 #undef PA
 
     // ---- plaintexts on device (K6) ----
@@ -1589,7 +1628,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     const u64* X = P.PX + (size_t)G * 2 * 2 * NB;
     auto ex = [&](const u64* base, int g, int poly, int k) { return base + (((size_t)g * 2 + poly) * 2 + k) * NB; };
     int rc;
-    add_memset(S, P.ACC, (size_t)2 * 2 * 2 * NB * 8);
+    add_memset(S, P.ACC, ((size_t)3 * 2 * 2 * NB + 8) * 8);  // accumulators + k_foldchain's barrier counter
     // T1 (acc[g] c0 transforms; c1 of g >= 1 inverted on both primes with the
     // CRT digit split fused: k_cl_intt2)
     std::vector<XJob> t1;
@@ -1666,15 +1705,27 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
     }
     rc = add_xf(S, t3); if (rc) return rc;
     u64* res[2] = {P.RES, P.RES + (size_t)2 * 2 * NB};  // [poly][prime][n] each
+    // the fold chain as one persistent kernel (foldchain.cuh) when D_1
+    // 16-CTA clusters can be co-resident; else two launches per fold
+    const bool chain = g_fc_clusters >= D1 && D1 <= 8 && P.F >= 1 && P.F <= FC_MAXF;
+    const int nacc = chain ? 3 : 2;  // accumulator buffers the folds rotate over
+    Step fst;
+    if (chain) {
+        fst.kind = ST_FOLD;
+        fst.njobs = P.F;
+        fst.fc.F = P.F;
+        fst.fc.D = D1;
+        fst.fc.bar = reinterpret_cast<unsigned*>(P.ACC + (size_t)3 * 2 * 2 * NB);
+    }
     for (int f = 0; f < P.F; f++) {
         u64* cur = res[f % 2];
         const DevKey* ka = need_key(h, P.t_fold[f]);
         const KsSpec* d0 = upload_spec(S, s0, &rc); if (rc) return rc;
         const KsSpec* d1 = upload_spec(S, s1, &rc); if (rc) return rc;
-        // the fold's digit products go to the other ACC buffer, so the res_f.c0
+        // the fold's digit products go to the next ACC buffer, so the res_f.c0
         // finish (which reads and re-zeroes this fold's buffer) can ride in the
         // digit-NTT launch; the chain is INTT2 -> digit NTTs, one stream
-        u64* acc_next = P.ACC + (size_t)((f + 1) % 2) * 2 * 2 * NB;
+        u64* acc_next = P.ACC + (size_t)((f + 1) % nacc) * 2 * 2 * NB;
         std::vector<XJob> f3, f1;
         Intt2Job ij{};
         for (int k = 0; k < 2; k++) {
@@ -1688,14 +1739,26 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
             f1.push_back(e);
         }
         ij.dig = P.digF;
-        digit_jobs(f3, P.digF, ka, acc_next);
-        rc = add_i2(S, std::vector<Intt2Job>{ij}); if (rc) return rc;
-        const size_t n0 = S.steps.size();
-        rc = add_xf(S, f3); if (rc) return rc;
-        if (S.steps[n0].cl && S.steps[n0].njobs >= 8) {
-            S.steps[n0].side = f1;
-        } else {  // no cluster launch to ride in: a separate transform-less launch
-            rc = add_xf(S, f1); if (rc) return rc;
+        if (chain) {
+            FcFold& F = fst.fc.f[f];
+            F.base1 = s1.base;  // res_{f-1}.c1, or acc[0].c1 for fold 0 (null when acc[0] is empty)
+            F.accf = s0.acc;    // ACC[f % 3]: c0 rows, then c1 rows at +2n
+            F.s0 = d0;
+            F.cur = cur;
+            F.igal = ka->igal;
+            F.key = ka->key;
+            F.acc_next = acc_next;
+            F.acc_zero = P.ACC + (size_t)((f + 2) % 3) * 2 * 2 * NB;
+        } else {
+            digit_jobs(f3, P.digF, ka, acc_next);
+            rc = add_i2(S, std::vector<Intt2Job>{ij}); if (rc) return rc;
+            const size_t n0 = S.steps.size();
+            rc = add_xf(S, f3); if (rc) return rc;
+            if (S.steps[n0].cl && S.steps[n0].njobs >= 8) {
+                S.steps[n0].side = f1;
+            } else {  // no cluster launch to ride in: a separate transform-less launch
+                rc = add_xf(S, f1); if (rc) return rc;
+            }
         }
         // res_{f+1} = res_f + rot(res_f, a)
         s0 = KsSpec{};
@@ -1712,6 +1775,7 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
         s0.t[0].c0src = cur;
         s0.t[0].perm = ka->perm;
     }
+    if (chain) S.steps.push_back(fst);
     // D1/D2: mul_plain(res_F, output_mask) level 1 -> 0
     u64* fin = res[P.F % 2];
     const KsSpec* d0 = upload_spec(S, s0, &rc); if (rc) return rc;
@@ -2793,6 +2857,16 @@ extern "C" int hc_trace_reset(void) {
     CU(cudaMemcpyToSymbol(g_trace, zero, sizeof(zero)));
 #endif
     return HC_OK;
+}
+extern "C" int hc_trace_read_tail(uint64_t* out) {
+#ifdef HC_TRACE
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpyFromSymbol(out, g_fc_trace, sizeof(g_fc_trace)));
+    return HC_OK;
+#else
+    (void)out;
+    return fail(HC_ERR_STATE, "library built without HC_TRACE");
+#endif
 }
 extern "C" int hc_trace_read(uint64_t* out) {
 #ifdef HC_TRACE

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol(max_level, plain_row):
     assert len(syms) >= 20
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
-    assert set(syms) <= set(_lib.EXPORTS) | {"hc_trace_reset", "hc_trace_read"}
+    assert set(syms) <= set(_lib.EXPORTS) | {"hc_trace_reset", "hc_trace_read", "hc_trace_read_tail"}
     assert L.hc_plain_row() == plain_row  # csrc/ctx.cuh PIDX = MAXL + 1: rows 0..MAXL are chain primes
 
 
