@@ -42,7 +42,7 @@ N_DEFAULT, S_DEFAULT, P_DEFAULT, RING = 1 << 14, 16, 65537, 8192
 
 
 # hcomp.cu StepKind -> the kernels behind it (hc_comp_profile's step kinds)
-STEP_KINDS = {0: "transforms (k_xf, k_xf_cl)", 1: "crt_digits (k_compose)", 2: "key_mac (k_ksmac)",
+STEP_KINDS = {10: "key_switch_fused (k_ksfused, HC_KSFUSED=1)", 0: "transforms (k_xf, k_xf_cl)", 1: "crt_digits (k_compose)", 2: "key_mac (k_ksmac)",
               3: "diag_mac (k_diagx)", 5: "memset", 6: "two_prime_intt (k_cl_intt2)",
               7: "key_mac_grouped (k_ksmac_mb)", 8: "add (k_addmod)", 9: "fold_chain (k_tail, persistent)"}
 
@@ -65,7 +65,9 @@ def make_parser() -> argparse.ArgumentParser:
     ap.add_argument("--p", type=int, default=0, help="plaintext prime (default: 65537, or per SURVEY F4 for N >= p)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-flush", type=int, default=1, help="flush L2 inside the streamed e2e loop (counted)")
+    ap.add_argument("--e2e-flush", type=int, default=1, help="single-context streamed e2e: flush L2 inside the loop (counted)")
+    ap.add_argument("--e2e-contexts", type=int, default=0,
+                    help="independent query contexts the streamed e2e rotates over (0: 3 below N=2^19, else 1)")
     ap.add_argument("--queries", type=int, default=0,
                     help="config 5: Q independent queries (own seeded keys and payloads, one shared database "
                          "shape) spread over the ranks; a step runs every query once; value = aggregate entries/s")
@@ -750,75 +752,99 @@ def main():
     e2e_serial_ms = sum(a.elapsed_time(b) for a, b in e2e_evs)
     e2e_ms = e2e_serial_ms
     e2e_stream_ms = None
+    e2e_rot = None
     if not shard:
-        # ---- streamed end to end: step i+1's inputs go up over PCIe (H2D
-        # stream) while step i computes, step i's result comes back (D2H
-        # stream) while step i+1 computes; every step still copies its own
-        # inputs in and its result out inside the timed region, and the L2
-        # flush stays in the loop (its time is counted).  Steps alternate
-        # between two DIFFERENT input sets (a second encryption of the same
-        # payload), and each result is copied on the compute stream into one
-        # of two device staging slots before its D2H, so step i+1's Comp
-        # never overwrites an answer still being read back: both final
-        # answers are checked against their own device-resident results ----
-        cts2 = P.encrypt_vector(dense, params, be, keys)
-        hint2 = P.encrypt_vector([1 if x else 0 for x in dense], params, be, keys)
-        cd2 = np.ascontiguousarray(np.stack([c.payload.res for c in cts2]))
-        cv2 = np.ascontiguousarray(np.stack([c.payload.res for c in hint2]))
-        dc.set_inputs(cd2, cv2)
-        dc.launch(sh)
-        out2 = output()
-        dc.set_inputs(cd, cv)
-        src_h = [(cd_h, cv_h), (torch.from_numpy(cd2).pin_memory(), torch.from_numpy(cv2).pin_memory())]
-        want = [out, out2]
+        # ---- streamed end to end: the serving pipeline.  Step i+1's inputs go
+        # up over PCIe (hc_comp_upload_async on a copy stream) while step i
+        # computes (hc_comp_launch) and step i-1's answer comes back
+        # (hc_comp_get_output_async on a third stream); every step still copies
+        # its own inputs in and its answer out inside the timed region.  The
+        # steps rotate over R independent query contexts -- own seeded keys,
+        # payload, plan (diagonals not shared) and device buffers -- whose
+        # keys + diagonals (R x ~117 MB at the headline) do not fit the 126 MB
+        # L2 together: between two uses of a context the other contexts'
+        # streams evict it, so every step starts cold WITHOUT a flush in the
+        # timed loop (the contract's "inputs larger than L2" option; checked
+        # below: the device-resident rotation runs at the flushed latency).
+        # Every context's final answer is checked against its own
+        # device-resident result ----
+        R = args.e2e_contexts if args.e2e_contexts > 0 else (3 if args.N < (1 << 19) else 1)
+        Cn = cd.shape[0]
+        ctxs = [dict(be=be, keys=keys, dc=dc, h=h, cd_h=cd_h, cv_h=cv_h, want=out)]
+        for r in range(1, R):
+            sd = 1000 + 16 * rank + r
+            be_r = P.B200BgvBackend(he, seed=sd, device=local, noise_guard=False)
+            keys_r = be_r.keygen(*P.plan_rotation_amounts(args.s, RING))
+            dense_r = plant(args.N, args.s, p, sd)
+            cd_r = np.ascontiguousarray(np.stack([c.payload.res for c in P.encrypt_vector(dense_r, params, be_r, keys_r)]))
+            cv_r = np.ascontiguousarray(np.stack([c.payload.res for c in P.encrypt_vector([1 if x else 0 for x in dense_r], params, be_r, keys_r)]))
+            dc_r = P.DeviceComp(be_r, params, keys_r)
+            dc_r.set_inputs(cd_r, cv_r)
+            dc_r.launch(sh)
+            torch.cuda.synchronize()
+            ctxs.append(dict(be=be_r, keys=keys_r, dc=dc_r, h=be_r._ctx(), cd_h=torch.from_numpy(cd_r).pin_memory(),
+                             cv_h=torch.from_numpy(cv_r).pin_memory(), want=dc_r.output()))
+        for c in ctxs:
+            c["out_h"] = torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
-        stage = [torch.empty((2,) + cd.shape, dtype=cd_h.dtype, device="cuda") for _ in range(2)]
-        outs_dev = [torch.empty((2, 1, RING), dtype=torch.int64, device="cuda") for _ in range(2)]
-        outs = [torch.empty((2, 1, RING), dtype=torch.int64).pin_memory() for _ in range(2)]
         ev = lambda: torch.cuda.Event()
-        h2d_done = [ev() for _ in range(args.steps)]
-        set_done = [ev() for _ in range(args.steps)]
-        comp_done = [ev() for _ in range(args.steps)]
-        d2h_done = [ev() for _ in range(args.steps)]
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
 
-        def upload(i):
-            with torch.cuda.stream(h2d_s):
-                if i >= 2:
-                    h2d_s.wait_event(set_done[i - 2])  # staging buffer free again
-                stage[i % 2][0].copy_(src_h[i % 2][0], non_blocking=True)
-                stage[i % 2][1].copy_(src_h[i % 2][1], non_blocking=True)
-                h2d_done[i].record(h2d_s)
+        def pipeline(nsteps, timed):
+            up_done = [ev() for _ in range(nsteps)]
+            comp_done = [ev() for _ in range(nsteps)]
+            d2h_done = [ev() for _ in range(nsteps)]
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
-        with torch.cuda.stream(stream):
-            t0.record(stream)
-            h2d_s.wait_event(t0)
-            upload(0)
-            for i in range(args.steps):
-                if i + 1 < args.steps:
-                    upload(i + 1)
-                if args.e2e_flush:
-                    flush.zero_()
-                stream.wait_event(h2d_done[i])
-                st_i = stage[i % 2]
-                _lib.check(L.hc_comp_set_inputs_device(h, st_i[0].data_ptr(), st_i[1].data_ptr(), cd.shape[0], sh))
-                set_done[i].record(stream)
-                dc.launch(sh)
-                if i >= 2:
-                    stream.wait_event(d2h_done[i - 2])  # staging slot read back
-                _lib.check(L.hc_comp_get_output_async(h, outs_dev[i % 2].data_ptr(), sh))  # device to device
-                comp_done[i].record(stream)
-                d2h_s.wait_event(comp_done[i])
-                with torch.cuda.stream(d2h_s):
-                    outs[i % 2].copy_(outs_dev[i % 2], non_blocking=True)
+            def upload(i):
+                c = ctxs[i % R]
+                if i >= R:
+                    h2d_s.wait_event(comp_done[i - R])  # this context's previous Comp has read its inputs
+                _lib.check(L.hc_comp_upload_async(c["h"], c["cd_h"].data_ptr(), c["cv_h"].data_ptr(), Cn, h2d_s.cuda_stream))
+                up_done[i].record(h2d_s)
+
+            with torch.cuda.stream(stream):
+                t0.record(stream)
+                h2d_s.wait_event(t0)
+                d2h_s.wait_event(t0)
+                upload(0)
+                for i in range(nsteps):
+                    c = ctxs[i % R]
+                    stream.wait_event(up_done[i])
+                    if i >= R:
+                        stream.wait_event(d2h_done[i - R])  # this context's previous answer was read back
+                    if R == 1 and args.e2e_flush and args.N < (1 << 19):
+                        flush.zero_()  # a single small context would stay L2-resident (counted)
+                    c["dc"].launch(sh)
+                    comp_done[i].record(stream)
+                    if i + 1 < nsteps:
+                        upload(i + 1)
+                    d2h_s.wait_event(comp_done[i])
+                    _lib.check(L.hc_comp_get_output_async(c["h"], c["out_h"].data_ptr(), d2h_s.cuda_stream))
                     d2h_done[i].record(d2h_s)
-            stream.wait_event(d2h_done[-1])
-            t1.record(stream)
+                stream.wait_event(d2h_done[-1])
+                t1.record(stream)
+            torch.cuda.synchronize()
+            return t0.elapsed_time(t1)
+
+        pipeline(2 * R, False)  # warm
+        if dist:
+            dist.barrier()
+        e2e_stream_ms = pipeline(args.steps, True)
+        for c in ctxs[: min(R, args.steps)]:
+            assert np.array_equal(c["out_h"].numpy().view(np.uint64), c["want"]), "streamed e2e answer differs"
+        # coldness check of the rotation: device-resident Comps round-robin over
+        # the contexts, no flush, against the flushed latency reported as `value`
+        rot_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        with torch.cuda.stream(stream):
+            for i in range(2 * R):
+                ctxs[i % R]["dc"].launch(sh)
+            for i, (a, b) in enumerate(rot_evs):
+                a.record(stream)
+                ctxs[i % R]["dc"].launch(sh)
+                b.record(stream)
         torch.cuda.synchronize()
-        e2e_stream_ms = t0.elapsed_time(t1)
-        for i in range(max(0, args.steps - 2), args.steps):
-            assert np.array_equal(outs[i % 2].numpy().view(np.uint64), want[i % 2]), "streamed e2e output differs"
+        e2e_rot = {"contexts": R, "device_resident_ms_per_step_no_flush": statistics.median(a.elapsed_time(b) for a, b in rot_evs),
+                   "device_resident_ms_per_step_flushed": statistics.median(step_ms)}
         # both are end to end (every step copies its inputs in and its answer
         # out inside the timed region); the line reports the faster schedule
         e2e_ms = min(e2e_serial_ms, e2e_stream_ms)
@@ -886,16 +912,19 @@ def main():
                       "memory, the Comp (hc_comp_async: one graph launch) and the D2H of the answer; L2 "
                       "flushed before every step, untimed as for value")
                      if e2e_stream_ms is None or e2e_serial_ms <= e2e_stream_ms else
-                     "streamed: step i+1's H2D and step i's D2H overlap computation on copy streams; L2 "
-                     "flush inside the timed loop (counted)"),
+                     "streamed: step i+1's H2D (hc_comp_upload_async, copy stream) and step i-1's D2H overlap "
+                     "step i's Comp; steps rotate over independent query contexts (own keys, plan, buffers) "
+                     "whose keys + diagonals exceed L2 together, so each step is cold without a flush"),
             "serial_ms_per_step": e2e_serial_ms / args.steps,
             "streamed_ms_per_step": (e2e_stream_ms / args.steps) if e2e_stream_ms else None,
+            "streamed_rotation": e2e_rot,
             "h2d_bytes_per_step": h2d_bytes,
             "d2h_bytes_per_step": 2 * RING * 8,
             "h2d_gbs_measured": h2d_gbs,
             "h2d_note": "pinned host memory; the two input lists go up on two copy engines (hc_comp_async)",
         },
-        "gpu_launches": int(info["kernel_launches"]) * args.steps * 2,
+        # timed regions: device-resident, serial e2e and (unsharded) streamed e2e, `steps` Comps each
+        "gpu_launches": int(info["kernel_launches"]) * args.steps * (2 if shard else 3),
         "kernel_launches_per_comp": int(info["kernel_launches"]),
         "roofline": rf,
         "clocks": clk,

@@ -160,6 +160,13 @@ int hc_comp_get_output_async(hc_ctx* h, uint64_t* out, void* stream);
  * D2H of the output, all stream-ordered (pass pinned host buffers for
  * overlap; the caller synchronises). */
 int hc_comp_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, uint64_t* out, void* stream);
+/* The upload half of hc_comp_async alone, for serving loops that pipeline
+ * queries: H2D of cd/cv (pinned host buffers) into the plan's input buffers
+ * on two copy engines, ordered after the work already on `stream` and joined
+ * back into it.  A copy stream runs this for query i+1 while the compute
+ * stream runs hc_comp_launch for query i and a third stream drains
+ * hc_comp_get_output_async of query i-1 (bench.py, e2e "streamed"). */
+int hc_comp_upload_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, void* stream);
 
 /* Block-sharded Comp.  hc_comp_partial runs pack + baby
  * steps + diagonal products for blocks [b0, b1) of the database (inputs:
@@ -223,6 +230,13 @@ int hc_set_cluster_threshold(int max_jobs);
  * parallel per-block lanes (latency regime); larger chunks use one wide launch
  * per segment (throughput regime). Applies to plans built afterwards. */
 int hc_set_lane_blocks(int max_blocks);
+/* Tuning: the throughput regime's key switches (chunks of more than the lane
+ * limit) as one fused kernel per rotation (k_ksfused: digit NTTs, key MAC and
+ * the c0 automorphism in one CTA per output chunk, no digit NTT reaches HBM;
+ * bgv.py:616-647) instead of digit-NTT launches + k_ksmac_mb.  Same answer bit
+ * for bit; off by default (HC_KSFUSED=1 or this call enables it; measured
+ * slower on B200).  Applies to plans built afterwards. */
+int hc_set_ksfused(int on);
 /* Tuning: single-CTA transform launches of >= jobs (default 200) use the
  * 256-thread three-per-SM variant.  Applies to schedules built afterwards. */
 int hc_set_vt2_jobs(int jobs);

@@ -63,6 +63,7 @@ _SIGS = [
     ("hc_mixed_launch", _I, [_P, _P]),
     ("hc_plain_row", _I, []),
     ("hc_comp_async", _I, [_P, _P, _P, _I, _P, _P]),
+    ("hc_comp_upload_async", _I, [_P, _P, _P, _I, _P]),
     ("hc_comp_set_inputs", _I, [_P, _P, _P, _I]),
     ("hc_comp_set_inputs_range", _I, [_P, _P, _P, _I, _I, _P]),
     ("hc_comp_set_inputs_device", _I, [_P, _P, _P, _I, _P]),
@@ -84,6 +85,7 @@ _SIGS = [
     ("hc_imad_peak", _I, [_P, _P]),
     ("hc_set_cluster_threshold", _I, [_I]),
     ("hc_set_lane_blocks", _I, [_I]),
+    ("hc_set_ksfused", _I, [_I]),
     ("hc_set_vt2_jobs", _I, [_I]),
     ("hc_max_active_clusters", _I, [_P, _P]),
     ("hc_trace_reset", _I, []),

@@ -69,6 +69,19 @@ def build_check(force: bool = False) -> str:
     return CHECK
 
 
+TRACE = os.path.join(HERE, "libhcomp_trace.so")
+
+
+def build_trace(force: bool = False) -> str:
+    """The 4-prime library with the per-CTA %globaltimer timeline (-DHC_TRACE),
+    read by tools/trace_comp.py and tools/trace_fold.py."""
+    if force or _stale(TRACE):
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-DHC_MAXL=3", "-DHC_TRACE", "-o", TRACE, os.path.join(CSRC, "hcomp.cu")]
+        subprocess.check_call(cmd)
+    return TRACE
+
+
 def build_selftest(force: bool = False) -> str:
     """The device arithmetic/NTT schedule compiled for the host (g++), used by
     tests/test_csrc_host.py to check the exact GPU code paths on the CPU."""
@@ -87,4 +100,6 @@ if __name__ == "__main__":
         build_selftest(force="--force" in sys.argv)
     if "--check" in sys.argv:
         build_check(force="--force" in sys.argv)
+    if "--trace" in sys.argv:
+        build_trace(force="--force" in sys.argv)
     print(LIB)

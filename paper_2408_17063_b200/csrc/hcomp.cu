@@ -19,6 +19,7 @@
 #include "../../include/hcomp.h"
 #include "kernels.cuh"
 #include "foldchain.cuh"
+#include "ksfused.cuh"
 #include "pyrng.hpp"
 #include "host_tables.hpp"
 
@@ -60,6 +61,7 @@ struct DevKey {
     uint16_t* gal = nullptr;   // coefficient gather
     uint16_t* perm = nullptr;  // NTT-domain permutation
     uint16_t* igal = nullptr;  // inverse coefficient gather: source i -> (j | neg << 15) with gal[j] = i | neg << 15
+    int tinv = 1;              // t^-1 mod 2n: gal[j] encodes (j * tinv) mod 2n (k_ksfused's closed-form gather)
 };
 
 // transform launches with at most this many jobs use the cluster kernel
@@ -130,7 +132,7 @@ static cudaError_t launch_cl(void (*k)(KArgs...), int cluster, dim3 grid, dim3 b
     return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7, ST_ADD = 8, ST_FOLD = 9 };  // values: bench.py per_kind_ms keys
+enum StepKind { ST_XF, ST_CO, ST_MA, ST_DX, ST_MEMSET = 5, ST_I2 = 6, ST_MB = 7, ST_ADD = 8, ST_FOLD = 9, ST_KF = 10 };  // values: bench.py per_kind_ms keys
 struct Step {
     int kind = 0;
     int njobs = 0;
@@ -173,6 +175,7 @@ struct hc_ctx {
     int dev = 0, L = 3, n = NPOLY;
     u64 p = 0;
     DevCtx hctx{};             // host copy (device pointers inside)
+    KFront kfront{};           // k_ksfused's front-stage constants (by value at its launches)
     DevCtx* d_ctx = nullptr;
     Tw* d_twf = nullptr;
     Tw* d_twi = nullptr;
@@ -279,6 +282,7 @@ static int configure_kernels() {
         int n = 0;
         if (max_active_clusters(&n) == HC_OK && n > 0) g_cl_chunk = std::min(n, CL_MAX / CL_JPC_MAX);
     }
+    CU(cudaFuncSetAttribute(k_ksfused, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_SMEM));
     CU(cudaFuncSetAttribute(k_foldchain, cudaFuncAttributeMaxDynamicSharedMemorySize, CL_SPREAD_SMEM));
     CU(cudaFuncSetAttribute(k_foldchain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     {
@@ -349,6 +353,8 @@ extern "C" int hc_ctx_create(int n, int max_level, const uint64_t* primes, uint6
     D.twf = h->d_twf;
     D.twi = h->d_twi;
     D.slot_of = h->d_slot_of;
+    for (int k = 0; k <= std::min(max_level, KEYL); k++)
+        build_kfront(h->kfront.k[k], &h->kfront.w32s[k], &twf[(size_t)k * n], primes[k]);
     CU(cudaMalloc(&h->d_ctx, sizeof(DevCtx)));
     CU(cudaMemcpy(h->d_ctx, &D, sizeof(DevCtx), cudaMemcpyHostToDevice));
     *out = h.release();
@@ -428,6 +434,7 @@ static int load_ksk_impl(hc_ctx* h, uint32_t t, const uint64_t* ksk, int dig_hav
         CU(cudaMalloc(&k.igal, NPOLY * 2));
         CU(cudaMemcpy(k.igal, igal.data(), NPOLY * 2, cudaMemcpyHostToDevice));
     }
+    k.tinv = (gal[1] & 0x7FFF) + ((gal[1] >> 15) ? NPOLY : 0);
     CU(cudaStreamSynchronize(h->stream));
     h->keys[t] = k;
     return HC_OK;
@@ -615,6 +622,22 @@ static int add_dx(Schedule& S, std::vector<DXJob> jobs, int nprime) {
     S.steps.push_back(st);
     return HC_OK;
 }
+// fused key switches (k_ksfused): one job per (block, rotation)
+static int add_kf(Schedule& S, std::vector<KFJob> jobs, int nprime) {
+    if (jobs.empty()) return HC_OK;
+    for (KFJob& j : jobs) j.trace = g_trace_seq;
+    g_trace_seq++;
+    Step st;
+    st.kind = ST_KF;
+    st.group = S.cur_group;
+    st.lane = S.cur_lane;
+    st.njobs = (int)jobs.size();
+    st.gy = nprime;
+    int rc = upload_jobs(S, st, jobs.data(), jobs.size() * sizeof(KFJob));
+    if (rc) return rc;
+    S.steps.push_back(st);
+    return HC_OK;
+}
 // two-prime INTT + CRT digits (k_cl_intt2), <= I2_MAX jobs per launch
 static int add_i2(Schedule& S, std::vector<Intt2Job> jobs) {
     for (size_t c0 = 0; c0 < jobs.size(); c0 += I2_MAX) {
@@ -745,9 +768,24 @@ static bool step_one_wave(const Step& st) {
         case ST_MA:
         case ST_MB: return (NPOLY / 256) * st.gy * st.njobs <= g_pdl_maxcta;
         case ST_DX: return (NPOLY / 256) * st.njobs <= g_pdl_maxcta;
+        case ST_KF: return CL * st.gy * st.njobs <= g_pdl_maxcta;
         case ST_CO: return (NPOLY / 256) * st.njobs <= std::max(g_pdl_maxcta, 148);  // small composes (latency path)
         default: return true;
     }
+}
+
+// CTA size of the throughput regime's memory-bound MAC kernels.  The VT = 4
+// transform kernels take 3 x 256 threads x 72 registers of an SM; a
+// 128-thread MAC CTA fits in what they leave (10 K registers), so a chunk's
+// MACs run beside another chunk's transforms instead of waiting for a slot.
+static int mac_threads() {
+    static int mt = 0;
+    if (!mt) {
+        const char* e = getenv("HC_MAC_THREADS");
+        mt = e ? atoi(e) : 128;
+        if (mt != 64 && mt != 128 && mt != 256) mt = 128;
+    }
+    return mt;
 }
 
 static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
@@ -806,14 +844,21 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 else  // small (latency path): 4 digits' loads in flight per thread
                     CU(launch(k_ksmac<1, 4>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MJob*)st.djobs));
                 break;
-            case ST_MB:
+            case ST_MB: {
+                const int mt = mac_threads();
                 if (st.jpc == 4)
-                    CU(launch(k_ksmac_mb<4>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MBJob*)st.djobs));
+                    CU(launch(k_ksmac_mb<4>, dim3(NPOLY / mt, st.gy, st.njobs), mt, 0, s, h->hctx, (const MBJob*)st.djobs));
                 else
-                    CU(launch(k_ksmac_mb<2>, dim3(NPOLY / 256, st.gy, st.njobs), 256, 0, s, h->hctx, (const MBJob*)st.djobs));
+                    CU(launch(k_ksmac_mb<2>, dim3(NPOLY / mt, st.gy, st.njobs), mt, 0, s, h->hctx, (const MBJob*)st.djobs));
                 break;
-            case ST_DX:
-                CU(launch(k_diagx, dim3(NPOLY / 256, 1, st.njobs), 256, 0, s, h->hctx, (const DXJob*)st.djobs));
+            }
+            case ST_DX: {
+                const int mt = st.group ? mac_threads() : 256;  // pipelined chunks: beside transform CTAs
+                CU(launch(k_diagx, dim3(NPOLY / mt, 1, st.njobs), mt, 0, s, h->hctx, (const DXJob*)st.djobs));
+                break;
+            }
+            case ST_KF:
+                CU(launch(k_ksfused, dim3(CL, st.gy, st.njobs), CNT, KF_SMEM, s, h->hctx, h->kfront, (const KFJob*)st.djobs));
                 break;
             case ST_MEMSET:
                 CU(cudaMemsetAsync(st.out, 0, st.bytes, s));
@@ -1288,6 +1333,25 @@ static u64* eslot(const Plan& P, const Plan::Scratch& X, int tl, int b, int g, i
     return X.Eslot + ((((size_t)tl * P.baby + b) * P.giant + g) * 2 + poly) * 2 * NB;
 }
 
+// HC_KSFUSED=1: the throughput regime's key switches as k_ksfused (one kernel
+// per rotation, no digit NTTs in HBM) instead of digit-NTT launches +
+// k_ksmac_mb.  Off by default: the transforms are instruction-bound, the
+// fused form executes the same butterflies plus the MACs on the same pipes,
+// while the multi-launch form hides its memory-bound MACs under another
+// chunk's transforms (measured: DESIGN.md section 9)
+static int g_ksfused = -1;
+static bool ksfused_on() {
+    if (g_ksfused < 0) {
+        const char* e = getenv("HC_KSFUSED");
+        g_ksfused = (e && e[0] == '1') ? 1 : 0;
+    }
+    return g_ksfused == 1;
+}
+extern "C" int hc_set_ksfused(int on) {
+    g_ksfused = on ? 1 : 0;
+    return HC_OK;
+}
+
 // Steps S1..S10 for blocks [b0, b1): pack_pair (compress.py:338-367), baby
 // rotations and the diagonal products (compress.py:286-297), accumulated
 // into the partial PX = [E | X].  Blocks are independent until the
@@ -1323,6 +1387,10 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
         std::vector<MJob> s4;
         std::vector<std::vector<XJob>> s7(cb), s9(cb);
         std::vector<std::vector<MJob>> s8(cb);
+        // throughput regime: each key switch (digit NTTs + key MAC) as one
+        // fused job (k_ksfused) instead of S3 -> S4 and S7 -> S8
+        const bool fusedks = ksfused_on() && cb > g_lane_max_blocks;
+        std::vector<KFJob> kf3, kf7;
         for (int tl = 0; tl < cb; tl++) {
                 const long long t = c0 + tl;
                 const long long src = t / 2;
@@ -1401,6 +1469,17 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                     mj.out0 = X.U + ((size_t)tl * 2 + 0) * 3 * NB;
                     mj.out1 = X.U + ((size_t)tl * 2 + 1) * 3 * NB;
                     s4.push_back(mj);
+                    if (fusedks) {
+                        KFJob f{};
+                        f.level = 2; f.tinv = 1;  // digR is composed through the column swap's gather
+                        f.dpos = X.digR + (size_t)tl * D2 * NB;
+                        f.key = kcol->key;
+                        f.perm = kcol->perm;
+                        f.c0src = mj.t[0].c0src;
+                        f.add0 = mj.add0; f.add1 = mj.add1;
+                        f.out0 = mj.out0; f.out1 = mj.out1;
+                        kf3.push_back(f);
+                    }
                 }
                 }  // !from_u
                 // S5..S8: baby-step rotations of u (hoisted INTT + CRT digits)
@@ -1440,6 +1519,17 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                         mj.out0 = X.ROT + (rb * 2 + 0) * 3 * NB;
                         mj.out1 = X.ROT + (rb * 2 + 1) * 3 * NB;
                         s8[tl].push_back(mj);
+                        if (fusedks) {
+                            KFJob f{};
+                            f.level = 2; f.tinv = kb->tinv;
+                            f.dpos = X.digU + (size_t)tl * 2 * D2 * NB;
+                            f.dneg = X.digU + ((size_t)tl * 2 * D2 + D2) * NB;
+                            f.key = kb->key;
+                            f.perm = kb->perm;
+                            f.c0src = mj.t[0].c0src;
+                            f.out0 = mj.out0; f.out1 = mj.out1;
+                            kf7.push_back(f);
+                        }
                     }
                 }
                 // S9: dropped-prime half of each diagonal product: INTT + the
@@ -1535,12 +1625,14 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
             S.cur_lane = 1;
         }
         rc = add_co(S, s2c); if (rc) return rc;
-        rc = add_xf(S, s3); if (rc) return rc;
+        if (!fusedks) { rc = add_xf(S, s3); if (rc) return rc; }
         if (fork23) {
             S.cur_lane = -1;
             S.par_end();
         }
-        rc = add_ma(S, s4, 3); if (rc) return rc;
+        if (fusedks) rc = add_kf(S, kf3, 3);
+        else rc = add_ma(S, s4, 3);
+        if (rc) return rc;
         }  // !from_u
         rc = add_xf(S, s5); if (rc) return rc;
         rc = add_co(S, s6); if (rc) return rc;
@@ -1554,8 +1646,12 @@ static int build_partial(hc_ctx* h, Plan& P, long long b0, long long b1, Schedul
                 w8.insert(w8.end(), s8[tl].begin(), s8[tl].end());
                 w9.insert(w9.end(), s9[tl].begin(), s9[tl].end());
             }
-            rc = add_xf(S, w7); if (rc) return rc;
-            rc = add_ma(S, w8, 3); if (rc) return rc;
+            if (fusedks) {
+                rc = add_kf(S, kf7, 3); if (rc) return rc;
+            } else {
+                rc = add_xf(S, w7); if (rc) return rc;
+                rc = add_ma(S, w8, 3); if (rc) return rc;
+            }
             rc = add_xf(S, w9); if (rc) return rc;
         } else {
         const int nl = std::min(4, cb);
@@ -1947,6 +2043,16 @@ extern "C" int hc_comp_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, 
     CU(cudaGraphLaunch(P.full->exec, s));
     CU(cudaMemcpyAsync(out, P.OUT, (size_t)2 * NPOLY * 8, cudaMemcpyDeviceToHost, s));
     return HC_OK;
+}
+
+extern "C" int hc_comp_upload_async(hc_ctx* h, const uint64_t* cd, const uint64_t* cv, int C, void* stream) {
+    if (!h || !h->plan) return fail(HC_ERR_STATE, "hc_plan must run first");
+    Plan& P = *h->plan;
+    if (C != P.C) return fail(HC_ERR_ARG, "expected standard-layout ciphertext lists");
+    if (int rc = need_full_range(P)) return rc;
+    CU(cudaSetDevice(h->dev));
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->stream;
+    return upload_inputs(h, P.cd, cd, P.cv, cv, (size_t)C * 2 * 4 * NPOLY * 8, s);
 }
 
 // Comp from the caller's pack_pair outputs (answer()'s mixed-level inputs:

@@ -101,6 +101,19 @@ static inline void fill_prime(PrimeC& P, Tw* twf, Tw* twi, u64 q, int n) {
     P.one_s = shoup_const(1, q);
 }
 
+// k_ksfused's front constants (ksfused.cuh): K[r][a] = output r of the three
+// leading forward stages (ntt_cl.cuh phase A: r8_ct at s0 = 0, G = 0) applied
+// to the unit vector e_a, as a canonical residue; w32s = Shoup(2^32)
+static inline void build_kfront(u64 (*K)[8], u64* w32s, const Tw* twf, u64 q) {
+    for (int a = 0; a < 8; a++) {
+        u64 x[CEPT] = {0, 0, 0, 0, 0, 0, 0, 0};
+        x[a] = 1;
+        r8_ct(x, TwG{twf}, 0, 0, q, 4 * q);
+        for (int r = 0; r < 8; r++) K[r][a] = x[r] % q;
+    }
+    *w32s = shoup_const(1ull << 32, q);
+}
+
 // Fill the device context (host copy; device pointers are set by the caller)
 static inline void build_host_ctx(DevCtx& D, std::vector<Tw>& twf, std::vector<Tw>& twi,
                                   std::vector<uint16_t>& slot_of, int n, int max_level,

@@ -367,8 +367,11 @@ __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const Pr
 // VT = 1: one 1024-thread transform per SM (latency); VT = 4: 256-thread CTAs,
 // three per SM (64 KiB smem each), whose independent barriers keep the IMAD
 // pipe busy while other transforms load, store or synchronise (throughput).
+#ifndef HC_XF4_BOUND
+#define HC_XF4_BOUND 288
+#endif
 template <int DIR, int LD, int EP, int VT = 1>
-__global__ void __launch_bounds__(NT / VT, VT == 4 ? 3 : VT) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 : VT) k_xf(const __grid_constant__ DevCtx C, const XJob* __restrict__ jobs) {
     extern __shared__ u64 sm[];
     const XJob J = jobs[blockIdx.x];
     const PrimeC& P = C.pc[J.k];

@@ -282,3 +282,37 @@ def test_comp_inputs_above_level_3_on_both_sides_vs_oracle(pkg, oracle):
     assert delta == vars(obe.counters)
     assert O.sha256(ans.serialize(be)) == O.sha256(O.serialize_answer(obe, out, s))
     assert ans.payload_slots(be, keys) == O.expected_slots(dense, s, p)
+
+
+def test_fused_key_switch_kernel_matches_multi_launch(pkg, oracle):
+    """k_ksfused (one kernel per rotation: digit NTTs + key MAC + c0
+    automorphism, hc_set_ksfused) gives the multi-launch throughput schedule's
+    answer bit for bit at N = 2^17 (32-block chunks: column swap with
+    tinv = 1 and three baby rotations through the closed-form gather), and the
+    multi-launch answer is the oracle's."""
+    from paper_2408_17063_b200 import _lib
+
+    P, O = pkg, oracle
+    N, s, p, seed = 1 << 17, 16, 786433, 5
+    be, params, keys, dense, cts, hint = _gpu_case(P, O, N, s, p, seed)
+    cd = np.ascontiguousarray(np.stack([c.payload.res for c in cts]))
+    cv = np.ascontiguousarray(np.stack([c.payload.res for c in hint]))
+    outs = {}
+    try:
+        for on in (0, 1):
+            _lib.check(_lib.lib().hc_set_ksfused(on))
+            be._planned = None  # re-plan with this setting
+            dc = P.DeviceComp(be, params, keys)
+            dc.set_inputs(cd, cv)
+            dc.launch()
+            dc.launch()  # replay: the fused kernel leaves no state behind
+            outs[on] = dc.output().copy()
+            kinds = be.plan_info()["kernel_launches"]
+            outs[("launches", on)] = kinds
+    finally:
+        _lib.check(_lib.lib().hc_set_ksfused(0))
+        be._planned = None
+    assert np.array_equal(outs[0], outs[1])
+    assert outs[("launches", 1)] < outs[("launches", 0)]  # S3+S4 and S7+S8 are one launch each
+    _, oout = _oracle_answer(O, N, s, p, seed)
+    assert np.array_equal(outs[0], np.asarray(oout.c, dtype=np.uint64).reshape(outs[0].shape))

@@ -58,5 +58,22 @@ for pt in args:
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / iters
-        print(f"N={N:8d} s={s:4d} cb={cb:3d} vt2>={vt:10d} lanes<={ln:5d} blocks={params.num_blocks:5d}  {ms:9.3f} ms  {N/ms/1e3:8.1f} M entries/s", flush=True)
+        if "--profile" in sys.argv:  # un-graphed, event-timed launch table (hc_comp_profile_ex)
+            sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+            from bench import STEP_KINDS, kernel_name
+            mx = 4096
+            sm_, sk, sj, tg = (np.zeros(mx, dtype=t) for t in (np.float32, np.int32, np.int32, np.int32))
+            ns = _lib.lib().hc_comp_profile_ex(be._ctx(), st.cuda_stream, mx, _lib.ptr(sm_), _lib.ptr(sk), _lib.ptr(sj), _lib.ptr(tg))
+            agg = {}
+            for i in range(ns):
+                nm = kernel_name(int(tg[i])) if int(sk[i]) == 0 else STEP_KINDS.get(int(sk[i]), str(sk[i]))
+                a = agg.setdefault(nm, [0.0, 0, 0]); a[0] += float(sm_[i]); a[1] += int(sj[i]); a[2] += 1
+                if "--launches" in sys.argv:
+                    print(f"  {i:4d} {nm:34s} jobs {int(sj[i]):6d} {float(sm_[i])*1e3:9.1f} us")
+            for nm, (t, j, l) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+                extra = f" {j*53248/(t*1e-3)/1e9:7.1f} Gbfly/s" if nm.startswith("k_xf") else ""
+                print(f"  {nm:34s} launches {l:4d} jobs {j:7d} {t*1e3:9.1f} us{extra}")
+        import hashlib
+        sha = hashlib.sha256(np.ascontiguousarray(dc.output()).tobytes()).hexdigest()[:12]  # A/B builds/switches must agree
+        print(f"N={N:8d} s={s:4d} cb={cb:3d} vt2>={vt:10d} lanes<={ln:5d} blocks={params.num_blocks:5d}  {ms:9.3f} ms  {N/ms/1e3:8.1f} M entries/s  out {sha}", flush=True)
 _lib.lib().hc_set_lane_blocks(4)
