@@ -66,6 +66,8 @@ def make_parser() -> argparse.ArgumentParser:
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-flush", type=int, default=1, help="single-context streamed e2e: flush L2 inside the loop (counted)")
+    ap.add_argument("--e2e-inflight", type=int, default=1,
+                    help="Comps in flight on the device in the streamed e2e (compute streams; needs contexts > inflight)")
     ap.add_argument("--e2e-contexts", type=int, default=0,
                     help="independent query contexts the streamed e2e rotates over (0: 3 below N=2^19, else 1)")
     ap.add_argument("--queries", type=int, default=0,
@@ -789,6 +791,9 @@ def main():
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
         ev = lambda: torch.cuda.Event()
 
+        K = max(1, args.e2e_inflight)  # Comps in flight on the device (compute streams)
+        cstreams = [stream] + [torch.cuda.Stream() for _ in range(K - 1)]
+
         def pipeline(nsteps, timed):
             up_done = [ev() for _ in range(nsteps)]
             comp_done = [ev() for _ in range(nsteps)]
@@ -804,24 +809,27 @@ def main():
 
             with torch.cuda.stream(stream):
                 t0.record(stream)
-                h2d_s.wait_event(t0)
-                d2h_s.wait_event(t0)
-                upload(0)
+                for st in [h2d_s, d2h_s] + cstreams[1:]:
+                    st.wait_event(t0)
+                for i in range(min(K, nsteps)):
+                    upload(i)
                 for i in range(nsteps):
                     c = ctxs[i % R]
-                    stream.wait_event(up_done[i])
+                    cs = cstreams[i % K]
+                    cs.wait_event(up_done[i])
                     if i >= R:
-                        stream.wait_event(d2h_done[i - R])  # this context's previous answer was read back
+                        cs.wait_event(d2h_done[i - R])  # this context's previous answer was read back
                     if R == 1 and args.e2e_flush and args.N < (1 << 19):
-                        flush.zero_()  # a single small context would stay L2-resident (counted)
-                    c["dc"].launch(sh)
-                    comp_done[i].record(stream)
-                    if i + 1 < nsteps:
-                        upload(i + 1)
+                        with torch.cuda.stream(cs):
+                            flush.zero_()  # a single small context would stay L2-resident (counted)
+                    c["dc"].launch(cs.cuda_stream)
+                    comp_done[i].record(cs)
+                    if i + K < nsteps:
+                        upload(i + K)
                     d2h_s.wait_event(comp_done[i])
                     _lib.check(L.hc_comp_get_output_async(c["h"], c["out_h"].data_ptr(), d2h_s.cuda_stream))
                     d2h_done[i].record(d2h_s)
-                stream.wait_event(d2h_done[-1])
+                stream.wait_event(d2h_done[-1])  # the D2H stream is in order: every answer is back
                 t1.record(stream)
             torch.cuda.synchronize()
             return t0.elapsed_time(t1)
