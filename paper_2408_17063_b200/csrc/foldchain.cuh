@@ -44,7 +44,16 @@ struct FcFold {
     const u64* key;       // its KSK [D_L][2][KL1][n], Montgomery
     u64* acc_next;        // ACC[(f+1) % 3]
     u64* acc_zero;        // ACC[(f+2) % 3] (c1 rows zeroed here; c0 rows by their reader)
+    // s0 decoded on the host (<= FC_C0T terms: one per fold, up to three
+    // giant steps before the first), so the c0 finish needs no dependent load
+    // of the spec: res_f.c0 = c0base + sum_i c0src_i[perm_i] + red(c0acc)
+    int c0n;              // terms (0: s0 does not fit -> generic path through F.s0)
+    const u64* c0base;    // nullable
+    const u64* c0src[3];
+    const uint16_t* c0perm[3];
+    u64* c0acc;
 };
+constexpr int FC_C0T = 3;
 struct FcArgs {
     int F, D;
     unsigned* bar;  // grid-barrier arrival counter, zeroed before the launch
@@ -179,8 +188,17 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
     // (b_d, a_d) at prime k at this CTA's NTT outputs
     unsigned ig[4];
     u64 kb[CEPT], ka[CEPT];
+    const int gtid = blockIdx.x * CNT + t, gthreads = gridDim.x * CNT;
+    unsigned c0pe[2][FC_C0T] = {};  // the c0 finish's permutation entries of this thread's <= 2 elements
     auto fetch = [&](int f) {
         const FcFold& F = A.f[f];
+        HC_UNROLL
+        for (int i = 0; i < 2; i++) {
+            const int e = gtid + i * gthreads;
+            HC_UNROLL
+            for (int tt = 0; tt < FC_C0T; tt++)
+                if (e < 2 * NPOLY && tt < F.c0n) c0pe[i][tt] = F.c0perm[tt][e & (NPOLY - 1)];
+        }
         const u64* kbp = F.key + ((size_t)(d * 2 + 0) * KL1 + k) * NPOLY + c * CTILE + t;
         const u64* kap = F.key + ((size_t)(d * 2 + 1) * KL1 + k) * NPOLY + c * CTILE + t;
         HC_UNROLL
@@ -196,7 +214,6 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");    // twiddle slices stored
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the giant step's accumulators are complete
     const TwL tlf{twf_sl, c}, tli{twi_sl, c};
-    const int gtid = blockIdx.x * CNT + t, gthreads = gridDim.x * CNT;
     unsigned gen = 0;
     for (int f = 0; f < A.F; f++) {
         const FcFold& F = A.f[f];
@@ -226,10 +243,19 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
         XJob JC[2];
         LdPre<LD_KSFIN, 1> cp[2];
         KsLd<1> cv[2];
+        const bool fast0 = F.c0n > 0;
+        u64 c0g[2][FC_C0T];
         HC_UNROLL
         for (int i = 0; i < 2; i++) {
             const int e = gtid + i * gthreads;
-            if (e < 2 * NPOLY) {
+            if (e < 2 * NPOLY && fast0) {  // three independent loads, permutation entry fetched a fold ahead
+                const size_t kofs = (size_t)(e >> 13) * NPOLY;
+                const int j = e & (NPOLY - 1);
+                cv[i].x[0] = F.c0base ? __ldcg(F.c0base + kofs + j) : 0;
+                cv[i].acc[0] = __ldcg(F.c0acc + kofs + j);
+                HC_UNROLL
+                for (int tt = 0; tt < FC_C0T; tt++) c0g[i][tt] = tt < F.c0n ? __ldcg(F.c0src[tt] + kofs + c0pe[i][tt]) : 0;
+            } else if (e < 2 * NPOLY) {
                 JC[i] = XJob{};
                 JC[i].dir = 1;
                 JC[i].k = e >> 13;
@@ -337,7 +363,17 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
         HC_UNROLL
         for (int i = 0; i < 2; i++) {
             const int e = gtid + i * gthreads;
-            if (e < 2 * NPOLY) {
+            if (e < 2 * NPOLY && fast0) {
+                const PrimeC& PC = C.pc[e >> 13];
+                const size_t kofs = (size_t)(e >> 13) * NPOLY;
+                const int j = e & (NPOLY - 1);
+                u64 v = add_mod(cv[i].x[0], red64(cv[i].acc[0], PC.q, PC.one_s), PC.q);
+                HC_UNROLL
+                for (int tt = 0; tt < FC_C0T; tt++) v = add_mod(v, c0g[i][tt], PC.q);  // absent terms are 0
+                F.cur[kofs + j] = v;
+                F.c0acc[kofs + j] = 0;
+                F.acc_zero[2 * NPOLY + e] = 0;
+            } else if (e < 2 * NPOLY) {
                 u64 y[1];
                 ksfin_finish<1>(JC[i], C.pc[JC[i].k], e & (NPOLY - 1), 0, cp[i], cv[i], y);
                 F.acc_zero[2 * NPOLY + e] = 0;

@@ -1845,6 +1845,17 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
             F.key = ka->key;
             F.acc_next = acc_next;
             F.acc_zero = P.ACC + (size_t)((f + 2) % 3) * 2 * 2 * NB;
+            bool fits = s0.nterm >= 1 && s0.nterm <= FC_C0T && s0.acc;
+            for (int i = 0; fits && i < s0.nterm; i++) fits = s0.t[i].c0src && s0.t[i].perm;
+            if (fits) {
+                F.c0n = s0.nterm;
+                F.c0base = s0.base;
+                F.c0acc = s0.acc;
+                for (int i = 0; i < s0.nterm; i++) {
+                    F.c0src[i] = s0.t[i].c0src;
+                    F.c0perm[i] = s0.t[i].perm;
+                }
+            }
         } else {
             digit_jobs(f3, P.digF, ka, acc_next);
             rc = add_i2(S, std::vector<Intt2Job>{ij}); if (rc) return rc;

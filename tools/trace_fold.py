@@ -34,3 +34,11 @@ for f in range(12):
     med = [(np.median(b[:, i]) - t0) / 1e3 for i in range(12)]
     mx = [(b[:, i].max() - t0) / 1e3 for i in range(12)]
     print(f"fold {f}: " + " ".join(f"{n} {m:6.2f}" for n, m in zip(names, med)) + f" | max slack {mx[11]:6.2f}")
+if "--clusters" in sys.argv:  # per-cluster medians of the first two folds (cluster d = CTAs 16d .. 16d+15)
+    for f in range(2):
+        b = tr[f].astype(np.int64)
+        for d in range(8):
+            rows = b[16 * d:16 * d + 16]
+            rows = rows[rows[:, 0] > 0]
+            if len(rows):
+                print(f"fold {f} cluster {d}: " + " ".join(f"{n} {(np.median(rows[:, i]) - t0) / 1e3:6.2f}" for i, n in enumerate(names)))
