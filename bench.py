@@ -67,9 +67,9 @@ def make_parser() -> argparse.ArgumentParser:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-flush", type=int, default=1, help="single-context streamed e2e: flush L2 inside the loop (counted)")
     ap.add_argument("--e2e-inflight", type=int, default=1,
-                    help="Comps in flight on the device in the streamed e2e (compute streams; needs contexts > inflight)")
+                    help="Comps in flight on the device in the reported streamed e2e (default 1, as `value`)")
     ap.add_argument("--e2e-contexts", type=int, default=0,
-                    help="independent query contexts the streamed e2e rotates over (0: 3 below N=2^19, else 1)")
+                    help="independent query contexts the streamed e2e rotates over (0: 4 below N=2^19, else 1)")
     ap.add_argument("--queries", type=int, default=0,
                     help="config 5: Q independent queries (own seeded keys and payloads, one shared database "
                          "shape) spread over the ranks; a step runs every query once; value = aggregate entries/s")
@@ -770,7 +770,7 @@ def main():
         # below: the device-resident rotation runs at the flushed latency).
         # Every context's final answer is checked against its own
         # device-resident result ----
-        R = args.e2e_contexts if args.e2e_contexts > 0 else (3 if args.N < (1 << 19) else 1)
+        R = args.e2e_contexts if args.e2e_contexts > 0 else (4 if args.N < (1 << 19) else 1)
         Cn = cd.shape[0]
         ctxs = [dict(be=be, keys=keys, dc=dc, h=h, cd_h=cd_h, cv_h=cv_h, want=out)]
         for r in range(1, R):
@@ -790,18 +790,32 @@ def main():
             c["out_h"] = torch.empty((2, 1, RING), dtype=torch.int64).pin_memory()
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
         ev = lambda: torch.cuda.Event()
+        stage = [[torch.empty_like(cd_h, device="cuda"), torch.empty_like(cv_h, device="cuda")] for _ in range(2)] if R == 1 else None
 
-        K = max(1, args.e2e_inflight)  # Comps in flight on the device (compute streams)
-        cstreams = [stream] + [torch.cuda.Stream() for _ in range(K - 1)]
+        # Comps in flight on the device (compute streams).  The reported e2e keeps
+        # ONE Comp on the GPU at a time (as `value` does); deeper pipelines are
+        # measured beside it (e2e.inflight) -- a query's serial level-1 tail
+        # leaves most SMs idle, which the next query's front end can use
+        cstreams = [stream] + [torch.cuda.Stream() for _ in range(3)]
 
-        def pipeline(nsteps, timed):
+        def pipeline(nsteps, K):
             up_done = [ev() for _ in range(nsteps)]
             comp_done = [ev() for _ in range(nsteps)]
             d2h_done = [ev() for _ in range(nsteps)]
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+            set_done = [ev() for _ in range(nsteps)]
+
             def upload(i):
                 c = ctxs[i % R]
+                if R == 1:  # one context: inputs land in one of two staging buffers, copied in on the compute stream
+                    if i >= 2:
+                        h2d_s.wait_event(set_done[i - 2])
+                    with torch.cuda.stream(h2d_s):
+                        stage[i % 2][0].copy_(c["cd_h"], non_blocking=True)
+                        stage[i % 2][1].copy_(c["cv_h"], non_blocking=True)
+                    up_done[i].record(h2d_s)
+                    return
                 if i >= R:
                     h2d_s.wait_event(comp_done[i - R])  # this context's previous Comp has read its inputs
                 _lib.check(L.hc_comp_upload_async(c["h"], c["cd_h"].data_ptr(), c["cv_h"].data_ptr(), Cn, h2d_s.cuda_stream))
@@ -822,6 +836,9 @@ def main():
                     if R == 1 and args.e2e_flush and args.N < (1 << 19):
                         with torch.cuda.stream(cs):
                             flush.zero_()  # a single small context would stay L2-resident (counted)
+                    if R == 1:
+                        _lib.check(L.hc_comp_set_inputs_device(c["h"], stage[i % 2][0].data_ptr(), stage[i % 2][1].data_ptr(), Cn, cs.cuda_stream))
+                        set_done[i].record(cs)
                     c["dc"].launch(cs.cuda_stream)
                     comp_done[i].record(cs)
                     if i + K < nsteps:
@@ -834,12 +851,23 @@ def main():
             torch.cuda.synchronize()
             return t0.elapsed_time(t1)
 
-        pipeline(2 * R, False)  # warm
+        def check_answers():
+            for c in ctxs[: min(R, args.steps)]:
+                assert np.array_equal(c["out_h"].numpy().view(np.uint64), c["want"]), "streamed e2e answer differs"
+                c["out_h"].zero_()
+
+        K0 = max(1, min(args.e2e_inflight, R - 1 if R > 1 else 1))
+        pipeline(2 * R, K0)  # warm
         if dist:
             dist.barrier()
-        e2e_stream_ms = pipeline(args.steps, True)
-        for c in ctxs[: min(R, args.steps)]:
-            assert np.array_equal(c["out_h"].numpy().view(np.uint64), c["want"]), "streamed e2e answer differs"
+        e2e_stream_ms = pipeline(args.steps, K0)
+        check_answers()
+        inflight = {}
+        for K in (2, 3):  # needs more contexts than Comps in flight
+            if K < R and K != K0:
+                pipeline(2 * R, K)
+                inflight[str(K)] = pipeline(args.steps, K) / args.steps
+                check_answers()
         # coldness check of the rotation: device-resident Comps round-robin over
         # the contexts, no flush, against the flushed latency reported as `value`
         rot_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -851,7 +879,8 @@ def main():
                 ctxs[i % R]["dc"].launch(sh)
                 b.record(stream)
         torch.cuda.synchronize()
-        e2e_rot = {"contexts": R, "device_resident_ms_per_step_no_flush": statistics.median(a.elapsed_time(b) for a, b in rot_evs),
+        e2e_rot = {"contexts": R, "comps_in_flight": K0, "ms_per_step_with_more_comps_in_flight": inflight,
+                   "device_resident_ms_per_step_no_flush": statistics.median(a.elapsed_time(b) for a, b in rot_evs),
                    "device_resident_ms_per_step_flushed": statistics.median(step_ms)}
         # both are end to end (every step copies its inputs in and its answer
         # out inside the timed region); the line reports the faster schedule

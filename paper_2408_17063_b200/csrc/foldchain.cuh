@@ -38,7 +38,6 @@ constexpr int FC_CL = 16;    // CTAs per cluster (non-portable size)
 struct FcFold {
     const u64* base1;     // res_{f-1}.c1 (or acc[0].c1 for f = 0) [2 primes][n], nullable
     const u64* accf;      // ACC[f % 3]: [2 polys][2 primes][n] key-switch sums of res_f
-    const KsSpec* s0;     // res_f.c0 finish spec (acc = ACC[f % 3] c0 rows, re-zeroed by its single reader)
     u64* cur;             // res_f: [2 polys][2 primes][n]
     const uint16_t* igal; // inverse coefficient Galois gather of rotation a_f
     const u64* key;       // its KSK [D_L][2][KL1][n], Montgomery
@@ -47,13 +46,13 @@ struct FcFold {
     // s0 decoded on the host (<= FC_C0T terms: one per fold, up to three
     // giant steps before the first), so the c0 finish needs no dependent load
     // of the spec: res_f.c0 = c0base + sum_i c0src_i[perm_i] + red(c0acc)
-    int c0n;              // terms (0: s0 does not fit -> generic path through F.s0)
+    int c0n;              // terms (the host falls back to two launches per fold when s0 does not fit)
     const u64* c0base;    // nullable
-    const u64* c0src[3];
-    const uint16_t* c0perm[3];
+    const u64* c0src[MAXTERM_KS];
+    const uint16_t* c0perm[MAXTERM_KS];
     u64* c0acc;
 };
-constexpr int FC_C0T = 3;
+constexpr int FC_C0T = 3;  // terms whose gathers are prefetched; further ones (fold 0 at giant > 4) load in the slack
 struct FcArgs {
     int F, D;
     unsigned* bar;  // grid-barrier arrival counter, zeroed before the launch
@@ -237,34 +236,21 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
                 if (aux) aux[jl + 128 * v] = x[v];
             }
         }
-        // res_f.c0 = base + sum_t perm_t(c0src_t) + red(ACC[f%3].c0) (bgv.py:643-645):
-        // its loads go out now, the sums are formed after the NTT (<= 2
-        // elements per thread; its single reader re-zeroes ACC[f%3].c0)
-        XJob JC[2];
-        LdPre<LD_KSFIN, 1> cp[2];
-        KsLd<1> cv[2];
-        const bool fast0 = F.c0n > 0;
-        u64 c0g[2][FC_C0T];
+        // res_f.c0 = c0base + sum_i c0src_i[perm_i] + red(ACC[f%3].c0) (bgv.py:643-645):
+        // its loads go out now (independent: operands decoded on the host,
+        // permutation entries fetched a fold ahead), the sums are formed after
+        // the NTT (<= 2 elements per thread; its single reader re-zeroes ACC[f%3].c0)
+        u64 c0x[2], c0a[2], c0g[2][FC_C0T];
         HC_UNROLL
         for (int i = 0; i < 2; i++) {
             const int e = gtid + i * gthreads;
-            if (e < 2 * NPOLY && fast0) {  // three independent loads, permutation entry fetched a fold ahead
+            if (e < 2 * NPOLY) {
                 const size_t kofs = (size_t)(e >> 13) * NPOLY;
                 const int j = e & (NPOLY - 1);
-                cv[i].x[0] = F.c0base ? __ldcg(F.c0base + kofs + j) : 0;
-                cv[i].acc[0] = __ldcg(F.c0acc + kofs + j);
+                c0x[i] = F.c0base ? __ldcg(F.c0base + kofs + j) : 0;
+                c0a[i] = __ldcg(F.c0acc + kofs + j);
                 HC_UNROLL
                 for (int tt = 0; tt < FC_C0T; tt++) c0g[i][tt] = tt < F.c0n ? __ldcg(F.c0src[tt] + kofs + c0pe[i][tt]) : 0;
-            } else if (e < 2 * NPOLY) {
-                JC[i] = XJob{};
-                JC[i].dir = 1;
-                JC[i].k = e >> 13;
-                JC[i].ld = LD_KSFIN;
-                JC[i].noxf = 1;
-                JC[i].ks = F.s0;
-                JC[i].aux = F.cur + (size_t)JC[i].k * NPOLY;
-                ksfin_pre<1>(JC[i], e & (NPOLY - 1), 0, cp[i]);
-                ksfin_load<1>(JC[i], C.pc[JC[i].k], e & (NPOLY - 1), 0, cp[i], cv[i]);
             }
         }
         FTRACE(f, 1);
@@ -363,19 +349,17 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
         HC_UNROLL
         for (int i = 0; i < 2; i++) {
             const int e = gtid + i * gthreads;
-            if (e < 2 * NPOLY && fast0) {
+            if (e < 2 * NPOLY) {
                 const PrimeC& PC = C.pc[e >> 13];
                 const size_t kofs = (size_t)(e >> 13) * NPOLY;
                 const int j = e & (NPOLY - 1);
-                u64 v = add_mod(cv[i].x[0], red64(cv[i].acc[0], PC.q, PC.one_s), PC.q);
+                u64 v = add_mod(c0x[i], red64(c0a[i], PC.q, PC.one_s), PC.q);
                 HC_UNROLL
                 for (int tt = 0; tt < FC_C0T; tt++) v = add_mod(v, c0g[i][tt], PC.q);  // absent terms are 0
+                for (int tt = FC_C0T; tt < F.c0n; tt++)
+                    v = add_mod(v, __ldcg(F.c0src[tt] + kofs + F.c0perm[tt][j]), PC.q);
                 F.cur[kofs + j] = v;
                 F.c0acc[kofs + j] = 0;
-                F.acc_zero[2 * NPOLY + e] = 0;
-            } else if (e < 2 * NPOLY) {
-                u64 y[1];
-                ksfin_finish<1>(JC[i], C.pc[JC[i].k], e & (NPOLY - 1), 0, cp[i], cv[i], y);
                 F.acc_zero[2 * NPOLY + e] = 0;
             }
         }

@@ -1098,7 +1098,9 @@ static int plan_impl(hc_ctx* h, int64_t N, int s, int chunk_blocks, const uint64
     P->F = (int)P->fold.size();
     P->D1 = h->digits[1];
     P->D2 = h->digits[2];
-    P->CB = chunk_blocks > 0 ? chunk_blocks : (int)std::min<long long>(P->B, 64);
+    // wide chunks: 64 blocks, 128 from 256 blocks on (launches twice the size,
+    // still >= 2 chunks to pipeline: N=2^20 s=16 5.26 -> 5.11 ms, N=2^22 20.4 -> 20.0)
+    P->CB = chunk_blocks > 0 ? chunk_blocks : (int)std::min<long long>(P->B, P->B >= 256 ? 128 : 64);
     // k_diagx sums CB*baby Montgomery products (each < q^2) before one REDC,
     // which needs the sum < q * 2^64, i.e. at most 1024 terms for 54-bit q
     P->CB = std::max(1, std::min(P->CB, 1024 / std::max(1, P->baby)));
@@ -1839,22 +1841,19 @@ static int build_finish(hc_ctx* h, Plan& P, Schedule& S) {
             FcFold& F = fst.fc.f[f];
             F.base1 = s1.base;  // res_{f-1}.c1, or acc[0].c1 for fold 0 (null when acc[0] is empty)
             F.accf = s0.acc;    // ACC[f % 3]: c0 rows, then c1 rows at +2n
-            F.s0 = d0;
             F.cur = cur;
             F.igal = ka->igal;
             F.key = ka->key;
             F.acc_next = acc_next;
             F.acc_zero = P.ACC + (size_t)((f + 2) % 3) * 2 * 2 * NB;
-            bool fits = s0.nterm >= 1 && s0.nterm <= FC_C0T && s0.acc;
-            for (int i = 0; fits && i < s0.nterm; i++) fits = s0.t[i].c0src && s0.t[i].perm;
-            if (fits) {
-                F.c0n = s0.nterm;
-                F.c0base = s0.base;
-                F.c0acc = s0.acc;
-                for (int i = 0; i < s0.nterm; i++) {
-                    F.c0src[i] = s0.t[i].c0src;
-                    F.c0perm[i] = s0.t[i].perm;
-                }
+            // res_f.c0's finish, decoded for the kernel (every term of s0 has a c0 source)
+            F.c0n = s0.nterm;
+            F.c0base = s0.base;
+            F.c0acc = s0.acc;
+            for (int i = 0; i < s0.nterm; i++) {
+                if (!s0.t[i].c0src || !s0.t[i].perm) return fail(HC_ERR_STATE, "fold chain: key-switch term without a c0 source");
+                F.c0src[i] = s0.t[i].c0src;
+                F.c0perm[i] = s0.t[i].perm;
             }
         } else {
             digit_jobs(f3, P.digF, ka, acc_next);

@@ -144,6 +144,55 @@ extern "C" void ht_modops(int k, int op, const uint64_t* a, const uint64_t* b, u
     }
 }
 
+// k_ksfused's digit NTT on the host (ksfused.cuh): the closed-form Galois
+// gather ((j * tinv) mod 2n into [digits of X | digits of Q - X]), the front
+// linear form of the three leading stages per output chunk, then the cluster
+// schedule's phase B on the chunk; canonical output in natural order
+extern "C" void ht_ksfused_ntt(int k, uint32_t t, const uint16_t* dpos, const uint16_t* dneg, uint64_t* out) {
+    const PrimeC& P = g_ctx.pc[k];
+    const Tw* tw = g_ctx.twf + (size_t)k * NPOLY;
+    std::vector<uint16_t> coef(NPOLY);
+    galois_tables_host(NPOLY, t, coef.data(), nullptr);
+    const unsigned tinv = (coef[1] & 0x7FFF) + ((coef[1] >> 15) ? NPOLY : 0);
+    u64 K[8][8], w32s;
+    build_kfront(K, &w32s, tw, P.q);
+    static Tw sl[CL][1023];
+    host_tw_slices(tw, sl);
+    static u64 tile[CTILE];
+    static u64 regs[CNT][CEPT];
+    for (int r = 0; r < CL; r++) {
+        u32 klo[8], khi[8];
+        for (int a = 0; a < 8; a++) {
+            klo[a] = (u32)K[r][a];
+            khi[a] = (u32)(K[r][a] >> 32);
+        }
+        const TwL twl{sl[r], r};
+        for (int tt = 0; tt < CNT; tt++) {
+            for (int e = 0; e < CEPT; e++) {
+                u32 dg[CEPT];
+                for (int a = 0; a < 8; a++) {
+                    const unsigned i = ((unsigned)(tt + 128 * e + 1024 * a) * tinv) & 16383u;
+                    dg[a] = i < (unsigned)NPOLY ? dpos[i] : dneg[i - NPOLY];
+                }
+                regs[tt][e] = kf_front(dg, klo, khi, w32s, P.q);
+            }
+            const CPass I = cpass(0, r, tt);
+            r8_ct(regs[tt], twl, I.s0, I.G, P.q, 2 * P.q2);
+            c_store(regs[tt], tile, I);
+        }
+        for (int p = 1; p < 3; p++) {
+            for (int tt = 0; tt < CNT; tt++) {
+                const CPass I = cpass(p, r, tt);
+                c_load(regs[tt], tile, I);
+                r8_ct(regs[tt], twl, I.s0, I.G, P.q, 2 * P.q2);
+            }
+            if (p == 2) host_st12(r, CNT, regs, twl, P.q, 2 * P.q2, P.one_s);
+            for (int tt = 0; tt < CNT; tt++) c_store(regs[tt], tile, cpass(p, r, tt));
+        }
+        for (int b = 0; b < CTILE; b++) out[r * CTILE + b] = tile[cswz(b)];
+    }
+}
+
 extern "C" void ht_galois(uint32_t t, uint16_t* coef, uint16_t* perm) { galois_tables_host(NPOLY, t, coef, perm); }
 
 extern "C" void ht_slot_of(uint16_t* out) {

@@ -135,17 +135,12 @@ __global__ void __launch_bounds__(CNT, 4) k_ksfused(const __grid_constant__ DevC
         unsigned cole = base2;
         HC_UNROLL
         for (int e = 0; e < CEPT; e++) {
-            u64 lo = 0, hi = 0;
             if (e) cole = (cole + s128) & 0x7FFEu;
+            u32 dg[CEPT];
             HC_UNROLL
-            for (int a = 0; a < 8; a++) {
-                const unsigned off = (cole + arow[a]) & 0x7FFEu;
-                const u32 dg = *reinterpret_cast<const uint16_t*>(dig + off);
-                lo += (u64)dg * klo[a];  // IMAD.WIDE.U32 with 64-bit accumulate
-                hi += (u64)dg * khi[a];
-            }
-            const u64 H = hi + (lo >> 32);  // value = H * 2^32 + (u32)lo, H < 2^42
-            x[e] = (H << 32) - mulhi(H, w32s) * q + (u32)lo;  // < 2q + 2^32 < 4q
+            for (int a = 0; a < 8; a++)
+                dg[a] = *reinterpret_cast<const uint16_t*>(dig + ((cole + arow[a]) & 0x7FFEu));
+            x[e] = kf_front(dg, klo, khi, w32s, q);
         }
         {
             const CPass I = cpass(0, r, t);

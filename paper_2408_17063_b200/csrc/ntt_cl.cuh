@@ -239,6 +239,23 @@ inline void host_st0(int c, int n, u64 (*regs)[CEPT], const TW& tw, u64 q, u64 q
     for (int t = 0; t < n; t++) st12_recv2(t & 1, regs[t], rcv[t], A[t], B[t]);
 }
 
+// k_ksfused's front (ksfused.cuh): output r of the three leading forward
+// stages on a column whose inputs are base-2^16 digits, as the linear form
+// sum_a K[r][a] * dg[a] (K = r8_ct at s0 = 0, G = 0 on the unit vectors, split
+// into 32-bit halves klo / khi): 16 products of 16 x 32 bits, two 64-bit sums
+// (< 2^51 and < 2^41), one Shoup reduction of the high part by 2^32.
+// Result in [0, 2q + 2^32) -- a valid lazy input of the remaining ten stages.
+HD u64 kf_front(const u32 (&dg)[CEPT], const u32 (&klo)[CEPT], const u32 (&khi)[CEPT], u64 w32s, u64 q) {
+    u64 lo = 0, hi = 0;
+    HC_UNROLL
+    for (int a = 0; a < CEPT; a++) {
+        lo += (u64)dg[a] * klo[a];  // IMAD.WIDE.U32 with 64-bit accumulate
+        hi += (u64)dg[a] * khi[a];
+    }
+    const u64 H = hi + (lo >> 32);  // value = H * 2^32 + (u32)lo, H < 2^42
+    return (H << 32) - mulhi(H, w32s) * q + (u32)lo;
+}
+
 // forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
 HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q4) { r8_ct(x, TwG{tw}, 0, 0, q, q4); }
 

@@ -30,6 +30,7 @@ def ht():
     L.ht_rescale_corr.argtypes = [ctypes.c_int, P, P]
     L.ht_modops.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
     L.ht_galois.argtypes = [ctypes.c_uint32, P, P]
+    L.ht_ksfused_ntt.argtypes = [ctypes.c_int, ctypes.c_uint32, P, P, P]
     L.ht_slot_of.argtypes = [P]
     L.ht_digits.argtypes = [ctypes.c_int]
     return L
@@ -206,6 +207,34 @@ def test_galois_tables_match_reference_maps(setup):
         src = coef & 0x7FFF
         sign = np.where(coef >> 15, -1, 1)
         assert np.array_equal(sign * c[src], want)
+
+
+def test_fused_key_switch_digit_ntt(setup):
+    """k_ksfused's digit transform on the host (ksfused.cuh: closed-form Galois
+    gather from [digits of X | digits of Q - X], the three leading stages as a
+    linear form of the 16-bit digits per output chunk, phase B on the chunk)
+    equals the reference NTT (bgv.py:178-199) of the rotation's digit
+    polynomial as LD_DIGGAL gathers it through the coefficient table
+    (bgv.py:273-284, 622-631), for every level-2 prime and for the identity,
+    three rotations and the column swap."""
+    ht, be, p = setup
+    import random
+
+    n = N8K
+    rng = random.Random(11)
+    dpos = np.array([rng.randrange(1 << 16) for _ in range(n)], dtype=np.uint16)
+    dneg = np.array([rng.randrange(1 << 16) for _ in range(n)], dtype=np.uint16)
+    dpos[:4] = (0, 1, 0xFFFF, 0x8000)  # extreme digits
+    for t in (1, 3, pow(3, 2, 2 * n), pow(3, 1024, 2 * n), 2 * n - 1):
+        coef = np.empty(n, dtype=np.uint16)
+        perm = np.empty(n, dtype=np.uint16)
+        ht.ht_galois(t, p_(coef), p_(perm))
+        x = np.where(coef >> 15, dneg[coef & 0x7FFF], dpos[coef & 0x7FFF]).astype(np.uint64)
+        for k in range(3):
+            want = be.ntt.fwd(x[None, :], [k])[0]
+            got = np.empty(n, dtype=np.uint64)
+            ht.ht_ksfused_ntt(k, t, p_(dpos), p_(dneg), p_(got))
+            assert np.array_equal(got, want), f"fused digit NTT mismatch: t={t}, prime {k}"
 
 
 def test_slot_map_matches_reference(setup):
