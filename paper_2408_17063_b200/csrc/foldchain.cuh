@@ -94,8 +94,11 @@ __device__ __forceinline__ unsigned fc_ld_acquire(const unsigned* p) {
     return v;
 }
 // grid barrier number `gen` (1, 2, ...) over `ncta` CTAs: every CTA's global
-// writes (stores and red.adds) before it are visible to every CTA after it;
-// the gpu-scope fence after the wait also drops this SM's stale L1 lines
+// writes (stores and red.adds) before it are visible to every CTA after it:
+// release = gpu-scope fence + arrival by thread 0 after the CTA barrier,
+// acquire = thread 0's ld.acquire.gpu poll, extended to the CTA by the
+// barrier.  Every load of data another CTA wrote is an L2 load (__ldcg), so
+// no L1 invalidation (a second gpu-scope fence) is needed after the wait
 __device__ __forceinline__ void fc_grid_bar(unsigned* ctr, unsigned gen, unsigned ncta) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -104,7 +107,9 @@ __device__ __forceinline__ void fc_grid_bar(unsigned* ctr, unsigned gen, unsigne
         const unsigned target = gen * ncta;
         for (unsigned it = 0; fc_ld_acquire(ctr) < target; it++)
             if (it > (1u << 24)) __trap();
+#ifdef HC_FC_FENCE2
         __threadfence();
+#endif
     }
     __syncthreads();
 }
