@@ -374,15 +374,37 @@ def roofline(L, h, sh, comp_ms):
     bfly_per_ntt = (RING // 2) * 13
     achieved = xf_jobs * bfly_per_ntt / (xf_ms * 1e-3) / 1e9 if xf_ms > 0 else 0.0
     peak_g = peak.value / 1e9
-    comp_level = xf_jobs * bfly_per_ntt / comp_ms / 1e6
+    # every transform of the Comp, the fold chain's 2 + 2 x 7 per fold included
+    fold_jobs = kinds.get(9, [0.0, 0, 0])[1] * 16
+    comp_level = (xf_jobs + fold_jobs) * bfly_per_ntt / comp_ms / 1e6
     dom_name = kernel_name(dom_tag)
     dom_achieved = (dom_jobs / dom_launches) * bfly_per_ntt / (dom_ms / dom_launches * 1e-3) / 1e9
     ncu_traffic = None
     try:  # DRAM bytes per launch of that kernel from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "r02_ncu_dominant_traffic.json")) as fh:
             ncu_traffic = json.load(fh).get(dom_name)
+        if ncu_traffic and ncu_traffic.get("jobs_per_launch"):
+            # the captured launch may have been a different size (chunk width): scale per job
+            k = (dom_jobs / dom_launches) / ncu_traffic["jobs_per_launch"]
+            ncu_traffic = dict(ncu_traffic, dram_bytes_per_launch=ncu_traffic["dram_bytes_per_launch"] * k,
+                               algorithmic_bytes_per_launch=int(ncu_traffic["algorithmic_bytes_per_launch"] * k),
+                               scaled_from_jobs_per_launch=ncu_traffic["jobs_per_launch"])
     except (OSError, ValueError):
         pass
+    # the persistent fold chain (one launch): algorithmic transforms per fold =
+    # the two INTTs of res.c1 + 2 x D_1 digit NTTs (the per-cluster recomputation
+    # of the INTT is not algorithmic work)
+    fold = None
+    fc_ms, fc_folds, fc_launches = kinds.get(9, [0.0, 0, 0])
+    if fc_launches:
+        D1 = 7  # base-2^16 digits of the two-prime level-1 modulus (108 bits)
+        fold_bf = fc_folds * (2 + 2 * D1) * (RING // 2) * 13
+        fold = {"kernel": "k_foldchain (persistent, 7 clusters of 16 CTAs)", "folds": fc_folds, "ms": fc_ms,
+                "share_of_profiled_step": fc_ms / prof_total if prof_total else None,
+                "us_per_fold": fc_ms * 1e3 / fc_folds if fc_folds else None,
+                "achieved_gbfly_s": fold_bf / (fc_ms * 1e-3) / 1e9,
+                "note": "latency-bound serial chain (bit-exactness forbids merging the folds): 26 butterfly stages, "
+                        "three DSMEM exchanges, one cluster and one grid barrier per fold on 4 warps per SM"}
     # independent ceiling: measured INT32 multiply-pipe rates x the shipped
     # transform kernel's fma-pipe instruction mix per butterfly (SASS)
     rates = (ctypes.c_double * 3)()
@@ -411,10 +433,11 @@ def roofline(L, h, sh, comp_ms):
         "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum of one launch of the dominant kernel, "
                          "ncu --set full capture in the timed region (profiles/r02_ncu_dominant_traffic.json); "
                          "algorithmic bytes per launch: " + str((ncu_traffic or {}).get("algorithmic_bytes_per_launch"))),
+        "fold_chain": dict(fold, frac=fold["achieved_gbfly_s"] / peak_g if peak_g else None) if fold else None,
         "comp_level_gbfly_s": comp_level,
         "comp_level_frac": comp_level / peak_g if peak_g else None,
         "xform_share_of_step": xf_ms / prof_total if prof_total else None,
-        "xform_jobs_per_comp": xf_jobs,
+        "xform_jobs_per_comp": xf_jobs + fold_jobs,
         "xform_launches_per_comp": xf_launch,
         "profiled_step_ms_ungraphed": prof_total,
         "per_kind_ms": {STEP_KINDS.get(k, str(k)): round(v[0], 4) for k, v in sorted(kinds.items())},

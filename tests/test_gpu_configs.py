@@ -316,3 +316,61 @@ def test_fused_key_switch_kernel_matches_multi_launch(pkg, oracle):
     assert outs[("launches", 1)] < outs[("launches", 0)]  # S3+S4 and S7+S8 are one launch each
     _, oout = _oracle_answer(O, N, s, p, seed)
     assert np.array_equal(outs[0], np.asarray(oout.c, dtype=np.uint64).reshape(outs[0].shape))
+
+
+def test_serving_pipeline_upload_launch_readback(pkg, oracle):
+    """The streamed serving path of bench.py's e2e: two query
+    contexts with their own keys; hc_comp_upload_async on a copy stream,
+    hc_comp_launch on the compute stream, hc_comp_get_output_async on a third,
+    chained by events over six steps.  Every answer equals the context's own
+    hc_comp result (itself pinned to the oracle by the tests above)."""
+    import torch
+
+    from paper_2408_17063_b200 import _lib
+
+    P, O = pkg, oracle
+    N, s, p = 1 << 13, 8, 65537
+    L = _lib.lib()
+    ctxs = []
+    for seed in (21, 22):
+        be, params, keys, dense, cts, hint = _gpu_case(P, O, N, s, p, seed)
+        cd = np.ascontiguousarray(np.stack([c.payload.res for c in cts]))
+        cv = np.ascontiguousarray(np.stack([c.payload.res for c in hint]))
+        want = P.comp(cts, params, be, keys, index_hint=hint).cts[0].payload.res.copy()
+        dc = P.DeviceComp(be, params, keys)
+        # start from wrong inputs: the pipeline's uploads must be what the Comps read
+        dc.set_inputs(np.zeros_like(cd), np.zeros_like(cv))
+        ctxs.append(dict(be=be, dc=dc, h=be._ctx(), want=want, C=cd.shape[0],
+                         cd_h=torch.from_numpy(cd).pin_memory(), cv_h=torch.from_numpy(cv).pin_memory(),
+                         out_h=torch.zeros((2, 1, RING), dtype=torch.int64).pin_memory()))
+    comp_s, h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    steps, R = 6, len(ctxs)
+    up = [torch.cuda.Event() for _ in range(steps)]
+    done = [torch.cuda.Event() for _ in range(steps)]
+    back = [torch.cuda.Event() for _ in range(steps)]
+
+    def upload(i):
+        c = ctxs[i % R]
+        if i >= R:
+            h2d_s.wait_event(done[i - R])
+        _lib.check(L.hc_comp_upload_async(c["h"], c["cd_h"].data_ptr(), c["cv_h"].data_ptr(), c["C"], h2d_s.cuda_stream))
+        up[i].record(h2d_s)
+
+    upload(0)
+    for i in range(steps):
+        c = ctxs[i % R]
+        comp_s.wait_event(up[i])
+        if i >= R:
+            comp_s.wait_event(back[i - R])
+        c["dc"].launch(comp_s.cuda_stream)
+        done[i].record(comp_s)
+        if i + 1 < steps:
+            upload(i + 1)
+        d2h_s.wait_event(done[i])
+        _lib.check(L.hc_comp_get_output_async(c["h"], c["out_h"].data_ptr(), d2h_s.cuda_stream))
+        back[i].record(d2h_s)
+    torch.cuda.synchronize()
+    for c in ctxs:
+        assert np.array_equal(c["out_h"].numpy().view(np.uint64).reshape(c["want"].shape), c["want"])
+    # argument checks of the new entry point
+    assert L.hc_comp_upload_async(ctxs[0]["h"], ctxs[0]["cd_h"].data_ptr(), ctxs[0]["cv_h"].data_ptr(), 99, None) != 0
