@@ -209,7 +209,7 @@ HD void st0_compute(int c, int t, const u64 (&x)[CEPT], const u64 (&r)[4], const
         Tw w = tw(tb + (odd ? i : 4 + i), 4096);
         const u64 d = X - Y + q2;
         A[i] = X + Y;
-        B[i] = d * w.w - mulhi_approx(d, w.ws) * q;
+        B[i] = mul_shoup_approx(d, w.w, w.ws, q);
         s[i] = odd ? A[i] : B[i];
     }
 }
