@@ -41,9 +41,9 @@ for r in diag_intt foldchain giant_ntt ksmac_lat compose pack_intt ksmac_2e20 di
 done
 python tools/ncu_summary.py $O/*.ncu-rep > $O/summary.txt 2>&1
 [ -f $O/diag_intt_raw.csv ] && python tools/ncu_traffic.py $O/diag_intt_raw.csv 'k_xf<1, 1, 5, 1>' 32 262144 > $O/traffic_diag_intt.json
-# N = 2^20: 6336 digit NTTs per launch, each reads 8192 u16 digits + the u16 gather table and writes 64 KiB
-[ -f $O/xf_dig_2e20_raw.csv ] && python tools/ncu_traffic.py $O/xf_dig_2e20_raw.csv 'k_xf<0, 5, 7, 4>' 6336 98304 > $O/traffic_xf_dig_2e20.json
-[ -f $O/ksfused_2e20_raw.csv ] && python tools/ncu_traffic.py $O/ksfused_2e20_raw.csv 'k_ksfused' 192 646144 > $O/traffic_ksfused_2e20.json
+# N = 2^20 (128-block chunks): 12672 digit NTTs per launch, each reads 8192 u16 digits + the u16 gather table and writes 64 KiB
+[ -f $O/xf_dig_2e20_raw.csv ] && python tools/ncu_traffic.py $O/xf_dig_2e20_raw.csv 'k_xf<0, 5, 7, 4>' 12672 98304 > $O/traffic_xf_dig_2e20.json
+[ -f $O/ksfused_2e20_raw.csv ] && python tools/ncu_traffic.py $O/ksfused_2e20_raw.csv 'k_ksfused' 384 646144 > $O/traffic_ksfused_2e20.json
 python tools/ncu_stalls.py $O/ksfused_2e20.ncu-rep $O/xf_dig_2e20.ncu-rep $O/diag_intt_2e20.ncu-rep $O/foldchain.ncu-rep > $O/stalls.txt 2>&1
 rm -f $O/*.ncu-rep
 cat $O/summary.txt | head -80
