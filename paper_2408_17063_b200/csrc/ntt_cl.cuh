@@ -113,9 +113,20 @@ HD void r8_ct(u64 (&x)[CEPT], const TW& tw, int s0, int G, u64 q, u64 q2) {
 }
 
 // 3 GS stages b0..b0+2 on 8 points: stage b0+u pairs v, v + (1 << u),
-// twiddle inv_tbl[2^(12-b0-u) + (G << (2-u) | v >> (u+1))]
+// twiddle inv_tbl[2^(12-b0-u) + (G << (2-u) | v >> (u+1))].
+// Inputs in [0, 4q).  The sums are NOT reduced inside the pass: a sum output
+// doubles its operands' bound (compile-time per register: after the three
+// stages x0 < 32q, x1 < 16q, x2, x3 < 8q; every product output is < 4q), the
+// differences take the matching multiple of q as offset (4q / 8q / 16q), and
+// seven conditional subtractions at the end (instead of one per butterfly,
+// twelve) bring every output back below 4q.  q < 2^54, so 32q < 2^59.
+HD void gs_csub(u64& x, u64 c) {  // x in [0, 2c) -> [0, c): the sign of x - c decides
+    const u64 d = x - c;
+    x = (long long)d < 0 ? x : d;
+}
 template <class TW>
 HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q4) {
+    const u64 q8 = 2 * q4, q16 = 4 * q4;
     HC_UNROLL
     for (int u = 0; u < 3; u++) {
         const int half = 1 << u;
@@ -124,10 +135,22 @@ HD void r8_gs(u64 (&x)[CEPT], const TW& tw, int b0, int G, u64 q, u64 q4) {
         for (int v = 0; v < CEPT; v++) {
             if (!(v & half)) {
                 Tw w = tw(tb + (v >> (u + 1)), 1 << (12 - b0 - u));
-                bf_gs_lazy(x[v], x[v + half], w.w, w.ws, q, q4);
+                // bound of both operands: 4q << (number of low bits of v below `half` that are 0 ... )
+                // u = 0: 4q; u = 1: v even -> 8q, v odd -> 4q; u = 2: v = 0 -> 16q, v = 1 -> 8q, v = 2, 3 -> 4q
+                const u64 off = u == 0 ? q4 : u == 1 ? ((v & 1) ? q4 : q8) : (v == 0 ? q16 : v == 1 ? q8 : q4);
+                const u64 a = x[v], b = x[v + half];
+                x[v] = a + b;
+                x[v + half] = mul_shoup_approx(a - b + off, w.w, w.ws, q);
             }
         }
     }
+    gs_csub(x[0], q16);
+    gs_csub(x[0], q8);
+    gs_csub(x[0], q4);
+    gs_csub(x[1], q8);
+    gs_csub(x[1], q4);
+    gs_csub(x[2], q4);
+    gs_csub(x[3], q4);
 }
 
 // forward bit-0 stage across lanes (t, t^1) in pass-2 layout:
