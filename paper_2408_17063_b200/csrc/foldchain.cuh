@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
         }
         FTRACE(f, 1);
         HC_UNROLL
-        for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+        for (int v = 0; v < CEPT; v++) tile[cswz(t) + 128 * v] = x[v];
         __syncthreads();
         HC_UNROLL
         for (int p = 0; p < 3; p++) {
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(CNT, 1) k_foldchain(const __grid_constant__ De
             u64* a1 = F.acc_next + (size_t)(2 + k) * NPOLY + c * CTILE + t;
             HC_UNROLL
             for (int v = 0; v < CEPT; v++) {
-                const u64 y = tile[cswz(t + 128 * v)];
+                const u64 y = tile[cswz(t) + 128 * v];
                 acc_add(a0 + 128 * v, mul_mont(y, kbs[v], P.q, P.qneg), KSACC_BOUND);
                 acc_add(a1 + 128 * v, mul_mont(y, kas[v], P.q, P.qneg), KSACC_BOUND);
             }

@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
         pdl_wait();
         load_post<LD, EPT>(C, J, P, t, NT, pre, x);
         HC_UNROLL
-        for (int e = 0; e < EPT; e++) sm[swz(t + NT * e)] = x[e];
+        for (int e = 0; e < EPT; e++) sm[swz(t) + NT * e] = x[e];
     } else {
         pdl_wait();
         HC_NOUNROLL
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
             u64 x[EPT];  // coefficients t + 1024 e
             load_n<LD, EPT>(C, J, P, t, NT, x);
             HC_UNROLL
-            for (int e = 0; e < EPT; e++) sm[swz(t + NT * e)] = x[e];
+            for (int e = 0; e < EPT; e++) sm[swz(t) + NT * e] = x[e];
         }
     }
     __syncthreads();
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
         const int t = threadIdx.x + v * (NT / VT);
         u64 x[EPT];
         HC_UNROLL
-        for (int e = 0; e < EPT; e++) x[e] = sm[swz(t + NT * e)];
+        for (int e = 0; e < EPT; e++) x[e] = sm[swz(t) + NT * e];
         store_n<EP, EPT>(C, J, P, t, NT, x);
     }
     TRACE(5);
@@ -650,7 +650,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
         TRACE(4);
         pdl_trigger();
         HC_UNROLL
-        for (int v = 0; v < CEPT; v++) x[v] = tile[cswz(t + 128 * v)];
+        for (int v = 0; v < CEPT; v++) x[v] = tile[cswz(t) + 128 * v];
         if (!valid) {
         } else if constexpr (EP == EP_KSACC) {
             HC_UNROLL
@@ -676,7 +676,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CNT * JPC)
             for (int v = 0; v < CEPT; v++) x[v] = 0;
         tw_commit(twsl, pre, t);
         HC_UNROLL
-        for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+        for (int v = 0; v < CEPT; v++) tile[cswz(t) + 128 * v] = x[v];
         __syncthreads();
         TRACE(1);
         HC_UNROLL
@@ -760,7 +760,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(2 * CNT)
     load_post<LD, CEPT>(C, J, P, jl, 128, lpre, x);
     tw_commit(twsl, pre, t);
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+    for (int v = 0; v < CEPT; v++) tile[cswz(t) + 128 * v] = x[v];
     __syncthreads();
     TRACE(1);
     const TwL twl{twsl, c};
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(CNT) k_cl16_intt2(const __grid_constant__ DevC
     load_post<LD, CEPT>(C, J, P, jl, 128, lpre, x);
     tw_commit(twsl, pre, t);
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) tile[cswz(t + 128 * v)] = x[v];
+    for (int v = 0; v < CEPT; v++) tile[cswz(t) + 128 * v] = x[v];
     __syncthreads();
     TRACE(1);
     const TwL twl{twsl, c};

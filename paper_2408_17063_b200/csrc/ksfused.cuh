@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(CNT, 4) k_ksfused(const __grid_constant__ DevC
         for (int v = 0; v < CEPT; v++) ka[v] = __ldcs(kp + (size_t)L1 * NPOLY + 128 * v);
         HC_UNROLL
         for (int v = 0; v < CEPT; v++) {
-            const u64 y = tile[cswz(t + 128 * v)];
+            const u64 y = tile[cswz(t) + 128 * v];
             mac128(h0[v], l0[v], y, kb[v]);
             mac128(h1[v], l1[v], y, ka[v]);
         }

@@ -38,11 +38,11 @@ HD CPass pass1k(int p, int t) {
 
 HD void t_load(u64 (&x)[EPT], const u64* sm, const CPass& I) {
     HC_UNROLL
-    for (int v = 0; v < EPT; v++) x[v] = sm[swz(I.base + v * I.stride)];
+    for (int v = 0; v < EPT; v++) x[v] = sm[cswz_elem(I.base, I.stride, v)];
 }
 HD void t_store(const u64 (&x)[EPT], u64* sm, const CPass& I) {
     HC_UNROLL
-    for (int v = 0; v < EPT; v++) sm[swz(I.base + v * I.stride)] = x[v];
+    for (int v = 0; v < EPT; v++) sm[cswz_elem(I.base, I.stride, v)] = x[v];
 }
 
 #if defined(__CUDACC__)

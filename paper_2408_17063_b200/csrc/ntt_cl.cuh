@@ -85,13 +85,27 @@ HD CPass cpass(int p, int c, int t) {
     return r;
 }
 
+// Swizzled index of element v of a pass, cswz(base + v * stride), in the form
+// that costs the fewest address instructions (the stride is a compile-time
+// constant wherever a pass is unrolled):
+//   stride >= 128: v * stride leaves bits 1..6 alone, so cswz(base) + v * stride
+//                  -- one address per pass, immediate offsets per element;
+//   stride 16:     base has bits 4..6 clear (pass layouts), so bits 4..6 = v and
+//                  the index is (base ^ 2v) + 16v -- one logic op per element;
+//   stride 2:      base has bits 1..3 clear, bits 4..6 fixed: base | (2v ^ T).
+HD int cswz_elem(int base, int stride, int v) {
+    if (stride >= 128) return cswz(base) + v * stride;
+    if (stride == 16) return (base ^ (2 * v)) + 16 * v;
+    if (stride == 2) return base | ((2 * v) ^ (((base >> 4) & 7) << 1));
+    return cswz(base + v * stride);
+}
 HD void c_load(u64 (&x)[CEPT], const u64* sm, const CPass& I) {
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) x[v] = sm[cswz(I.base + v * I.stride)];
+    for (int v = 0; v < CEPT; v++) x[v] = sm[cswz_elem(I.base, I.stride, v)];
 }
 HD void c_store(const u64 (&x)[CEPT], u64* sm, const CPass& I) {
     HC_UNROLL
-    for (int v = 0; v < CEPT; v++) sm[cswz(I.base + v * I.stride)] = x[v];
+    for (int v = 0; v < CEPT; v++) sm[cswz_elem(I.base, I.stride, v)] = x[v];
 }
 
 // 3 CT stages s0..s0+2 on 8 points: stage s0+u pairs v, v + (4 >> u),
