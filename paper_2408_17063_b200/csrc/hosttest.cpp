@@ -34,6 +34,12 @@ extern "C" void ht_ntt(int k, uint64_t* a, int inverse) {
     else host_emulate_fwd(a, g_ctx.twf + (size_t)k * NPOLY, g_ctx.pc[k]);
 }
 
+// k_xf's form: bit-0 stage in registers at the kernel's edge (ntt1k.cuh)
+extern "C" void ht_ntt_edge(int k, uint64_t* a, int inverse) {
+    if (inverse) host_emulate_inv_edge(a, g_ctx.twi + (size_t)k * NPOLY, g_ctx.pc[k]);
+    else host_emulate_fwd_edge(a, g_ctx.twf + (size_t)k * NPOLY, g_ctx.pc[k]);
+}
+
 extern "C" void ht_ntt_cl(int k, uint64_t* a, int inverse) {
     if (inverse) host_emulate_cl_inv(a, g_ctx.twi + (size_t)k * NPOLY, g_ctx.pc[k]);
     else host_emulate_cl_fwd(a, g_ctx.twf + (size_t)k * NPOLY, g_ctx.pc[k]);

@@ -376,7 +376,40 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
     const XJob J = jobs[blockIdx.x];
     const PrimeC& P = C.pc[J.k];
     TRACE(0);
-    if constexpr (VT == 1) {
+    // The bit-0 stage runs in registers at the kernel's edge (ntt1k.cuh): the
+    // inverse transform's loader and the forward transform's epilogue own the
+    // coefficient pairs (j, j + 1), j = 2t + 2048m; the other side keeps the
+    // coefficients t + 1024e.
+    const Tw* tw = (DIR ? C.twi : C.twf) + (size_t)J.k * NPOLY;
+    if constexpr (DIR == 1) {
+        if constexpr (VT == 1) {
+            const int t = threadIdx.x;
+            u64 xe[4], xo[4];
+            LdPre<LD, 4> pe, po;
+            load_pre<LD, 4>(J, 2 * t, 2048, pe);
+            load_pre<LD, 4>(J, 2 * t + 1, 2048, po);
+            pdl_wait();
+            load_post<LD, 4>(C, J, P, 2 * t, 2048, pe, xe);
+            load_post<LD, 4>(C, J, P, 2 * t + 1, 2048, po, xo);
+            inv_first_stage(xe, xo, tw, t, P);
+            HC_UNROLL
+            for (int m = 0; m < 4; m++)
+                *reinterpret_cast<ulonglong2*>(sm + pair_index(t, m)) = make_ulonglong2(xe[m], xo[m]);
+        } else {
+            pdl_wait();
+            HC_NOUNROLL
+            for (int v = 0; v < VT; v++) {
+                const int t = threadIdx.x + v * (NT / VT);
+                u64 xe[4], xo[4];
+                load_n<LD, 4>(C, J, P, 2 * t, 2048, xe);
+                load_n<LD, 4>(C, J, P, 2 * t + 1, 2048, xo);
+                inv_first_stage(xe, xo, tw, t, P);
+                HC_UNROLL
+                for (int m = 0; m < 4; m++)
+                    *reinterpret_cast<ulonglong2*>(sm + pair_index(t, m)) = make_ulonglong2(xe[m], xo[m]);
+            }
+        }
+    } else if constexpr (VT == 1) {
         const int t = threadIdx.x;
         u64 x[EPT];  // coefficients t + 1024 e
         LdPre<LD, EPT> pre;
@@ -400,17 +433,30 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
     TRACE(1);
     // forward outputs that only feed Montgomery products stay lazy (< 2^60)
     constexpr bool lazy = EP == EP_KSACC || EP == EP_STORE_LAZY;
-    if (DIR == 0) cta_ntt_fwd<lazy, VT>(C.twf + (size_t)J.k * NPOLY, P, sm);
-    else cta_ntt_inv<VT>(C.twi + (size_t)J.k * NPOLY, P, sm);
+    if (DIR == 0) cta_ntt_fwd_core<VT>(tw, P, sm);
+    else cta_ntt_inv_core<VT>(tw, P, sm);
     TRACE(4);
     pdl_trigger();
     HC_NOUNROLL
     for (int v = 0; v < VT; v++) {
         const int t = threadIdx.x + v * (NT / VT);
-        u64 x[EPT];
-        HC_UNROLL
-        for (int e = 0; e < EPT; e++) x[e] = sm[swz(t) + NT * e];
-        store_n<EP, EPT>(C, J, P, t, NT, x);
+        if constexpr (DIR == 0) {
+            u64 xe[4], xo[4];
+            HC_UNROLL
+            for (int m = 0; m < 4; m++) {
+                const ulonglong2 pr = *reinterpret_cast<const ulonglong2*>(sm + pair_index(t, m));
+                xe[m] = pr.x;
+                xo[m] = pr.y;
+            }
+            fwd_last_stage(xe, xo, tw, t, P, lazy);
+            store_n<EP, 4>(C, J, P, 2 * t, 2048, xe);
+            store_n<EP, 4>(C, J, P, 2 * t + 1, 2048, xo);
+        } else {
+            u64 x[EPT];
+            HC_UNROLL
+            for (int e = 0; e < EPT; e++) x[e] = sm[swz(t) + NT * e];
+            store_n<EP, EPT>(C, J, P, t, NT, x);
+        }
     }
     TRACE(5);
 }

@@ -97,6 +97,80 @@ __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* 
 }
 #endif
 
+// k_xf's form of the same transforms: the bit-0 stage runs in REGISTERS at
+// the edge of the kernel instead of across lane pairs -- the forward
+// transform's epilogue (the inverse transform's loader) owns the four
+// coefficient pairs (j, j + 1), j = 2t + 2048m, so the stage needs no shuffle
+// and none of c_st12 / c_st0's even/odd selects (~100 of ~1400 instructions
+// per schedule thread), and the pairs move as 128-bit shared-memory accesses.
+HD void fwd_last_stage(u64 (&xe)[4], u64 (&xo)[4], const Tw* tw, int t, const PrimeC& P, bool lazy) {
+    HC_UNROLL
+    for (int m = 0; m < 4; m++) {
+        const Tw w = ldtw(tw, 4096 + t + 1024 * m);  // tbl[4096 + (j >> 1)]
+        bf_ct_lazy(xe[m], xo[m], w.w, w.ws, P.q, 2 * P.q2);
+        if (!lazy) {
+            xe[m] = canon_any(xe[m], P.q, P.one_s);
+            xo[m] = canon_any(xo[m], P.q, P.one_s);
+        }
+    }
+}
+// inverse bit-0 stage on loader outputs in [0, 2q): sums < 4q, products < 4q
+HD void inv_first_stage(u64 (&xe)[4], u64 (&xo)[4], const Tw* tw, int t, const PrimeC& P) {
+    HC_UNROLL
+    for (int m = 0; m < 4; m++) {
+        const Tw w = ldtw(tw, 4096 + t + 1024 * m);
+        const u64 X = xe[m], Y = xo[m];
+        xe[m] = X + Y;
+        xo[m] = mul_shoup_approx(X - Y + P.q2, w.w, w.ws, P.q);
+    }
+}
+// tile index of the pair (2t + 2048m, +1): swz leaves bit 0 alone and 2048m
+// leaves bits 1..6 alone, so one swizzled base and immediate offsets
+HD int pair_index(int t, int m) { return swz(2 * t) + 2048 * m; }
+
+#if defined(__CUDACC__)
+template <int VT = 1>
+__device__ __forceinline__ void cta_ntt_fwd_core(const Tw* tw, const PrimeC& P, u64* sm) {  // stages 0..11
+    const TwG tg{tw};
+    u64 x[EPT];
+    HC_UNROLL
+    for (int p = 0; p < 4; p++) {
+        HC_NOUNROLL
+        for (int v = 0; v < VT; v++) {
+            const CPass I = pass1k(p, threadIdx.x + v * (NT / VT));
+            t_load(x, sm, I);
+            r8_ct(x, tg, I.s0, I.G, P.q, 2 * P.q2);
+            t_store(x, sm, I);
+        }
+        __syncthreads();
+    }
+}
+template <int VT = 1>
+__device__ __forceinline__ void cta_ntt_inv_core(const Tw* tw, const PrimeC& P, u64* sm) {  // stages 1..12 (bit 0 done)
+    const TwG tg{tw};
+    u64 x[EPT];
+    HC_UNROLL
+    for (int p = 0; p < 3; p++) {
+        HC_NOUNROLL
+        for (int v = 0; v < VT; v++) {
+            const CPass I = pass1k(3 - p, threadIdx.x + v * (NT / VT));
+            t_load(x, sm, I);
+            r8_gs(x, tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
+            t_store(x, sm, I);
+        }
+        __syncthreads();
+    }
+    HC_NOUNROLL
+    for (int v = 0; v < VT; v++) {
+        const CPass I = pass1k(0, threadIdx.x + v * (NT / VT));
+        t_load(x, sm, I);
+        c_phaseA_inv(x, tw, P);
+        t_store(x, sm, I);
+    }
+    __syncthreads();
+}
+#endif
+
 // ---- host emulation of the 1024-thread schedule (CPU self-test only) ------
 inline void host_emulate_fwd(u64* a, const Tw* tw, const PrimeC& P) {
     static u64 regs[NT][EPT];
@@ -128,6 +202,67 @@ inline void host_emulate_inv(u64* a, const Tw* tw, const PrimeC& P) {
             r8_gs(regs[t], tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
             t_store(regs[t], sm, I);
         }
+    }
+    for (int t = 0; t < NT; t++) {
+        CPass I = pass1k(0, t);
+        t_load(regs[t], sm, I);
+        c_phaseA_inv(regs[t], tw, P);
+        t_store(regs[t], sm, I);
+    }
+    for (int j = 0; j < NPOLY; j++) a[j] = sm[swz(j)];
+}
+
+
+// host emulation of k_xf's edge-stage form (fwd_last_stage / inv_first_stage)
+inline void host_emulate_fwd_edge(u64* a, const Tw* tw, const PrimeC& P) {
+    static u64 regs[NT][EPT];
+    static u64 sm[NPOLY];
+    const TwG tg{tw};
+    for (int j = 0; j < NPOLY; j++) sm[swz(j)] = a[j];
+    for (int p = 0; p < 4; p++) {
+        for (int t = 0; t < NT; t++) {
+            CPass I = pass1k(p, t);
+            t_load(regs[t], sm, I);
+            r8_ct(regs[t], tg, I.s0, I.G, P.q, 2 * P.q2);
+        }
+        for (int t = 0; t < NT; t++) t_store(regs[t], sm, pass1k(p, t));
+    }
+    for (int t = 0; t < NT; t++) {
+        u64 xe[4], xo[4];
+        for (int m = 0; m < 4; m++) {
+            xe[m] = sm[pair_index(t, m)];
+            xo[m] = sm[pair_index(t, m) + 1];
+        }
+        fwd_last_stage(xe, xo, tw, t, P, false);
+        for (int m = 0; m < 4; m++) {
+            a[2 * t + 2048 * m] = xe[m];
+            a[2 * t + 2048 * m + 1] = xo[m];
+        }
+    }
+}
+inline void host_emulate_inv_edge(u64* a, const Tw* tw, const PrimeC& P) {
+    static u64 regs[NT][EPT];
+    static u64 sm[NPOLY];
+    const TwG tg{tw};
+    for (int t = 0; t < NT; t++) {
+        u64 xe[4], xo[4];
+        for (int m = 0; m < 4; m++) {
+            xe[m] = a[2 * t + 2048 * m];
+            xo[m] = a[2 * t + 2048 * m + 1];
+        }
+        inv_first_stage(xe, xo, tw, t, P);
+        for (int m = 0; m < 4; m++) {
+            sm[pair_index(t, m)] = xe[m];
+            sm[pair_index(t, m) + 1] = xo[m];
+        }
+    }
+    for (int p = 0; p < 3; p++) {
+        for (int t = 0; t < NT; t++) {
+            CPass I = pass1k(3 - p, t);
+            t_load(regs[t], sm, I);
+            r8_gs(regs[t], tg, 1 + 3 * p, I.G, P.q, 2 * P.q2);
+        }
+        for (int t = 0; t < NT; t++) t_store(regs[t], sm, pass1k(3 - p, t));
     }
     for (int t = 0; t < NT; t++) {
         CPass I = pass1k(0, t);

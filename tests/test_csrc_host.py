@@ -24,6 +24,7 @@ def ht():
     L.ht_init.argtypes = [P, ctypes.c_int, ctypes.c_uint64]
     L.ht_ntt.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_ntt_cl.argtypes = [ctypes.c_int, P, ctypes.c_int]
+    L.ht_ntt_edge.argtypes = [ctypes.c_int, P, ctypes.c_int]
     L.ht_compose.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P]
     L.ht_compose2_check.argtypes = [P, P, ctypes.c_int]
     L.ht_rescale_rd_check.argtypes = [ctypes.c_int, P, ctypes.c_int]
@@ -69,6 +70,13 @@ def test_ntt_schedule_matches_reference_transform(setup):
         got = a.copy()
         ht.ht_ntt(t, p_(got), 1)
         assert np.array_equal(got, want_i), f"inverse NTT mismatch for prime {k}"
+        # k_xf's form (bit-0 stage in registers at the kernel's edge) on the same data
+        got = a.copy()
+        ht.ht_ntt_edge(t, p_(got), 0)
+        assert np.array_equal(got, want_f), f"edge-stage forward NTT mismatch for prime {k}"
+        got = a.copy()
+        ht.ht_ntt_edge(t, p_(got), 1)
+        assert np.array_equal(got, want_i), f"edge-stage inverse NTT mismatch for prime {k}"
         # cluster schedule (8 CTAs, DSMEM exchange) on the same data
         got = a.copy()
         ht.ht_ntt_cl(t, p_(got), 0)
