@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
         load_pre<LD, EPT>(J, t, NT, pre);
         pdl_wait();
         load_post<LD, EPT>(C, J, P, t, NT, pre, x);
+        // one schedule thread per thread: the loader's coefficients are pass
+        // 0's, so stages 0..2 run before the first trip through the tile
+        r8_ct(x, TwG{tw}, 0, 0, P.q, 2 * P.q2);
         HC_UNROLL
         for (int e = 0; e < EPT; e++) sm[swz(t) + NT * e] = x[e];
     } else {
@@ -433,8 +436,8 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
     TRACE(1);
     // forward outputs that only feed Montgomery products stay lazy (< 2^60)
     constexpr bool lazy = EP == EP_KSACC || EP == EP_STORE_LAZY;
-    if (DIR == 0) cta_ntt_fwd_core<VT>(tw, P, sm);
-    else cta_ntt_inv_core<VT>(tw, P, sm);
+    if (DIR == 0) cta_ntt_fwd_core<VT, VT == 1 ? 1 : 0>(tw, P, sm);
+    else cta_ntt_inv_core<VT, VT == 1>(tw, P, sm);
     TRACE(4);
     pdl_trigger();
     HC_NOUNROLL
@@ -455,6 +458,7 @@ __global__ void __launch_bounds__(VT == 4 ? HC_XF4_BOUND : NT / VT, VT == 4 ? 3 
             u64 x[EPT];
             HC_UNROLL
             for (int e = 0; e < EPT; e++) x[e] = sm[swz(t) + NT * e];
+            if constexpr (VT == 1) c_phaseA_inv(x, tw, P);  // the last pass, in the epilogue's registers
             store_n<EP, EPT>(C, J, P, t, NT, x);
         }
     }

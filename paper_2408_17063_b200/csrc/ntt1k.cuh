@@ -129,12 +129,14 @@ HD void inv_first_stage(u64 (&xe)[4], u64 (&xo)[4], const Tw* tw, int t, const P
 HD int pair_index(int t, int m) { return swz(2 * t) + 2048 * m; }
 
 #if defined(__CUDACC__)
-template <int VT = 1>
+// P0: first pass to run (1: the caller did pass 0 -- stages 0..2 on the
+// coefficients t + 1024e its loader holds -- in registers and stored them)
+template <int VT = 1, int P0 = 0>
 __device__ __forceinline__ void cta_ntt_fwd_core(const Tw* tw, const PrimeC& P, u64* sm) {  // stages 0..11
     const TwG tg{tw};
     u64 x[EPT];
     HC_UNROLL
-    for (int p = 0; p < 4; p++) {
+    for (int p = P0; p < 4; p++) {
         HC_NOUNROLL
         for (int v = 0; v < VT; v++) {
             const CPass I = pass1k(p, threadIdx.x + v * (NT / VT));
@@ -145,7 +147,9 @@ __device__ __forceinline__ void cta_ntt_fwd_core(const Tw* tw, const PrimeC& P, 
         __syncthreads();
     }
 }
-template <int VT = 1>
+// LASTREG: the last pass (stages 10..12, n^-1 folded) is left to the caller,
+// which runs it in registers on the coefficients t + 1024e its epilogue owns
+template <int VT = 1, bool LASTREG = false>
 __device__ __forceinline__ void cta_ntt_inv_core(const Tw* tw, const PrimeC& P, u64* sm) {  // stages 1..12 (bit 0 done)
     const TwG tg{tw};
     u64 x[EPT];
@@ -160,6 +164,7 @@ __device__ __forceinline__ void cta_ntt_inv_core(const Tw* tw, const PrimeC& P, 
         }
         __syncthreads();
     }
+    if constexpr (LASTREG) return;
     HC_NOUNROLL
     for (int v = 0; v < VT; v++) {
         const CPass I = pass1k(0, threadIdx.x + v * (NT / VT));
