@@ -104,25 +104,17 @@ __device__ __forceinline__ void cta_ntt_inv(const Tw* tw, const PrimeC& P, u64* 
 // and none of c_st12 / c_st0's even/odd selects (~100 of ~1400 instructions
 // per schedule thread), and the pairs move as 128-bit shared-memory accesses.
 HD void fwd_last_stage(u64 (&xe)[4], u64 (&xo)[4], const Tw* tw, int t, const PrimeC& P, bool lazy) {
+    Tw w[4];
     HC_UNROLL
-    for (int m = 0; m < 4; m++) {
-        const Tw w = ldtw(tw, 4096 + t + 1024 * m);  // tbl[4096 + (j >> 1)]
-        bf_ct_lazy(xe[m], xo[m], w.w, w.ws, P.q, 2 * P.q2);
-        if (!lazy) {
-            xe[m] = canon_any(xe[m], P.q, P.one_s);
-            xo[m] = canon_any(xo[m], P.q, P.one_s);
-        }
-    }
+    for (int m = 0; m < 4; m++) w[m] = ldtw(tw, 4096 + t + 1024 * m);  // tbl[4096 + (j >> 1)]
+    edge_fwd(xe, xo, w, P, lazy);
 }
 // inverse bit-0 stage on loader outputs in [0, 2q): sums < 4q, products < 4q
 HD void inv_first_stage(u64 (&xe)[4], u64 (&xo)[4], const Tw* tw, int t, const PrimeC& P) {
+    Tw w[4];
     HC_UNROLL
-    for (int m = 0; m < 4; m++) {
-        const Tw w = ldtw(tw, 4096 + t + 1024 * m);
-        const u64 X = xe[m], Y = xo[m];
-        xe[m] = X + Y;
-        xo[m] = mul_shoup_approx(X - Y + P.q2, w.w, w.ws, P.q);
-    }
+    for (int m = 0; m < 4; m++) w[m] = ldtw(tw, 4096 + t + 1024 * m);
+    edge_inv(xe, xo, w, P);
 }
 // tile index of the pair (2t + 2048m, +1): swz leaves bit 0 alone and 2048m
 // leaves bits 1..6 alone, so one swizzled base and immediate offsets

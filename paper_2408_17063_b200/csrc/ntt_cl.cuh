@@ -293,6 +293,36 @@ HD u64 kf_front(const u32 (&dg)[CEPT], const u32 (&klo)[CEPT], const u32 (&khi)[
     return (H << 32) - mulhi(H, w32s) * q + (u32)lo;
 }
 
+// The bit-0 stage at the EDGE of a transform, in registers: the thread owns
+// four coefficient pairs (j, j + 1) and w[m] = tbl[4096 + (j_m >> 1)].  The
+// forward transform ends with it (epilogue side), the inverse starts with it
+// (loader side); no lane exchange, none of c_st12 / c_st0's even/odd selects.
+// Forward outputs canonical, or (lazy) below 2^60; inverse inputs in [0, 2q),
+// outputs in [0, 4q).
+HD void edge_fwd(u64 (&xe)[4], u64 (&xo)[4], const Tw (&w)[4], const PrimeC& P, bool lazy) {
+    HC_UNROLL
+    for (int m = 0; m < 4; m++) {
+        bf_ct_lazy(xe[m], xo[m], w[m].w, w[m].ws, P.q, 2 * P.q2);
+        if (!lazy) {
+            xe[m] = canon_any(xe[m], P.q, P.one_s);
+            xo[m] = canon_any(xo[m], P.q, P.one_s);
+        }
+    }
+}
+HD void edge_inv(u64 (&xe)[4], u64 (&xo)[4], const Tw (&w)[4], const PrimeC& P) {
+    HC_UNROLL
+    for (int m = 0; m < 4; m++) {
+        const u64 X = xe[m], Y = xo[m];
+        xe[m] = X + Y;
+        xo[m] = mul_shoup_approx(X - Y + P.q2, w[m].w, w[m].ws, P.q);
+    }
+}
+// cluster schedule: CTA c's thread t owns the local pairs 2t + 256m (tile
+// index cswz(2t) + 256m: bit 0 and bits >= 7 are outside the swizzle), global
+// coefficient c*1024 + 2t + 256m, twiddle index 4096 + 512c + t + 128m
+HD int cpair_index(int t, int m) { return cswz(2 * t) + 256 * m; }
+HD int cpair_tw(int c, int t, int m) { return 4096 + (c << 9) + t + 128 * m; }
+
 // forward phase A: stages 0..2 on the column (x[a] = coefficient a*1024 + b)
 HD void c_phaseA_fwd(u64 (&x)[CEPT], const Tw* tw, u64 q, u64 q4) { r8_ct(x, TwG{tw}, 0, 0, q, q4); }
 
