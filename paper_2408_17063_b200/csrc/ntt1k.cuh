@@ -156,15 +156,16 @@ __device__ __forceinline__ void cta_ntt_inv_core(const Tw* tw, const PrimeC& P, 
         }
         __syncthreads();
     }
-    if constexpr (LASTREG) return;
-    HC_NOUNROLL
-    for (int v = 0; v < VT; v++) {
-        const CPass I = pass1k(0, threadIdx.x + v * (NT / VT));
-        t_load(x, sm, I);
-        c_phaseA_inv(x, tw, P);
-        t_store(x, sm, I);
+    if constexpr (!LASTREG) {
+        HC_NOUNROLL
+        for (int v = 0; v < VT; v++) {
+            const CPass I = pass1k(0, threadIdx.x + v * (NT / VT));
+            t_load(x, sm, I);
+            c_phaseA_inv(x, tw, P);
+            t_store(x, sm, I);
+        }
+        __syncthreads();
     }
-    __syncthreads();
 }
 #endif
 
