@@ -80,6 +80,14 @@ HD u64 mul_mont(u64 a, u64 bm, u64 q, u64 qneg) {
     return redc(hi, lo, q, qneg);
 }
 
+// the same without the final conditional subtraction: result in [0, 2q)
+// (loader outputs of the inverse transforms, whose first stage takes < 2q)
+HD u64 mul_mont_lazy(u64 a, u64 bm, u64 q, u64 qneg) {
+    u64 hi, lo;
+    mul128(hi, lo, a, bm);
+    return redc_lazy(hi, lo, q, qneg);
+}
+
 // -q^-1 mod 2^64 (q odd)
 HD u64 mont_qneg(u64 q) {
     u64 x = 1;

@@ -199,15 +199,16 @@ HD u64 red64(u64 a, u64 q, u64 one_s) { return reduce_once(mul_shoup_lazy(a, 1, 
 // (r, d), so a sum of corrections is formed from the sums of r and d (exact in
 // int64 for up to 1024 terms) with one multiply per coefficient (k_diagx).
 HD void rescale_rd(const RescaleK& R, u64 x, long long& r, long long& d) {
-    const int neg = x > R.half_qd;
-    const u64 mag = neg ? R.ql - x : x;
-    u64 rm = mag - mulhi(mag, R.pbar) * R.p;  // Barrett: [0, 2p)
-    if (rm >= R.p) rm -= R.p;
-    if (neg && rm) rm = R.p - rm;  // r mod p in [0, p)
-    const int dneg = rm > R.half_p;
-    const u64 dmag = dneg ? R.p - rm : rm;
-    r = neg ? -(long long)mag : (long long)mag;
-    d = dneg ? -(long long)dmag : (long long)dmag;
+    const bool neg = x > R.half_qd;
+    r = (long long)(x - (neg ? R.ql : 0));  // centered residue, |r| <= q_l / 2
+    // r mod p: every chain prime is 1 mod p (hc_ctx_create checks), so
+    // r = x - neg * q_l = x - neg (mod p); p < 2^31, 32-bit from here on
+    const u64 xm = x - mulhi(x, R.pbar) * R.p;  // Barrett: [0, 2p)
+    const u32 p = (u32)R.p;
+    u32 m = (u32)xm;
+    m = m >= p ? m - p : m;                      // x mod p
+    m = neg ? (m ? m - 1 : p - 1) : m;           // r mod p in [0, p)
+    d = m > (u32)R.half_p ? (long long)m - (long long)p : (long long)m;
 }
 
 // signed 64-bit -> [0, q)

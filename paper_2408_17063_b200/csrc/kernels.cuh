@@ -62,7 +62,7 @@ constexpr u64 PX_BOUND = 1ull << 61;     // diagonal-MAC atomics: < 4q (block la
 // ---------------------------------------------------------------------------
 enum : int {
     LD_U64 = 0,    // a[j]
-    LD_MONT = 1,   // a[j] * b[j] (b in Montgomery form)
+    LD_MONT = 1,   // a[j] * b[j] (b in Montgomery form), in [0, 2q): inverse transforms only
     LD_ADD = 2,    // a[j] + b[j] mod q
     LD_RED = 3,    // a[j] reduced from any u64 (+ b[j] likewise if b)
     LD_DIG = 4,    // u16 digit a[j]
@@ -267,7 +267,8 @@ __device__ __forceinline__ void load_post(const DevCtx& C, const XJob& J, const 
         HC_UNROLL
         for (int e = 0; e < N; e++) { x[e] = J.a[j0 + e * stride]; b[e] = J.b[j0 + e * stride]; }
         HC_UNROLL
-        for (int e = 0; e < N; e++) x[e] = LD == LD_MONT ? mul_mont(x[e], b[e], P.q, P.qneg) : add_mod(x[e], b[e], P.q);
+        // LD_MONT feeds inverse transforms only (XF_COMBOS), whose first stage takes [0, 2q)
+        for (int e = 0; e < N; e++) x[e] = LD == LD_MONT ? mul_mont_lazy(x[e], b[e], P.q, P.qneg) : add_mod(x[e], b[e], P.q);
     } else if constexpr (LD == LD_RED) {
         HC_UNROLL
         for (int e = 0; e < N; e++) x[e] = J.a[j0 + e * stride];
