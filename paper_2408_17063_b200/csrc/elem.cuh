@@ -171,21 +171,23 @@ HD RescaleK rescale_consts_rd(const DevCtx& D, int l) {
 // writes e_k for k < l.
 template <int NQ>
 HD void rescale_corr(const RescaleKT<NQ>& R, u64 x, u64* e) {
-    const int neg = x > R.half_qd;
-    const u64 mag = neg ? R.ql - x : x;  // |r|
-    u64 rm = mag - mulhi(mag, R.pbar) * R.p;  // Barrett: [0, 2p)
-    if (rm >= R.p) rm -= R.p;
-    if (neg && rm) rm = R.p - rm;  // r mod p in [0, p)
-    const int dneg = rm > R.half_p;
-    const u64 dmag = dneg ? R.p - rm : rm;  // |d|
+    const bool neg = x > R.half_qd;
+    const u64 mag = neg ? R.ql - x : x;  // |r| <= q_l / 2 < 2^53 <= q_k
+    // d = centered_p(r mod p), r = x - neg (mod p) since q_l = 1 (mod p); 32-bit
+    const u64 xm = x - mulhi(x, R.pbar) * R.p;  // Barrett: [0, 2p)
+    const u32 p = (u32)R.p;
+    u32 m = (u32)xm;
+    m = m >= p ? m - p : m;
+    m = neg ? (m ? m - 1 : p - 1) : m;
+    const long long d = m > (u32)R.half_p ? (long long)m - (long long)p : (long long)m;
     HC_UNROLL
     for (int k = 0; k < NQ; k++) {
         if (k >= R.l) break;
         const u64 q = R.q[k];
-        const u64 rk = neg ? (mag ? q - mag : 0) : mag;  // r mod q_k (|r| < q_k)
-        const u64 t = mul_shoup(rk, R.qinv[k], R.qinv_s[k], q);
-        const u64 dk = dneg ? (dmag ? q - dmag : 0) : dmag;
-        e[k] = sub_mod(dk, t, q);
+        // e_k = d - r q_l^-1 = d -+ |r| q_l^-1 (mod q_k), from residues in [0, q)
+        const u64 u = mul_shoup(mag, R.qinv[k], R.qinv_s[k], q);
+        const u64 dk = d < 0 ? q + (u64)d : (u64)d;  // d mod q_k (|d| < p / 2)
+        e[k] = reduce_once(dk + (neg ? u : q - u), q);  // q - u = q when u = 0: the sum stays < 2q
     }
 }
 

@@ -168,6 +168,18 @@ def test_rescale_correction_equals_mod_switch(setup, oracle):
         x[:, :4] = 0
         x[level, 1] = be.q[level] >> 1          # r = +floor(q/2)
         x[level, 2] = (be.q[level] >> 1) + 1    # r = -floor(q/2)
+        # boundaries of both centrings: r around 0 and +-q/2, d = centered_p(r mod p)
+        # around 0 and +-p/2 (residues k p + {p/2 - 1 .. p/2 + 2}, from both ends)
+        qd_, edge = be.q[level], []
+        for t in range(24):
+            edge += [t, qd_ - 1 - t, (qd_ >> 1) - t, (qd_ >> 1) + 1 + t]
+        for kk in (0, 1, 5, qd_ // (2 * p) - 1, qd_ // (2 * p), qd_ // p - 2):
+            for dlt in (-1, 0, 1, 2):
+                for sgn in (0, 1):  # r = +(k p + p/2 + dlt) and r = -(...)
+                    v = kk * p + (p >> 1) + dlt
+                    edge.append(v if sgn == 0 else qd_ - v)
+        edge = [v % qd_ for v in edge]
+        x[level, 8:8 + len(edge)] = edge
         want = np.empty((level, N8K), dtype=np.uint64)
         qv = np.asarray(be.q[:P], dtype=np.uint64)
         oracle.lib().orc_rescale(p_(np.ascontiguousarray(x)), p_(want), P, N8K, p_(qv), p)
