@@ -205,10 +205,9 @@ static void release_key(DevKey& k) {
     X(1, LD_U64, EP_STORE)            \
     X(0, LD_RED, EP_STORE)            \
     X(1, LD_RED, EP_STORE)            \
-    X(1, LD_MONT, EP_RESCALE)         \
+    X(1, LD_MONT, EP_RS)              \
     X(1, LD_MONT, EP_RESCALE_RD)      \
     X(1, LD_MONT, EP_RESCALE4)        \
-    X(1, LD_MONT, EP_STORE)           \
     X(0, LD_U64, EP_ADDMONT)          \
     X(0, LD_DIG, EP_STORE_LAZY)       \
     X(0, LD_DIGGAL, EP_STORE_LAZY)    \
@@ -468,7 +467,8 @@ static int add_xf(Schedule& S, const std::vector<XJob>& jobs) {
         std::vector<XJob> sel;
         for (size_t k = i; k < jobs.size(); k++) {
             const XJob &a = jobs[i], &b = jobs[k];
-            if (!taken[k] && a.dir == b.dir && a.ld == b.ld && a.ep == b.ep && a.noxf == b.noxf) {
+            if (!taken[k] && a.dir == b.dir && a.ld == b.ld && kernel_ep(a.dir, a.ld, a.ep) == kernel_ep(b.dir, b.ld, b.ep) &&
+                a.noxf == b.noxf) {
                 sel.push_back(b);
                 taken[k] = 1;
             }
@@ -816,7 +816,7 @@ static int enqueue_step(const hc_ctx* h, const Step& st, cudaStream_t s) {
                 }
                 bool done = false;
 #define XF_LAUNCH(D, L, E)                                                                               \
-    if (!done && j0.dir == D && j0.ld == L && j0.ep == E) {                                              \
+    if (!done && j0.dir == D && j0.ld == L && kernel_ep(j0.dir, j0.ld, j0.ep) == E) {                    \
         if (clu) {                                                                                       \
             switch (st.jpc) {                                                                            \
                 case 1: CU(launch(k_xf_cl<D, L, E, 1>, ncl * CL, CNT, CL_SMEM, s, h->hctx, cj)); break;     \
@@ -2789,7 +2789,7 @@ static int comp_profile(hc_ctx* h, void* stream, int max_steps, float* step_ms, 
                 const XJob& j = st.hjobs[0];
                 const bool clu = st.cl && st.njobs <= CL_MAX;
                 const int vt = clu ? st.jpc : (st.njobs >= g_vt2_jobs ? 4 : 1);
-                tag = (clu ? 1 << 20 : 0) | (j.dir << 16) | (j.ld << 12) | (j.ep << 8) | (j.noxf << 4) | vt;
+                tag = (clu ? 1 << 20 : 0) | (j.dir << 16) | (j.ld << 12) | (kernel_ep(j.dir, j.ld, j.ep) << 8) | (j.noxf << 4) | vt;
             }
             step_tag[k] = tag;
         }

@@ -97,7 +97,16 @@ enum : int {
     EP_KSACC = 6,          // key-switch digit product: out[j] += x*ea[j], out[ostride+j] += x*eb[j]
     EP_STORE_LAZY = 7,     // out[j] = x, x < 2^60 not canonicalised (forward NTT feeding k_ksmac)
     EP_RESCALE4 = 8,       // EP_RESCALE from level 4 (answer()'s Mask / pack products; 4 kept primes)
+    // kernel instantiation only (never a job's ep): EP_RESCALE and EP_STORE jobs
+    // of one step in ONE launch, the job's own ep picked per CTA -- pack_pair's
+    // dropped-prime and kept-prime INTTs (S1) as one launch instead of two
+    // cluster kernels side by side
+    EP_RS = 9,
 };
+// the instantiation a job's epilogue runs in
+__host__ __device__ inline int kernel_ep(int dir, int ld, int ep) {
+    return (dir == 1 && ld == LD_MONT && (ep == EP_RESCALE || ep == EP_STORE)) ? EP_RS : ep;
+}
 
 struct XJob {
     int dir;    // 0 forward, 1 inverse
@@ -309,7 +318,10 @@ __device__ __forceinline__ void load_n(const DevCtx& C, const XJob& J, const Pri
 template <int EP, int N>
 __device__ __forceinline__ void store_n(const DevCtx& D, const XJob& J, const PrimeC& P, int j0, int stride,
                                         const u64 (&x)[N]) {
-    if constexpr (EP == EP_ADDMONT || EP == EP_KSACC) {
+    if constexpr (EP == EP_RS) {  // uniform per CTA (per thread group in cluster launches)
+        if (J.ep == EP_STORE) store_n<EP_STORE, N>(D, J, P, j0, stride, x);
+        else store_n<EP_RESCALE, N>(D, J, P, j0, stride, x);
+    } else if constexpr (EP == EP_ADDMONT || EP == EP_KSACC) {
         u64 a[N], b[N];
         HC_UNROLL
         for (int e = 0; e < N; e++) { a[e] = J.ea[j0 + e * stride]; b[e] = J.eb[j0 + e * stride]; }

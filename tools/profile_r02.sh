@@ -27,7 +27,7 @@ cap foldchain   'k_foldchain'            0 $B
 cap giant_ntt   'k_xf_cl<\(int\)0, \(int\)5, \(int\)6, \(int\)3>'    0 $B
 cap ksmac_lat   'k_ksmac<\(int\)1, \(int\)4>'          1 $B
 cap compose     'k_compose'              0 $B
-cap pack_intt   'k_xf_cl<\(int\)1, \(int\)1, \(int\)4, \(int\)2>'    0 $B
+cap pack_intt   'k_xf_cl<\(int\)1, \(int\)1, \(int\)9, \(int\)2>'    0 $B
 cap ksmac_2e20  'k_ksmac_mb'             1 python bench.py --N 1048576 --sparsity 16 --steps 1 --warmup 3 --no-cpu-baseline --no-parity
 cap diagx_2e20  'k_diagx'                1 python bench.py --N 1048576 --sparsity 16 --steps 1 --warmup 3 --no-cpu-baseline --no-parity
 cap xf_dig_2e20 'k_xf<\(int\)0, \(int\)5, \(int\)7, \(int\)4>'       1 python bench.py --N 1048576 --sparsity 16 --steps 1 --warmup 3 --no-cpu-baseline --no-parity
